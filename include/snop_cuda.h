@@ -1,0 +1,170 @@
+/*
+ * snop_cuda.h — C-ABI of the B200-native S_N transport hot path (libsnop_cuda.so).
+ *
+ * Drop-in boundary for the reference's planned `snop::` solver API. The reference ships no
+ * solver headers (only proj/core/include/snop/{binary_io,errors,parallel,rng}.hpp); its API
+ * exists as the SPEC [OP] signatures cited on each entry point below. Every entry point:
+ *   - takes plain pointers + sizes (no C++ / torch types),
+ *   - never throws; returns snop_status (1:1 with proj/core/include/snop/errors.hpp:8-41),
+ *     with a thread-local message from snop_last_error(),
+ *   - reports per-instance non-convergence as data (converged[b] = 0), never as an error
+ *     (SPEC.md:129,183),
+ *   - accepts HOST pointers (SNOP_MEM_HOST: the call copies in/out, synchronous) or DEVICE
+ *     pointers (SNOP_MEM_DEVICE: enqueued on the context's stream, asynchronous; caller syncs
+ *     with snop_ctx_synchronize()).
+ *
+ * Array layouts (row-major, fp64 unless noted), B = batch, G = groups, Nc = cells:
+ *   per-cell single group  [B][Nc]
+ *   multigroup             [B][G][Nc]
+ *   scattering matrix      [B][G][G][Nc], entry [b][g'][g][i] = Sigma_s0^{g'->g}(x_i)
+ *   fission spectrum chi   [B][G]
+ */
+#ifndef SNOP_CUDA_H
+#define SNOP_CUDA_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SNOP_ABI_VERSION 1
+
+typedef enum {
+  SNOP_OK = 0,
+  SNOP_INVALID_ARGUMENT = 1,   /* snop::InvalidArgument  (errors.hpp:13-17)  */
+  SNOP_NUMERICAL_ERROR = 2,    /* snop::NumericalError   (errors.hpp:19-23)  */
+  SNOP_DEGENERATE_PROBLEM = 3, /* snop::DegenerateProblem(errors.hpp:25-29)  */
+  SNOP_IO_ERROR = 4,           /* snop::IoError          (errors.hpp:31-35)  */
+  SNOP_CONFIG_ERROR = 5,       /* snop::ConfigError      (errors.hpp:37-41)  */
+  SNOP_CUDA_ERROR = 6          /* device/runtime failure (no reference analogue) */
+} snop_status;
+
+typedef enum { SNOP_MEM_HOST = 0, SNOP_MEM_DEVICE = 1 } snop_memspace;
+typedef enum { SNOP_BC_VACUUM = 0, SNOP_BC_REFLECTIVE = 1 } snop_boundary;
+typedef enum { SNOP_NORM_REL_LINF = 0, SNOP_NORM_REL_L2 = 1 } snop_norm;
+typedef enum { SNOP_ACT_RELU = 0, SNOP_ACT_TANH = 1, SNOP_ACT_GELU = 2 } snop_activation;
+typedef enum { SNOP_RECAST_CONVERGED = 0, SNOP_RECAST_MAXED = 1, SNOP_RECAST_DIVERGED = 2 } snop_recast_status;
+
+/* Grid1D: uniform slab, dx = length / n_cells, x_i = (i + 1/2) dx. */
+typedef struct {
+  double length_cm;
+  int32_t n_cells;
+  int32_t reserved;
+} snop_grid;
+
+/* SolverConfig with the eigen tolerances split. */
+typedef struct {
+  double tolerance;       /* fixed-source / inner tolerance (default 1e-4) */
+  double tolerance_k;     /* eigen |dk|/k (default = tolerance) */
+  double tolerance_phi;   /* eigen outer flux change (default = tolerance) */
+  int32_t max_inner;      /* default 10000 */
+  int32_t max_outer;      /* default 5000 */
+  int32_t bc_left;        /* snop_boundary */
+  int32_t bc_right;       /* snop_boundary */
+  int32_t norm;           /* snop_norm */
+  int32_t reserved;
+} snop_solver_config;
+
+typedef struct snop_ctx snop_ctx;  /* owns one CUDA stream + device workspace */
+typedef struct snop_op snop_op;    /* SolutionOperator handle */
+
+int32_t snop_abi_version(void);
+const char* snop_last_error(void);
+
+snop_status snop_ctx_create(int32_t device, snop_ctx** out);
+snop_status snop_ctx_destroy(snop_ctx* ctx);
+snop_status snop_ctx_synchronize(snop_ctx* ctx);
+/* Number of snop kernels this context has launched (for the bench's gpu_launches claim). */
+int64_t snop_ctx_launch_count(const snop_ctx* ctx);
+/* The CUDA stream (cudaStream_t) the context enqueues on, as an opaque pointer. */
+void* snop_ctx_stream(snop_ctx* ctx);
+
+/* gauss_legendre: nodes ascending, mu[n] = -mu[order-1-n]. Host pointers. */
+snop_status snop_gauss_legendre(int32_t order, double* mu, double* w);
+
+/*
+ * Batched single-group fixed-source solve — replaces
+ *   source_iteration(grid, quadrature, materials, external_source, config, initial_phi)
+ *   (sweep SPEC.md:115-123), for B independent instances.
+ * sigma_s1 (P1 within-group moment, Eq. 25) and initial_phi may be NULL (isotropic / zero guess).
+ * current_out may be NULL. iterations = sweeps performed.
+ */
+snop_status snop_source_iteration_batched(
+    snop_ctx* ctx, int32_t memspace, const snop_grid* grid, int32_t order, int32_t batch,
+    const double* sigma_t, const double* sigma_s0, const double* sigma_s1, const double* source,
+    const snop_solver_config* cfg, const double* initial_phi,
+    double* phi_out, double* current_out, int32_t* iterations, uint8_t* converged);
+
+/*
+ * Batched k-eigenvalue power iteration — replaces
+ *   power_iteration(grid, quadrature, materials, config, inner_solver, initial)
+ *   (decisions :206-209) with the model-based inner solver, G >= 1 groups,
+ *   Gauss-Seidel over groups including upscatter.
+ * initial_k / initial_phi may be NULL (flat flux, k = 1).
+ * Any instance with a zero fission integral fails the call with SNOP_DEGENERATE_PROBLEM.
+ */
+snop_status snop_power_iteration_batched(
+    snop_ctx* ctx, int32_t memspace, const snop_grid* grid, int32_t order, int32_t batch, int32_t n_groups,
+    const double* sigma_t, const double* sigma_s0, const double* sigma_s1, const double* nu_sigma_f,
+    const double* chi, const snop_solver_config* cfg, const double* initial_k, const double* initial_phi,
+    double* k_out, double* phi_out, int32_t* outer_iterations, int64_t* inner_iterations, uint8_t* converged);
+
+/* recast_source (paper Eq. 24): out = S + [(Ss0 - Ss0*) - (St - St*)] phi. */
+snop_status snop_recast_source(
+    snop_ctx* ctx, int32_t memspace, int32_t batch, int32_t n_cells, const double* source,
+    const double* phi, const double* sigma_t, const double* sigma_s0, double sigma_t_star,
+    double sigma_s0_star, double* out);
+
+/* ---- SolutionOperators ---------------------------------------------
+ * DenseNetwork parameters are packed per layer l as W_l [n_out][n_in] then b_l [n_out] (fp32).
+ * (sigma_t_star, sigma_s0_star) is the reference parameter set p* the operator was built at
+ * ("reference_params"); recast_* uses it.
+ * FNO parameters (fp32) are packed as: lift_W [width][2], lift_b [width]; per layer:
+ *   R_re [modes][width][width] (in,out), R_im [modes][width][width], W [width][width] (out,in),
+ *   b [width]; then P1_W [hidden][width], P1_b [hidden], P2_W [hidden], P2_b [1].
+ */
+snop_status snop_deeponet_create(
+    snop_ctx* ctx, const snop_grid* grid, double sigma_t_star, double sigma_s0_star, int32_t activation,
+    int32_t n_branch_sizes, const int32_t* branch_sizes, const float* branch_params,
+    int32_t n_trunk_sizes, const int32_t* trunk_sizes, const float* trunk_params,
+    int32_t has_bias0, float bias0, snop_op** out);
+
+snop_status snop_fno_create(
+    snop_ctx* ctx, const snop_grid* grid, double sigma_t_star, double sigma_s0_star, int32_t activation, int32_t width, int32_t modes,
+    int32_t n_layers, int32_t proj_hidden, const float* params, snop_op** out);
+
+/* The "exact operator": the model-based solve at p* = (St*, Ss0*) wrapped as a
+ * SolutionOperator; uses `cfg` for its inner solves. */
+snop_status snop_exact_operator_create(
+    snop_ctx* ctx, const snop_grid* grid, int32_t order, double sigma_t_star, double sigma_s0_star,
+    const snop_solver_config* cfg, snop_op** out);
+
+snop_status snop_op_destroy(snop_op* op);
+
+/* predict(model, source) for a batch [B][Nc]; fp64 in/out, the neural
+ * operators compute in fp32. */
+snop_status snop_op_predict(snop_ctx* ctx, snop_op* op, int32_t memspace, int32_t batch,
+                            const double* source, double* out);
+
+/* recast_fixed_point: phi^{k+1} = op(recast(S, phi^k)), phi^0 = op(S) or
+ * initial_phi. status[b] is snop_recast_status. */
+snop_status snop_recast_fixed_point(
+    snop_ctx* ctx, snop_op* op, int32_t memspace, int32_t batch, const double* source,
+    const double* sigma_t, const double* sigma_s0, double recast_tolerance, int32_t recast_max_iterations,
+    int32_t norm, const double* initial_phi, double* phi_out, int32_t* iterations, int32_t* status);
+
+/* precondition_fixed_source (paper Eq. 10): recast fixed point, then the
+ * batched source iteration on the full target problem warm-started from phi_NO. */
+snop_status snop_precondition_fixed_source(
+    snop_ctx* ctx, snop_op* op, int32_t memspace, int32_t order, int32_t batch,
+    const double* sigma_t, const double* sigma_s0, const double* sigma_s1, const double* source,
+    double recast_tolerance, int32_t recast_max_iterations, const snop_solver_config* cfg,
+    double* phi_out, int32_t* precond_iterations, int32_t* recast_status,
+    int32_t* refine_iterations, uint8_t* converged);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SNOP_CUDA_H */

@@ -1,0 +1,361 @@
+// snop ORACLE — TEST INFRASTRUCTURE ONLY. extern "C" layer so pytest (ctypes) can drive the
+// CPU restatement with exactly the argument layout of the product C-ABI (include/snop_cuda.h),
+// host pointers only. Batched entry points parallelise over instances with the restated
+// parallel_chunks (proj/core/include/snop/parallel.hpp:17-48): one chunk per instance, so
+// results are bit-identical at any thread count.
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <string>
+
+#include "../include/snop_cuda.h"
+#include "snop_oracle.hpp"
+
+using namespace snop::oracle;
+
+namespace {
+thread_local std::string g_err;
+
+int map_exc() {
+  try {
+    throw;
+  } catch (const DegenerateProblem& e) {
+    g_err = e.what();
+    return SNOP_DEGENERATE_PROBLEM;
+  } catch (const NumericalError& e) {
+    g_err = e.what();
+    return SNOP_NUMERICAL_ERROR;
+  } catch (const InvalidArgument& e) {
+    g_err = e.what();
+    return SNOP_INVALID_ARGUMENT;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SNOP_NUMERICAL_ERROR;
+  }
+}
+
+SolverConfig to_cfg(const snop_solver_config* c) {
+  SolverConfig s;
+  s.tolerance = c->tolerance;
+  s.tolerance_k = c->tolerance_k;
+  s.tolerance_phi = c->tolerance_phi;
+  s.max_inner = c->max_inner;
+  s.max_outer = c->max_outer;
+  s.left = static_cast<Boundary>(c->bc_left);
+  s.right = static_cast<Boundary>(c->bc_right);
+  s.norm = static_cast<Norm>(c->norm);
+  return s;
+}
+
+DenseNetwork unpack_dense(int n_sizes, const int32_t* sizes, const float* params, Activation act) {
+  DenseNetwork d;
+  d.act = act;
+  d.sizes.assign(sizes, sizes + n_sizes);
+  std::size_t off = 0;
+  for (int l = 0; l + 1 < n_sizes; ++l) {
+    const std::size_t nw = (std::size_t)sizes[l] * sizes[l + 1];
+    d.W.emplace_back(params + off, params + off + nw);
+    off += nw;
+    d.b.emplace_back(params + off, params + off + sizes[l + 1]);
+    off += sizes[l + 1];
+  }
+  return d;
+}
+
+struct OracleOp {
+  int kind = 0;  // 0 deeponet, 1 fno, 2 exact
+  Grid1D grid;
+  double tstar = 1.0, sstar = 0.5;
+  DeepONet don;
+  FNO fno;
+  Quadrature quad;
+  SolverConfig cfg;
+  void predict(const double* s, double* out) const {
+    if (kind == 0) {
+      deeponet_predict(don, grid, s, out);
+    } else if (kind == 1) {
+      fno_predict(fno, grid, s, out);
+    } else {
+      const int n = grid.n_cells;
+      std::vector<double> st(n, tstar), ss(n, sstar);
+      std::fill(out, out + n, 0.0);
+      source_iteration(grid, quad, st.data(), ss.data(), nullptr, s, cfg, out, nullptr);
+    }
+  }
+};
+}  // namespace
+
+extern "C" {
+
+const char* oracle_last_error(void) { return g_err.c_str(); }
+unsigned oracle_hardware_threads(void) { return std::thread::hardware_concurrency(); }
+
+int oracle_gauss_legendre(int32_t order, double* mu, double* w) {
+  try {
+    const Quadrature q = gauss_legendre(order);
+    std::memcpy(mu, q.mu.data(), sizeof(double) * order);
+    std::memcpy(w, q.w.data(), sizeof(double) * order);
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+// The reference's own parallel_chunks partition, restated (golden-checked in tests).
+void oracle_chunk_bounds(uint64_t n_items, uint64_t n_chunks, uint64_t* begins /* n_chunks+1 */) {
+  if (n_chunks == 0 || n_chunks > n_items) n_chunks = n_items;
+  const uint64_t base = n_items / n_chunks, extra = n_items % n_chunks;
+  for (uint64_t c = 0; c <= n_chunks; ++c) begins[c] = c * base + std::min(c, extra);
+}
+
+void oracle_rng_stream(uint64_t seed, int32_t n_u64, uint64_t* u64, int32_t n_uniform, double* uni,
+                       int32_t n_normal, double* nrm) {
+  Rng a(seed);
+  for (int i = 0; i < n_u64; ++i) u64[i] = a.next_u64();
+  Rng b(seed);
+  for (int i = 0; i < n_uniform; ++i) uni[i] = b.uniform();
+  Rng c(seed);
+  for (int i = 0; i < n_normal; ++i) nrm[i] = c.normal();
+}
+
+int oracle_source_iteration_batched(const snop_grid* grid, int32_t order, int32_t batch,
+                                    const double* st, const double* ss0, const double* ss1,
+                                    const double* src, const snop_solver_config* ccfg,
+                                    const double* init_phi, double* phi_out, double* cur_out,
+                                    int32_t* iters, uint8_t* conv, double* leak /* [B][2] or null */,
+                                    int32_t n_threads) {
+  try {
+    const Grid1D g{grid->length_cm, grid->n_cells};
+    const Quadrature q = gauss_legendre(order);
+    const SolverConfig cfg = to_cfg(ccfg);
+    const std::size_t Nc = g.n_cells;
+    std::string err;
+    int code = 0;
+    std::mutex mu;
+    parallel_chunks(batch, batch, [&](std::size_t, std::size_t b0, std::size_t b1) {
+      for (std::size_t b = b0; b < b1; ++b) {
+        try {
+          double* phi = phi_out + b * Nc;
+          if (init_phi) std::memcpy(phi, init_phi + b * Nc, sizeof(double) * Nc);
+          else std::fill(phi, phi + Nc, 0.0);
+          const SIResult r = source_iteration(g, q, st + b * Nc, ss0 + b * Nc, ss1 ? ss1 + b * Nc : nullptr,
+                                              src + b * Nc, cfg, phi, cur_out ? cur_out + b * Nc : nullptr);
+          iters[b] = r.iterations;
+          conv[b] = r.converged ? 1 : 0;
+          if (leak) { leak[2 * b] = r.out_left; leak[2 * b + 1] = r.out_right; }
+        } catch (...) {
+          std::lock_guard<std::mutex> lk(mu);
+          code = map_exc();
+          err = g_err;
+        }
+      }
+    }, n_threads);
+    if (code) { g_err = err; return code; }
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+int oracle_power_iteration_batched(const snop_grid* grid, int32_t order, int32_t batch, int32_t G,
+                                   const double* st, const double* ss0, const double* ss1, const double* nsf,
+                                   const double* chi, const snop_solver_config* ccfg, const double* init_k,
+                                   const double* init_phi, double* k_out, double* phi_out, int32_t* outer,
+                                   int64_t* inner, uint8_t* conv, int32_t n_threads) {
+  try {
+    const Grid1D g{grid->length_cm, grid->n_cells};
+    const Quadrature q = gauss_legendre(order);
+    const SolverConfig cfg = to_cfg(ccfg);
+    const std::size_t Nc = g.n_cells, GN = (std::size_t)G * Nc;
+    std::string err;
+    int code = 0;
+    std::mutex mu;
+    parallel_chunks(batch, batch, [&](std::size_t, std::size_t b0, std::size_t b1) {
+      for (std::size_t b = b0; b < b1; ++b) {
+        try {
+          MGView m;
+          m.G = G;
+          m.sigma_t = st + b * GN;
+          m.sigma_s0 = ss0 + b * GN * G;
+          m.sigma_s1 = ss1 ? ss1 + b * GN : nullptr;
+          m.nu_sigma_f = nsf + b * GN;
+          m.chi = chi + b * G;
+          double* phi = phi_out + b * GN;
+          if (init_phi) std::memcpy(phi, init_phi + b * GN, sizeof(double) * GN);
+          else std::fill(phi, phi + GN, 1.0);  // SPEC.md:209 flat flux
+          const EigenResult r = power_iteration(g, q, m, cfg, phi, true, init_k ? init_k[b] : 1.0, nullptr);
+          k_out[b] = r.k;
+          outer[b] = r.outer;
+          inner[b] = r.inner;
+          conv[b] = r.converged ? 1 : 0;
+        } catch (...) {
+          std::lock_guard<std::mutex> lk(mu);
+          code = map_exc();
+          err = g_err;
+        }
+      }
+    }, n_threads);
+    if (code) { g_err = err; return code; }
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+int oracle_infinite_medium_k(int32_t G, const double* st, const double* ss0, const double* nsf,
+                             const double* chi, double* k) {
+  try {
+    *k = infinite_medium_k(G, st, ss0, nsf, chi);
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+int oracle_recast_source(int32_t batch, int32_t n, const double* S, const double* phi, const double* st,
+                         const double* ss0, double tstar, double sstar, double* out) {
+  for (int b = 0; b < batch; ++b)
+    recast_source(n, S + (std::size_t)b * n, phi + (std::size_t)b * n, st + (std::size_t)b * n,
+                  ss0 + (std::size_t)b * n, tstar, sstar, out + (std::size_t)b * n);
+  return 0;
+}
+
+void* oracle_deeponet_create(const snop_grid* grid, double tstar, double sstar, int32_t act,
+                             int32_t nb, const int32_t* bs, const float* bp, int32_t nt, const int32_t* ts,
+                             const float* tp, int32_t has_bias0, float bias0) {
+  auto* op = new OracleOp;
+  op->kind = 0;
+  op->grid = Grid1D{grid->length_cm, grid->n_cells};
+  op->tstar = tstar;
+  op->sstar = sstar;
+  op->don.branch = unpack_dense(nb, bs, bp, static_cast<Activation>(act));
+  op->don.trunk = unpack_dense(nt, ts, tp, static_cast<Activation>(act));
+  op->don.has_bias0 = has_bias0 != 0;
+  op->don.bias0 = bias0;
+  return op;
+}
+
+void* oracle_fno_create(const snop_grid* grid, double tstar, double sstar, int32_t act, int32_t width,
+                        int32_t modes, int32_t layers, int32_t hidden, const float* p) {
+  auto* op = new OracleOp;
+  op->kind = 1;
+  op->grid = Grid1D{grid->length_cm, grid->n_cells};
+  op->tstar = tstar;
+  op->sstar = sstar;
+  FNO& f = op->fno;
+  f.width = width;
+  f.modes = modes;
+  f.layers = layers;
+  f.proj_hidden = hidden;
+  f.act = static_cast<Activation>(act);
+  const std::size_t C = width, M = modes;
+  auto take = [&](std::size_t n) { std::vector<float> v(p, p + n); p += n; return v; };
+  f.lift_W = take(C * 2);
+  f.lift_b = take(C);
+  for (int l = 0; l < layers; ++l) {
+    f.R_re.push_back(take(M * C * C));
+    f.R_im.push_back(take(M * C * C));
+    f.W.push_back(take(C * C));
+    f.b.push_back(take(C));
+  }
+  f.P1_W = take((std::size_t)hidden * C);
+  f.P1_b = take(hidden);
+  f.P2_W = take(hidden);
+  f.P2_b = take(1);
+  return op;
+}
+
+void* oracle_exact_operator_create(const snop_grid* grid, int32_t order, double tstar, double sstar,
+                                   const snop_solver_config* cfg) {
+  auto* op = new OracleOp;
+  op->kind = 2;
+  op->grid = Grid1D{grid->length_cm, grid->n_cells};
+  op->tstar = tstar;
+  op->sstar = sstar;
+  op->quad = gauss_legendre(order);
+  op->cfg = to_cfg(cfg);
+  return op;
+}
+
+void oracle_op_destroy(void* op) { delete static_cast<OracleOp*>(op); }
+
+int oracle_op_predict(void* vop, int32_t batch, const double* src, double* out, int32_t n_threads) {
+  try {
+    const auto* op = static_cast<const OracleOp*>(vop);
+    const std::size_t Nc = op->grid.n_cells;
+    parallel_chunks(batch, batch, [&](std::size_t, std::size_t b0, std::size_t b1) {
+      for (std::size_t b = b0; b < b1; ++b) op->predict(src + b * Nc, out + b * Nc);
+    }, n_threads);
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+int oracle_recast_fixed_point(void* vop, int32_t batch, const double* src, const double* st, const double* ss0,
+                              double tol, int32_t max_it, int32_t norm, const double* init_phi, double* phi_out,
+                              int32_t* iters, int32_t* status, int32_t n_threads) {
+  try {
+    const auto* op = static_cast<const OracleOp*>(vop);
+    const std::size_t Nc = op->grid.n_cells;
+    parallel_chunks(batch, batch, [&](std::size_t, std::size_t b0, std::size_t b1) {
+      for (std::size_t b = b0; b < b1; ++b) {
+        const RecastResult r = recast_fixed_point(
+            (int)Nc, src + b * Nc, st + b * Nc, ss0 + b * Nc, op->tstar, op->sstar,
+            [&](const double* s, double* o) { op->predict(s, o); }, tol, max_it, static_cast<Norm>(norm),
+            init_phi ? init_phi + b * Nc : nullptr, phi_out + b * Nc);
+        iters[b] = r.iterations;
+        status[b] = static_cast<int32_t>(r.status);
+      }
+    }, n_threads);
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+// recast fixed point, then source iteration on the full target warm-started.
+int oracle_precondition_fixed_source(void* vop, int32_t order, int32_t batch, const double* st,
+                                     const double* ss0, const double* ss1, const double* src, double rtol,
+                                     int32_t rmax, const snop_solver_config* ccfg, double* phi_out,
+                                     int32_t* piters, int32_t* rstatus, int32_t* riters, uint8_t* conv,
+                                     int32_t n_threads) {
+  try {
+    const auto* op = static_cast<const OracleOp*>(vop);
+    const Grid1D& g = op->grid;
+    const Quadrature q = gauss_legendre(order);
+    const SolverConfig cfg = to_cfg(ccfg);
+    const std::size_t Nc = g.n_cells;
+    parallel_chunks(batch, batch, [&](std::size_t, std::size_t b0, std::size_t b1) {
+      for (std::size_t b = b0; b < b1; ++b) {
+        double* phi = phi_out + b * Nc;
+        const RecastResult r = recast_fixed_point(
+            (int)Nc, src + b * Nc, st + b * Nc, ss0 + b * Nc, op->tstar, op->sstar,
+            [&](const double* s, double* o) { op->predict(s, o); }, rtol, rmax, cfg.norm, nullptr, phi);
+        piters[b] = r.iterations;
+        rstatus[b] = static_cast<int32_t>(r.status);
+        const SIResult s = source_iteration(g, q, st + b * Nc, ss0 + b * Nc, ss1 ? ss1 + b * Nc : nullptr,
+                                            src + b * Nc, cfg, phi, nullptr);
+        riters[b] = s.iterations;
+        conv[b] = s.converged ? 1 : 0;
+      }
+    }, n_threads);
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+int oracle_balance_residual(const snop_grid* grid, const double* st, const double* ss0, const double* src,
+                            const double* phi, double leak_left, double leak_right, double* out) {
+  try {
+    const Grid1D g{grid->length_cm, grid->n_cells};
+    *out = balance_residual(g, st, ss0, src, phi, leak_left, leak_right);
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,38 @@
+"""ctypes mirrors of the plain-C structs in include/snop_cuda.h (shared by the product binding
+and by the test-side oracle binding, which takes the same struct layout)."""
+from __future__ import annotations
+
+import ctypes as C
+
+
+class SnopGrid(C.Structure):
+    _fields_ = [("length_cm", C.c_double), ("n_cells", C.c_int32), ("reserved", C.c_int32)]
+
+
+class SnopSolverConfig(C.Structure):
+    _fields_ = [
+        ("tolerance", C.c_double),
+        ("tolerance_k", C.c_double),
+        ("tolerance_phi", C.c_double),
+        ("max_inner", C.c_int32),
+        ("max_outer", C.c_int32),
+        ("bc_left", C.c_int32),
+        ("bc_right", C.c_int32),
+        ("norm", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+
+def make_grid(length: float, n_cells: int) -> SnopGrid:
+    return SnopGrid(float(length), int(n_cells), 0)
+
+
+def make_config(tolerance=1e-4, tolerance_k=None, tolerance_phi=None, max_inner=10000, max_outer=5000,
+                bc_left=0, bc_right=0, norm=0) -> SnopSolverConfig:
+    return SnopSolverConfig(float(tolerance), float(tolerance if tolerance_k is None else tolerance_k),
+                            float(tolerance if tolerance_phi is None else tolerance_phi), int(max_inner),
+                            int(max_outer), int(bc_left), int(bc_right), int(norm), 0)
+
+
+STATUS_NAMES = {0: "OK", 1: "INVALID_ARGUMENT", 2: "NUMERICAL_ERROR", 3: "DEGENERATE_PROBLEM",
+                4: "IO_ERROR", 5: "CONFIG_ERROR", 6: "CUDA_ERROR"}
