@@ -1,0 +1,371 @@
+// capi.cu — the extern "C" boundary (include/snop_cuda.h): argument validation, host<->device
+// staging for SNOP_MEM_HOST calls, error mapping onto the reference's exception classes
+// (proj/core/include/snop/errors.hpp:8-41) and the per-context stream/workspace.
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "snop_internal.h"
+
+namespace snop_impl {
+
+namespace {
+thread_local std::string g_err;
+}
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+void* Ctx::slot(size_t i, size_t bytes) {
+  if (slots.size() <= i) slots.resize(i + 1);
+  DevBuf& b = slots[i];
+  if (b.bytes < bytes) {
+    if (b.ptr) cudaFree(b.ptr);
+    b.ptr = nullptr;
+    b.bytes = 0;
+    if (cudaMalloc(&b.ptr, bytes) != cudaSuccess) {
+      b.ptr = nullptr;
+      return nullptr;
+    }
+    b.bytes = bytes;
+  }
+  return b.ptr;
+}
+
+Ctx::~Ctx() {
+  for (auto& b : slots)
+    if (b.ptr) cudaFree(b.ptr);
+  if (d_flags) cudaFree(d_flags);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+// Gauss-Legendre nodes (same Newton recurrence as SPEC.md:64-72 requires; mirrored symmetric).
+static bool gauss_legendre_host(int N, double* mu, double* w) {
+  if (N < 2 || N > 128 || N % 2) return false;
+  const double pi = 3.14159265358979323846;
+  for (int i = 0; i < N / 2; ++i) {
+    double x = std::cos(pi * (i + 0.75) / (N + 0.5)), dp = 1.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = x;
+      for (int k = 2; k <= N; ++k) {
+        const double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = N * (x * p1 - p0) / (x * x - 1.0);
+      const double d = p1 / dp;
+      x -= d;
+      if (std::fabs(d) < 1e-16) break;
+    }
+    double p0 = 1.0, p1 = x;
+    for (int k = 2; k <= N; ++k) {
+      const double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+      p0 = p1;
+      p1 = p2;
+    }
+    dp = N * (x * p1 - p0) / (x * x - 1.0);
+    const double wt = 2.0 / ((1.0 - x * x) * dp * dp);
+    mu[N - 1 - i] = x;
+    mu[i] = -x;
+    w[N - 1 - i] = wt;
+    w[i] = wt;
+  }
+  return true;
+}
+
+snop_dev::SweepConsts make_consts(const snop_grid& g, int order) {
+  snop_dev::SweepConsts sc{};
+  double mu[128], w[128];
+  gauss_legendre_host(order, mu, w);
+  sc.n_cells = g.n_cells;
+  sc.n_pairs = order / 2;
+  sc.dx = g.length_cm / g.n_cells;
+  sc.inv_dx = 1.0 / sc.dx;
+  for (int p = 0; p < order / 2; ++p) {
+    const double m = mu[order / 2 + p];
+    sc.c[p] = 2.0 * m / sc.dx;
+    sc.wmu[p] = w[order / 2 + p] * m;
+    sc.mu3[p] = 3.0 * m;
+  }
+  return sc;
+}
+
+}  // namespace snop_impl
+
+using namespace snop_impl;
+
+namespace {
+
+#define SNOP_TRY(expr)                  \
+  do {                                  \
+    const snop_status _s = (expr);      \
+    if (_s != SNOP_OK) return _s;       \
+  } while (0)
+
+snop_status cuda_fail(const char* what, cudaError_t e) {
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return SNOP_CUDA_ERROR;
+}
+
+snop_status invalid(const std::string& m) {
+  set_error(m);
+  return SNOP_INVALID_ARGUMENT;
+}
+
+snop_status check_grid(const snop_grid* g, int order) {
+  if (!g) return invalid("grid is NULL");
+  if (!(g->length_cm > 0.0) || g->n_cells < 1) return invalid("grid: length and n_cells must be positive");
+  if (g->n_cells > kMaxCells) return invalid("grid: n_cells > 4096 exceeds the per-CTA sweep limit");
+  if (order < 2 || order > 128 || order % 2) return invalid("quadrature order must be even in [2,128]");
+  return SNOP_OK;
+}
+
+snop_status check_cfg(const snop_solver_config* c) {
+  if (!c) return invalid("config is NULL");
+  if (!(c->tolerance > 0.0) || !(c->tolerance_k > 0.0) || !(c->tolerance_phi > 0.0))
+    return invalid("config: tolerances must be positive");
+  if (c->max_inner < 1 || c->max_outer < 1) return invalid("config: iteration limits must be >= 1");
+  if ((c->bc_left != 0 && c->bc_left != 1) || (c->bc_right != 0 && c->bc_right != 1))
+    return invalid("config: boundary must be vacuum(0) or reflective(1)");
+  if (c->norm != 0 && c->norm != 1) return invalid("config: norm must be rel-Linf(0) or rel-L2(1)");
+  return SNOP_OK;
+}
+
+// Kernel-raised flags -> status (reads and clears the context's flag word; synchronises).
+snop_status drain_flags(Ctx& ctx) {
+  int flags = 0;
+  cudaError_t e = cudaMemcpyAsync(&flags, ctx.d_flags, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx.stream);
+  if (e != cudaSuccess) return cuda_fail("synchronize", e);
+  if (flags) cudaMemsetAsync(ctx.d_flags, 0, sizeof(int), ctx.stream);
+  if (flags & FLAG_BAD_SIGMA_T) return invalid("nonpositive sigma_t (or initial k) in at least one instance");
+  if (flags & FLAG_DEGENERATE) {
+    set_error("zero fission integral in at least one instance");
+    return SNOP_DEGENERATE_PROBLEM;
+  }
+  if (flags & FLAG_NONFINITE) {
+    set_error("non-finite values produced");
+    return SNOP_NUMERICAL_ERROR;
+  }
+  return SNOP_OK;
+}
+
+// Host staging: copy `bytes` from host `src` into ctx slot `i` (nullptr passes through).
+template <class T>
+snop_status stage_in(Ctx& ctx, size_t i, const T* src, size_t n, const T** dst) {
+  if (!src) {
+    *dst = nullptr;
+    return SNOP_OK;
+  }
+  void* d = ctx.slot(i, n * sizeof(T));
+  if (!d) return cuda_fail("cudaMalloc", cudaErrorMemoryAllocation);
+  const cudaError_t e = cudaMemcpyAsync(d, src, n * sizeof(T), cudaMemcpyHostToDevice, ctx.stream);
+  if (e != cudaSuccess) return cuda_fail("H2D copy", e);
+  *dst = static_cast<const T*>(d);
+  return SNOP_OK;
+}
+
+template <class T>
+snop_status stage_out_alloc(Ctx& ctx, size_t i, T* host, size_t n, T** dst) {
+  if (!host) {
+    *dst = nullptr;
+    return SNOP_OK;
+  }
+  void* d = ctx.slot(i, n * sizeof(T));
+  if (!d) return cuda_fail("cudaMalloc", cudaErrorMemoryAllocation);
+  *dst = static_cast<T*>(d);
+  return SNOP_OK;
+}
+
+template <class T>
+snop_status copy_out(Ctx& ctx, T* host, const T* dev, size_t n) {
+  if (!host) return SNOP_OK;
+  const cudaError_t e = cudaMemcpyAsync(host, dev, n * sizeof(T), cudaMemcpyDeviceToHost, ctx.stream);
+  if (e != cudaSuccess) return cuda_fail("D2H copy", e);
+  return SNOP_OK;
+}
+
+}  // namespace
+
+namespace snop_impl {
+const char* last_error_cstr() { return g_err.c_str(); }
+}  // namespace snop_impl
+
+extern "C" {
+
+int32_t snop_abi_version(void) { return SNOP_ABI_VERSION; }
+
+const char* snop_last_error(void) { return snop_impl::last_error_cstr(); }
+
+snop_status snop_ctx_create(int32_t device, snop_ctx** out) {
+  if (!out) return invalid("out is NULL");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) return cuda_fail("no CUDA device", e == cudaSuccess ? cudaErrorNoDevice : e);
+  if (device < 0 || device >= n) return invalid("device index out of range");
+  if ((e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail("cudaSetDevice", e);
+  cudaDeviceProp prop;
+  if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) return cuda_fail("cudaGetDeviceProperties", e);
+  if (prop.major != 10) {
+    set_error("libsnop_cuda is built for sm_100a (B200); device is sm_" + std::to_string(prop.major) +
+              std::to_string(prop.minor));
+    return SNOP_CUDA_ERROR;
+  }
+  auto* c = new (std::nothrow) snop_ctx;
+  if (!c) return cuda_fail("alloc ctx", cudaErrorMemoryAllocation);
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaMalloc(&c->d_flags, sizeof(int))) != cudaSuccess ||
+      (e = cudaMemset(c->d_flags, 0, sizeof(int))) != cudaSuccess) {
+    delete c;
+    return cuda_fail("ctx init", e);
+  }
+  *out = c;
+  return SNOP_OK;
+}
+
+snop_status snop_ctx_destroy(snop_ctx* ctx) {
+  if (!ctx) return SNOP_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  delete ctx;
+  return SNOP_OK;
+}
+
+snop_status snop_ctx_synchronize(snop_ctx* ctx) {
+  if (!ctx) return invalid("ctx is NULL");
+  return drain_flags(*ctx);
+}
+
+int64_t snop_ctx_launch_count(const snop_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+void* snop_ctx_stream(snop_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+snop_status snop_gauss_legendre(int32_t order, double* mu, double* w) {
+  if (!mu || !w) return invalid("mu/w NULL");
+  if (!gauss_legendre_host(order, mu, w)) return invalid("gauss_legendre: order must be even in [2,128]");
+  return SNOP_OK;
+}
+
+snop_status snop_source_iteration_batched(snop_ctx* ctx, int32_t memspace, const snop_grid* grid, int32_t order,
+                                          int32_t batch, const double* sigma_t, const double* sigma_s0,
+                                          const double* sigma_s1, const double* source,
+                                          const snop_solver_config* cfg, const double* initial_phi,
+                                          double* phi_out, double* current_out, int32_t* iterations,
+                                          uint8_t* converged) {
+  if (!ctx) return invalid("ctx is NULL");
+  SNOP_TRY(check_grid(grid, order));
+  SNOP_TRY(check_cfg(cfg));
+  if (batch < 0) return invalid("batch must be >= 0");
+  if (batch == 0) return SNOP_OK;
+  if (!sigma_t || !sigma_s0 || !source || !phi_out || !iterations || !converged)
+    return invalid("required array pointer is NULL");
+  cudaSetDevice(ctx->device);
+  const size_t n = (size_t)batch * grid->n_cells;
+  if (memspace == SNOP_MEM_DEVICE) {
+    return launch_source_iteration(*ctx, *grid, order, batch, sigma_t, sigma_s0, sigma_s1, source, *cfg,
+                                   initial_phi, phi_out, current_out, iterations, converged);
+  }
+  if (memspace != SNOP_MEM_HOST) return invalid("memspace must be HOST(0) or DEVICE(1)");
+  const double *st, *ss, *s1, *src, *p0;
+  double *phi, *cur;
+  int32_t* it;
+  uint8_t* cv;
+  SNOP_TRY(stage_in(*ctx, 0, sigma_t, n, &st));
+  SNOP_TRY(stage_in(*ctx, 1, sigma_s0, n, &ss));
+  SNOP_TRY(stage_in(*ctx, 2, sigma_s1, n, &s1));
+  SNOP_TRY(stage_in(*ctx, 3, source, n, &src));
+  SNOP_TRY(stage_in(*ctx, 4, initial_phi, n, &p0));
+  SNOP_TRY(stage_out_alloc(*ctx, 5, phi_out, n, &phi));
+  SNOP_TRY(stage_out_alloc(*ctx, 6, current_out, n, &cur));
+  SNOP_TRY(stage_out_alloc(*ctx, 7, iterations, (size_t)batch, &it));
+  SNOP_TRY(stage_out_alloc(*ctx, 8, converged, (size_t)batch, &cv));
+  SNOP_TRY(launch_source_iteration(*ctx, *grid, order, batch, st, ss, s1, src, *cfg, p0, phi, cur, it, cv));
+  SNOP_TRY(copy_out(*ctx, phi_out, phi, n));
+  SNOP_TRY(copy_out(*ctx, current_out, cur, n));
+  SNOP_TRY(copy_out(*ctx, iterations, it, (size_t)batch));
+  SNOP_TRY(copy_out(*ctx, converged, cv, (size_t)batch));
+  return drain_flags(*ctx);
+}
+
+snop_status snop_power_iteration_batched(snop_ctx* ctx, int32_t memspace, const snop_grid* grid, int32_t order,
+                                         int32_t batch, int32_t n_groups, const double* sigma_t,
+                                         const double* sigma_s0, const double* sigma_s1, const double* nu_sigma_f,
+                                         const double* chi, const snop_solver_config* cfg, const double* initial_k,
+                                         const double* initial_phi, double* k_out, double* phi_out,
+                                         int32_t* outer_iterations, int64_t* inner_iterations,
+                                         uint8_t* converged) {
+  if (!ctx) return invalid("ctx is NULL");
+  SNOP_TRY(check_grid(grid, order));
+  SNOP_TRY(check_cfg(cfg));
+  if (batch < 0) return invalid("batch must be >= 0");
+  if (n_groups < 1 || n_groups > 64) return invalid("n_groups must be in [1,64]");
+  if (batch == 0) return SNOP_OK;
+  if (!sigma_t || !sigma_s0 || !nu_sigma_f || !chi || !k_out || !phi_out || !outer_iterations ||
+      !inner_iterations || !converged)
+    return invalid("required array pointer is NULL");
+  cudaSetDevice(ctx->device);
+  const size_t G = n_groups, Nc = grid->n_cells, B = batch;
+  const size_t n = B * G * Nc;
+  double* old = static_cast<double*>(ctx->slot(20, n * sizeof(double)));
+  if (!old) return cuda_fail("cudaMalloc", cudaErrorMemoryAllocation);
+  if (memspace == SNOP_MEM_DEVICE) {
+    return launch_power_iteration(*ctx, *grid, order, batch, n_groups, sigma_t, sigma_s0, sigma_s1, nu_sigma_f,
+                                  chi, *cfg, initial_k, initial_phi, k_out, phi_out, old, outer_iterations,
+                                  inner_iterations, converged);
+  }
+  if (memspace != SNOP_MEM_HOST) return invalid("memspace must be HOST(0) or DEVICE(1)");
+  const double *st, *ss, *s1, *nsf, *ch, *k0, *p0;
+  double *k, *phi;
+  int32_t* outer;
+  int64_t* inner;
+  uint8_t* cv;
+  SNOP_TRY(stage_in(*ctx, 0, sigma_t, n, &st));
+  SNOP_TRY(stage_in(*ctx, 1, sigma_s0, n * G, &ss));
+  SNOP_TRY(stage_in(*ctx, 2, sigma_s1, n, &s1));
+  SNOP_TRY(stage_in(*ctx, 3, nu_sigma_f, n, &nsf));
+  SNOP_TRY(stage_in(*ctx, 4, chi, B * G, &ch));
+  SNOP_TRY(stage_in(*ctx, 5, initial_k, B, &k0));
+  SNOP_TRY(stage_in(*ctx, 6, initial_phi, n, &p0));
+  SNOP_TRY(stage_out_alloc(*ctx, 7, k_out, B, &k));
+  SNOP_TRY(stage_out_alloc(*ctx, 8, phi_out, n, &phi));
+  SNOP_TRY(stage_out_alloc(*ctx, 9, outer_iterations, B, &outer));
+  SNOP_TRY(stage_out_alloc(*ctx, 10, inner_iterations, B, &inner));
+  SNOP_TRY(stage_out_alloc(*ctx, 11, converged, B, &cv));
+  SNOP_TRY(launch_power_iteration(*ctx, *grid, order, batch, n_groups, st, ss, s1, nsf, ch, *cfg, k0, p0, k, phi,
+                                  old, outer, inner, cv));
+  SNOP_TRY(copy_out(*ctx, k_out, k, B));
+  SNOP_TRY(copy_out(*ctx, phi_out, phi, n));
+  SNOP_TRY(copy_out(*ctx, outer_iterations, outer, B));
+  SNOP_TRY(copy_out(*ctx, inner_iterations, inner, B));
+  SNOP_TRY(copy_out(*ctx, converged, cv, B));
+  return drain_flags(*ctx);
+}
+
+snop_status snop_recast_source(snop_ctx* ctx, int32_t memspace, int32_t batch, int32_t n_cells, const double* source,
+                               const double* phi, const double* sigma_t, const double* sigma_s0,
+                               double sigma_t_star, double sigma_s0_star, double* out) {
+  if (!ctx) return invalid("ctx is NULL");
+  if (batch < 0 || n_cells < 1) return invalid("batch must be >= 0 and n_cells >= 1");
+  if (batch == 0) return SNOP_OK;
+  if (!source || !phi || !sigma_t || !sigma_s0 || !out) return invalid("required array pointer is NULL");
+  cudaSetDevice(ctx->device);
+  const size_t n = (size_t)batch * n_cells;
+  if (memspace == SNOP_MEM_DEVICE)
+    return launch_recast(*ctx, n, source, phi, sigma_t, sigma_s0, sigma_t_star, sigma_s0_star, out);
+  if (memspace != SNOP_MEM_HOST) return invalid("memspace must be HOST(0) or DEVICE(1)");
+  const double *S, *p, *st, *ss;
+  double* o;
+  SNOP_TRY(stage_in(*ctx, 0, source, n, &S));
+  SNOP_TRY(stage_in(*ctx, 1, phi, n, &p));
+  SNOP_TRY(stage_in(*ctx, 2, sigma_t, n, &st));
+  SNOP_TRY(stage_in(*ctx, 3, sigma_s0, n, &ss));
+  SNOP_TRY(stage_out_alloc(*ctx, 4, out, n, &o));
+  SNOP_TRY(launch_recast(*ctx, n, S, p, st, ss, sigma_t_star, sigma_s0_star, o));
+  SNOP_TRY(copy_out(*ctx, out, o, n));
+  return drain_flags(*ctx);
+}
+
+}  // extern "C"

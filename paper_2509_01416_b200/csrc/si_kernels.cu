@@ -1,0 +1,365 @@
+// si_kernels.cu — K1 (fused fixed-source source iteration) and K2 (fused power iteration,
+// single- and multi-group) for sm_100a. One CTA = one instance for the whole solve; see
+// snop_device.cuh and DESIGN.md §K1/§K2.
+#include <cmath>
+
+#include "snop_internal.h"
+
+using namespace snop_dev;
+
+namespace {
+
+template <int NT>
+constexpr int min_blocks() { return NT <= 128 ? 4 : (NT <= 256 ? 2 : 1); }
+
+template <int K, int NT>
+size_t smem_bytes(bool aniso) {
+  return sizeof(SweepSmem<K, NT>) + (aniso ? sizeof(double) * K * NT : 0);
+}
+
+// ---------------------------------------------------------------------------------------------
+// K1: batched fixed-source solve, SPEC.md:125-134 (one CTA per instance).
+// ---------------------------------------------------------------------------------------------
+template <int K, int NT, bool ANISO, bool CUR>
+__global__ void __launch_bounds__(NT, min_blocks<NT>())
+si_fixed_source_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig cfg,
+                       const double* __restrict__ st_g, const double* __restrict__ ss0_g,
+                       const double* __restrict__ ss1_g, const double* __restrict__ src_g,
+                       const double* __restrict__ phi0_g, double* __restrict__ phi_g,
+                       double* __restrict__ cur_g, int32_t* __restrict__ iters, uint8_t* __restrict__ conv,
+                       int* __restrict__ flags) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<SweepSmem<K, NT>*>(smem_raw);
+  double* ss1s = ANISO ? reinterpret_cast<double*>(smem_raw + sizeof(SweepSmem<K, NT>)) : nullptr;
+  const int t = threadIdx.x, Nc = sc.n_cells;
+  const size_t base = (size_t)blockIdx.x * Nc;
+  const int c0 = t * K;
+  double st[K];
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const int i = c0 + j;
+    sm.jc[j * NT + t] = 0.0;
+    if (i < Nc) {
+      st[j] = st_g[base + i];
+      bad |= !(st[j] > 0.0);
+      sm.ss0[j * NT + t] = ss0_g[base + i];
+      sm.src[j * NT + t] = src_g[base + i];
+      if constexpr (ANISO) ss1s[j * NT + t] = ss1_g[base + i];
+      sm.phi[j * NT + t] = phi0_g ? phi0_g[base + i] : 0.0;
+    } else {
+      st[j] = 1.0;
+      sm.ss0[j * NT + t] = 0.0;
+      sm.src[j * NT + t] = 0.0;
+      if constexpr (ANISO) ss1s[j * NT + t] = 0.0;
+      sm.phi[j * NT + t] = 0.0;
+    }
+  }
+  if (__syncthreads_or(bad)) {  // nonpositive Sigma_t -> invalid argument
+    if (t == 0) {
+      atomicOr(flags, snop_impl::FLAG_BAD_SIGMA_T);
+      iters[blockIdx.x] = 0;
+      conv[blockIdx.x] = 0;
+    }
+    return;
+  }
+  bool converged = false;
+  const int it = si_solve<K, NT, ANISO, CUR>(sc, cfg, sm, ss1s, st, &converged);
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const int i = c0 + j;
+    if (i < Nc) {
+      phi_g[base + i] = sm.phi[j * NT + t];
+      if constexpr (CUR) cur_g[base + i] = sm.jc[j * NT + t];
+    }
+  }
+  if (t == 0) {
+    iters[blockIdx.x] = it;
+    conv[blockIdx.x] = converged ? 1 : 0;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// K2: batched k-eigenvalue power iteration, SPEC.md:179-189 + decisions :206-209, SURVEY §9 #5
+// (Gauss-Seidel over groups with upscatter, newest flux), #10 (inner solves warm-started).
+// The fission source, inscatter source, k update, renormalisation and dual convergence test are
+// all fused into the same persistent CTA. Group fluxes live in the output array (L2-resident,
+// thread-private cells), the previous-outer copy in a workspace.
+// ---------------------------------------------------------------------------------------------
+struct EigenParams {
+  int G;
+  double tol_k, tol_phi;
+  int max_outer;
+  int norm;
+};
+
+template <int K, int NT, bool ANISO>
+__global__ void __launch_bounds__(NT, min_blocks<NT>())
+power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig icfg, const EigenParams ep,
+                       const double* __restrict__ st_g, const double* __restrict__ ss0_g,
+                       const double* __restrict__ ss1_g, const double* __restrict__ nsf_g,
+                       const double* __restrict__ chi_g, const double* __restrict__ k0_g,
+                       const double* __restrict__ phi0_g, double* __restrict__ k_g, double* __restrict__ phi_g,
+                       double* __restrict__ old_g, int32_t* __restrict__ outer_g, int64_t* __restrict__ inner_g,
+                       uint8_t* __restrict__ conv_g, int* __restrict__ flags) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<SweepSmem<K, NT>*>(smem_raw);
+  double* ss1s = ANISO ? reinterpret_cast<double*>(smem_raw + sizeof(SweepSmem<K, NT>)) : nullptr;
+  const int t = threadIdx.x, Nc = sc.n_cells, G = ep.G;
+  const int b = blockIdx.x;
+  const int c0 = t * K;
+  const size_t GN = (size_t)G * Nc;
+  const double* st_b = st_g + (size_t)b * GN;
+  const double* ss_b = ss0_g + (size_t)b * GN * G;
+  const double* nsf_b = nsf_g + (size_t)b * GN;
+  double* phi_b = phi_g + (size_t)b * GN;
+  double* old_b = old_g + (size_t)b * GN;
+  auto cell = [&](int g, int j) -> size_t { return (size_t)g * Nc + c0 + j; };
+
+  // validation + initial flux (flat) and k
+  bool bad = false;
+  for (int g = 0; g < G; ++g) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (c0 + j < Nc) {
+        bad |= !(st_b[cell(g, j)] > 0.0);
+        phi_b[cell(g, j)] = phi0_g ? phi0_g[(size_t)b * GN + cell(g, j)] : 1.0;
+      }
+    }
+  }
+  double k = k0_g ? k0_g[b] : 1.0;
+  int rphase = 0;
+  auto fission_integral = [&]() {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (c0 + j < Nc) {
+        double f = 0.0;
+        for (int g = 0; g < G; ++g) f = fma(nsf_b[cell(g, j)], phi_b[cell(g, j)], f);
+        s += f;
+      }
+    }
+    return block_sum<NT>(s, sm.red2, rphase++) * sc.dx;
+  };
+  auto fail = [&](int flag) {
+    if (t == 0) {
+      atomicOr(flags, flag);
+      k_g[b] = __longlong_as_double(0x7ff8000000000000ll);
+      outer_g[b] = 0;
+      inner_g[b] = 0;
+      conv_g[b] = 0;
+    }
+  };
+  if (__syncthreads_or(bad) || !(k > 0.0)) {
+    fail(snop_impl::FLAG_BAD_SIGMA_T);
+    return;
+  }
+  double F = fission_integral();
+  if (!(F != 0.0) || !isfinite(F)) {
+    fail(snop_impl::FLAG_DEGENERATE);
+    return;
+  }
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if (c0 + j < Nc) phi_b[cell(g, j)] /= F;
+
+  int64_t inner_total = 0;
+  int outer = 0;
+  bool converged = false;
+  double fiss[K];
+  while (outer < ep.max_outer) {
+    ++outer;
+    // fission density from the flux at the start of the outer (frozen during the GS pass)
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      fiss[j] = 0.0;
+      if (c0 + j < Nc) {
+        for (int g = 0; g < G; ++g) {
+          const double v = phi_b[cell(g, j)];
+          old_b[cell(g, j)] = v;
+          fiss[j] = fma(nsf_b[cell(g, j)], v, fiss[j]);
+        }
+      }
+    }
+    const double inv_k = 1.0 / k;
+    for (int g = 0; g < G; ++g) {
+      const double chig = chi_g[(size_t)b * G + g] * inv_k;
+      double st[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        sm.jc[j * NT + t] = 0.0;
+        if (c0 + j < Nc) {
+          const size_t i = (size_t)c0 + j;
+          double q = chig * fiss[j];
+          for (int gp = 0; gp < G; ++gp)
+            if (gp != g) q = fma(ss_b[((size_t)gp * G + g) * Nc + i], phi_b[(size_t)gp * Nc + i], q);
+          sm.src[j * NT + t] = q;
+          sm.ss0[j * NT + t] = ss_b[((size_t)g * G + g) * Nc + i];
+          if constexpr (ANISO) ss1s[j * NT + t] = ss1_g[(size_t)b * GN + (size_t)g * Nc + i];
+          st[j] = st_b[(size_t)g * Nc + i];
+          sm.phi[j * NT + t] = phi_b[(size_t)g * Nc + i];
+        } else {
+          sm.src[j * NT + t] = 0.0;
+          sm.ss0[j * NT + t] = 0.0;
+          if constexpr (ANISO) ss1s[j * NT + t] = 0.0;
+          st[j] = 1.0;
+          sm.phi[j * NT + t] = 0.0;
+        }
+      }
+      bool ic = false;
+      inner_total += si_solve<K, NT, ANISO, false>(sc, icfg, sm, ss1s, st, &ic);
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (c0 + j < Nc) phi_b[cell(g, j)] = sm.phi[j * NT + t];
+    }
+    const double F1 = fission_integral();
+    if (!(F1 != 0.0) || !isfinite(F1)) {
+      fail(snop_impl::FLAG_DEGENERATE);
+      return;
+    }
+    const double k_new = k * F1;
+    const double inv_F1 = 1.0 / F1;
+    double num = 0.0, den = 0.0;
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (c0 + j < Nc) {
+          const double pn = phi_b[cell(g, j)] / F1;
+          phi_b[cell(g, j)] = pn;
+          const double d = pn - old_b[cell(g, j)];
+          if (ep.norm == 0) {
+            num = fmax(num, fabs(d));
+            den = fmax(den, fabs(pn));
+          } else {
+            num = fma(d, d, num);
+            den = fma(pn, pn, den);
+          }
+        }
+      }
+    }
+    (void)inv_F1;
+    if (ep.norm == 0) block_max2<NT>(num, den, sm.red2, rphase++);
+    else block_sum2<NT>(num, den, sm.red2, rphase++);
+    const double dphi = rel_change(num, den, ep.norm);
+    const double dk = fabs(k_new - k) / fabs(k_new);
+    k = k_new;
+    if (dk < ep.tol_k && dphi < ep.tol_phi) {
+      converged = true;
+      break;
+    }
+  }
+  if (t == 0) {
+    k_g[b] = k;
+    outer_g[b] = outer;
+    inner_g[b] = inner_total;
+    conv_g[b] = converged ? 1 : 0;
+  }
+}
+
+template <int K, int NT>
+snop_status launch_si_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveConfig& cfg, int batch,
+                        const double* st, const double* ss0, const double* ss1, const double* src,
+                        const double* phi0, double* phi, double* cur, int32_t* iters, uint8_t* conv) {
+  const bool aniso = ss1 != nullptr;
+  const size_t smem = smem_bytes<K, NT>(aniso);
+  auto kern = aniso ? si_fixed_source_kernel<K, NT, true, true>
+                    : (cur ? si_fixed_source_kernel<K, NT, false, true> : si_fixed_source_kernel<K, NT, false, false>);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<batch, NT, smem, ctx.stream>>>(sc, cfg, st, ss0, ss1, src, phi0, phi, cur, iters, conv, ctx.d_flags);
+  ctx.launches++;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snop_impl::set_error(std::string("si_fixed_source_kernel launch: ") + cudaGetErrorString(e));
+    return SNOP_CUDA_ERROR;
+  }
+  return SNOP_OK;
+}
+
+template <int K, int NT>
+snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveConfig& icfg, const EigenParams& ep,
+                        int batch, const double* st, const double* ss0, const double* ss1, const double* nsf,
+                        const double* chi, const double* k0, const double* phi0, double* k, double* phi,
+                        double* old, int32_t* outer, int64_t* inner, uint8_t* conv) {
+  const bool aniso = ss1 != nullptr;
+  const size_t smem = smem_bytes<K, NT>(aniso);
+  auto kern = aniso ? power_iteration_kernel<K, NT, true> : power_iteration_kernel<K, NT, false>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<batch, NT, smem, ctx.stream>>>(sc, icfg, ep, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner,
+                                        conv, ctx.d_flags);
+  ctx.launches++;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snop_impl::set_error(std::string("power_iteration_kernel launch: ") + cudaGetErrorString(e));
+    return SNOP_CUDA_ERROR;
+  }
+  return SNOP_OK;
+}
+
+// Block size: K = 8 cells per thread, NT = smallest power of two >= ceil(Nc/8) (>= 32).
+int pick_nt(int n_cells) {
+  const int need = (n_cells + 7) / 8;
+  int nt = 32;
+  while (nt < need) nt <<= 1;
+  return nt;
+}
+
+SolveConfig inner_cfg(const snop_solver_config& c) {
+  SolveConfig s;
+  s.tol = c.tolerance;
+  s.max_it = c.max_inner;
+  s.bc_left = c.bc_left;
+  s.bc_right = c.bc_right;
+  s.norm = c.norm;
+  return s;
+}
+
+}  // namespace
+
+namespace snop_impl {
+
+snop_status launch_source_iteration(Ctx& ctx, const snop_grid& g, int order, int batch, const double* st,
+                                    const double* ss0, const double* ss1, const double* src,
+                                    const snop_solver_config& cfg, const double* phi0, double* phi, double* cur,
+                                    int32_t* iters, uint8_t* conv) {
+  if (batch == 0) return SNOP_OK;
+  const SweepConsts sc = make_consts(g, order);
+  const SolveConfig c = inner_cfg(cfg);
+  switch (pick_nt(g.n_cells)) {
+    case 32: return launch_si_t<8, 32>(ctx, sc, c, batch, st, ss0, ss1, src, phi0, phi, cur, iters, conv);
+    case 64: return launch_si_t<8, 64>(ctx, sc, c, batch, st, ss0, ss1, src, phi0, phi, cur, iters, conv);
+    case 128: return launch_si_t<8, 128>(ctx, sc, c, batch, st, ss0, ss1, src, phi0, phi, cur, iters, conv);
+    case 256: return launch_si_t<8, 256>(ctx, sc, c, batch, st, ss0, ss1, src, phi0, phi, cur, iters, conv);
+    case 512: return launch_si_t<8, 512>(ctx, sc, c, batch, st, ss0, ss1, src, phi0, phi, cur, iters, conv);
+    default:
+      set_error("n_cells exceeds the per-CTA register-resident sweep limit (4096)");
+      return SNOP_INVALID_ARGUMENT;
+  }
+}
+
+snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int batch, int G, const double* st,
+                                   const double* ss0, const double* ss1, const double* nsf, const double* chi,
+                                   const snop_solver_config& cfg, const double* k0, const double* phi0, double* k,
+                                   double* phi, double* old, int32_t* outer, int64_t* inner, uint8_t* conv) {
+  if (batch == 0) return SNOP_OK;
+  const SweepConsts sc = make_consts(g, order);
+  const SolveConfig ic = inner_cfg(cfg);
+  EigenParams ep;
+  ep.G = G;
+  ep.tol_k = cfg.tolerance_k;
+  ep.tol_phi = cfg.tolerance_phi;
+  ep.max_outer = cfg.max_outer;
+  ep.norm = cfg.norm;
+  switch (pick_nt(g.n_cells)) {
+    case 32: return launch_pi_t<8, 32>(ctx, sc, ic, ep, batch, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv);
+    case 64: return launch_pi_t<8, 64>(ctx, sc, ic, ep, batch, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv);
+    case 128: return launch_pi_t<8, 128>(ctx, sc, ic, ep, batch, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv);
+    case 256: return launch_pi_t<8, 256>(ctx, sc, ic, ep, batch, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv);
+    case 512: return launch_pi_t<8, 512>(ctx, sc, ic, ep, batch, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv);
+    default:
+      set_error("n_cells exceeds the per-CTA register-resident sweep limit (4096)");
+      return SNOP_INVALID_ARGUMENT;
+  }
+}
+
+}  // namespace snop_impl

@@ -1,0 +1,60 @@
+// snop_internal.h — host-side internals shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/snop_cuda.h"
+#include "snop_device.cuh"
+
+namespace snop_impl {
+
+// Error flags written by kernels into ctx->d_flags (bitwise OR).
+enum : int { FLAG_BAD_SIGMA_T = 1, FLAG_DEGENERATE = 2, FLAG_NONFINITE = 4 };
+
+void set_error(const std::string& msg);
+
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int* d_flags = nullptr;
+  int sm_count = 148;
+  std::atomic<int64_t> launches{0};
+  std::vector<DevBuf> slots;  // scratch buffers for host-memspace staging and workspaces
+  void* slot(size_t i, size_t bytes);  // grow-only
+  ~Ctx();
+};
+
+// Builds the per-launch quadrature/mesh constants (mu_p > 0 ascending).
+snop_dev::SweepConsts make_consts(const snop_grid& g, int order);
+
+// Kernel launchers (si_kernels.cu). All pointers are device pointers.
+snop_status launch_source_iteration(Ctx& ctx, const snop_grid& g, int order, int batch, const double* st,
+                                    const double* ss0, const double* ss1, const double* src,
+                                    const snop_solver_config& cfg, const double* phi0, double* phi,
+                                    double* cur, int32_t* iters, uint8_t* conv);
+
+snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int batch, int G, const double* st,
+                                   const double* ss0, const double* ss1, const double* nsf, const double* chi,
+                                   const snop_solver_config& cfg, const double* k0, const double* phi0,
+                                   double* k, double* phi, double* phi_old_ws, int32_t* outer, int64_t* inner,
+                                   uint8_t* conv);
+
+snop_status launch_recast(Ctx& ctx, size_t n, const double* S, const double* phi, const double* st,
+                          const double* ss, double tstar, double sstar, double* out);
+
+// Largest n_cells the register-resident CTA sweep supports.
+constexpr int kMaxCells = 4096;
+
+}  // namespace snop_impl
+
+struct snop_ctx : snop_impl::Ctx {};

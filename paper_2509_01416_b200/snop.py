@@ -1,0 +1,261 @@
+"""Host-side mirror of the reference's ``snop::`` solver API for the S_N hot path, batched.
+
+Every function here is a thin shim over one C-ABI entry point of libsnop_cuda.so
+(include/snop_cuda.h); the computation runs in the sm_100a kernels, never on the host and never
+in PyTorch. Arrays may be numpy (host memory: the call stages H2D/D2H) or CUDA torch tensors
+(device memory: enqueued on the context's stream). Reference contracts:
+
+  gauss_legendre
+  source_iteration          SPEC.md:125-134 (sweep :115-123)
+  power_iteration           SPEC.md:179-189 (+ decisions :206-209)
+  recast_source
+  predict
+  recast_fixed_point
+  precondition_fixed_source SPEC.md:413-421
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from ._types import SnopGrid, SnopSolverConfig, make_grid
+
+VACUUM, REFLECTIVE = 0, 1
+REL_LINF, REL_L2 = 0, 1
+RELU, TANH, GELU = 0, 1, 2
+RECAST_CONVERGED, RECAST_MAXED, RECAST_DIVERGED = 0, 1, 2
+
+
+@dataclass(frozen=True)
+class Grid1D:
+    """SPEC.md:22-27"""
+    length_cm: float
+    n_cells: int
+
+    @property
+    def dx(self) -> float:
+        return self.length_cm / self.n_cells
+
+    @property
+    def centers(self) -> np.ndarray:
+        return (np.arange(self.n_cells) + 0.5) * self.dx
+
+    def c(self) -> SnopGrid:
+        return make_grid(self.length_cm, self.n_cells)
+
+
+@dataclass(frozen=True)
+class AngularQuadrature:
+    """SPEC.md:29-35 (nodes ascending, symmetric)."""
+    order: int
+    mu: np.ndarray
+    w: np.ndarray
+
+
+def gauss_legendre(order: int) -> AngularQuadrature:
+    mu = np.empty(order)
+    w = np.empty(order)
+    _capi.check(_capi.load().snop_gauss_legendre(order, mu.ctypes.data, w.ctypes.data))
+    return AngularQuadrature(order, mu, w)
+
+
+@dataclass
+class SolverConfig:
+    """SPEC.md:57-61; eigen tolerances split."""
+    tolerance: float = 1e-4
+    tolerance_k: float | None = None
+    tolerance_phi: float | None = None
+    max_inner_iterations: int = 10000
+    max_outer_iterations: int = 5000
+    boundary_left: int = VACUUM
+    boundary_right: int = VACUUM
+    convergence_norm: int = REL_LINF
+
+    def c(self) -> SnopSolverConfig:
+        t = self.tolerance
+        return SnopSolverConfig(float(t), float(t if self.tolerance_k is None else self.tolerance_k),
+                                float(t if self.tolerance_phi is None else self.tolerance_phi),
+                                int(self.max_inner_iterations), int(self.max_outer_iterations),
+                                int(self.boundary_left), int(self.boundary_right), int(self.convergence_norm), 0)
+
+
+class Context:
+    """One CUDA device + stream + workspace (snop_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = _capi.load()
+        h = C.c_void_p()
+        _capi.check(self._lib.snop_ctx_create(int(device), C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self._lib.snop_ctx_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        _capi.check(self._lib.snop_ctx_synchronize(self.h))
+
+    @property
+    def launch_count(self) -> int:
+        return int(self._lib.snop_ctx_launch_count(self.h))
+
+    @property
+    def stream_ptr(self) -> int:
+        return int(self._lib.snop_ctx_stream(self.h) or 0)
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+# ---- array plumbing -----------------------------------------------------------------------
+def _is_dev(a) -> bool:
+    return a is not None and hasattr(a, "is_cuda") and bool(a.is_cuda)
+
+
+class _Args:
+    """Collects pointers for one call; all arrays must be in the same memory space."""
+
+    def __init__(self, *arrays):
+        present = [a for a in arrays if a is not None]
+        dev = [_is_dev(a) for a in present]
+        if any(dev) and not all(dev):
+            raise ValueError("mix of host (numpy) and device (torch CUDA) arrays in one call")
+        self.device = bool(dev) and all(dev)
+        self.keep = []
+
+    @property
+    def memspace(self) -> int:
+        return 1 if self.device else 0
+
+    def inp(self, a, dtype=np.float64, shape=None):
+        if a is None:
+            return None
+        if self.device:
+            import torch
+            tdt = {np.float64: torch.float64, np.float32: torch.float32, np.int32: torch.int32}[dtype]
+            if a.dtype != tdt or not a.is_contiguous():
+                a = a.to(tdt).contiguous()
+            if shape is not None and tuple(a.shape) != tuple(shape):
+                a = a.reshape(shape)
+            self.keep.append(a)
+            return a.data_ptr()
+        a = np.ascontiguousarray(a, dtype=dtype)
+        if shape is not None and a.shape != tuple(shape):
+            a = a.reshape(shape)
+        self.keep.append(a)
+        return a.ctypes.data
+
+    def out(self, shape, dtype=np.float64):
+        if self.device:
+            import torch
+            tdt = {np.float64: torch.float64, np.float32: torch.float32, np.int32: torch.int32,
+                   np.int64: torch.int64, np.uint8: torch.uint8}[dtype]
+            t = torch.empty(shape, dtype=tdt, device="cuda")
+            return t, t.data_ptr()
+        a = np.empty(shape, dtype=dtype)
+        return a, a.ctypes.data
+
+
+@dataclass
+class FixedSourceResult:
+    """(FluxField, iterations, converged) of SPEC.md:125, batched."""
+    phi: object
+    iterations: object
+    converged: object
+    current: object = None
+
+
+def source_iteration(grid: Grid1D, order: int, sigma_t, sigma_s0, source, config: SolverConfig | None = None,
+                     initial_phi=None, sigma_s1=None, want_current: bool = False,
+                     ctx: Context | None = None) -> FixedSourceResult:
+    """Batched single-group fixed-source solve. Arrays are [B][Nc]."""
+    ctx = ctx or default_context()
+    config = config or SolverConfig()
+    a = _Args(sigma_t, sigma_s0, source, initial_phi, sigma_s1)
+    B = int(sigma_t.shape[0])
+    n = grid.n_cells
+    st, ss, src = a.inp(sigma_t, shape=(B, n)), a.inp(sigma_s0, shape=(B, n)), a.inp(source, shape=(B, n))
+    s1, p0 = a.inp(sigma_s1, shape=(B, n)), a.inp(initial_phi, shape=(B, n))
+    phi, phi_p = a.out((B, n))
+    cur, cur_p = a.out((B, n)) if want_current else (None, None)
+    it, it_p = a.out((B,), np.int32)
+    cv, cv_p = a.out((B,), np.uint8)
+    g, cfg = grid.c(), config.c()
+    _capi.check(ctx._lib.snop_source_iteration_batched(ctx.h, a.memspace, C.byref(g), int(order), B, st, ss, s1,
+                                                       src, C.byref(cfg), p0, phi_p, cur_p, it_p, cv_p))
+    if a.device:
+        ctx.synchronize()
+    return FixedSourceResult(phi, it, cv, cur)
+
+
+@dataclass
+class EigenSolution:
+    """SPEC.md:172-176, batched."""
+    k: object
+    phi: object
+    outer_iterations: object
+    total_inner_iterations: object
+    converged: object
+
+
+def power_iteration(grid: Grid1D, order: int, sigma_t, sigma_s0, nu_sigma_f, chi,
+                    config: SolverConfig | None = None, initial_k=None, initial_phi=None, sigma_s1=None,
+                    ctx: Context | None = None) -> EigenSolution:
+    """Batched k-eigenvalue power iteration. sigma_t/nu_sigma_f/sigma_s1:
+    [B][G][Nc]; sigma_s0: [B][G][G][Nc] ([g'][g] = g'->g); chi: [B][G]."""
+    ctx = ctx or default_context()
+    config = config or SolverConfig()
+    a = _Args(sigma_t, sigma_s0, nu_sigma_f, chi, initial_k, initial_phi, sigma_s1)
+    B, G, n = (int(x) for x in sigma_t.shape)
+    if n != grid.n_cells:
+        raise ValueError("sigma_t last dim must equal grid.n_cells")
+    st = a.inp(sigma_t, shape=(B, G, n))
+    ss = a.inp(sigma_s0, shape=(B, G, G, n))
+    nsf = a.inp(nu_sigma_f, shape=(B, G, n))
+    ch = a.inp(chi, shape=(B, G))
+    s1 = a.inp(sigma_s1, shape=(B, G, n))
+    k0 = a.inp(initial_k, shape=(B,))
+    p0 = a.inp(initial_phi, shape=(B, G, n))
+    k, k_p = a.out((B,))
+    phi, phi_p = a.out((B, G, n))
+    outer, o_p = a.out((B,), np.int32)
+    inner, i_p = a.out((B,), np.int64)
+    cv, cv_p = a.out((B,), np.uint8)
+    g, cfg = grid.c(), config.c()
+    _capi.check(ctx._lib.snop_power_iteration_batched(ctx.h, a.memspace, C.byref(g), int(order), B, G, st, ss, s1,
+                                                      nsf, ch, C.byref(cfg), k0, p0, k_p, phi_p, o_p, i_p, cv_p))
+    if a.device:
+        ctx.synchronize()
+    return EigenSolution(k, phi, outer, inner, cv)
+
+
+def recast_source(source, phi, sigma_t, sigma_s0, reference_params=(1.0, 0.5), ctx: Context | None = None):
+    """SPEC.md:393-401 (paper Eq. 24), batched [B][Nc]."""
+    ctx = ctx or default_context()
+    a = _Args(source, phi, sigma_t, sigma_s0)
+    B, n = (int(x) for x in source.shape)
+    s, p, st, ss = (a.inp(x, shape=(B, n)) for x in (source, phi, sigma_t, sigma_s0))
+    out, out_p = a.out((B, n))
+    _capi.check(ctx._lib.snop_recast_source(ctx.h, a.memspace, B, n, s, p, st, ss, float(reference_params[0]),
+                                            float(reference_params[1]), out_p))
+    if a.device:
+        ctx.synchronize()
+    return out

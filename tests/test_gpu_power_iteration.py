@@ -1,0 +1,98 @@
+"""Parity of the fused power-iteration kernel (K2) against the CPU oracle."""
+import numpy as np
+import pytest
+
+from paper_2509_01416_b200 import snop, workloads as W
+from paper_2509_01416_b200.errors import DegenerateProblem
+from tests import oracle_lib as O
+
+pytestmark = pytest.mark.gpu
+
+K_RTOL = 1e-10  # north_star: k_eff within 1e-10 relative
+
+
+def _cfg(p, **kw):
+    d = dict(tolerance=p.tolerance_inner, tolerance_k=p.tolerance_k, tolerance_phi=p.tolerance_phi,
+             boundary_left=p.bc_left, boundary_right=p.bc_right)
+    d.update(kw)
+    return snop.SolverConfig(**d)
+
+
+def _both(p, cfg, **kw):
+    g = snop.Grid1D(p.length, p.n_cells)
+    r = snop.power_iteration(g, p.order, p.sigma_t, p.sigma_s0, p.nu_sigma_f, p.chi, cfg, **kw)
+    o = O.power_iteration(p.length, p.n_cells, p.order, p.n_groups, p.sigma_t, p.sigma_s0, p.nu_sigma_f, p.chi,
+                          cfg.c(), **kw)
+    return r, o
+
+
+def test_table9_three_group_k():
+    # PAPER.md:379 model-based k = 1.30621 (vacuum, N=32, dx=0.1, L=10)
+    p = W.three_group_table9()
+    r, o = _both(p, _cfg(p))
+    assert abs(r.k[0] - 1.30621) < 5e-5
+    assert abs(int(r.outer_iterations[0]) - int(o["outer"][0])) <= 1
+    if r.outer_iterations[0] == o["outer"][0]:
+        assert abs(r.k[0] - o["k"][0]) / o["k"][0] < K_RTOL
+
+
+def test_reflective_three_group_equals_dense():
+    p = W.three_group_table9(bc=1)
+    r, _ = _both(p, _cfg(p, tolerance=1e-10, tolerance_k=1e-11, tolerance_phi=1e-10))
+    kinf = O.infinite_medium_k(p.sigma_t[0, :, 0], p.sigma_s0[0, :, :, 0], p.nu_sigma_f[0, :, 0], p.chi[0])
+    assert abs(r.k[0] - kinf) < 1e-6
+
+
+def test_single_group_kinf():
+    # reflective, St=1, Ss0=0.5, nuSf=0.9 -> k = 1.8
+    n = 50
+    p = W.EigenProblem("k", 10.0, n, 8, 1, np.ones((1, 1, n)), np.full((1, 1, 1, n), 0.5), np.full((1, 1, n), 0.9),
+                       np.ones((1, 1)), bc_left=1, bc_right=1, tolerance_k=1e-8, tolerance_phi=1e-6,
+                       tolerance_inner=1e-6)
+    r, _ = _both(p, _cfg(p))
+    assert abs(r.k[0] - 1.8) < 1e-4
+
+
+def test_c3_subset_parity():
+    p = W.config3(batch=6, n_cells=1024)
+    r, o = _both(p, _cfg(p))
+    assert np.all(np.abs(r.outer_iterations.astype(int) - o["outer"].astype(int)) <= 1)
+    assert np.max(np.abs(r.k - o["k"]) / o["k"]) < 1e-9
+
+
+def test_c4_subset_parity():
+    p = W.config4(batch=3, n_cells=500)
+    r, o = _both(p, _cfg(p))
+    assert np.all(np.abs(r.outer_iterations.astype(int) - o["outer"].astype(int)) <= 1)
+    assert np.max(np.abs(r.k - o["k"]) / o["k"]) < 1e-9
+
+
+def test_fixed_outer_flux_parity():
+    p = W.config4(batch=2, n_cells=300)
+    cfg = _cfg(p, tolerance_k=1e-300, tolerance_phi=1e-300, max_outer_iterations=3, max_inner_iterations=4,
+               tolerance=1e-300)
+    r, o = _both(p, cfg)
+    assert (r.outer_iterations == 3).all()
+    assert (r.total_inner_iterations == o["inner"]).all()
+    assert np.max(np.abs(r.phi - o["phi"])) / np.max(np.abs(o["phi"])) < K_RTOL
+    assert np.max(np.abs(r.k - o["k"]) / o["k"]) < K_RTOL
+
+
+def test_scale_invariance_initial_guess():
+    # SPEC.md:201
+    p = W.three_group_table9()
+    cfg = _cfg(p)
+    g = snop.Grid1D(p.length, p.n_cells)
+    a = snop.power_iteration(g, p.order, p.sigma_t, p.sigma_s0, p.nu_sigma_f, p.chi, cfg,
+                             initial_phi=np.full((1, 3, p.n_cells), 1.0))
+    b = snop.power_iteration(g, p.order, p.sigma_t, p.sigma_s0, p.nu_sigma_f, p.chi, cfg,
+                             initial_phi=np.full((1, 3, p.n_cells), 7.5))
+    assert abs(a.k[0] - b.k[0]) < 1e-10
+
+
+def test_zero_fission_is_degenerate():
+    n = 20
+    p = W.EigenProblem("d", 10.0, n, 8, 1, np.ones((1, 1, n)), np.full((1, 1, 1, n), 0.5), np.zeros((1, 1, n)),
+                       np.ones((1, 1)))
+    with pytest.raises(DegenerateProblem):
+        snop.power_iteration(snop.Grid1D(10.0, n), 8, p.sigma_t, p.sigma_s0, p.nu_sigma_f, p.chi, _cfg(p))
