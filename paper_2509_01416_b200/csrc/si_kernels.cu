@@ -2,6 +2,7 @@
 // single- and multi-group) for sm_100a. One CTA = one instance for the whole solve; see
 // snop_device.cuh and DESIGN.md §K1/§K2.
 #include <cmath>
+#include <cstdlib>
 
 #include "snop_internal.h"
 
@@ -9,49 +10,50 @@ using namespace snop_dev;
 
 namespace {
 
-template <int NT>
-constexpr int min_blocks() { return NT <= 128 ? 4 : (NT <= 256 ? 2 : 1); }
+// Register budget: 128 regs/thread (16 resident warps per SM at NT*minBlocks = 512).
+template <int K, int NT>
+constexpr int min_blocks() {
+  return NT <= 128 ? 512 / NT : (NT <= 256 ? 2 : 1);
+}
 
 template <int K, int NT>
-size_t smem_bytes(bool aniso) {
-  return sizeof(SweepSmem<K, NT>) + (aniso ? sizeof(double) * K * NT : 0);
+size_t smem_bytes() {
+  return sizeof(SweepSmem<K, NT>);
 }
 
 // ---------------------------------------------------------------------------------------------
 // K1: batched fixed-source solve, SPEC.md:125-134 (one CTA per instance).
 // ---------------------------------------------------------------------------------------------
 template <int K, int NT, bool ANISO, bool CUR>
-__global__ void __launch_bounds__(NT, min_blocks<NT>())
+__global__ void __launch_bounds__(NT, min_blocks<K, NT>())
 si_fixed_source_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig cfg,
                        const double* __restrict__ st_g, const double* __restrict__ ss0_g,
                        const double* __restrict__ ss1_g, const double* __restrict__ src_g,
                        const double* __restrict__ phi0_g, double* __restrict__ phi_g,
-                       double* __restrict__ cur_g, int32_t* __restrict__ iters, uint8_t* __restrict__ conv,
+                       double* __restrict__ jc_g, int32_t* __restrict__ iters, uint8_t* __restrict__ conv,
                        int* __restrict__ flags) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(32) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<SweepSmem<K, NT>*>(smem_raw);
-  double* ss1s = ANISO ? reinterpret_cast<double*>(smem_raw + sizeof(SweepSmem<K, NT>)) : nullptr;
   const int t = threadIdx.x, Nc = sc.n_cells;
   const size_t base = (size_t)blockIdx.x * Nc;
   const int c0 = t * K;
-  double st[K];
+  CellIO io;
+  io.ss0 = ss0_g + base;
+  io.src = src_g + base;
+  io.ss1 = ANISO ? ss1_g + base : nullptr;
+  io.jc = (ANISO || CUR) ? jc_g + base : nullptr;
   bool bad = false;
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const int i = c0 + j;
-    sm.jc[j * NT + t] = 0.0;
     if (i < Nc) {
-      st[j] = st_g[base + i];
-      bad |= !(st[j] > 0.0);
-      sm.ss0[j * NT + t] = ss0_g[base + i];
-      sm.src[j * NT + t] = src_g[base + i];
-      if constexpr (ANISO) ss1s[j * NT + t] = ss1_g[base + i];
+      const double stv = st_g[base + i];
+      sm.st[j * NT + t] = stv;
+      bad |= !(stv > 0.0);
       sm.phi[j * NT + t] = phi0_g ? phi0_g[base + i] : 0.0;
+      if constexpr (ANISO) io.jc[i] = 0.0;
     } else {
-      st[j] = 1.0;
-      sm.ss0[j * NT + t] = 0.0;
-      sm.src[j * NT + t] = 0.0;
-      if constexpr (ANISO) ss1s[j * NT + t] = 0.0;
+      sm.st[j * NT + t] = 0.0;  // padding: identity map (see sweep_pair_group)
       sm.phi[j * NT + t] = 0.0;
     }
   }
@@ -64,14 +66,11 @@ si_fixed_source_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
     return;
   }
   bool converged = false;
-  const int it = si_solve<K, NT, ANISO, CUR>(sc, cfg, sm, ss1s, st, &converged);
+  const int it = si_solve<K, NT, ANISO, CUR>(sc, cfg, sm, io, &converged);
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const int i = c0 + j;
-    if (i < Nc) {
-      phi_g[base + i] = sm.phi[j * NT + t];
-      if constexpr (CUR) cur_g[base + i] = sm.jc[j * NT + t];
-    }
+    if (i < Nc) phi_g[base + i] = sm.phi[j * NT + t];
   }
   if (t == 0) {
     iters[blockIdx.x] = it;
@@ -94,17 +93,17 @@ struct EigenParams {
 };
 
 template <int K, int NT, bool ANISO>
-__global__ void __launch_bounds__(NT, min_blocks<NT>())
+__global__ void __launch_bounds__(NT, min_blocks<K, NT>())
 power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig icfg, const EigenParams ep,
                        const double* __restrict__ st_g, const double* __restrict__ ss0_g,
                        const double* __restrict__ ss1_g, const double* __restrict__ nsf_g,
                        const double* __restrict__ chi_g, const double* __restrict__ k0_g,
                        const double* __restrict__ phi0_g, double* __restrict__ k_g, double* __restrict__ phi_g,
-                       double* __restrict__ old_g, int32_t* __restrict__ outer_g, int64_t* __restrict__ inner_g,
+                       double* __restrict__ old_g, double* __restrict__ qext_g, double* __restrict__ jc_g,
+                       int32_t* __restrict__ outer_g, int64_t* __restrict__ inner_g,
                        uint8_t* __restrict__ conv_g, int* __restrict__ flags) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(32) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<SweepSmem<K, NT>*>(smem_raw);
-  double* ss1s = ANISO ? reinterpret_cast<double*>(smem_raw + sizeof(SweepSmem<K, NT>)) : nullptr;
   const int t = threadIdx.x, Nc = sc.n_cells, G = ep.G;
   const int b = blockIdx.x;
   const int c0 = t * K;
@@ -114,6 +113,8 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   const double* nsf_b = nsf_g + (size_t)b * GN;
   double* phi_b = phi_g + (size_t)b * GN;
   double* old_b = old_g + (size_t)b * GN;
+  double* qext_b = qext_g + (size_t)b * Nc;
+  double* jc_b = ANISO ? jc_g + (size_t)b * Nc : nullptr;
   auto cell = [&](int g, int j) -> size_t { return (size_t)g * Nc + c0 + j; };
 
   // validation + initial flux (flat) and k
@@ -185,30 +186,29 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
     const double inv_k = 1.0 / k;
     for (int g = 0; g < G; ++g) {
       const double chig = chi_g[(size_t)b * G + g] * inv_k;
-      double st[K];
 #pragma unroll
       for (int j = 0; j < K; ++j) {
-        sm.jc[j * NT + t] = 0.0;
         if (c0 + j < Nc) {
           const size_t i = (size_t)c0 + j;
           double q = chig * fiss[j];
           for (int gp = 0; gp < G; ++gp)
             if (gp != g) q = fma(ss_b[((size_t)gp * G + g) * Nc + i], phi_b[(size_t)gp * Nc + i], q);
-          sm.src[j * NT + t] = q;
-          sm.ss0[j * NT + t] = ss_b[((size_t)g * G + g) * Nc + i];
-          if constexpr (ANISO) ss1s[j * NT + t] = ss1_g[(size_t)b * GN + (size_t)g * Nc + i];
-          st[j] = st_b[(size_t)g * Nc + i];
+          qext_b[i] = q;
+          if constexpr (ANISO) jc_b[i] = 0.0;
+          sm.st[j * NT + t] = st_b[(size_t)g * Nc + i];
           sm.phi[j * NT + t] = phi_b[(size_t)g * Nc + i];
         } else {
-          sm.src[j * NT + t] = 0.0;
-          sm.ss0[j * NT + t] = 0.0;
-          if constexpr (ANISO) ss1s[j * NT + t] = 0.0;
-          st[j] = 1.0;
+          sm.st[j * NT + t] = 0.0;  // padding: identity map (see sweep_pair_group)
           sm.phi[j * NT + t] = 0.0;
         }
       }
+      CellIO io;
+      io.ss0 = ss_b + ((size_t)g * G + g) * Nc;
+      io.src = qext_b;
+      io.ss1 = ANISO ? ss1_g + (size_t)b * GN + (size_t)g * Nc : nullptr;
+      io.jc = jc_b;
       bool ic = false;
-      inner_total += si_solve<K, NT, ANISO, false>(sc, icfg, sm, ss1s, st, &ic);
+      inner_total += si_solve<K, NT, ANISO, false>(sc, icfg, sm, io, &ic);
 #pragma unroll
       for (int j = 0; j < K; ++j)
         if (c0 + j < Nc) phi_b[cell(g, j)] = sm.phi[j * NT + t];
@@ -262,11 +262,19 @@ snop_status launch_si_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveC
                         const double* st, const double* ss0, const double* ss1, const double* src,
                         const double* phi0, double* phi, double* cur, int32_t* iters, uint8_t* conv) {
   const bool aniso = ss1 != nullptr;
-  const size_t smem = smem_bytes<K, NT>(aniso);
+  const size_t smem = smem_bytes<K, NT>();
   auto kern = aniso ? si_fixed_source_kernel<K, NT, true, true>
                     : (cur ? si_fixed_source_kernel<K, NT, false, true> : si_fixed_source_kernel<K, NT, false, false>);
+  double* jc = cur;
+  if (aniso && !jc) {  // P1 needs the cell current even when the caller does not want it
+    jc = static_cast<double*>(ctx.slot(21, (size_t)batch * sc.n_cells * sizeof(double)));
+    if (!jc) {
+      snop_impl::set_error("cudaMalloc (current workspace) failed");
+      return SNOP_CUDA_ERROR;
+    }
+  }
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<batch, NT, smem, ctx.stream>>>(sc, cfg, st, ss0, ss1, src, phi0, phi, cur, iters, conv, ctx.d_flags);
+  kern<<<batch, NT, smem, ctx.stream>>>(sc, cfg, st, ss0, ss1, src, phi0, phi, jc, iters, conv, ctx.d_flags);
   ctx.launches++;
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -282,11 +290,18 @@ snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveC
                         const double* chi, const double* k0, const double* phi0, double* k, double* phi,
                         double* old, int32_t* outer, int64_t* inner, uint8_t* conv) {
   const bool aniso = ss1 != nullptr;
-  const size_t smem = smem_bytes<K, NT>(aniso);
+  const size_t smem = smem_bytes<K, NT>();
   auto kern = aniso ? power_iteration_kernel<K, NT, true> : power_iteration_kernel<K, NT, false>;
+  const size_t n = (size_t)batch * sc.n_cells;
+  double* qext = static_cast<double*>(ctx.slot(22, n * sizeof(double)));
+  double* jc = aniso ? static_cast<double*>(ctx.slot(21, n * sizeof(double))) : nullptr;
+  if (!qext || (aniso && !jc)) {
+    snop_impl::set_error("cudaMalloc (eigen workspace) failed");
+    return SNOP_CUDA_ERROR;
+  }
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<batch, NT, smem, ctx.stream>>>(sc, icfg, ep, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner,
-                                        conv, ctx.d_flags);
+  kern<<<batch, NT, smem, ctx.stream>>>(sc, icfg, ep, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, qext, jc, outer,
+                                        inner, conv, ctx.d_flags);
   ctx.launches++;
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -296,9 +311,18 @@ snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveC
   return SNOP_OK;
 }
 
-// Block size: K = 8 cells per thread, NT = smallest power of two >= ceil(Nc/8) (>= 32).
-int pick_nt(int n_cells) {
-  const int need = (n_cells + 7) / 8;
+// Block shape: K cells per thread (compile-time, register arrays), NT = smallest power of two
+// >= ceil(Nc/K), NT >= 32. K = 8 by default; SNOP_CELLS_PER_THREAD=16 selects the K = 16 variant.
+int pick_k() {
+  static const int k = [] {
+    const char* e = std::getenv("SNOP_CELLS_PER_THREAD");
+    return (e && std::atoi(e) == 8) ? 8 : 16;
+  }();
+  return k;
+}
+
+int pick_nt(int n_cells, int K) {
+  const int need = (n_cells + K - 1) / K;
   int nt = 32;
   while (nt < need) nt <<= 1;
   return nt;
@@ -325,13 +349,15 @@ snop_status launch_source_iteration(Ctx& ctx, const snop_grid& g, int order, int
   if (batch == 0) return SNOP_OK;
   const SweepConsts sc = make_consts(g, order);
   const SolveConfig c = inner_cfg(cfg);
-  switch (pick_nt(g.n_cells)) {
-    case 32: return launch_si_t<8, 32>(ctx, sc, c, batch, st, ss0, ss1, src, phi0, phi, cur, iters, conv);
-    case 64: return launch_si_t<8, 64>(ctx, sc, c, batch, st, ss0, ss1, src, phi0, phi, cur, iters, conv);
-    case 128: return launch_si_t<8, 128>(ctx, sc, c, batch, st, ss0, ss1, src, phi0, phi, cur, iters, conv);
-    case 256: return launch_si_t<8, 256>(ctx, sc, c, batch, st, ss0, ss1, src, phi0, phi, cur, iters, conv);
-    case 512: return launch_si_t<8, 512>(ctx, sc, c, batch, st, ss0, ss1, src, phi0, phi, cur, iters, conv);
-    default:
+  const int K = pick_k();
+#define SNOP_SI(KK, NN) \
+  if (K == KK && pick_nt(g.n_cells, KK) == NN) \
+    return launch_si_t<KK, NN>(ctx, sc, c, batch, st, ss0, ss1, src, phi0, phi, cur, iters, conv);
+  SNOP_SI(8, 32) SNOP_SI(8, 64) SNOP_SI(8, 128) SNOP_SI(8, 256) SNOP_SI(8, 512)
+  SNOP_SI(16, 32) SNOP_SI(16, 64) SNOP_SI(16, 128) SNOP_SI(16, 256)
+
+#undef SNOP_SI
+  {
       set_error("n_cells exceeds the per-CTA register-resident sweep limit (4096)");
       return SNOP_INVALID_ARGUMENT;
   }
@@ -350,13 +376,15 @@ snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int 
   ep.tol_phi = cfg.tolerance_phi;
   ep.max_outer = cfg.max_outer;
   ep.norm = cfg.norm;
-  switch (pick_nt(g.n_cells)) {
-    case 32: return launch_pi_t<8, 32>(ctx, sc, ic, ep, batch, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv);
-    case 64: return launch_pi_t<8, 64>(ctx, sc, ic, ep, batch, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv);
-    case 128: return launch_pi_t<8, 128>(ctx, sc, ic, ep, batch, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv);
-    case 256: return launch_pi_t<8, 256>(ctx, sc, ic, ep, batch, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv);
-    case 512: return launch_pi_t<8, 512>(ctx, sc, ic, ep, batch, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv);
-    default:
+  const int K = pick_k();
+#define SNOP_PI(KK, NN) \
+  if (K == KK && pick_nt(g.n_cells, KK) == NN) \
+    return launch_pi_t<KK, NN>(ctx, sc, ic, ep, batch, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv);
+  SNOP_PI(8, 32) SNOP_PI(8, 64) SNOP_PI(8, 128) SNOP_PI(8, 256) SNOP_PI(8, 512)
+  SNOP_PI(16, 32) SNOP_PI(16, 64) SNOP_PI(16, 128) SNOP_PI(16, 256)
+
+#undef SNOP_PI
+  {
       set_error("n_cells exceeds the per-CTA register-resident sweep limit (4096)");
       return SNOP_INVALID_ARGUMENT;
   }

@@ -151,37 +151,196 @@ __device__ __forceinline__ double rel_change(double num, double den, int norm) {
   return num > 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : 0.0;
 }
 
+// Predicated FP64 ops (no select instructions in the scan; the predicate is lane-constant).
+__device__ __forceinline__ void pfma(double& d, double a, double b, double c, bool p) {
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t@q fma.rn.f64 %0, %1, %2, %3;\n\t}"
+      : "+d"(d) : "d"(a), "d"(b), "d"(c), "r"((unsigned)p));
+}
+__device__ __forceinline__ void pmul(double& d, double a, double b, bool p) {
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q mul.rn.f64 %0, %1, %2;\n\t}"
+      : "+d"(d) : "d"(a), "d"(b), "r"((unsigned)p));
+}
+
 // Shared-memory workspace of one CTA solver (the P1 moment array, when present, is a separate
-// dynamic-smem region passed as a pointer so isotropic launches do not pay for it).
+// dynamic-smem region passed as a pointer so isotropic launches do not pay for it). Per-cell
+// arrays use the [j][t] layout: thread t's cell j sits at j*NT + t (conflict-free, private).
 template <int K, int NT>
 struct SweepSmem {
   static constexpr int NW = NT / 32;
-  double ss0[K * NT];          // within-group Sigma_s0 of own cells, [j][t] (conflict-free)
-  double src[K * NT];          // external isotropic source S (or q_ext), [j][t]
-  double phi[K * NT];          // scalar flux of own cells, [j][t]
-  double jc[K * NT];           // cell-average current (P1 emission / optional output), [j][t]
-  double tot[2][NW][4];        // per-warp scan totals {Afwd, Bfwd, Abwd, Bbwd}, double-buffered
+  double st[K * NT];           // Sigma_t (0 on padding cells)
+  double q2[K * NT];           // 2 x isotropic emission: Ss0 phi + S (rebuilt every iteration)
+  double phi[K * NT];          // scalar flux
+  alignas(32) double tot[2][2][NW][4];  // scan totals [slot][pair-in-group][warp] {Af,Bf,Ab,Bb}
   double jfirst[NT + 1];       // J at each thread's first edge (+ J at the last edge, slot NT)
   double red[4 * NW];          // reductions inside si_solve
   double red2[4 * NW];         // reductions of the enclosing (eigen) kernel
   double lag[2][kMaxPairs];    // both-reflective: lagged mu>0 outflow at x=L, by iteration parity
 };
 
-// One CTA solves one within-group fixed-source problem by source iteration (SPEC.md:125-134).
-// On entry: st[] own sigma_t (>0; 1 on padding cells); sm.phi initial flux, sm.jc initial cell
-// current (read only when ANISO), sm.ss0/src (and ss1s when ANISO) filled for own cells.
-// On exit: sm.phi final flux, sm.jc cell-average current of the last sweep (written when
-// ANISO || CUR). Returns sweeps performed; *converged is uniform across the CTA.
-template <int K, int NT, bool ANISO, bool CUR>
-__device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem<K, NT>& sm,
-                        const double* __restrict__ ss1s, const double (&st)[K], bool* converged) {
+// Per-cell inputs that are touched once per iteration stay in global memory (L2-resident for
+// the active instances), natural layout, already offset to the instance: g[c0 + j] for thread
+// t's cell j (c0 = t*K). Padding cells (c0 + j >= Nc) are never read.
+struct CellIO {
+  const double* __restrict__ ss0;  // within-group Sigma_s0
+  const double* __restrict__ src;  // external isotropic source
+  const double* __restrict__ ss1;  // P1 moment (ANISO only)
+  double* __restrict__ jc;         // cell-average current (ANISO / CUR)
+};
+
+struct SweepCtl {
+  int t, lane, warp, it, slot;
+  bool rl, rr, owns_last;
+};
+
+// Sweeps NP (1 or 2) +/-mu pairs starting at p0 and accumulates their edge currents into Jl /
+// Jend. The NP pairs are independent chains the scheduler interleaves (ILP); one barrier per
+// group. Padding cells carry St = q2 = 0, so alpha = 2c/c - 1 = 1 (to 1 ulp) and beta = 0.
+template <int K, int NT, bool ANISO, int NP>
+__device__ __forceinline__ void sweep_pair_group(const SweepConsts& sc, SweepSmem<K, NT>& sm, const CellIO& io,
+                                                 int p0, const SweepCtl& w, double (&Jl)[K], double& Jend) {
   constexpr int NW = NT / 32;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int t = w.t, lane = w.lane, warp = w.warp;
+  double c[NP], c2[NP], wm[NP];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    c[q] = sc.c[p0 + q];
+    c2[q] = 2.0 * c[q];
+    wm[q] = sc.wmu[p0 + q];
+  }
+  double al[NP][K], bp[NP][K], bm[NP][K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const double stj = sm.st[j * NT + t], qj = sm.q2[j * NT + t];
+    double a3base = 0.0;
+    if constexpr (ANISO) a3base = (t * K + j < sc.n_cells) ? io.ss1[t * K + j] * io.jc[t * K + j] : 0.0;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const double r = rcp_fast(stj + c[q]);
+      al[q][j] = fma(c2[q], r, -1.0);
+      if constexpr (ANISO) {
+        const double a3 = sc.mu3[p0 + q] * a3base;
+        bp[q][j] = (qj + a3) * r;
+        bm[q][j] = (qj - a3) * r;
+      } else {
+        bp[q][j] = qj * r;
+        bm[q][j] = bp[q][j];
+      }
+    }
+  }
+  // compose own chunk: forward (ascending) and backward (descending)
+  double Af[NP], Bf[NP], Ab[NP], Bb[NP];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    Af[q] = al[q][0];
+    Bf[q] = bp[q][0];
+    Bb[q] = bm[q][K - 1];
+  }
+#pragma unroll
+  for (int j = 1; j < K; ++j)
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      Bf[q] = fma(al[q][j], Bf[q], bp[q][j]);
+      Af[q] *= al[q][j];
+      Bb[q] = fma(al[q][K - 1 - j], Bb[q], bm[q][K - 1 - j]);
+    }
+#pragma unroll
+  for (int q = 0; q < NP; ++q) Ab[q] = Af[q];
+  // warp scans (Kogge-Stone): forward inclusive prefix, backward inclusive suffix; predicated
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const bool up = lane >= o, dn = lane + o < 32;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const double ap = shfl_up_d(Af[q], o), bpv = shfl_up_d(Bf[q], o);
+      const double an = shfl_down_d(Ab[q], o), bnv = shfl_down_d(Bb[q], o);
+      pfma(Bf[q], Af[q], bpv, Bf[q], up);
+      pmul(Af[q], Af[q], ap, up);
+      pfma(Bb[q], Ab[q], bnv, Bb[q], dn);
+      pmul(Ab[q], Ab[q], an, dn);
+    }
+  }
+  double4* tot = reinterpret_cast<double4*>(&sm.tot[w.slot][0][0][0]);
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    if (lane == 31) { tot[q * NW + warp].x = Af[q]; tot[q * NW + warp].y = Bf[q]; }
+    if (lane == 0) { tot[q * NW + warp].z = Ab[q]; tot[q * NW + warp].w = Bb[q]; }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    const double4* T4 = tot + q * NW;
+    const int p = p0 + q;
+    // boundary values (SURVEY §9 #2 ordering); only the reflective cases need full totals
+    double psi_right_in = 0.0, psi_left_in = 0.0;
+    if (w.rr || w.rl) {
+      if (w.rr && !w.rl) {
+        double v = 0.0;
+#pragma unroll
+        for (int u = 0; u < NW; ++u) { const double4 T = T4[u]; v = fma(T.x, v, T.y); }
+        psi_right_in = v;
+      } else {
+        if (w.rr) psi_right_in = sm.lag[w.it & 1][p];
+        if (w.rl) {
+          double v = psi_right_in;
+#pragma unroll
+          for (int u = NW - 1; u >= 0; --u) { const double4 T = T4[u]; v = fma(T.z, v, T.w); }
+          psi_left_in = v;
+        }
+        if (w.rr && w.rl && t == 0) {
+          double v = psi_left_in;
+#pragma unroll
+          for (int u = 0; u < NW; ++u) { const double4 T = T4[u]; v = fma(T.x, v, T.y); }
+          sm.lag[(w.it + 1) & 1][p] = v;
+        }
+      }
+    }
+    // psi entering this warp (fixed trip count, predicated)
+    double wf_in = psi_left_in, wb_in = psi_right_in;
+#pragma unroll
+    for (int u = 0; u < NW - 1; ++u) {
+      const double4 T = T4[u];
+      pfma(wf_in, T.x, wf_in, T.y, u < warp);
+      const double4 U = T4[NW - 1 - u];
+      pfma(wb_in, U.z, wb_in, U.w, NW - 1 - u > warp);
+    }
+    // psi entering this lane's chunk = psi leaving the neighbour lane's chunk
+    double psi = shfl_up_d(fma(Af[q], wf_in, Bf[q]), 1);
+    if (lane == 0) psi = wf_in;
+    double psib = shfl_down_d(fma(Ab[q], wb_in, Bb[q]), 1);
+    if (lane == 31) psib = wb_in;
+    const double psib_in = psib;  // psi- entering from the right (= inflow at x=L for the owner)
+    // replay: accumulate the edge currents J_e += w mu (psi+ - psi-)
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      Jl[j] = fma(wm[q], psi, Jl[j]);
+      psi = fma(al[q][j], psi, bp[q][j]);
+      psib = fma(al[q][K - 1 - j], psib, bm[q][K - 1 - j]);
+      Jl[K - 1 - j] = fma(-wm[q], psib, Jl[K - 1 - j]);
+    }
+    if (w.owns_last) Jend = fma(wm[q], psi - psib_in, Jend);  // J at x = L
+  }
+}
+
+// One CTA solves one within-group fixed-source problem by source iteration (SPEC.md:125-134).
+// On entry sm.st (>0; 0 on padding) and sm.phi (initial flux; 0 on padding) hold the own cells;
+// io.ss0 / io.src (0 on padding), io.ss1 and io.jc (initial cell current; ANISO) are the
+// thread-ordered global arrays. On exit sm.phi holds the final flux and io.jc the cell-average
+// current of the last sweep (written when ANISO || CUR). Returns sweeps performed;
+// *converged is uniform in the CTA.
+template <int K, int NT, bool ANISO, bool CUR, int NP = 1>
+__device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem<K, NT>& sm, const CellIO& io,
+                        bool* converged) {
+  const int t = threadIdx.x;
   const int c0 = t * K;
   const int Nc = sc.n_cells, P = sc.n_pairs;
-  const bool owns_last = (c0 <= Nc - 1) && (Nc - 1 < c0 + K);
+  SweepCtl w;
+  w.t = t;
+  w.lane = t & 31;
+  w.warp = t >> 5;
+  w.owns_last = (c0 <= Nc - 1) && (Nc - 1 < c0 + K);
+  w.rl = cfg.bc_left == 1;
+  w.rr = cfg.bc_right == 1;
   const int jlast = Nc - 1 - c0;
-  const bool rl = cfg.bc_left == 1, rr = cfg.bc_right == 1;
 
   if (t < kMaxPairs) {
     sm.lag[0][t] = 0.0;
@@ -189,116 +348,35 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
   }
   __syncthreads();
 
-  double Q[K];
   int it = 0;
   bool conv = false;
   int rphase = 0;
+  w.slot = 0;
   while (it < cfg.max_it) {
     ++it;
-    // emission (x2): Q = Ss0 phi + S ; angular q_n = Q/2 + 3/2 Ss1 mu_n J
+    w.it = it;
+    // emission (x2): q2 = Ss0 phi + S ; angular q_n = q2/2 + 3/2 Ss1 mu_n J
 #pragma unroll
-    for (int j = 0; j < K; ++j) Q[j] = fma(sm.ss0[j * NT + t], sm.phi[j * NT + t], sm.src[j * NT + t]);
+    for (int j = 0; j < K; ++j)
+      sm.q2[j * NT + t] = (c0 + j < Nc) ? fma(io.ss0[c0 + j], sm.phi[j * NT + t], io.src[c0 + j]) : 0.0;
     double Jl[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) Jl[j] = 0.0;
     double Jend = 0.0;
-
-    for (int p = 0; p < P; ++p) {
-      const double c = sc.c[p], c2 = 2.0 * c, wm = sc.wmu[p];
-      double al[K], bp[K], bm[K];
-#pragma unroll
-      for (int j = 0; j < K; ++j) {
-        if (c0 + j < Nc) {
-          const double r = rcp_fast(st[j] + c);
-          al[j] = fma(c2, r, -1.0);
-          if constexpr (ANISO) {
-            const double a3 = sc.mu3[p] * ss1s[j * NT + t] * sm.jc[j * NT + t];
-            bp[j] = (Q[j] + a3) * r;
-            bm[j] = (Q[j] - a3) * r;
-          } else {
-            bp[j] = Q[j] * r;
-            bm[j] = bp[j];
-          }
-        } else {  // padding cell: identity map
-          al[j] = 1.0;
-          bp[j] = 0.0;
-          bm[j] = 0.0;
-        }
+    int p = 0;
+    if constexpr (NP == 2) {
+      for (; p + 1 < P; p += 2) {
+        sweep_pair_group<K, NT, ANISO, 2>(sc, sm, io, p, w, Jl, Jend);
+        w.slot ^= 1;
       }
-      // compose own chunk: forward (cells ascending) and backward (descending)
-      double Af = al[0], Bf = bp[0];
-#pragma unroll
-      for (int j = 1; j < K; ++j) {
-        Bf = fma(al[j], Bf, bp[j]);
-        Af *= al[j];
-      }
-      double Bb = bm[K - 1];
-#pragma unroll
-      for (int j = K - 2; j >= 0; --j) Bb = fma(al[j], Bb, bm[j]);
-      double Ab = Af;
-      // warp scans: forward inclusive prefix, backward inclusive suffix (Kogge-Stone)
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const double ap = shfl_up_d(Af, o), bpv = shfl_up_d(Bf, o);
-        const double an = shfl_down_d(Ab, o), bnv = shfl_down_d(Bb, o);
-        if (lane >= o) {
-          Bf = fma(Af, bpv, Bf);
-          Af *= ap;
-        }
-        if (lane + o < 32) {
-          Bb = fma(Ab, bnv, Bb);
-          Ab *= an;
-        }
-      }
-      double* tot = &sm.tot[p & 1][0][0];
-      if (lane == 31) { tot[warp * 4 + 0] = Af; tot[warp * 4 + 1] = Bf; }
-      if (lane == 0) { tot[warp * 4 + 2] = Ab; tot[warp * 4 + 3] = Bb; }
-      __syncthreads();
-      // boundary values (SURVEY §9 #2 ordering) and the psi entering this warp, composed
-      // serially from broadcast smem reads of the warp totals (warp-uniform work).
-      double psi_right_in = 0.0, psi_left_in = 0.0;
-      if (rr && !rl) {
-        double v = 0.0;
-        for (int w = 0; w < NW; ++w) v = fma(tot[w * 4 + 0], v, tot[w * 4 + 1]);
-        psi_right_in = v;
-      } else {
-        if (rr) psi_right_in = sm.lag[it & 1][p];
-        if (rl) {
-          double v = psi_right_in;
-          for (int w = NW - 1; w >= 0; --w) v = fma(tot[w * 4 + 2], v, tot[w * 4 + 3]);
-          psi_left_in = v;
-        }
-        if (rr && rl && t == 0) {
-          double v = psi_left_in;
-          for (int w = 0; w < NW; ++w) v = fma(tot[w * 4 + 0], v, tot[w * 4 + 1]);
-          sm.lag[(it + 1) & 1][p] = v;
-        }
-      }
-      double wf_in = psi_left_in;
-      for (int w = 0; w < warp; ++w) wf_in = fma(tot[w * 4 + 0], wf_in, tot[w * 4 + 1]);
-      double wb_in = psi_right_in;
-      for (int w = NW - 1; w > warp; --w) wb_in = fma(tot[w * 4 + 2], wb_in, tot[w * 4 + 3]);
-      // psi entering this lane's chunk = psi leaving the neighbour lane's chunk
-      double psi = shfl_up_d(fma(Af, wf_in, Bf), 1);
-      if (lane == 0) psi = wf_in;
-      double psib = shfl_down_d(fma(Ab, wb_in, Bb), 1);
-      if (lane == 31) psib = wb_in;
-      // replay: accumulate the edge currents J_e += w mu (psi+ - psi-)
-#pragma unroll
-      for (int j = 0; j < K; ++j) {
-        Jl[j] = fma(wm, psi, Jl[j]);
-        psi = fma(al[j], psi, bp[j]);
-      }
-      if (owns_last) Jend = fma(wm, psi - psib, Jend);
-#pragma unroll
-      for (int j = K - 1; j >= 0; --j) {
-        psib = fma(al[j], psib, bm[j]);
-        Jl[j] = fma(-wm, psib, Jl[j]);
-      }
+    }
+    for (; p < P; ++p) {
+      sweep_pair_group<K, NT, ANISO, 1>(sc, sm, io, p, w, Jl, Jend);
+      w.slot ^= 1;
     }
     // edge-current exchange: J at the right edge of own last cell = next thread's first edge
     sm.jfirst[t] = Jl[0];
-    if (owns_last) sm.jfirst[NT] = Jend;
+    if (w.owns_last) sm.jfirst[NT] = Jend;
     __syncthreads();
     const double Jnext = sm.jfirst[t + 1 < NT ? t + 1 : NT];
     const double Jlastv = sm.jfirst[NT];
@@ -307,10 +385,10 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
     for (int j = 0; j < K; ++j) {
       if (c0 + j < Nc) {
         double JR = (j + 1 < K) ? Jl[j + 1] : Jnext;
-        if (owns_last && j == jlast) JR = Jlastv;
+        if (w.owns_last && j == jlast) JR = Jlastv;
         // balance form of phi = sum_n w_n psi_avg,n
-        const double pn = (Q[j] - (JR - Jl[j]) * sc.inv_dx) / st[j];
-        if constexpr (ANISO || CUR) sm.jc[j * NT + t] = 0.5 * (Jl[j] + JR);
+        const double pn = (sm.q2[j * NT + t] - (JR - Jl[j]) * sc.inv_dx) / sm.st[j * NT + t];
+        if constexpr (ANISO || CUR) io.jc[c0 + j] = 0.5 * (Jl[j] + JR);
         const double d = pn - sm.phi[j * NT + t];
         if (cfg.norm == 0) {
           num = fmax(num, fabs(d));

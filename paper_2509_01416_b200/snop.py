@@ -185,8 +185,10 @@ class FixedSourceResult:
 
 def source_iteration(grid: Grid1D, order: int, sigma_t, sigma_s0, source, config: SolverConfig | None = None,
                      initial_phi=None, sigma_s1=None, want_current: bool = False,
-                     ctx: Context | None = None) -> FixedSourceResult:
-    """Batched single-group fixed-source solve. Arrays are [B][Nc]."""
+                     ctx: Context | None = None, sync: bool = True) -> FixedSourceResult:
+    """Batched single-group fixed-source solve. Arrays are [B][Nc].
+    Device (torch CUDA) arrays: enqueued on ctx's stream; with sync=False the caller must call
+    ctx.synchronize() (which also reports kernel-raised argument errors) before using results."""
     ctx = ctx or default_context()
     config = config or SolverConfig()
     a = _Args(sigma_t, sigma_s0, source, initial_phi, sigma_s1)
@@ -201,7 +203,7 @@ def source_iteration(grid: Grid1D, order: int, sigma_t, sigma_s0, source, config
     g, cfg = grid.c(), config.c()
     _capi.check(ctx._lib.snop_source_iteration_batched(ctx.h, a.memspace, C.byref(g), int(order), B, st, ss, s1,
                                                        src, C.byref(cfg), p0, phi_p, cur_p, it_p, cv_p))
-    if a.device:
+    if a.device and sync:
         ctx.synchronize()
     return FixedSourceResult(phi, it, cv, cur)
 
