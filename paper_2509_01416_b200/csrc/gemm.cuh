@@ -1,0 +1,104 @@
+// gemm.cuh — strided, batched fp32 GEMM used by the neural-operator forwards:
+//   C(b, m, n) = act( alpha * sum_k A(b, m, k) B(b, n, k) + beta * C(b, m, n) + bias[n] )
+// with arbitrary element strides for every operand (so the FNO's per-sample DFT, inverse DFT
+// and channel mixing need no transposes). fp32 FFMA accumulation (exact-fp32 class numerics).
+// The tcgen05 engine (gemm_tc.cu) replaces this for the large contractions; this kernel stays
+// the fallback for tiny/odd shapes and the cross-check in tests.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace snop_ops {
+
+enum Act : int { ACT_RELU = 0, ACT_TANH = 1, ACT_GELU = 2, ACT_NONE = 3 };
+
+__device__ __forceinline__ float act_f(float x, int act) {
+  switch (act) {
+    case ACT_RELU: return x > 0.f ? x : 0.f;
+    case ACT_TANH: return tanhf(x);
+    case ACT_GELU: return 0.5f * x * (1.f + erff(x * 0.70710678118654752440f));
+    default: return x;
+  }
+}
+
+struct GemmArgs {
+  int M, N, K, batch;
+  const float* A;
+  int64_t sam, sak, sab;
+  const float* B;
+  int64_t sbn, sbk, sbb;
+  float* C;          // fp32 output (or nullptr when Cd is used)
+  double* Cd;        // optional fp64 output (same strides)
+  int64_t scm, scn, scb;
+  const float* bias; // [N] or nullptr
+  float alpha, beta; // beta applies to the existing fp32 C
+  int act;
+};
+
+constexpr int GBM = 64, GBN = 64, GBK = 16, GTHREADS = 256;
+
+__global__ void __launch_bounds__(GTHREADS) gemm_f32_kernel(const GemmArgs a) {
+  __shared__ float As[GBK][GBM + 4];
+  __shared__ float Bs[GBK][GBN + 4];
+  const int b = blockIdx.z;
+  const int m0 = blockIdx.x * GBM, n0 = blockIdx.y * GBN;  // M on x (2^31 limit)
+  const int tid = threadIdx.x;
+  const int tm = (tid / 16) * 4, tn = (tid % 16) * 4;
+  const float* A = a.A + (int64_t)b * a.sab;
+  const float* B = a.B + (int64_t)b * a.sbb;
+  float acc[4][4] = {};
+  const bool a_kfast = a.sak == 1, b_kfast = a.sbk == 1;
+  for (int k0 = 0; k0 < a.K; k0 += GBK) {
+#pragma unroll
+    for (int r = 0; r < (GBM * GBK) / GTHREADS; ++r) {
+      const int e = tid + r * GTHREADS;
+      const int mm = a_kfast ? e / GBK : e % GBM, kk = a_kfast ? e % GBK : e / GBM;
+      const int gm = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gm < a.M && gk < a.K) ? A[gm * a.sam + gk * a.sak] : 0.f;
+      const int nn = b_kfast ? e / GBK : e % GBN, kb = b_kfast ? e % GBK : e / GBN;
+      const int gn = n0 + nn, gkb = k0 + kb;
+      Bs[kb][nn] = (gn < a.N && gkb < a.K) ? B[gn * a.sbn + gkb * a.sbk] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GBK; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[kk][tm + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tn + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + tm + i;
+    if (gm >= a.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gn = n0 + tn + j;
+      if (gn >= a.N) continue;
+      const int64_t off = (int64_t)b * a.scb + (int64_t)gm * a.scm + (int64_t)gn * a.scn;
+      float v = a.alpha * acc[i][j];
+      if (a.beta != 0.f) v += a.beta * a.C[off];
+      if (a.bias) v += a.bias[gn];
+      v = act_f(v, a.act);
+      if (a.Cd) a.Cd[off] = (double)v;
+      else a.C[off] = v;
+    }
+  }
+}
+
+inline cudaError_t gemm_f32(const GemmArgs& a, cudaStream_t s) {
+  if (a.M <= 0 || a.N <= 0 || a.batch <= 0) return cudaSuccess;
+  dim3 grid((a.M + GBM - 1) / GBM, (a.N + GBN - 1) / GBN, a.batch);
+  gemm_f32_kernel<<<grid, GTHREADS, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace snop_ops

@@ -1,0 +1,10 @@
+// Explicit instantiations: K2 power-iteration kernels, K = 8.
+#include "si_kernels.cuh"
+
+namespace snop_si {
+template snop_status launch_pi_t<8, 32>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, const EigenParams&, int, const double*, const double*, const double*, const double*, const double*, const double*, const double*, double*, double*, double*, int32_t*, int64_t*, uint8_t*);
+template snop_status launch_pi_t<8, 64>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, const EigenParams&, int, const double*, const double*, const double*, const double*, const double*, const double*, const double*, double*, double*, double*, int32_t*, int64_t*, uint8_t*);
+template snop_status launch_pi_t<8, 128>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, const EigenParams&, int, const double*, const double*, const double*, const double*, const double*, const double*, const double*, double*, double*, double*, int32_t*, int64_t*, uint8_t*);
+template snop_status launch_pi_t<8, 256>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, const EigenParams&, int, const double*, const double*, const double*, const double*, const double*, const double*, const double*, double*, double*, double*, int32_t*, int64_t*, uint8_t*);
+template snop_status launch_pi_t<8, 512>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, const EigenParams&, int, const double*, const double*, const double*, const double*, const double*, const double*, const double*, double*, double*, double*, int32_t*, int64_t*, uint8_t*);
+}  // namespace snop_si

@@ -1,14 +1,14 @@
-// si_kernels.cu — K1 (fused fixed-source source iteration) and K2 (fused power iteration,
+// si_kernels.cuh — K1 (fused fixed-source source iteration) and K2 (fused power iteration,
 // single- and multi-group) for sm_100a. One CTA = one instance for the whole solve; see
 // snop_device.cuh and DESIGN.md §K1/§K2.
 #include <cmath>
 #include <cstdlib>
 
+#pragma once
 #include "snop_internal.h"
 
+namespace snop_si {
 using namespace snop_dev;
-
-namespace {
 
 // Register budget: 128 regs/thread (16 resident warps per SM at NT*minBlocks = 512).
 template <int K, int NT>
@@ -258,7 +258,7 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
 }
 
 template <int K, int NT>
-snop_status launch_si_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveConfig& cfg, int batch,
+inline snop_status launch_si_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveConfig& cfg, int batch,
                         const double* st, const double* ss0, const double* ss1, const double* src,
                         const double* phi0, double* phi, double* cur, int32_t* iters, uint8_t* conv) {
   const bool aniso = ss1 != nullptr;
@@ -285,7 +285,7 @@ snop_status launch_si_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveC
 }
 
 template <int K, int NT>
-snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveConfig& icfg, const EigenParams& ep,
+inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveConfig& icfg, const EigenParams& ep,
                         int batch, const double* st, const double* ss0, const double* ss1, const double* nsf,
                         const double* chi, const double* k0, const double* phi0, double* k, double* phi,
                         double* old, int32_t* outer, int64_t* inner, uint8_t* conv) {
@@ -311,83 +311,14 @@ snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveC
   return SNOP_OK;
 }
 
-// Block shape: K cells per thread (compile-time, register arrays), NT = smallest power of two
-// >= ceil(Nc/K), NT >= 32. K = 8 by default; SNOP_CELLS_PER_THREAD=16 selects the K = 16 variant.
-int pick_k() {
-  static const int k = [] {
-    const char* e = std::getenv("SNOP_CELLS_PER_THREAD");
-    return (e && std::atoi(e) == 8) ? 8 : 16;
-  }();
-  return k;
-}
 
-int pick_nt(int n_cells, int K) {
-  const int need = (n_cells + K - 1) / K;
-  int nt = 32;
-  while (nt < need) nt <<= 1;
-  return nt;
-}
+// Explicitly instantiated in si_k{8,16}_{fixed,eigen}.cu (one TU per variant, parallel build).
+#define SNOP_DECL_SI(KK, NN) \
+  extern template snop_status launch_si_t<KK, NN>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, int, \
+      const double*, const double*, const double*, const double*, const double*, double*, double*, int32_t*, uint8_t*);
+#define SNOP_DECL_PI(KK, NN) \
+  extern template snop_status launch_pi_t<KK, NN>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, \
+      const EigenParams&, int, const double*, const double*, const double*, const double*, const double*, \
+      const double*, const double*, double*, double*, double*, int32_t*, int64_t*, uint8_t*);
 
-SolveConfig inner_cfg(const snop_solver_config& c) {
-  SolveConfig s;
-  s.tol = c.tolerance;
-  s.max_it = c.max_inner;
-  s.bc_left = c.bc_left;
-  s.bc_right = c.bc_right;
-  s.norm = c.norm;
-  return s;
-}
-
-}  // namespace
-
-namespace snop_impl {
-
-snop_status launch_source_iteration(Ctx& ctx, const snop_grid& g, int order, int batch, const double* st,
-                                    const double* ss0, const double* ss1, const double* src,
-                                    const snop_solver_config& cfg, const double* phi0, double* phi, double* cur,
-                                    int32_t* iters, uint8_t* conv) {
-  if (batch == 0) return SNOP_OK;
-  const SweepConsts sc = make_consts(g, order);
-  const SolveConfig c = inner_cfg(cfg);
-  const int K = pick_k();
-#define SNOP_SI(KK, NN) \
-  if (K == KK && pick_nt(g.n_cells, KK) == NN) \
-    return launch_si_t<KK, NN>(ctx, sc, c, batch, st, ss0, ss1, src, phi0, phi, cur, iters, conv);
-  SNOP_SI(8, 32) SNOP_SI(8, 64) SNOP_SI(8, 128) SNOP_SI(8, 256) SNOP_SI(8, 512)
-  SNOP_SI(16, 32) SNOP_SI(16, 64) SNOP_SI(16, 128) SNOP_SI(16, 256)
-
-#undef SNOP_SI
-  {
-      set_error("n_cells exceeds the per-CTA register-resident sweep limit (4096)");
-      return SNOP_INVALID_ARGUMENT;
-  }
-}
-
-snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int batch, int G, const double* st,
-                                   const double* ss0, const double* ss1, const double* nsf, const double* chi,
-                                   const snop_solver_config& cfg, const double* k0, const double* phi0, double* k,
-                                   double* phi, double* old, int32_t* outer, int64_t* inner, uint8_t* conv) {
-  if (batch == 0) return SNOP_OK;
-  const SweepConsts sc = make_consts(g, order);
-  const SolveConfig ic = inner_cfg(cfg);
-  EigenParams ep;
-  ep.G = G;
-  ep.tol_k = cfg.tolerance_k;
-  ep.tol_phi = cfg.tolerance_phi;
-  ep.max_outer = cfg.max_outer;
-  ep.norm = cfg.norm;
-  const int K = pick_k();
-#define SNOP_PI(KK, NN) \
-  if (K == KK && pick_nt(g.n_cells, KK) == NN) \
-    return launch_pi_t<KK, NN>(ctx, sc, ic, ep, batch, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv);
-  SNOP_PI(8, 32) SNOP_PI(8, 64) SNOP_PI(8, 128) SNOP_PI(8, 256) SNOP_PI(8, 512)
-  SNOP_PI(16, 32) SNOP_PI(16, 64) SNOP_PI(16, 128) SNOP_PI(16, 256)
-
-#undef SNOP_PI
-  {
-      set_error("n_cells exceeds the per-CTA register-resident sweep limit (4096)");
-      return SNOP_INVALID_ARGUMENT;
-  }
-}
-
-}  // namespace snop_impl
+}  // namespace snop_si

@@ -261,3 +261,134 @@ def recast_source(source, phi, sigma_t, sigma_s0, reference_params=(1.0, 0.5), c
     if a.device:
         ctx.synchronize()
     return out
+
+
+# ---- SolutionOperators and the MD-PNOP drivers ---------------------------------------------
+class SolutionOperator:
+    """Device-resident SolutionOperator: DeepONet, FNO or the exact model-based
+    solve at p*. ``reference_params`` = p* = (Sigma_t*, Sigma_s0*)."""
+
+    def __init__(self, handle, grid: Grid1D, reference_params, ctx: Context, keep=()):
+        self.h = handle
+        self.grid = grid
+        self.reference_params = tuple(reference_params)
+        self.ctx = ctx
+        self._keep = keep
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.ctx._lib.snop_op_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @classmethod
+    def deeponet(cls, grid: Grid1D, params, reference_params=(1.0, 0.5), ctx: Context | None = None):
+        ctx = ctx or default_context()
+        bs = np.ascontiguousarray(params.branch.sizes, dtype=np.int32)
+        ts = np.ascontiguousarray(params.trunk.sizes, dtype=np.int32)
+        bp, tp = params.branch.packed(), params.trunk.packed()
+        h = C.c_void_p()
+        g = grid.c()
+        _capi.check(ctx._lib.snop_deeponet_create(
+            ctx.h, C.byref(g), float(reference_params[0]), float(reference_params[1]), int(params.activation),
+            len(bs), bs.ctypes.data, bp.ctypes.data, len(ts), ts.ctypes.data, tp.ctypes.data,
+            int(params.bias0 is not None), float(params.bias0 or 0.0), C.byref(h)))
+        return cls(h, grid, reference_params, ctx)
+
+    @classmethod
+    def fno(cls, grid: Grid1D, params, reference_params=(1.0, 0.8), ctx: Context | None = None):
+        ctx = ctx or default_context()
+        p = params.packed()
+        h = C.c_void_p()
+        g = grid.c()
+        _capi.check(ctx._lib.snop_fno_create(ctx.h, C.byref(g), float(reference_params[0]),
+                                             float(reference_params[1]), int(params.activation), int(params.width),
+                                             int(params.modes), int(params.layers), int(params.hidden),
+                                             p.ctypes.data, C.byref(h)))
+        return cls(h, grid, reference_params, ctx)
+
+    @classmethod
+    def exact(cls, grid: Grid1D, order: int, reference_params=(1.0, 0.5), config: SolverConfig | None = None,
+              ctx: Context | None = None):
+        ctx = ctx or default_context()
+        cfg = (config or SolverConfig(tolerance=1e-10)).c()
+        h = C.c_void_p()
+        g = grid.c()
+        _capi.check(ctx._lib.snop_exact_operator_create(ctx.h, C.byref(g), int(order), float(reference_params[0]),
+                                                        float(reference_params[1]), C.byref(cfg), C.byref(h)))
+        return cls(h, grid, reference_params, ctx)
+
+    def predict(self, source, sync: bool = True):
+        """predict(model, source) (SPEC.md:319-322), batched [B][Nc]."""
+        a = _Args(source)
+        B = int(source.shape[0])
+        n = self.grid.n_cells
+        s = a.inp(source, shape=(B, n))
+        out, out_p = a.out((B, n))
+        _capi.check(self.ctx._lib.snop_op_predict(self.ctx.h, self.h, a.memspace, B, s, out_p))
+        if a.device and sync:
+            self.ctx.synchronize()
+        return out
+
+
+@dataclass
+class RecastResult:
+    phi: object
+    iterations: object
+    status: object
+
+
+def recast_fixed_point(op: SolutionOperator, source, sigma_t, sigma_s0, tolerance: float = 1e-4,
+                       max_iterations: int = 50, norm: int = REL_LINF, initial_phi=None) -> RecastResult:
+    """phi^{k+1} = op(recast(S, phi^k)); status 0 converged / 1 maxed / 2 diverged."""
+    a = _Args(source, sigma_t, sigma_s0, initial_phi)
+    B = int(source.shape[0])
+    n = op.grid.n_cells
+    S, st, ss = (a.inp(x, shape=(B, n)) for x in (source, sigma_t, sigma_s0))
+    p0 = a.inp(initial_phi, shape=(B, n))
+    phi, phi_p = a.out((B, n))
+    it, it_p = a.out((B,), np.int32)
+    stt, st_p = a.out((B,), np.int32)
+    _capi.check(op.ctx._lib.snop_recast_fixed_point(op.ctx.h, op.h, a.memspace, B, S, st, ss, float(tolerance),
+                                                    int(max_iterations), int(norm), p0, phi_p, it_p, st_p))
+    if a.device:
+        op.ctx.synchronize()
+    return RecastResult(phi, it, stt)
+
+
+@dataclass
+class PreconditionedResult:
+    phi: object
+    precond_iterations: object
+    recast_status: object
+    refine_iterations: object
+    converged: object
+
+
+def precondition_fixed_source(op: SolutionOperator, order: int, sigma_t, sigma_s0, source,
+                              config: SolverConfig | None = None, recast_tolerance: float = 1e-4,
+                              recast_max_iterations: int = 50, sigma_s1=None) -> PreconditionedResult:
+    """SPEC.md:413-421 (paper Eq. 10): recast fixed point, then source iteration warm-started."""
+    config = config or SolverConfig()
+    a = _Args(sigma_t, sigma_s0, source, sigma_s1)
+    B = int(source.shape[0])
+    n = op.grid.n_cells
+    st, ss, S = (a.inp(x, shape=(B, n)) for x in (sigma_t, sigma_s0, source))
+    s1 = a.inp(sigma_s1, shape=(B, n))
+    phi, phi_p = a.out((B, n))
+    pit, pit_p = a.out((B,), np.int32)
+    rst, rst_p = a.out((B,), np.int32)
+    rit, rit_p = a.out((B,), np.int32)
+    cv, cv_p = a.out((B,), np.uint8)
+    cfg = config.c()
+    _capi.check(op.ctx._lib.snop_precondition_fixed_source(
+        op.ctx.h, op.h, a.memspace, int(order), B, st, ss, s1, S, float(recast_tolerance), int(recast_max_iterations),
+        C.byref(cfg), phi_p, pit_p, rst_p, rit_p, cv_p))
+    if a.device:
+        op.ctx.synchronize()
+    return PreconditionedResult(phi, pit, rst, rit, cv)
