@@ -50,7 +50,8 @@ def peaks():
 
 
 def dist_env():
-    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+    from paper_2509_01416_b200.distributed import env
+    return env()
 
 
 class ClockSampler:
@@ -167,7 +168,8 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = snop.Context(local)
     stream = torch.cuda.ExternalStream(ctx.stream_ptr, device=torch.device("cuda", local))
-    p = W.config2(batch=args.batch, n_cells=2000, seed=2000 + 100000 * rank)
+    from paper_2509_01416_b200.distributed import rank_seed, reduce_max, reduce_sum
+    p = W.config2(batch=args.batch, n_cells=2000, seed=rank_seed(rank))
     g = snop.Grid1D(p.length, p.n_cells)
     cfg = snop.SolverConfig(tolerance=p.tolerance)
     dev = torch.device("cuda", local)
@@ -201,17 +203,8 @@ def run_gpu(args):
     launches = ctx.launch_count - launches0
     torch.cuda.synchronize()
     t_local = float(np.sum(times))
-    if world > 1:
-        t = torch.tensor([t_local], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_max = float(t.item())
-        u = torch.tensor([updates_per_step], dtype=torch.float64, device=dev)
-        dist.all_reduce(u, op=dist.ReduceOp.SUM)
-        total_updates = float(u.item()) * args.steps
-        dist.barrier()
-    else:
-        t_max = t_local
-        total_updates = float(updates_per_step) * args.steps
+    t_max = reduce_max(t_local, dev)                      # device time, max over ranks
+    total_updates = reduce_sum(updates_per_step, dev) * args.steps
     value = total_updates / t_max
     ms_per_step = 1e3 * t_max / args.steps
     solves_per_s = p.batch * world * args.steps / t_max
@@ -228,12 +221,8 @@ def run_gpu(args):
         rh = snop.source_iteration(g, p.order, *host, cfg, ctx=ctx)
         e2e_times.append(time.perf_counter() - t0)
     upd_h = int(np.asarray(rh.iterations, dtype=np.int64).sum()) * p.n_cells * p.order
-    e2e_t = float(np.sum(e2e_times))
-    if world > 1:
-        t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_t = float(t.item())
-    e2e_value = upd_h * world * args.steps / e2e_t
+    e2e_t = reduce_max(float(np.sum(e2e_times)), dev)
+    e2e_value = reduce_sum(upd_h, dev) * args.steps / e2e_t
     h2d = 3 * p.batch * p.n_cells * 8
     d2h = p.batch * p.n_cells * 8 + p.batch * 4 + p.batch
 
