@@ -15,11 +15,11 @@ SNOP_DECL_PI(16, 32) SNOP_DECL_PI(16, 64) SNOP_DECL_PI(16, 128) SNOP_DECL_PI(16,
 namespace {
 
 // Block shape: K cells per thread (compile-time, register arrays), NT = smallest power of two
-// >= ceil(Nc/K), NT >= 32. K = 8 by default; SNOP_CELLS_PER_THREAD=16 selects the K = 16 variant.
+// >= ceil(Nc/K), NT >= 32. K = 8 by default (measured fastest on C2-C5); SNOP_CELLS_PER_THREAD=16 selects K = 16.
 int pick_k() {
   static const int k = [] {
     const char* e = std::getenv("SNOP_CELLS_PER_THREAD");
-    return (e && std::atoi(e) == 8) ? 8 : 16;
+    return (e && std::atoi(e) == 16) ? 16 : 8;
   }();
   return k;
 }

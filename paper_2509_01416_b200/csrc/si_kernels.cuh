@@ -11,6 +11,7 @@ namespace snop_si {
 using namespace snop_dev;
 
 // Register budget: 128 regs/thread (16 resident warps per SM at NT*minBlocks = 512).
+// Register budget: 128 regs/thread (16 resident warps per SM at NT * minBlocks = 512).
 template <int K, int NT>
 constexpr int min_blocks() {
   return NT <= 128 ? 512 / NT : (NT <= 256 ? 2 : 1);
@@ -85,6 +86,16 @@ si_fixed_source_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
 // all fused into the same persistent CTA. Group fluxes live in the output array (L2-resident,
 // thread-private cells), the previous-outer copy in a workspace.
 // ---------------------------------------------------------------------------------------------
+// The power-iteration kernel calls the inner solver through a non-inlined boundary: the outer
+// loop's live state is saved once per group solve instead of competing with the sweep's
+// per-cell maps for registers inside the hot loop.
+template <int K, int NT, bool ANISO>
+__device__ __noinline__ int si_solve_call(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem<K, NT>& sm,
+                                          const CellIO& io) {
+  bool c = false;
+  return si_solve<K, NT, ANISO, false>(sc, cfg, sm, io, &c);
+}
+
 struct EigenParams {
   int G;
   double tol_k, tol_phi;
@@ -207,8 +218,7 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
       io.src = qext_b;
       io.ss1 = ANISO ? ss1_g + (size_t)b * GN + (size_t)g * Nc : nullptr;
       io.jc = jc_b;
-      bool ic = false;
-      inner_total += si_solve<K, NT, ANISO, false>(sc, icfg, sm, io, &ic);
+      inner_total += si_solve_call<K, NT, ANISO>(sc, icfg, sm, io);
 #pragma unroll
       for (int j = 0; j < K; ++j)
         if (c0 + j < Nc) phi_b[cell(g, j)] = sm.phi[j * NT + t];

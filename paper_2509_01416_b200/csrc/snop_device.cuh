@@ -170,7 +170,14 @@ struct SweepSmem {
   double st[K * NT];           // Sigma_t (0 on padding cells)
   double q2[K * NT];           // 2 x isotropic emission: Ss0 phi + S (rebuilt every iteration)
   double phi[K * NT];          // scalar flux
-  alignas(32) double tot[2][2][NW][4];  // scan totals [slot][pair-in-group][warp] {Af,Bf,Ab,Bb}
+  // chunk-indexed arrays use spos(): one pad slot per E = NT/32 entries, so the scan warp's
+  // lane-strided reads (lane l owns chunks l*E .. l*E+E-1) are bank-conflict free
+  static constexpr int E = NT / 32;
+  static constexpr int NP_PAD = NT + (E > 1 ? 32 : 0);
+  __device__ static constexpr int spos(int idx) { return E > 1 ? idx + idx / E : idx; }
+  double agg[2][3][NP_PAD];    // chunk maps of the current pair group: [q][{A, Bfwd, Bbwd}][chunk]
+  double xmap[2][4][NP_PAD];   // exclusive maps entering each chunk: [q][{Af, Bf, Ab, Bb}][chunk]
+  double total[2][4];          // whole-domain maps [q][{Af, Bf, Ab, Bb}]
   double jfirst[NT + 1];       // J at each thread's first edge (+ J at the last edge, slot NT)
   double red[4 * NW];          // reductions inside si_solve
   double red2[4 * NW];         // reductions of the enclosing (eigen) kernel
@@ -188,26 +195,15 @@ struct CellIO {
 };
 
 struct SweepCtl {
-  int t, lane, warp, it, slot;
+  int t, lane, warp, it;
   bool rl, rr, owns_last;
 };
 
-// Sweeps NP (1 or 2) +/-mu pairs starting at p0 and accumulates their edge currents into Jl /
-// Jend. The NP pairs are independent chains the scheduler interleaves (ILP); one barrier per
-// group. Padding cells carry St = q2 = 0, so alpha = 2c/c - 1 = 1 (to 1 ulp) and beta = 0.
+// Phase A: per-cell affine maps of NP pairs (registers) and their per-thread chunk compositions
+// (-> shared memory). Padding cells carry St = q2 = 0: alpha = 2c/c - 1 = 1 (to 1 ulp), beta = 0.
 template <int K, int NT, bool ANISO, int NP>
-__device__ __forceinline__ void sweep_pair_group(const SweepConsts& sc, SweepSmem<K, NT>& sm, const CellIO& io,
-                                                 int p0, const SweepCtl& w, double (&Jl)[K], double& Jend) {
-  constexpr int NW = NT / 32;
-  const int t = w.t, lane = w.lane, warp = w.warp;
-  double c[NP], c2[NP], wm[NP];
-#pragma unroll
-  for (int q = 0; q < NP; ++q) {
-    c[q] = sc.c[p0 + q];
-    c2[q] = 2.0 * c[q];
-    wm[q] = sc.wmu[p0 + q];
-  }
-  double al[NP][K], bp[NP][K], bm[NP][K];
+__device__ __forceinline__ void maps_phase(const SweepConsts& sc, SweepSmem<K, NT>& sm, const CellIO& io, int p0,
+                                           int t, double (&al)[NP][K], double (&bp)[NP][K], double (&bm)[NP][K]) {
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const double stj = sm.st[j * NT + t], qj = sm.q2[j * NT + t];
@@ -215,8 +211,9 @@ __device__ __forceinline__ void sweep_pair_group(const SweepConsts& sc, SweepSme
     if constexpr (ANISO) a3base = (t * K + j < sc.n_cells) ? io.ss1[t * K + j] * io.jc[t * K + j] : 0.0;
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
-      const double r = rcp_fast(stj + c[q]);
-      al[q][j] = fma(c2[q], r, -1.0);
+      const double c = sc.c[p0 + q];
+      const double r = rcp_fast(stj + c);
+      al[q][j] = fma(2.0 * c, r, -1.0);
       if constexpr (ANISO) {
         const double a3 = sc.mu3[p0 + q] * a3base;
         bp[q][j] = (qj + a3) * r;
@@ -227,99 +224,123 @@ __device__ __forceinline__ void sweep_pair_group(const SweepConsts& sc, SweepSme
       }
     }
   }
-  // compose own chunk: forward (ascending) and backward (descending)
-  double Af[NP], Bf[NP], Ab[NP], Bb[NP];
 #pragma unroll
   for (int q = 0; q < NP; ++q) {
-    Af[q] = al[q][0];
-    Bf[q] = bp[q][0];
-    Bb[q] = bm[q][K - 1];
-  }
+    double A = al[q][0], Bf = bp[q][0], Bb = bm[q][K - 1];
 #pragma unroll
-  for (int j = 1; j < K; ++j)
-#pragma unroll
-    for (int q = 0; q < NP; ++q) {
-      Bf[q] = fma(al[q][j], Bf[q], bp[q][j]);
-      Af[q] *= al[q][j];
-      Bb[q] = fma(al[q][K - 1 - j], Bb[q], bm[q][K - 1 - j]);
+    for (int j = 1; j < K; ++j) {
+      Bf = fma(al[q][j], Bf, bp[q][j]);
+      A *= al[q][j];
+      Bb = fma(al[q][K - 1 - j], Bb, bm[q][K - 1 - j]);
     }
-#pragma unroll
-  for (int q = 0; q < NP; ++q) Ab[q] = Af[q];
-  // warp scans (Kogge-Stone): forward inclusive prefix, backward inclusive suffix; predicated
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const bool up = lane >= o, dn = lane + o < 32;
-#pragma unroll
-    for (int q = 0; q < NP; ++q) {
-      const double ap = shfl_up_d(Af[q], o), bpv = shfl_up_d(Bf[q], o);
-      const double an = shfl_down_d(Ab[q], o), bnv = shfl_down_d(Bb[q], o);
-      pfma(Bf[q], Af[q], bpv, Bf[q], up);
-      pmul(Af[q], Af[q], ap, up);
-      pfma(Bb[q], Ab[q], bnv, Bb[q], dn);
-      pmul(Ab[q], Ab[q], an, dn);
-    }
-  }
-  double4* tot = reinterpret_cast<double4*>(&sm.tot[w.slot][0][0][0]);
-#pragma unroll
-  for (int q = 0; q < NP; ++q) {
-    if (lane == 31) { tot[q * NW + warp].x = Af[q]; tot[q * NW + warp].y = Bf[q]; }
-    if (lane == 0) { tot[q * NW + warp].z = Ab[q]; tot[q * NW + warp].w = Bb[q]; }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < NP; ++q) {
-    const double4* T4 = tot + q * NW;
-    const int p = p0 + q;
-    // boundary values (SURVEY §9 #2 ordering); only the reflective cases need full totals
-    double psi_right_in = 0.0, psi_left_in = 0.0;
-    if (w.rr || w.rl) {
-      if (w.rr && !w.rl) {
-        double v = 0.0;
-#pragma unroll
-        for (int u = 0; u < NW; ++u) { const double4 T = T4[u]; v = fma(T.x, v, T.y); }
-        psi_right_in = v;
-      } else {
-        if (w.rr) psi_right_in = sm.lag[w.it & 1][p];
-        if (w.rl) {
-          double v = psi_right_in;
-#pragma unroll
-          for (int u = NW - 1; u >= 0; --u) { const double4 T = T4[u]; v = fma(T.z, v, T.w); }
-          psi_left_in = v;
-        }
-        if (w.rr && w.rl && t == 0) {
-          double v = psi_left_in;
-#pragma unroll
-          for (int u = 0; u < NW; ++u) { const double4 T = T4[u]; v = fma(T.x, v, T.y); }
-          sm.lag[(w.it + 1) & 1][p] = v;
-        }
-      }
-    }
-    // psi entering this warp (fixed trip count, predicated)
-    double wf_in = psi_left_in, wb_in = psi_right_in;
-#pragma unroll
-    for (int u = 0; u < NW - 1; ++u) {
-      const double4 T = T4[u];
-      pfma(wf_in, T.x, wf_in, T.y, u < warp);
-      const double4 U = T4[NW - 1 - u];
-      pfma(wb_in, U.z, wb_in, U.w, NW - 1 - u > warp);
-    }
-    // psi entering this lane's chunk = psi leaving the neighbour lane's chunk
-    double psi = shfl_up_d(fma(Af[q], wf_in, Bf[q]), 1);
-    if (lane == 0) psi = wf_in;
-    double psib = shfl_down_d(fma(Ab[q], wb_in, Bb[q]), 1);
-    if (lane == 31) psib = wb_in;
-    const double psib_in = psib;  // psi- entering from the right (= inflow at x=L for the owner)
-    // replay: accumulate the edge currents J_e += w mu (psi+ - psi-)
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      Jl[j] = fma(wm[q], psi, Jl[j]);
-      psi = fma(al[q][j], psi, bp[q][j]);
-      psib = fma(al[q][K - 1 - j], psib, bm[q][K - 1 - j]);
-      Jl[K - 1 - j] = fma(-wm[q], psib, Jl[K - 1 - j]);
-    }
-    if (w.owns_last) Jend = fma(wm[q], psi - psib_in, Jend);  // J at x = L
+    const int pt = SweepSmem<K, NT>::spos(t);
+    sm.agg[q][0][pt] = A;
+    sm.agg[q][1][pt] = Bf;
+    sm.agg[q][2][pt] = Bb;
   }
 }
+
+// Phase B: one warp per (pair, direction) scans the NT chunk maps of the CTA: each lane composes
+// E = NT/32 consecutive chunks serially, a 5-step shuffle scan joins the lanes, and every chunk
+// gets the exclusive map that carries the boundary inflow to its first edge. Forward = prefix
+// (left to right), backward = suffix (right to left).
+template <int K, int NT, int NP>
+__device__ __forceinline__ void scan_phase(SweepSmem<K, NT>& sm, int lane, int warp) {
+  constexpr int NW = NT / 32, E = NT / 32;
+  for (int s = warp; s < 2 * NP; s += NW) {
+    const int q = s >> 1;
+    const bool fwd = (s & 1) == 0;
+    const double* Ag = sm.agg[q][0];
+    const double* Bg = sm.agg[q][fwd ? 1 : 2];
+    // lane order = sweep order; operands are re-read from shared memory in the second pass so
+    // the scan adds no register pressure on top of the live per-cell maps
+    auto at = [&](int e) { return SweepSmem<K, NT>::spos(fwd ? lane * E + e : NT - 1 - (lane * E + e)); };
+    double A = Ag[at(0)], B = Bg[at(0)];
+#pragma unroll 4
+    for (int e = 1; e < E; ++e) {
+      const double ae = Ag[at(e)];
+      B = fma(ae, B, Bg[at(e)]);
+      A *= ae;
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double ap = __shfl_up_sync(0xffffffffu, A, o), bq = __shfl_up_sync(0xffffffffu, B, o);
+      if (lane >= o) {
+        B = fma(A, bq, B);
+        A *= ap;
+      }
+    }
+    double Ax = __shfl_up_sync(0xffffffffu, A, 1), Bx = __shfl_up_sync(0xffffffffu, B, 1);
+    if (lane == 0) {
+      Ax = 1.0;
+      Bx = 0.0;
+    }
+    if (lane == 31) {
+      sm.total[q][fwd ? 0 : 2] = A;
+      sm.total[q][fwd ? 1 : 3] = B;
+    }
+    double* XA = sm.xmap[q][fwd ? 0 : 2];
+    double* XB = sm.xmap[q][fwd ? 1 : 3];
+#pragma unroll 4
+    for (int e = 0; e < E; ++e) {
+      const int idx = at(e);
+      const double ae = Ag[idx], be = Bg[idx];
+      XA[idx] = Ax;
+      XB[idx] = Bx;
+      Bx = fma(ae, Bx, be);
+      Ax *= ae;
+    }
+  }
+}
+
+// Phase C: boundary inflows (SURVEY §9 #2 ordering), the inflow of this thread's chunk, and the
+// replay that accumulates the edge currents J_e += w mu (psi+ - psi-).
+template <int K, int NT, int NP>
+__device__ __forceinline__ void replay_phase(const SweepConsts& sc, SweepSmem<K, NT>& sm, int p0, const SweepCtl& w,
+                                             const double (&al)[NP][K], const double (&bp)[NP][K],
+                                             const double (&bm)[NP][K], double (&Jl)[K], double& Jend) {
+  const int t = w.t;
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    const int p = p0 + q;
+    const double wm = sc.wmu[p];
+    double psi_right_in = 0.0, psi_left_in = 0.0;
+    if (w.rr || w.rl) {
+      const double TAf = sm.total[q][0], TBf = sm.total[q][1], TAb = sm.total[q][2], TBb = sm.total[q][3];
+      if (w.rr && !w.rl) {
+        psi_right_in = TBf;  // mu>0 outflow at x=L with vacuum left
+      } else {
+        if (w.rr) psi_right_in = sm.lag[w.it & 1][p];
+        if (w.rl) psi_left_in = fma(TAb, psi_right_in, TBb);
+        if (w.rr && w.rl && t == 0) sm.lag[(w.it + 1) & 1][p] = fma(TAf, psi_left_in, TBf);
+      }
+    }
+    const int pt = SweepSmem<K, NT>::spos(t);
+    double psi = fma(sm.xmap[q][0][pt], psi_left_in, sm.xmap[q][1][pt]);
+    double psib = fma(sm.xmap[q][2][pt], psi_right_in, sm.xmap[q][3][pt]);
+    const double psib_in = psib;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      Jl[j] = fma(wm, psi, Jl[j]);
+      psi = fma(al[q][j], psi, bp[q][j]);
+      psib = fma(al[q][K - 1 - j], psib, bm[q][K - 1 - j]);
+      Jl[K - 1 - j] = fma(-wm, psib, Jl[K - 1 - j]);
+    }
+    if (w.owns_last) Jend = fma(wm, psi - psib_in, Jend);  // J at x = L
+  }
+}
+
+template <int K, int NT, bool ANISO, int NP>
+__device__ __forceinline__ void sweep_pair_group(const SweepConsts& sc, SweepSmem<K, NT>& sm, const CellIO& io,
+                                                 int p0, const SweepCtl& w, double (&Jl)[K], double& Jend) {
+  double al[NP][K], bp[NP][K], bm[NP][K];
+  maps_phase<K, NT, ANISO, NP>(sc, sm, io, p0, w.t, al, bp, bm);
+  __syncthreads();
+  scan_phase<K, NT, NP>(sm, w.lane, w.warp);
+  __syncthreads();
+  replay_phase<K, NT, NP>(sc, sm, p0, w, al, bp, bm, Jl, Jend);
+}
+
 
 // One CTA solves one within-group fixed-source problem by source iteration.
 // On entry sm.st (>0; 0 on padding) and sm.phi (initial flux; 0 on padding) hold the own cells;
@@ -327,7 +348,7 @@ __device__ __forceinline__ void sweep_pair_group(const SweepConsts& sc, SweepSme
 // thread-ordered global arrays. On exit sm.phi holds the final flux and io.jc the cell-average
 // current of the last sweep (written when ANISO || CUR). Returns sweeps performed;
 // *converged is uniform in the CTA.
-template <int K, int NT, bool ANISO, bool CUR, int NP = 1>
+template <int K, int NT, bool ANISO, bool CUR, int NP = (K <= 8 ? 2 : 1)>
 __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem<K, NT>& sm, const CellIO& io,
                         bool* converged) {
   const int t = threadIdx.x;
@@ -351,7 +372,6 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
   int it = 0;
   bool conv = false;
   int rphase = 0;
-  w.slot = 0;
   while (it < cfg.max_it) {
     ++it;
     w.it = it;
@@ -365,15 +385,9 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
     double Jend = 0.0;
     int p = 0;
     if constexpr (NP == 2) {
-      for (; p + 1 < P; p += 2) {
-        sweep_pair_group<K, NT, ANISO, 2>(sc, sm, io, p, w, Jl, Jend);
-        w.slot ^= 1;
-      }
+      for (; p + 1 < P; p += 2) sweep_pair_group<K, NT, ANISO, 2>(sc, sm, io, p, w, Jl, Jend);
     }
-    for (; p < P; ++p) {
-      sweep_pair_group<K, NT, ANISO, 1>(sc, sm, io, p, w, Jl, Jend);
-      w.slot ^= 1;
-    }
+    for (; p < P; ++p) sweep_pair_group<K, NT, ANISO, 1>(sc, sm, io, p, w, Jl, Jend);
     // edge-current exchange: J at the right edge of own last cell = next thread's first edge
     sm.jfirst[t] = Jl[0];
     if (w.owns_last) sm.jfirst[NT] = Jend;
