@@ -1,34 +1,55 @@
-// si_dispatch.cu — picks the (K, NT) instantiation of K1/K2 for a launch.
+// si_dispatch.cu — picks the block shape (K cells per thread, NT threads per CTA) and the cluster
+// size (CS CTAs per instance) of K1/K2 for a launch.
 #include <cstdlib>
 
 #include "si_kernels.cuh"
 
-using namespace snop_si;
-
 namespace snop_si {
-SNOP_DECL_SI(8, 32) SNOP_DECL_SI(8, 64) SNOP_DECL_SI(8, 128) SNOP_DECL_SI(8, 256) SNOP_DECL_SI(8, 512)
-SNOP_DECL_SI(16, 32) SNOP_DECL_SI(16, 64) SNOP_DECL_SI(16, 128) SNOP_DECL_SI(16, 256)
-SNOP_DECL_PI(8, 32) SNOP_DECL_PI(8, 64) SNOP_DECL_PI(8, 128) SNOP_DECL_PI(8, 256) SNOP_DECL_PI(8, 512)
-SNOP_DECL_PI(16, 32) SNOP_DECL_PI(16, 64) SNOP_DECL_PI(16, 128) SNOP_DECL_PI(16, 256)
+SNOP_DECL_SI(8, 32, false) SNOP_DECL_SI(8, 64, false) SNOP_DECL_SI(8, 128, false) SNOP_DECL_SI(8, 256, false)
+SNOP_DECL_SI(8, 512, false)
+SNOP_DECL_SI(8, 32, true) SNOP_DECL_SI(8, 64, true) SNOP_DECL_SI(8, 128, true) SNOP_DECL_SI(8, 256, true)
+SNOP_DECL_PI(8, 32, false) SNOP_DECL_PI(8, 64, false) SNOP_DECL_PI(8, 128, false) SNOP_DECL_PI(8, 256, false)
+SNOP_DECL_PI(8, 512, false)
+SNOP_DECL_PI(8, 32, true) SNOP_DECL_PI(8, 64, true) SNOP_DECL_PI(8, 128, true) SNOP_DECL_PI(8, 256, true)
 }  // namespace snop_si
+
+using namespace snop_si;
 
 namespace {
 
-// Block shape: K cells per thread (compile-time, register arrays), NT = smallest power of two
-// >= ceil(Nc/K), NT >= 32. K = 8 by default (measured fastest on C2-C5); SNOP_CELLS_PER_THREAD=16 selects K = 16.
-int pick_k() {
-  static const int k = [] {
-    const char* e = std::getenv("SNOP_CELLS_PER_THREAD");
-    return (e && std::atoi(e) == 16) ? 16 : 8;
-  }();
-  return k;
+constexpr int K = 8;
+
+int pow2_at_least(int v, int lo) {
+  int p = lo;
+  while (p < v) p <<= 1;
+  return p;
 }
 
-int pick_nt(int n_cells, int K) {
-  const int need = (n_cells + K - 1) / K;
-  int nt = 32;
-  while (nt < need) nt <<= 1;
-  return nt;
+struct Shape {
+  int cs, nt;
+};
+
+// Cluster size: one CTA per instance by default. Spreading an instance over a thread-block
+// cluster (cells split across SMs, joined through DSMEM) is correct but measured slower on every
+// BASELINE config (C2-C5, DESIGN.md §K1 "clusters"): the per-pair-group cluster barrier costs more
+// than the split saves. SNOP_CLUSTER=2|4|8 selects it explicitly.
+Shape pick_shape(int n_cells, int batch, int sm_count) {
+  (void)batch;
+  (void)sm_count;
+  int cs = 1;
+  if (const char* e = std::getenv("SNOP_CLUSTER")) {
+    const int v = std::atoi(e);
+    cs = (v == 2 || v == 4 || v == 8) ? v : 1;
+  }
+  const int per_cta = (n_cells + cs - 1) / cs;
+  int nt = pow2_at_least((per_cta + K - 1) / K, 32);
+  if (cs > 1 && nt > 256) {  // clusters are instantiated up to NT = 256
+    while (cs < 8 && nt > 256) {
+      cs <<= 1;
+      nt = pow2_at_least(((n_cells + cs - 1) / cs + K - 1) / K, 32);
+    }
+  }
+  return {cs, nt};
 }
 
 SolveConfig inner_cfg(const snop_solver_config& c) {
@@ -52,18 +73,15 @@ snop_status launch_source_iteration(Ctx& ctx, const snop_grid& g, int order, int
   if (batch == 0) return SNOP_OK;
   const SweepConsts sc = make_consts(g, order);
   const SolveConfig c = inner_cfg(cfg);
-  const int K = pick_k();
-#define SNOP_SI(KK, NN) \
-  if (K == KK && pick_nt(g.n_cells, KK) == NN) \
-    return launch_si_t<KK, NN>(ctx, sc, c, batch, st, ss0, ss1, src, phi0, phi, cur, iters, conv);
-  SNOP_SI(8, 32) SNOP_SI(8, 64) SNOP_SI(8, 128) SNOP_SI(8, 256) SNOP_SI(8, 512)
-  SNOP_SI(16, 32) SNOP_SI(16, 64) SNOP_SI(16, 128) SNOP_SI(16, 256)
-
+  const Shape s = pick_shape(g.n_cells, batch, ctx.sm_count);
+#define SNOP_SI(NN, CC)                       \
+  if (s.nt == NN && (s.cs > 1) == CC)         \
+    return launch_si_t<K, NN, CC>(ctx, sc, c, batch, s.cs, st, ss0, ss1, src, phi0, phi, cur, iters, conv);
+  SNOP_SI(32, false) SNOP_SI(64, false) SNOP_SI(128, false) SNOP_SI(256, false) SNOP_SI(512, false)
+  SNOP_SI(32, true) SNOP_SI(64, true) SNOP_SI(128, true) SNOP_SI(256, true)
 #undef SNOP_SI
-  {
-      set_error("n_cells exceeds the per-CTA register-resident sweep limit (4096)");
-      return SNOP_INVALID_ARGUMENT;
-  }
+  set_error("n_cells exceeds the register-resident sweep limit (4096 per instance)");
+  return SNOP_INVALID_ARGUMENT;
 }
 
 snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int batch, int G, const double* st,
@@ -79,18 +97,15 @@ snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int 
   ep.tol_phi = cfg.tolerance_phi;
   ep.max_outer = cfg.max_outer;
   ep.norm = cfg.norm;
-  const int K = pick_k();
-#define SNOP_PI(KK, NN) \
-  if (K == KK && pick_nt(g.n_cells, KK) == NN) \
-    return launch_pi_t<KK, NN>(ctx, sc, ic, ep, batch, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv);
-  SNOP_PI(8, 32) SNOP_PI(8, 64) SNOP_PI(8, 128) SNOP_PI(8, 256) SNOP_PI(8, 512)
-  SNOP_PI(16, 32) SNOP_PI(16, 64) SNOP_PI(16, 128) SNOP_PI(16, 256)
-
+  const Shape s = pick_shape(g.n_cells, batch, ctx.sm_count);
+#define SNOP_PI(NN, CC)               \
+  if (s.nt == NN && (s.cs > 1) == CC) \
+    return launch_pi_t<K, NN, CC>(ctx, sc, ic, ep, batch, s.cs, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv);
+  SNOP_PI(32, false) SNOP_PI(64, false) SNOP_PI(128, false) SNOP_PI(256, false) SNOP_PI(512, false)
+  SNOP_PI(32, true) SNOP_PI(64, true) SNOP_PI(128, true) SNOP_PI(256, true)
 #undef SNOP_PI
-  {
-      set_error("n_cells exceeds the per-CTA register-resident sweep limit (4096)");
-      return SNOP_INVALID_ARGUMENT;
-  }
+  set_error("n_cells exceeds the register-resident sweep limit (4096 per instance)");
+  return SNOP_INVALID_ARGUMENT;
 }
 
 }  // namespace snop_impl

@@ -1,10 +1,10 @@
-// Explicit instantiations: K2 power-iteration kernels, K = 8.
+// Explicit instantiations: K2 power-iteration kernels, K = 8, cluster mode = false.
 #include "si_kernels.cuh"
 
 namespace snop_si {
-template snop_status launch_pi_t<8, 32>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, const EigenParams&, int, const double*, const double*, const double*, const double*, const double*, const double*, const double*, double*, double*, double*, int32_t*, int64_t*, uint8_t*);
-template snop_status launch_pi_t<8, 64>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, const EigenParams&, int, const double*, const double*, const double*, const double*, const double*, const double*, const double*, double*, double*, double*, int32_t*, int64_t*, uint8_t*);
-template snop_status launch_pi_t<8, 128>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, const EigenParams&, int, const double*, const double*, const double*, const double*, const double*, const double*, const double*, double*, double*, double*, int32_t*, int64_t*, uint8_t*);
-template snop_status launch_pi_t<8, 256>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, const EigenParams&, int, const double*, const double*, const double*, const double*, const double*, const double*, const double*, double*, double*, double*, int32_t*, int64_t*, uint8_t*);
-template snop_status launch_pi_t<8, 512>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, const EigenParams&, int, const double*, const double*, const double*, const double*, const double*, const double*, const double*, double*, double*, double*, int32_t*, int64_t*, uint8_t*);
+SNOP_INST_PI(8, 32, false)
+SNOP_INST_PI(8, 64, false)
+SNOP_INST_PI(8, 128, false)
+SNOP_INST_PI(8, 256, false)
+SNOP_INST_PI(8, 512, false)
 }  // namespace snop_si

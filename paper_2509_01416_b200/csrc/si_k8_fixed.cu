@@ -1,10 +1,10 @@
-// Explicit instantiations: K1 fixed-source kernels, K = 8.
+// Explicit instantiations: K1 fixed-source kernels, K = 8, cluster mode = false.
 #include "si_kernels.cuh"
 
 namespace snop_si {
-template snop_status launch_si_t<8, 32>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, int, const double*, const double*, const double*, const double*, const double*, double*, double*, int32_t*, uint8_t*);
-template snop_status launch_si_t<8, 64>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, int, const double*, const double*, const double*, const double*, const double*, double*, double*, int32_t*, uint8_t*);
-template snop_status launch_si_t<8, 128>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, int, const double*, const double*, const double*, const double*, const double*, double*, double*, int32_t*, uint8_t*);
-template snop_status launch_si_t<8, 256>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, int, const double*, const double*, const double*, const double*, const double*, double*, double*, int32_t*, uint8_t*);
-template snop_status launch_si_t<8, 512>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, int, const double*, const double*, const double*, const double*, const double*, double*, double*, int32_t*, uint8_t*);
+SNOP_INST_SI(8, 32, false)
+SNOP_INST_SI(8, 64, false)
+SNOP_INST_SI(8, 128, false)
+SNOP_INST_SI(8, 256, false)
+SNOP_INST_SI(8, 512, false)
 }  // namespace snop_si

@@ -1,16 +1,17 @@
 // si_kernels.cuh — K1 (fused fixed-source source iteration) and K2 (fused power iteration,
-// single- and multi-group) for sm_100a. One CTA = one instance for the whole solve; see
-// snop_device.cuh and DESIGN.md §K1/§K2.
+// single- and multi-group) for sm_100a. One CTA (or, CL = true, one thread-block cluster of CS
+// CTAs, cells split across SMs and joined through DSMEM) = one instance for the whole solve;
+// see snop_device.cuh and DESIGN.md §K1/§K2.
+#pragma once
+
 #include <cmath>
 #include <cstdlib>
 
-#pragma once
 #include "snop_internal.h"
 
 namespace snop_si {
 using namespace snop_dev;
 
-// Register budget: 128 regs/thread (16 resident warps per SM at NT*minBlocks = 512).
 // Register budget: 128 regs/thread (16 resident warps per SM at NT * minBlocks = 512).
 template <int K, int NT>
 constexpr int min_blocks() {
@@ -22,10 +23,22 @@ size_t smem_bytes() {
   return sizeof(SweepSmem<K, NT>);
 }
 
+// instance index and cluster rank of this CTA
+template <bool CL>
+__device__ __forceinline__ void instance_of_block(int& b, int& rank) {
+  if constexpr (CL) {
+    rank = cl_rank();
+    b = blockIdx.x / cl_size();
+  } else {
+    rank = 0;
+    b = blockIdx.x;
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
-// K1: batched fixed-source solve, SPEC.md:125-134 (one CTA per instance).
+// K1: batched fixed-source solve.
 // ---------------------------------------------------------------------------------------------
-template <int K, int NT, bool ANISO, bool CUR>
+template <int K, int NT, bool ANISO, bool CUR, bool CL>
 __global__ void __launch_bounds__(NT, min_blocks<K, NT>())
 si_fixed_source_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig cfg,
                        const double* __restrict__ st_g, const double* __restrict__ ss0_g,
@@ -36,8 +49,10 @@ si_fixed_source_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   extern __shared__ __align__(32) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<SweepSmem<K, NT>*>(smem_raw);
   const int t = threadIdx.x, Nc = sc.n_cells;
-  const size_t base = (size_t)blockIdx.x * Nc;
-  const int c0 = t * K;
+  int b, rank;
+  instance_of_block<CL>(b, rank);
+  const size_t base = (size_t)b * Nc;
+  const int c0 = rank * NT * K + t * K;
   CellIO io;
   io.ss0 = ss0_g + base;
   io.src = src_g + base;
@@ -54,28 +69,28 @@ si_fixed_source_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
       sm.phi[j * NT + t] = phi0_g ? phi0_g[base + i] : 0.0;
       if constexpr (ANISO) io.jc[i] = 0.0;
     } else {
-      sm.st[j * NT + t] = 0.0;  // padding: identity map (see sweep_pair_group)
+      sm.st[j * NT + t] = 0.0;  // padding: identity map (see maps_phase)
       sm.phi[j * NT + t] = 0.0;
     }
   }
-  if (__syncthreads_or(bad)) {  // nonpositive Sigma_t -> invalid argument
-    if (t == 0) {
+  if (cluster_any<NT, CL>(bad, sm)) {  // nonpositive Sigma_t -> invalid argument
+    if (t == 0 && rank == 0) {
       atomicOr(flags, snop_impl::FLAG_BAD_SIGMA_T);
-      iters[blockIdx.x] = 0;
-      conv[blockIdx.x] = 0;
+      iters[b] = 0;
+      conv[b] = 0;
     }
     return;
   }
   bool converged = false;
-  const int it = si_solve<K, NT, ANISO, CUR>(sc, cfg, sm, io, &converged);
+  const int it = si_solve<K, NT, ANISO, CUR, CL>(sc, cfg, sm, io, &converged);
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const int i = c0 + j;
     if (i < Nc) phi_g[base + i] = sm.phi[j * NT + t];
   }
-  if (t == 0) {
-    iters[blockIdx.x] = it;
-    conv[blockIdx.x] = converged ? 1 : 0;
+  if (t == 0 && rank == 0) {
+    iters[b] = it;
+    conv[b] = converged ? 1 : 0;
   }
 }
 
@@ -83,17 +98,16 @@ si_fixed_source_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
 // K2: batched k-eigenvalue power iteration, SPEC.md:179-189 + decisions :206-209, SURVEY §9 #5
 // (Gauss-Seidel over groups with upscatter, newest flux), #10 (inner solves warm-started).
 // The fission source, inscatter source, k update, renormalisation and dual convergence test are
-// all fused into the same persistent CTA. Group fluxes live in the output array (L2-resident,
-// thread-private cells), the previous-outer copy in a workspace.
+// all fused into the same persistent CTA / cluster. Group fluxes live in the output array
+// (L2-resident, thread-private cells), the previous-outer copy in a workspace.
 // ---------------------------------------------------------------------------------------------
-// The power-iteration kernel calls the inner solver through a non-inlined boundary: the outer
-// loop's live state is saved once per group solve instead of competing with the sweep's
-// per-cell maps for registers inside the hot loop.
-template <int K, int NT, bool ANISO>
+// The inner solver is called through a non-inlined boundary: the outer loop's live state is
+// saved once per group solve instead of competing with the sweep's maps for registers.
+template <int K, int NT, bool ANISO, bool CL>
 __device__ __noinline__ int si_solve_call(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem<K, NT>& sm,
                                           const CellIO& io) {
   bool c = false;
-  return si_solve<K, NT, ANISO, false>(sc, cfg, sm, io, &c);
+  return si_solve<K, NT, ANISO, false, CL>(sc, cfg, sm, io, &c);
 }
 
 struct EigenParams {
@@ -103,7 +117,7 @@ struct EigenParams {
   int norm;
 };
 
-template <int K, int NT, bool ANISO>
+template <int K, int NT, bool ANISO, bool CL>
 __global__ void __launch_bounds__(NT, min_blocks<K, NT>())
 power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig icfg, const EigenParams ep,
                        const double* __restrict__ st_g, const double* __restrict__ ss0_g,
@@ -116,8 +130,9 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   extern __shared__ __align__(32) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<SweepSmem<K, NT>*>(smem_raw);
   const int t = threadIdx.x, Nc = sc.n_cells, G = ep.G;
-  const int b = blockIdx.x;
-  const int c0 = t * K;
+  int b, rank;
+  instance_of_block<CL>(b, rank);
+  const int c0 = rank * NT * K + t * K;
   const size_t GN = (size_t)G * Nc;
   const double* st_b = st_g + (size_t)b * GN;
   const double* ss_b = ss0_g + (size_t)b * GN * G;
@@ -142,7 +157,7 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   double k = k0_g ? k0_g[b] : 1.0;
   int rphase = 0;
   auto fission_integral = [&]() {
-    double s = 0.0;
+    double s = 0.0, dummy = 0.0;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       if (c0 + j < Nc) {
@@ -151,18 +166,20 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
         s += f;
       }
     }
-    return block_sum<NT>(s, sm.red2, rphase++) * sc.dx;
+    reduce2<NT, CL>(s, dummy, false, sm.red2, sm.cred2, rphase++, sm);
+    return s * sc.dx;
   };
   auto fail = [&](int flag) {
-    if (t == 0) {
+    if (t == 0 && rank == 0) {
       atomicOr(flags, flag);
       k_g[b] = __longlong_as_double(0x7ff8000000000000ll);
       outer_g[b] = 0;
       inner_g[b] = 0;
       conv_g[b] = 0;
     }
+    if constexpr (CL) cl_sync();  // no CTA of the cluster leaves while others may read its smem
   };
-  if (__syncthreads_or(bad) || !(k > 0.0)) {
+  if (cluster_any<NT, CL>(bad, sm) || !(k > 0.0)) {
     fail(snop_impl::FLAG_BAD_SIGMA_T);
     return;
   }
@@ -179,10 +196,10 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   int64_t inner_total = 0;
   int outer = 0;
   bool converged = false;
-  double fiss[K];
   while (outer < ep.max_outer) {
     ++outer;
     // fission density from the flux at the start of the outer (frozen during the GS pass)
+    double fiss[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       fiss[j] = 0.0;
@@ -209,7 +226,7 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
           sm.st[j * NT + t] = st_b[(size_t)g * Nc + i];
           sm.phi[j * NT + t] = phi_b[(size_t)g * Nc + i];
         } else {
-          sm.st[j * NT + t] = 0.0;  // padding: identity map (see sweep_pair_group)
+          sm.st[j * NT + t] = 0.0;  // padding: identity map (see maps_phase)
           sm.phi[j * NT + t] = 0.0;
         }
       }
@@ -218,7 +235,7 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
       io.src = qext_b;
       io.ss1 = ANISO ? ss1_g + (size_t)b * GN + (size_t)g * Nc : nullptr;
       io.jc = jc_b;
-      inner_total += si_solve_call<K, NT, ANISO>(sc, icfg, sm, io);
+      inner_total += si_solve_call<K, NT, ANISO, CL>(sc, icfg, sm, io);
 #pragma unroll
       for (int j = 0; j < K; ++j)
         if (c0 + j < Nc) phi_b[cell(g, j)] = sm.phi[j * NT + t];
@@ -229,7 +246,6 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
       return;
     }
     const double k_new = k * F1;
-    const double inv_F1 = 1.0 / F1;
     double num = 0.0, den = 0.0;
     for (int g = 0; g < G; ++g) {
 #pragma unroll
@@ -248,9 +264,7 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
         }
       }
     }
-    (void)inv_F1;
-    if (ep.norm == 0) block_max2<NT>(num, den, sm.red2, rphase++);
-    else block_sum2<NT>(num, den, sm.red2, rphase++);
+    reduce2<NT, CL>(num, den, ep.norm == 0, sm.red2, sm.cred2, rphase++, sm);
     const double dphi = rel_change(num, den, ep.norm);
     const double dk = fabs(k_new - k) / fabs(k_new);
     k = k_new;
@@ -259,22 +273,47 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
       break;
     }
   }
-  if (t == 0) {
+  if (t == 0 && rank == 0) {
     k_g[b] = k;
     outer_g[b] = outer;
     inner_g[b] = inner_total;
     conv_g[b] = converged ? 1 : 0;
   }
+  if constexpr (CL) cl_sync();
 }
 
-template <int K, int NT>
-inline snop_status launch_si_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveConfig& cfg, int batch,
-                        const double* st, const double* ss0, const double* ss1, const double* src,
-                        const double* phi0, double* phi, double* cur, int32_t* iters, uint8_t* conv) {
+// Launch helper: plain launch for CS = 1, cluster launch (CS CTAs per instance) otherwise.
+template <class Kern, class... Args>
+inline cudaError_t launch_k(Kern kern, int batch, int cs, int nt, size_t smem, cudaStream_t s, Args... args) {
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cs <= 1) {
+    kern<<<batch, nt, smem, s>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(batch * cs));
+  cfg.blockDim = dim3((unsigned)nt);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+template <int K, int NT, bool CL>
+inline snop_status launch_si_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveConfig& cfg, int batch, int cs,
+                               const double* st, const double* ss0, const double* ss1, const double* src,
+                               const double* phi0, double* phi, double* cur, int32_t* iters, uint8_t* conv) {
   const bool aniso = ss1 != nullptr;
   const size_t smem = smem_bytes<K, NT>();
-  auto kern = aniso ? si_fixed_source_kernel<K, NT, true, true>
-                    : (cur ? si_fixed_source_kernel<K, NT, false, true> : si_fixed_source_kernel<K, NT, false, false>);
+  auto kern = aniso ? si_fixed_source_kernel<K, NT, true, true, CL>
+                    : (cur ? si_fixed_source_kernel<K, NT, false, true, CL>
+                           : si_fixed_source_kernel<K, NT, false, false, CL>);
   double* jc = cur;
   if (aniso && !jc) {  // P1 needs the cell current even when the caller does not want it
     jc = static_cast<double*>(ctx.slot(21, (size_t)batch * sc.n_cells * sizeof(double)));
@@ -283,10 +322,9 @@ inline snop_status launch_si_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
       return SNOP_CUDA_ERROR;
     }
   }
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<batch, NT, smem, ctx.stream>>>(sc, cfg, st, ss0, ss1, src, phi0, phi, jc, iters, conv, ctx.d_flags);
+  const cudaError_t e = launch_k(kern, batch, CL ? cs : 1, NT, smem, ctx.stream, sc, cfg, st, ss0, ss1, src, phi0,
+                                 phi, jc, iters, conv, ctx.d_flags);
   ctx.launches++;
-  const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     snop_impl::set_error(std::string("si_fixed_source_kernel launch: ") + cudaGetErrorString(e));
     return SNOP_CUDA_ERROR;
@@ -294,14 +332,15 @@ inline snop_status launch_si_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
   return SNOP_OK;
 }
 
-template <int K, int NT>
-inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveConfig& icfg, const EigenParams& ep,
-                        int batch, const double* st, const double* ss0, const double* ss1, const double* nsf,
-                        const double* chi, const double* k0, const double* phi0, double* k, double* phi,
-                        double* old, int32_t* outer, int64_t* inner, uint8_t* conv) {
+template <int K, int NT, bool CL>
+inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveConfig& icfg,
+                               const EigenParams& ep, int batch, int cs, const double* st, const double* ss0,
+                               const double* ss1, const double* nsf, const double* chi, const double* k0,
+                               const double* phi0, double* k, double* phi, double* old, int32_t* outer,
+                               int64_t* inner, uint8_t* conv) {
   const bool aniso = ss1 != nullptr;
   const size_t smem = smem_bytes<K, NT>();
-  auto kern = aniso ? power_iteration_kernel<K, NT, true> : power_iteration_kernel<K, NT, false>;
+  auto kern = aniso ? power_iteration_kernel<K, NT, true, CL> : power_iteration_kernel<K, NT, false, CL>;
   const size_t n = (size_t)batch * sc.n_cells;
   double* qext = static_cast<double*>(ctx.slot(22, n * sizeof(double)));
   double* jc = aniso ? static_cast<double*>(ctx.slot(21, n * sizeof(double))) : nullptr;
@@ -309,11 +348,9 @@ inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
     snop_impl::set_error("cudaMalloc (eigen workspace) failed");
     return SNOP_CUDA_ERROR;
   }
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<batch, NT, smem, ctx.stream>>>(sc, icfg, ep, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, qext, jc, outer,
-                                        inner, conv, ctx.d_flags);
+  const cudaError_t e = launch_k(kern, batch, CL ? cs : 1, NT, smem, ctx.stream, sc, icfg, ep, st, ss0, ss1, nsf,
+                                 chi, k0, phi0, k, phi, old, qext, jc, outer, inner, conv, ctx.d_flags);
   ctx.launches++;
-  const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     snop_impl::set_error(std::string("power_iteration_kernel launch: ") + cudaGetErrorString(e));
     return SNOP_CUDA_ERROR;
@@ -321,14 +358,17 @@ inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
   return SNOP_OK;
 }
 
-
-// Explicitly instantiated in si_k{8,16}_{fixed,eigen}.cu (one TU per variant, parallel build).
-#define SNOP_DECL_SI(KK, NN) \
-  extern template snop_status launch_si_t<KK, NN>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, int, \
-      const double*, const double*, const double*, const double*, const double*, double*, double*, int32_t*, uint8_t*);
-#define SNOP_DECL_PI(KK, NN) \
-  extern template snop_status launch_pi_t<KK, NN>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, \
-      const EigenParams&, int, const double*, const double*, const double*, const double*, const double*, \
-      const double*, const double*, double*, double*, double*, int32_t*, int64_t*, uint8_t*);
+// Explicitly instantiated in si_k8_{fixed,eigen}{,_cl}.cu (one TU per variant, parallel build).
+#define SNOP_SI_ARGS                                                                                          \
+  snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, int, int, const double*, const double*, const double*, \
+      const double*, const double*, double*, double*, int32_t*, uint8_t*
+#define SNOP_PI_ARGS                                                                                          \
+  snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, const EigenParams&, int, int, const double*,          \
+      const double*, const double*, const double*, const double*, const double*, const double*, double*, double*, \
+      double*, int32_t*, int64_t*, uint8_t*
+#define SNOP_DECL_SI(KK, NN, CC) extern template snop_status launch_si_t<KK, NN, CC>(SNOP_SI_ARGS);
+#define SNOP_DECL_PI(KK, NN, CC) extern template snop_status launch_pi_t<KK, NN, CC>(SNOP_PI_ARGS);
+#define SNOP_INST_SI(KK, NN, CC) template snop_status launch_si_t<KK, NN, CC>(SNOP_SI_ARGS);
+#define SNOP_INST_PI(KK, NN, CC) template snop_status launch_pi_t<KK, NN, CC>(SNOP_PI_ARGS);
 
 }  // namespace snop_si

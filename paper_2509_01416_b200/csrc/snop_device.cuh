@@ -22,6 +22,7 @@
 //     the L2 sums use a fixed lane/warp order.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -182,7 +183,77 @@ struct SweepSmem {
   double red[4 * NW];          // reductions inside si_solve
   double red2[4 * NW];         // reductions of the enclosing (eigen) kernel
   double lag[2][kMaxPairs];    // both-reflective: lagged mu>0 outflow at x=L, by iteration parity
+  // cluster mode (one instance spread over the CTAs of a thread-block cluster): per-CTA values
+  // published for the other CTAs, read through distributed shared memory
+  double ctot[2][2][4];        // CTA-level scan totals [group slot][q][{Af,Bf,Ab,Bb}]
+  double cred[2][2];           // CTA-level reduction results (si_solve), by phase
+  double cred2[2][2];          // CTA-level reduction results (enclosing kernel), by phase
+  int cflag[2];                // CTA-level flags (validation)
 };
+
+// ---- thread-block-cluster helpers ----------------------------------------------------------
+__device__ __forceinline__ int cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return (int)r;
+}
+__device__ __forceinline__ int cl_size() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return (int)r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+template <class T>
+__device__ __forceinline__ T* cl_map(T* local, int rank) {
+  return cooperative_groups::this_cluster().map_shared_rank(local, (unsigned)rank);
+}
+
+// Block- then cluster-wide reduction of two values (max if is_max else sum). Ranks are combined
+// in rank order, so every CTA of the cluster obtains the bit-identical result.
+template <int NT, bool CL, class Smem>
+__device__ __forceinline__ void reduce2(double& a, double& b, bool is_max, double* scratch, double (*cred)[2],
+                                        int phase, Smem& sm) {
+  if (is_max) block_max2<NT>(a, b, scratch, phase);
+  else block_sum2<NT>(a, b, scratch, phase);
+  if constexpr (CL) {
+    const int s = phase & 1;
+    if (threadIdx.x == 0) {
+      cred[s][0] = a;
+      cred[s][1] = b;
+    }
+    cl_sync();
+    const int n = cl_size();
+    double ra = 0.0, rb = 0.0;
+    for (int r = 0; r < n; ++r) {
+      const double* rc = cl_map(&cred[s][0], r);
+      const double x = rc[0], y = rc[1];
+      if (r == 0) { ra = x; rb = y; }
+      else if (is_max) { ra = fmax(ra, x); rb = fmax(rb, y); }
+      else { ra += x; rb += y; }
+    }
+    a = ra;
+    b = rb;
+  }
+  (void)sm;
+}
+
+// any() over the CTA (and the cluster when CL).
+template <int NT, bool CL, class Smem>
+__device__ __forceinline__ bool cluster_any(bool v, Smem& sm) {
+  const bool blk = __syncthreads_or(v);
+  if constexpr (!CL) {
+    return blk;
+  } else {
+    if (threadIdx.x == 0) sm.cflag[0] = blk ? 1 : 0;
+    cl_sync();
+    bool any = false;
+    for (int r = 0; r < cl_size(); ++r) any |= *cl_map(&sm.cflag[0], r) != 0;
+    cl_sync();  // no CTA may leave (and free its shared memory) before all reads are done
+    return any;
+  }
+}
 
 // Per-cell inputs that are touched once per iteration stay in global memory (L2-resident for
 // the active instances), natural layout, already offset to the instance: g[c0 + j] for thread
@@ -195,7 +266,9 @@ struct CellIO {
 };
 
 struct SweepCtl {
-  int t, lane, warp, it;
+  int t, lane, warp, it, gslot;
+  int cbase;      // global index of this CTA's first cell (cluster mode: rank * NT * K)
+  int crank, csz; // cluster rank / size (0 / 1 without clusters)
   bool rl, rr, owns_last;
 };
 
@@ -203,12 +276,17 @@ struct SweepCtl {
 // (-> shared memory). Padding cells carry St = q2 = 0: alpha = 2c/c - 1 = 1 (to 1 ulp), beta = 0.
 template <int K, int NT, bool ANISO, int NP>
 __device__ __forceinline__ void maps_phase(const SweepConsts& sc, SweepSmem<K, NT>& sm, const CellIO& io, int p0,
-                                           int t, double (&al)[NP][K], double (&bp)[NP][K], double (&bm)[NP][K]) {
+                                           const SweepCtl& w, double (&al)[NP][K], double (&bp)[NP][K],
+                                           double (&bm)[NP][K]) {
+  const int t = w.t;
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const double stj = sm.st[j * NT + t], qj = sm.q2[j * NT + t];
     double a3base = 0.0;
-    if constexpr (ANISO) a3base = (t * K + j < sc.n_cells) ? io.ss1[t * K + j] * io.jc[t * K + j] : 0.0;
+    if constexpr (ANISO) {
+      const int i = w.cbase + t * K + j;
+      a3base = (i < sc.n_cells) ? io.ss1[i] * io.jc[i] : 0.0;
+    }
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       const double c = sc.c[p0 + q];
@@ -242,10 +320,11 @@ __device__ __forceinline__ void maps_phase(const SweepConsts& sc, SweepSmem<K, N
 
 // Phase B: one warp per (pair, direction) scans the NT chunk maps of the CTA: each lane composes
 // E = NT/32 consecutive chunks serially, a 5-step shuffle scan joins the lanes, and every chunk
-// gets the exclusive map that carries the boundary inflow to its first edge. Forward = prefix
-// (left to right), backward = suffix (right to left).
-template <int K, int NT, int NP>
-__device__ __forceinline__ void scan_phase(SweepSmem<K, NT>& sm, int lane, int warp) {
+// gets the exclusive map that carries the CTA's inflow to its first edge. Forward = prefix (left
+// to right), backward = suffix (right to left). In cluster mode the CTA totals are also
+// published (ctot) for the other CTAs of the cluster.
+template <int K, int NT, int NP, bool CL>
+__device__ __forceinline__ void scan_phase(SweepSmem<K, NT>& sm, int lane, int warp, int gslot) {
   constexpr int NW = NT / 32, E = NT / 32;
   for (int s = warp; s < 2 * NP; s += NW) {
     const int q = s >> 1;
@@ -278,6 +357,10 @@ __device__ __forceinline__ void scan_phase(SweepSmem<K, NT>& sm, int lane, int w
     if (lane == 31) {
       sm.total[q][fwd ? 0 : 2] = A;
       sm.total[q][fwd ? 1 : 3] = B;
+      if constexpr (CL) {
+        sm.ctot[gslot][q][fwd ? 0 : 2] = A;
+        sm.ctot[gslot][q][fwd ? 1 : 3] = B;
+      }
     }
     double* XA = sm.xmap[q][fwd ? 0 : 2];
     double* XB = sm.xmap[q][fwd ? 1 : 3];
@@ -293,9 +376,10 @@ __device__ __forceinline__ void scan_phase(SweepSmem<K, NT>& sm, int lane, int w
   }
 }
 
-// Phase C: boundary inflows (SURVEY §9 #2 ordering), the inflow of this thread's chunk, and the
+// Phase C: boundary inflows (SURVEY §9 #2 ordering), the inflow of this CTA (cluster mode:
+// composed from the other CTAs' totals read through DSMEM) and of this thread's chunk, then the
 // replay that accumulates the edge currents J_e += w mu (psi+ - psi-).
-template <int K, int NT, int NP>
+template <int K, int NT, int NP, bool CL>
 __device__ __forceinline__ void replay_phase(const SweepConsts& sc, SweepSmem<K, NT>& sm, int p0, const SweepCtl& w,
                                              const double (&al)[NP][K], const double (&bp)[NP][K],
                                              const double (&bm)[NP][K], double (&Jl)[K], double& Jend) {
@@ -304,9 +388,39 @@ __device__ __forceinline__ void replay_phase(const SweepConsts& sc, SweepSmem<K,
   for (int q = 0; q < NP; ++q) {
     const int p = p0 + q;
     const double wm = sc.wmu[p];
+    // whole-domain totals (needed for reflective faces) and this CTA's entry maps
+    double TAf, TBf, TAb, TBb;           // whole domain
+    double EfA = 1.0, EfB = 0.0;         // composition of CTAs left of this one (forward)
+    double EbA = 1.0, EbB = 0.0;         // composition of CTAs right of this one (backward)
+    if constexpr (CL) {
+      double fa = 1.0, fb = 0.0;
+      for (int r = 0; r < w.csz; ++r) {  // forward: ranks ascending
+        const double* T = cl_map(&sm.ctot[w.gslot][q][0], r);
+        if (r == w.crank) { EfA = fa; EfB = fb; }
+        const double a = T[0], b = T[1];
+        fb = fma(a, fb, b);
+        fa *= a;
+      }
+      TAf = fa;
+      TBf = fb;
+      double ba = 1.0, bb = 0.0;
+      for (int r = w.csz - 1; r >= 0; --r) {  // backward: ranks descending
+        const double* T = cl_map(&sm.ctot[w.gslot][q][0], r);
+        if (r == w.crank) { EbA = ba; EbB = bb; }
+        const double a = T[2], b = T[3];
+        bb = fma(a, bb, b);
+        ba *= a;
+      }
+      TAb = ba;
+      TBb = bb;
+    } else {
+      TAf = sm.total[q][0];
+      TBf = sm.total[q][1];
+      TAb = sm.total[q][2];
+      TBb = sm.total[q][3];
+    }
     double psi_right_in = 0.0, psi_left_in = 0.0;
     if (w.rr || w.rl) {
-      const double TAf = sm.total[q][0], TBf = sm.total[q][1], TAb = sm.total[q][2], TBb = sm.total[q][3];
       if (w.rr && !w.rl) {
         psi_right_in = TBf;  // mu>0 outflow at x=L with vacuum left
       } else {
@@ -315,9 +429,11 @@ __device__ __forceinline__ void replay_phase(const SweepConsts& sc, SweepSmem<K,
         if (w.rr && w.rl && t == 0) sm.lag[(w.it + 1) & 1][p] = fma(TAf, psi_left_in, TBf);
       }
     }
+    const double cta_left = fma(EfA, psi_left_in, EfB);
+    const double cta_right = fma(EbA, psi_right_in, EbB);
     const int pt = SweepSmem<K, NT>::spos(t);
-    double psi = fma(sm.xmap[q][0][pt], psi_left_in, sm.xmap[q][1][pt]);
-    double psib = fma(sm.xmap[q][2][pt], psi_right_in, sm.xmap[q][3][pt]);
+    double psi = fma(sm.xmap[q][0][pt], cta_left, sm.xmap[q][1][pt]);
+    double psib = fma(sm.xmap[q][2][pt], cta_right, sm.xmap[q][3][pt]);
     const double psib_in = psib;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
@@ -330,34 +446,40 @@ __device__ __forceinline__ void replay_phase(const SweepConsts& sc, SweepSmem<K,
   }
 }
 
-template <int K, int NT, bool ANISO, int NP>
+template <int K, int NT, bool ANISO, int NP, bool CL>
 __device__ __forceinline__ void sweep_pair_group(const SweepConsts& sc, SweepSmem<K, NT>& sm, const CellIO& io,
-                                                 int p0, const SweepCtl& w, double (&Jl)[K], double& Jend) {
+                                                 int p0, SweepCtl& w, double (&Jl)[K], double& Jend) {
   double al[NP][K], bp[NP][K], bm[NP][K];
-  maps_phase<K, NT, ANISO, NP>(sc, sm, io, p0, w.t, al, bp, bm);
+  maps_phase<K, NT, ANISO, NP>(sc, sm, io, p0, w, al, bp, bm);
   __syncthreads();
-  scan_phase<K, NT, NP>(sm, w.lane, w.warp);
-  __syncthreads();
-  replay_phase<K, NT, NP>(sc, sm, p0, w, al, bp, bm, Jl, Jend);
+  scan_phase<K, NT, NP, CL>(sm, w.lane, w.warp, w.gslot);
+  if constexpr (CL) cl_sync();
+  else __syncthreads();
+  replay_phase<K, NT, NP, CL>(sc, sm, p0, w, al, bp, bm, Jl, Jend);
+  w.gslot ^= 1;
 }
 
-
-// One CTA solves one within-group fixed-source problem by source iteration.
-// On entry sm.st (>0; 0 on padding) and sm.phi (initial flux; 0 on padding) hold the own cells;
-// io.ss0 / io.src (0 on padding), io.ss1 and io.jc (initial cell current; ANISO) are the
-// thread-ordered global arrays. On exit sm.phi holds the final flux and io.jc the cell-average
-// current of the last sweep (written when ANISO || CUR). Returns sweeps performed;
-// *converged is uniform in the CTA.
-template <int K, int NT, bool ANISO, bool CUR, int NP = (K <= 8 ? 2 : 1)>
+// One CTA (or, with CL, one thread-block cluster) solves one within-group fixed-source problem
+// by source iteration. Thread t of cluster rank r owns the K cells starting at
+// global cell r*NT*K + t*K. On entry sm.st (>0; 0 on padding) and sm.phi (initial flux; 0 on
+// padding) hold the own cells; io.ss0 / io.src, io.ss1 and io.jc (initial cell current; ANISO)
+// are the natural-layout global arrays of the instance. On exit sm.phi holds the final flux and
+// io.jc the cell-average current of the last sweep (written when ANISO || CUR). Returns sweeps
+// performed; *converged is uniform across the CTA / cluster.
+template <int K, int NT, bool ANISO, bool CUR, bool CL = false, int NP = (K <= 8 ? 2 : 1)>
 __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem<K, NT>& sm, const CellIO& io,
                         bool* converged) {
   const int t = threadIdx.x;
-  const int c0 = t * K;
   const int Nc = sc.n_cells, P = sc.n_pairs;
   SweepCtl w;
   w.t = t;
   w.lane = t & 31;
   w.warp = t >> 5;
+  w.crank = CL ? cl_rank() : 0;
+  w.csz = CL ? cl_size() : 1;
+  w.cbase = w.crank * NT * K;
+  w.gslot = 0;
+  const int c0 = w.cbase + t * K;
   w.owns_last = (c0 <= Nc - 1) && (Nc - 1 < c0 + K);
   w.rl = cfg.bc_left == 1;
   w.rr = cfg.bc_right == 1;
@@ -367,7 +489,8 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
     sm.lag[0][t] = 0.0;
     sm.lag[1][t] = 0.0;
   }
-  __syncthreads();
+  if constexpr (CL) cl_sync();
+  else __syncthreads();
 
   int it = 0;
   bool conv = false;
@@ -385,14 +508,19 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
     double Jend = 0.0;
     int p = 0;
     if constexpr (NP == 2) {
-      for (; p + 1 < P; p += 2) sweep_pair_group<K, NT, ANISO, 2>(sc, sm, io, p, w, Jl, Jend);
+      for (; p + 1 < P; p += 2) sweep_pair_group<K, NT, ANISO, 2, CL>(sc, sm, io, p, w, Jl, Jend);
     }
-    for (; p < P; ++p) sweep_pair_group<K, NT, ANISO, 1>(sc, sm, io, p, w, Jl, Jend);
+    for (; p < P; ++p) sweep_pair_group<K, NT, ANISO, 1, CL>(sc, sm, io, p, w, Jl, Jend);
     // edge-current exchange: J at the right edge of own last cell = next thread's first edge
+    // (cluster mode: the last thread of a CTA reads the next CTA's first edge through DSMEM)
     sm.jfirst[t] = Jl[0];
     if (w.owns_last) sm.jfirst[NT] = Jend;
-    __syncthreads();
-    const double Jnext = sm.jfirst[t + 1 < NT ? t + 1 : NT];
+    if constexpr (CL) cl_sync();
+    else __syncthreads();
+    double Jnext;
+    if (t + 1 < NT) Jnext = sm.jfirst[t + 1];
+    else if (CL && w.crank + 1 < w.csz) Jnext = *cl_map(&sm.jfirst[0], w.crank + 1);
+    else Jnext = sm.jfirst[NT];
     const double Jlastv = sm.jfirst[NT];
     double num = 0.0, den = 0.0;
 #pragma unroll
@@ -414,8 +542,7 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
         sm.phi[j * NT + t] = pn;
       }
     }
-    if (cfg.norm == 0) block_max2<NT>(num, den, sm.red, rphase++);
-    else block_sum2<NT>(num, den, sm.red, rphase++);
+    reduce2<NT, CL>(num, den, cfg.norm == 0, sm.red, sm.cred, rphase++, sm);
     const double rel = rel_change(num, den, cfg.norm);
     if (!(rel == rel)) break;  // NaN: stop, reported non-converged
     if (rel < cfg.tol) {
@@ -423,6 +550,7 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
       break;
     }
   }
+  if constexpr (CL) cl_sync();  // keep shared memory alive until every remote read is done
   *converged = conv;
   return it;
 }
