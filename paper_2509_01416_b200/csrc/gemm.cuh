@@ -38,7 +38,7 @@ struct GemmArgs {
 
 constexpr int GBM = 64, GBN = 64, GBK = 16, GTHREADS = 256;
 
-__global__ void __launch_bounds__(GTHREADS) gemm_f32_kernel(const GemmArgs a) {
+static __global__ void __launch_bounds__(GTHREADS) gemm_f32_kernel(const GemmArgs a) {
   __shared__ float As[GBK][GBM + 4];
   __shared__ float Bs[GBK][GBN + 4];
   const int b = blockIdx.z;
@@ -94,7 +94,10 @@ __global__ void __launch_bounds__(GTHREADS) gemm_f32_kernel(const GemmArgs a) {
   }
 }
 
-inline cudaError_t gemm_f32(const GemmArgs& a, cudaStream_t s) {
+// Tensor-core (tcgen05, 3xTF32) engine, gemm_tc.cu. mfold > 0 folds the batch into M.
+cudaError_t gemm_tc(const GemmArgs& g, cudaStream_t st, int64_t mfold = 0);
+
+static inline cudaError_t gemm_f32(const GemmArgs& a, cudaStream_t s) {
   if (a.M <= 0 || a.N <= 0 || a.batch <= 0) return cudaSuccess;
   dim3 grid((a.M + GBM - 1) / GBM, (a.N + GBN - 1) / GBN, a.batch);
   gemm_f32_kernel<<<grid, GTHREADS, 0, s>>>(a);

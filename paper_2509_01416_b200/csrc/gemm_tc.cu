@@ -1,0 +1,356 @@
+// gemm_tc.cu — tcgen05 (5th-gen tensor core) GEMM for the neural-operator contractions, sm_100a.
+//
+//   C(b, m, n) = act( alpha * sum_k A(b, m, k) B(b, n, k) + beta * C(b, m, n) + bias[n] )
+//
+// fp32 operands, fp32-class accuracy through the 3xTF32 split: every operand x = hi + lo with
+// hi = x rounded to TF32 and lo = x - hi (exact in fp32), and D = A_hi B_hi + A_hi B_lo + A_lo B_hi
+// accumulated in TMEM by tcgen05.mma.kind::tf32 (plain TF32 would miss the 1e-5 operator
+// tolerance by two orders of magnitude). One CTA = 128 threads = one 128 x NTILE output tile:
+//   * all threads stage a 128 x 32 A chunk and an NTILE x 32 B chunk from global memory (generic
+//     strides, so the FNO's per-sample / transposed operands need no copies), split hi/lo and store
+//     them in the UMMA no-swizzle K-major core-matrix layout (8 rows x 16 B per core matrix);
+//   * one elected thread issues 4 k-steps x 3 tcgen05.mma (M=128, N=NTILE, K=8) per chunk and
+//     commits them to the chunk buffer's mbarrier; staging of chunk c+1 overlaps the MMAs of c
+//     (double-buffered shared memory);
+//   * the epilogue reads the fp32 accumulator with tcgen05.ld (each warp its 32 TMEM lanes) and
+//     applies alpha / beta / bias / activation, writing fp32 or fp64.
+#include <cstdint>
+#include <cstdio>
+
+#include "gemm.cuh"
+
+namespace snop_ops {
+
+namespace tc {
+
+constexpr int TM = 128;  // rows per tile (cta_group::1 M = 128: TMEM lane i = row i)
+constexpr int KC = 32;   // K elements per staged chunk (4 MMA k-steps of 8)
+constexpr int THREADS = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// K-major, no-swizzle core-matrix layout: element (r, k) of a [rows][KC] fp32 tile.
+// Core matrix = 8 rows x 4 fp32 (16 B per row, 128 B contiguous); core matrices adjacent in K
+// are LBO = 128 B apart, 8-row groups are SBO = (KC/4) * 128 B apart.
+__device__ __forceinline__ int core_off(int r, int k) {
+  return ((r >> 3) * (KC / 4) + (k >> 2)) * 32 + (r & 7) * 4 + (k & 3);  // in floats
+}
+constexpr uint32_t LBO_BYTES = 128;
+constexpr uint32_t SBO_BYTES = (KC / 4) * 128;
+
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  // base_offset = 0, lbo_mode = 0, layout_type = 0 (SWIZZLE_NONE)
+  return d;
+}
+
+// Instruction descriptor, kind::tf32: D fp32, A/B TF32, both K-major, M = 128, N = n.
+__host__ __device__ constexpr uint32_t make_idesc(int n) {
+  return (1u << 4)                           // c_format = F32
+         | (2u << 7)                         // a_format = TF32
+         | (2u << 10)                        // b_format = TF32
+         | ((uint32_t)(n >> 3) << 17)        // N >> 3
+         | ((uint32_t)(TM >> 4) << 24);      // M >> 4
+}
+
+__device__ __forceinline__ float tf32_hi(float x) {
+  uint32_t u = __float_as_uint(x);
+  u = (u + 0x1000u) & 0xFFFFE000u;  // round to nearest (ties away) at the TF32 mantissa width
+  return __uint_as_float(u);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int N>
+struct Smem {
+  float a_hi[2][TM * KC];
+  float a_lo[2][TM * KC];
+  float b_hi[2][N * KC];
+  float b_lo[2][N * KC];
+  uint64_t bar[2];     // chunk buffers: MMAs reading the buffer have completed
+  uint64_t accbar[2];  // split mode: all MMAs of the segment accumulating into TMEM slot s are done
+  uint32_t tmem_base;
+};
+
+// Long-K contractions (K > SPLIT_K: DeepONet branch K = 2000, FNO forward DFT K = 1024) use split
+// accumulation: every KC = 32-wide chunk accumulates in one of two TMEM accumulators, which is
+// drained into fp32 registers while the tensor core works on the next chunk. This bounds the
+// accumulation length inside the tensor core (its fp32 accumulation rounding grows with K), and
+// these chunks also add the lo*lo product (4xTF32), so long-K results match fp32 FFMA accuracy.
+constexpr int DR = 1;
+constexpr int SPLIT_K = 4 * KC;
+
+template <int N, bool SPLIT>
+__global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const GemmArgs g, int64_t mfold, int64_t sab_fold) {
+  extern __shared__ __align__(1024) unsigned char raw[];
+  auto& s = *reinterpret_cast<Smem<N>*>(raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int b = blockIdx.z;
+  const int64_t m0 = (int64_t)blockIdx.x * TM;
+  const int n0 = blockIdx.y * N;
+  constexpr uint32_t NACC = SPLIT ? 2 : 1;
+  constexpr uint32_t TCOLS = (N * NACC) <= 32 ? 32 : (N * NACC) <= 64 ? 64 : (N * NACC) <= 128 ? 128 : 256;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s.tmem_base)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(&s.bar[0], 1);
+    mbar_init(&s.bar[1], 1);
+    mbar_init(&s.accbar[0], 1);
+    mbar_init(&s.accbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s.tmem_base;
+  const uint32_t tlane = tmem + ((uint32_t)(warp * 32) << 16);  // this warp's TMEM lanes
+
+  const float* A = g.A + (int64_t)b * g.sab;
+  const float* B = g.B + (int64_t)b * g.sbb;
+  const bool a_kfast = g.sak == 1, b_kfast = g.sbk == 1;
+  const int nchunks = (g.K + KC - 1) / KC;
+  uint32_t phase[2] = {0u, 0u}, aphase[2] = {0u, 0u};
+  constexpr uint32_t idesc = make_idesc(N);
+  float sum[SPLIT ? N : 1];
+  if constexpr (SPLIT) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) sum[j] = 0.f;
+  }
+  // drain TMEM accumulator slot `slot` (segment finished) into the register sums
+  auto drain = [&](int slot) {
+    mbar_wait(&s.accbar[slot], aphase[slot]);
+    aphase[slot] ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+    for (int c0 = 0; c0 < N; c0 += 16) {
+      uint32_t v[16];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(tlane + (uint32_t)(slot * N + c0)));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if constexpr (SPLIT) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sum[c0 + j] += __uint_as_float(v[j]);
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  };
+
+  for (int c = 0; c < nchunks; ++c) {
+    const int buf = c & 1;
+    if (c >= 2) {  // buffer reuse: wait for the MMAs issued on it two chunks ago
+      mbar_wait(&s.bar[buf], phase[buf]);
+      phase[buf] ^= 1u;
+    }
+    const int k0 = c * KC;
+    // stage A (128 x KC) and B (N x KC), split into TF32 hi/lo, core-matrix layout
+#pragma unroll 4
+    for (int e = tid; e < TM * KC; e += THREADS) {
+      const int r = a_kfast ? e / KC : e % TM, kk = a_kfast ? e % KC : e / TM;
+      const int64_t gm = m0 + r;
+      const int gk = k0 + kk;
+      float v = 0.f;
+      if (gm < g.M && gk < g.K) {
+        const int64_t row = mfold > 0 ? (gm / mfold) * sab_fold + (gm % mfold) * g.sam : gm * g.sam;
+        v = A[row + (int64_t)gk * g.sak];
+      }
+      const float hi = tf32_hi(v);
+      const int o = core_off(r, kk);
+      s.a_hi[buf][o] = hi;
+      s.a_lo[buf][o] = v - hi;
+    }
+#pragma unroll 4
+    for (int e = tid; e < N * KC; e += THREADS) {
+      const int r = b_kfast ? e / KC : e % N, kk = b_kfast ? e % KC : e / N;
+      const int gn = n0 + r, gk = k0 + kk;
+      const float v = (gn < g.N && gk < g.K) ? B[(int64_t)gn * g.sbn + (int64_t)gk * g.sbk] : 0.f;
+      const float hi = tf32_hi(v);
+      const int o = core_off(r, kk);
+      s.b_hi[buf][o] = hi;
+      s.b_lo[buf][o] = v - hi;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> async proxy
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int seg = SPLIT ? c / DR : 0;
+    const int slot = SPLIT ? (seg & 1) : 0;
+    const bool seg_start = SPLIT ? (c % DR == 0) : (c == 0);
+    const bool seg_end = SPLIT && (c % DR == DR - 1 || c == nchunks - 1);
+    if (tid == 0) {
+      const uint32_t ah = smem_u32(s.a_hi[buf]), al = smem_u32(s.a_lo[buf]);
+      const uint32_t bh = smem_u32(s.b_hi[buf]), bl = smem_u32(s.b_lo[buf]);
+      const uint32_t td = tmem + (uint32_t)(slot * N);
+#pragma unroll
+      for (int ks = 0; ks < KC / 8; ++ks) {
+        const uint32_t off = ks * 2 * 128;  // two core matrices along K per k-step
+        const uint64_t dah = make_sdesc(ah + off, LBO_BYTES, SBO_BYTES);
+        const uint64_t dal = make_sdesc(al + off, LBO_BYTES, SBO_BYTES);
+        const uint64_t dbh = make_sdesc(bh + off, LBO_BYTES, SBO_BYTES);
+        const uint64_t dbl = make_sdesc(bl + off, LBO_BYTES, SBO_BYTES);
+        const uint32_t acc0 = (!seg_start || ks > 0) ? 1u : 0u;
+        if (SPLIT) mma_tf32(td, dal, dbl, idesc, acc0);  // 4xTF32 on the long-K path
+        const uint32_t acc1 = SPLIT ? 1u : acc0;
+        mma_tf32(td, dal, dbh, idesc, acc1);  // small terms first
+        mma_tf32(td, dah, dbl, idesc, 1u);
+        mma_tf32(td, dah, dbh, idesc, 1u);
+      }
+      mma_commit(&s.bar[buf]);
+      if (seg_end) mma_commit(&s.accbar[slot]);
+    }
+    __syncwarp();
+    // split mode: once the next segment is queued on the tensor core, drain the previous one
+    if constexpr (SPLIT) {
+      if (seg_start && seg > 0) drain((seg - 1) & 1);
+    }
+  }
+  if constexpr (SPLIT) {
+    drain(((nchunks - 1) / DR) & 1);
+  } else {
+    const int last = (nchunks - 1) & 1;
+    mbar_wait(&s.bar[last], phase[last]);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
+
+  // epilogue: warp w owns TMEM lanes (rows) 32w..32w+31
+  const int64_t gm = m0 + warp * 32 + lane;
+  const int64_t row = mfold > 0 ? (gm / mfold) * g.scb + (gm % mfold) * g.scm : (int64_t)b * g.scb + gm * g.scm;
+#pragma unroll
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    float x16[16];
+    if constexpr (SPLIT) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) x16[j] = sum[c0 + j];
+    } else {
+      uint32_t v[16];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(tlane + (uint32_t)c0));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 16; ++j) x16[j] = __uint_as_float(v[j]);
+    }
+    if (gm < g.M) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int gn = n0 + c0 + j;
+        if (gn >= g.N) continue;
+        const int64_t off = row + (int64_t)gn * g.scn;
+        float x = g.alpha * x16[j];
+        if (g.beta != 0.f) x += g.beta * g.C[off];
+        if (g.bias) x += g.bias[gn];
+        x = act_f(x, g.act);
+        if (g.Cd) g.Cd[off] = (double)x;
+        else g.C[off] = x;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+}
+
+template <int N, bool SPLIT>
+cudaError_t launch(const GemmArgs& g, int64_t mfold, int64_t sab_fold, cudaStream_t st) {
+  const size_t smem = sizeof(Smem<N>);
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(gemm_tc_kernel<N, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t mt = (g.M + TM - 1) / TM;
+  dim3 grid((unsigned)mt, (unsigned)((g.N + N - 1) / N), (unsigned)(mfold > 0 ? 1 : g.batch));
+  gemm_tc_kernel<N, SPLIT><<<grid, THREADS, smem, st>>>(g, mfold, sab_fold);
+  return cudaGetLastError();
+}
+
+}  // namespace tc
+
+// Tensor-core GEMM. mfold > 0 folds the batch into M: row r of the GEMM is row (r % mfold) of
+// batch (r / mfold), i.e. A row offset (r / mfold) * sab + (r % mfold) * sam, C row offset
+// (r / mfold) * scb + (r % mfold) * scm (used for the FNO forward DFT over B x C rows).
+cudaError_t gemm_tc(const GemmArgs& g, cudaStream_t st, int64_t mfold) {
+  if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
+  const int64_t sab_fold = g.sab;
+  const bool split = g.K > tc::SPLIT_K;  // long K: chunk-wise accumulation (<= 64-wide tiles)
+  if (g.N <= 32) return split ? tc::launch<32, true>(g, mfold, sab_fold, st) : tc::launch<32, false>(g, mfold, sab_fold, st);
+  if (g.N <= 64 || split) return split ? tc::launch<64, true>(g, mfold, sab_fold, st) : tc::launch<64, false>(g, mfold, sab_fold, st);
+  return tc::launch<128, false>(g, mfold, sab_fold, st);
+}
+
+}  // namespace snop_ops
+
+// Test hook (C linkage, not part of the public C-ABI): runs one GEMM on device pointers with both
+// engines so tests can pin the tensor-core path against the FFMA path.
+extern "C" int snop_internal_gemm_test(int engine, int M, int N, int K, int batch, const float* A, long long sam,
+                                       long long sak, long long sab, const float* B, long long sbn, long long sbk,
+                                       long long sbb, float* C, long long scm, long long scn, long long scb,
+                                       const float* bias, float alpha, float beta, int act, long long mfold) {
+  snop_ops::GemmArgs g{};
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.batch = batch;
+  g.A = A;
+  g.sam = sam;
+  g.sak = sak;
+  g.sab = sab;
+  g.B = B;
+  g.sbn = sbn;
+  g.sbk = sbk;
+  g.sbb = sbb;
+  g.C = C;
+  g.scm = scm;
+  g.scn = scn;
+  g.scb = scb;
+  g.bias = bias;
+  g.alpha = alpha;
+  g.beta = beta;
+  g.act = act;
+  cudaError_t e = engine == 1 ? snop_ops::gemm_tc(g, 0, mfold) : snop_ops::gemm_f32(g, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  return (int)e;
+}

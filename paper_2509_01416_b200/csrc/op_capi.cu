@@ -5,6 +5,7 @@
 // engine); the elementwise parts (lift, spectral mixing, recast, row projection, fixed-point
 // bookkeeping) are small fused kernels here. Neural operators compute in fp32; the API is fp64.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -243,8 +244,20 @@ unsigned grid_for(const Ctx& c, size_t n, int threads = 256) {
   return (unsigned)(blocks ? blocks : 1);
 }
 
-snop_status gemm(Ctx& ctx, const GemmArgs& a) {
+// Dense contractions run on the tcgen05 3xTF32 engine (gemm_tc.cu); SNOP_GEMM=ffma selects the
+// FFMA engine (cross-check / fallback for debugging only).
+bool use_tc() {
+  static const bool tc = [] {
+    const char* e = std::getenv("SNOP_GEMM");
+    return !(e && std::string(e) == "ffma");
+  }();
+  return tc;
+}
+
+snop_status gemm(Ctx& ctx, const GemmArgs& a, int64_t mfold = 0) {
   ctx.launches++;
+  if (use_tc()) return cuda_status("gemm_tc", gemm_tc(a, ctx.stream, mfold));
+  if (mfold > 0) return invalid("batch-folded GEMM requires the tensor-core engine");
   return cuda_status("gemm", gemm_f32(a, ctx.stream));
 }
 
