@@ -14,7 +14,7 @@ from ._types import STATUS_NAMES, SnopGrid, SnopSolverConfig
 from .errors import raise_for_status
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libsnop_cuda.so"
+LIB_PATH = Path(os.environ["SNOP_LIB"]) if os.environ.get("SNOP_LIB") else PKG / "libsnop_cuda.so"
 
 # Every entry point include/snop_cuda.h declares (checked by tests/test_capi_symbols.py).
 EXPORTS = [

@@ -34,7 +34,25 @@ struct GemmArgs {
   const float* bias; // [N] or nullptr
   float alpha, beta; // beta applies to the existing fp32 C
   int act;
+  // optional second K segment: for k >= ksplit, A/B elements come from A2/B2 at k - ksplit
+  // (fuses e.g. the FNO inverse DFT [G | V] x [U | W]^T into one contraction). ksplit = 0: none.
+  int ksplit;
+  const float* A2;
+  int64_t sam2, sak2, sab2;
+  const float* B2;
+  int64_t sbn2, sbk2, sbb2;
 };
+
+__device__ __forceinline__ float gemm_a(const GemmArgs& a, int b, int64_t m, int k) {
+  if (a.ksplit > 0 && k >= a.ksplit)
+    return a.A2[(int64_t)b * a.sab2 + m * a.sam2 + (int64_t)(k - a.ksplit) * a.sak2];
+  return a.A[(int64_t)b * a.sab + m * a.sam + (int64_t)k * a.sak];
+}
+__device__ __forceinline__ float gemm_b(const GemmArgs& a, int b, int64_t n, int k) {
+  if (a.ksplit > 0 && k >= a.ksplit)
+    return a.B2[(int64_t)b * a.sbb2 + n * a.sbn2 + (int64_t)(k - a.ksplit) * a.sbk2];
+  return a.B[(int64_t)b * a.sbb + n * a.sbn + (int64_t)k * a.sbk];
+}
 
 constexpr int GBM = 64, GBN = 64, GBK = 16, GTHREADS = 256;
 
@@ -45,8 +63,6 @@ static __global__ void __launch_bounds__(GTHREADS) gemm_f32_kernel(const GemmArg
   const int m0 = blockIdx.x * GBM, n0 = blockIdx.y * GBN;  // M on x (2^31 limit)
   const int tid = threadIdx.x;
   const int tm = (tid / 16) * 4, tn = (tid % 16) * 4;
-  const float* A = a.A + (int64_t)b * a.sab;
-  const float* B = a.B + (int64_t)b * a.sbb;
   float acc[4][4] = {};
   const bool a_kfast = a.sak == 1, b_kfast = a.sbk == 1;
   for (int k0 = 0; k0 < a.K; k0 += GBK) {
@@ -55,10 +71,10 @@ static __global__ void __launch_bounds__(GTHREADS) gemm_f32_kernel(const GemmArg
       const int e = tid + r * GTHREADS;
       const int mm = a_kfast ? e / GBK : e % GBM, kk = a_kfast ? e % GBK : e / GBM;
       const int gm = m0 + mm, gk = k0 + kk;
-      As[kk][mm] = (gm < a.M && gk < a.K) ? A[gm * a.sam + gk * a.sak] : 0.f;
+      As[kk][mm] = (gm < a.M && gk < a.K) ? gemm_a(a, b, gm, gk) : 0.f;
       const int nn = b_kfast ? e / GBK : e % GBN, kb = b_kfast ? e % GBK : e / GBN;
       const int gn = n0 + nn, gkb = k0 + kb;
-      Bs[kb][nn] = (gn < a.N && gkb < a.K) ? B[gn * a.sbn + gkb * a.sbk] : 0.f;
+      Bs[kb][nn] = (gn < a.N && gkb < a.K) ? gemm_b(a, b, gn, gkb) : 0.f;
     }
     __syncthreads();
 #pragma unroll

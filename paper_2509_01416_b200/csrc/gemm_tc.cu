@@ -101,7 +101,7 @@ struct Smem {
   float b_hi[2][N * KC];
   float b_lo[2][N * KC];
   uint64_t bar[2];     // chunk buffers: MMAs reading the buffer have completed
-  uint64_t accbar[2];  // split mode: all MMAs of the segment accumulating into TMEM slot s are done
+  uint64_t accbar[2];  // split mode: all MMAs of the chunk accumulating into TMEM slot s are done
   uint32_t tmem_base;
 };
 
@@ -113,8 +113,73 @@ struct Smem {
 constexpr int DR = 1;
 constexpr int SPLIT_K = 4 * KC;
 
+// One operand's staging for a chunk: ROWS x KC fp32 = ROWS * KC / 4 float4 groups; thread tid
+// handles groups tid + i * THREADS, group -> (row = g % ROWS, kq = g / ROWS): consecutive lanes
+// take consecutive rows, so the float4 stores into the core-matrix layout are bank-conflict free
+// (8 lanes fill one 128 B core matrix) and MN-contiguous operands load coalesced.
+template <int ROWS>
+struct Stage {
+  static constexpr int G = ROWS * KC / 4 / THREADS;
+  float4 v[G];
+};
+
+template <int ROWS, bool IS_A>
+__device__ __forceinline__ void load_chunk(Stage<ROWS>& st, const GemmArgs& g, int b, int64_t row0, int k0,
+                                           int64_t mfold, int tid) {
+  const int64_t nrows = IS_A ? (int64_t)g.M : (int64_t)g.N;
+#pragma unroll
+  for (int i = 0; i < Stage<ROWS>::G; ++i) {
+    const int grp = tid + i * THREADS;
+    const int r = grp % ROWS, kq = grp / ROWS;
+    const int64_t gr = row0 + r;
+    const int kg = k0 + kq * 4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (gr < nrows && kg < g.K) {
+      const bool seg2 = g.ksplit > 0 && kg >= g.ksplit;
+      const int kk = seg2 ? kg - g.ksplit : kg;
+      const float* base;
+      int64_t sk;
+      if (IS_A) {
+        const int64_t sam = seg2 ? g.sam2 : g.sam, sab = seg2 ? g.sab2 : g.sab;
+        sk = seg2 ? g.sak2 : g.sak;
+        const int64_t roff = mfold > 0 ? (gr / mfold) * sab + (gr % mfold) * sam : (int64_t)b * sab + gr * sam;
+        base = (seg2 ? g.A2 : g.A) + roff;
+      } else {
+        const int64_t sbn = seg2 ? g.sbn2 : g.sbn, sbb = seg2 ? g.sbb2 : g.sbb;
+        sk = seg2 ? g.sbk2 : g.sbk;
+        base = (seg2 ? g.B2 : g.B) + (int64_t)b * sbb + gr * sbn;
+      }
+      const float* p = base + (int64_t)kk * sk;
+      if (sk == 1 && kg + 3 < g.K && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+        v = __ldg(reinterpret_cast<const float4*>(p));
+      } else {
+        v.x = __ldg(p);
+        if (kg + 1 < g.K) v.y = __ldg(p + sk);
+        if (kg + 2 < g.K) v.z = __ldg(p + 2 * sk);
+        if (kg + 3 < g.K) v.w = __ldg(p + 3 * sk);
+      }
+    }
+    st.v[i] = v;
+  }
+}
+
+template <int ROWS>
+__device__ __forceinline__ void store_chunk(const Stage<ROWS>& st, float* hi, float* lo, int tid) {
+#pragma unroll
+  for (int i = 0; i < Stage<ROWS>::G; ++i) {
+    const int grp = tid + i * THREADS;
+    const int r = grp % ROWS, kq = grp / ROWS;
+    const float4 v = st.v[i];
+    const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+    const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+    const int o = core_off(r, kq * 4);
+    *reinterpret_cast<float4*>(hi + o) = h;
+    *reinterpret_cast<float4*>(lo + o) = l;
+  }
+}
+
 template <int N, bool SPLIT>
-__global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const GemmArgs g, int64_t mfold, int64_t sab_fold) {
+__global__ void __launch_bounds__(THREADS, 2) gemm_tc_kernel(const GemmArgs g, int64_t mfold) {
   extern __shared__ __align__(1024) unsigned char raw[];
   auto& s = *reinterpret_cast<Smem<N>*>(raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -142,9 +207,6 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const GemmArgs g, i
   const uint32_t tmem = s.tmem_base;
   const uint32_t tlane = tmem + ((uint32_t)(warp * 32) << 16);  // this warp's TMEM lanes
 
-  const float* A = g.A + (int64_t)b * g.sab;
-  const float* B = g.B + (int64_t)b * g.sbb;
-  const bool a_kfast = g.sak == 1, b_kfast = g.sbk == 1;
   const int nchunks = (g.K + KC - 1) / KC;
   uint32_t phase[2] = {0u, 0u}, aphase[2] = {0u, 0u};
   constexpr uint32_t idesc = make_idesc(N);
@@ -153,7 +215,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const GemmArgs g, i
 #pragma unroll
     for (int j = 0; j < N; ++j) sum[j] = 0.f;
   }
-  // drain TMEM accumulator slot `slot` (segment finished) into the register sums
+  // drain TMEM accumulator slot `slot` (chunk finished) into the register sums
   auto drain = [&](int slot) {
     mbar_wait(&s.accbar[slot], aphase[slot]);
     aphase[slot] ^= 1u;
@@ -175,47 +237,27 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const GemmArgs g, i
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   };
 
+  Stage<TM> sa;
+  Stage<N> sb;
+  load_chunk<TM, true>(sa, g, b, m0, 0, mfold, tid);
+  load_chunk<N, false>(sb, g, b, n0, 0, 0, tid);
   for (int c = 0; c < nchunks; ++c) {
     const int buf = c & 1;
     if (c >= 2) {  // buffer reuse: wait for the MMAs issued on it two chunks ago
       mbar_wait(&s.bar[buf], phase[buf]);
       phase[buf] ^= 1u;
     }
-    const int k0 = c * KC;
-    // stage A (128 x KC) and B (N x KC), split into TF32 hi/lo, core-matrix layout
-#pragma unroll 4
-    for (int e = tid; e < TM * KC; e += THREADS) {
-      const int r = a_kfast ? e / KC : e % TM, kk = a_kfast ? e % KC : e / TM;
-      const int64_t gm = m0 + r;
-      const int gk = k0 + kk;
-      float v = 0.f;
-      if (gm < g.M && gk < g.K) {
-        const int64_t row = mfold > 0 ? (gm / mfold) * sab_fold + (gm % mfold) * g.sam : gm * g.sam;
-        v = A[row + (int64_t)gk * g.sak];
-      }
-      const float hi = tf32_hi(v);
-      const int o = core_off(r, kk);
-      s.a_hi[buf][o] = hi;
-      s.a_lo[buf][o] = v - hi;
-    }
-#pragma unroll 4
-    for (int e = tid; e < N * KC; e += THREADS) {
-      const int r = b_kfast ? e / KC : e % N, kk = b_kfast ? e % KC : e / N;
-      const int gn = n0 + r, gk = k0 + kk;
-      const float v = (gn < g.N && gk < g.K) ? B[(int64_t)gn * g.sbn + (int64_t)gk * g.sbk] : 0.f;
-      const float hi = tf32_hi(v);
-      const int o = core_off(r, kk);
-      s.b_hi[buf][o] = hi;
-      s.b_lo[buf][o] = v - hi;
+    store_chunk<TM>(sa, s.a_hi[buf], s.a_lo[buf], tid);
+    store_chunk<N>(sb, s.b_hi[buf], s.b_lo[buf], tid);
+    if (c + 1 < nchunks) {  // prefetch the next chunk: global latency overlaps this chunk's MMAs
+      load_chunk<TM, true>(sa, g, b, m0, (c + 1) * KC, mfold, tid);
+      load_chunk<N, false>(sb, g, b, n0, (c + 1) * KC, 0, tid);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> async proxy
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int seg = SPLIT ? c / DR : 0;
-    const int slot = SPLIT ? (seg & 1) : 0;
-    const bool seg_start = SPLIT ? (c % DR == 0) : (c == 0);
-    const bool seg_end = SPLIT && (c % DR == DR - 1 || c == nchunks - 1);
+    const int slot = SPLIT ? (c & 1) : 0;
     if (tid == 0) {
       const uint32_t ah = smem_u32(s.a_hi[buf]), al = smem_u32(s.a_lo[buf]);
       const uint32_t bh = smem_u32(s.b_hi[buf]), bl = smem_u32(s.b_lo[buf]);
@@ -227,24 +269,23 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const GemmArgs g, i
         const uint64_t dal = make_sdesc(al + off, LBO_BYTES, SBO_BYTES);
         const uint64_t dbh = make_sdesc(bh + off, LBO_BYTES, SBO_BYTES);
         const uint64_t dbl = make_sdesc(bl + off, LBO_BYTES, SBO_BYTES);
-        const uint32_t acc0 = (!seg_start || ks > 0) ? 1u : 0u;
-        if (SPLIT) mma_tf32(td, dal, dbl, idesc, acc0);  // 4xTF32 on the long-K path
-        const uint32_t acc1 = SPLIT ? 1u : acc0;
-        mma_tf32(td, dal, dbh, idesc, acc1);  // small terms first
+        const uint32_t first = (SPLIT ? ks == 0 : (c == 0 && ks == 0)) ? 0u : 1u;
+        if (SPLIT) mma_tf32(td, dal, dbl, idesc, first);  // 4xTF32 on the long-K path
+        mma_tf32(td, dal, dbh, idesc, SPLIT ? 1u : first);  // small terms first
         mma_tf32(td, dah, dbl, idesc, 1u);
         mma_tf32(td, dah, dbh, idesc, 1u);
       }
       mma_commit(&s.bar[buf]);
-      if (seg_end) mma_commit(&s.accbar[slot]);
+      if (SPLIT) mma_commit(&s.accbar[slot]);
     }
     __syncwarp();
-    // split mode: once the next segment is queued on the tensor core, drain the previous one
+    // split mode: once chunk c is queued on the tensor core, drain chunk c-1's accumulator
     if constexpr (SPLIT) {
-      if (seg_start && seg > 0) drain((seg - 1) & 1);
+      if (c > 0) drain((c - 1) & 1);
     }
   }
   if constexpr (SPLIT) {
-    drain(((nchunks - 1) / DR) & 1);
+    drain((nchunks - 1) & 1);
   } else {
     const int last = (nchunks - 1) & 1;
     mbar_wait(&s.bar[last], phase[last]);
@@ -292,7 +333,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const GemmArgs g, i
 }
 
 template <int N, bool SPLIT>
-cudaError_t launch(const GemmArgs& g, int64_t mfold, int64_t sab_fold, cudaStream_t st) {
+cudaError_t launch(const GemmArgs& g, int64_t mfold, cudaStream_t st) {
   const size_t smem = sizeof(Smem<N>);
   static bool attr = false;
   if (!attr) {
@@ -303,7 +344,7 @@ cudaError_t launch(const GemmArgs& g, int64_t mfold, int64_t sab_fold, cudaStrea
   }
   const int64_t mt = (g.M + TM - 1) / TM;
   dim3 grid((unsigned)mt, (unsigned)((g.N + N - 1) / N), (unsigned)(mfold > 0 ? 1 : g.batch));
-  gemm_tc_kernel<N, SPLIT><<<grid, THREADS, smem, st>>>(g, mfold, sab_fold);
+  gemm_tc_kernel<N, SPLIT><<<grid, THREADS, smem, st>>>(g, mfold);
   return cudaGetLastError();
 }
 
@@ -314,11 +355,10 @@ cudaError_t launch(const GemmArgs& g, int64_t mfold, int64_t sab_fold, cudaStrea
 // (r / mfold) * scb + (r % mfold) * scm (used for the FNO forward DFT over B x C rows).
 cudaError_t gemm_tc(const GemmArgs& g, cudaStream_t st, int64_t mfold) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
-  const int64_t sab_fold = g.sab;
-  const bool split = g.K > tc::SPLIT_K;  // long K: chunk-wise accumulation (<= 64-wide tiles)
-  if (g.N <= 32) return split ? tc::launch<32, true>(g, mfold, sab_fold, st) : tc::launch<32, false>(g, mfold, sab_fold, st);
-  if (g.N <= 64 || split) return split ? tc::launch<64, true>(g, mfold, sab_fold, st) : tc::launch<64, false>(g, mfold, sab_fold, st);
-  return tc::launch<128, false>(g, mfold, sab_fold, st);
+  if (g.ksplit > 0 && g.ksplit % tc::KC != 0) return cudaErrorInvalidValue;  // segment = whole chunks
+  const bool split = g.K > tc::SPLIT_K;  // long K: chunk-wise drained accumulation
+  if (g.N <= 32) return split ? tc::launch<32, true>(g, mfold, st) : tc::launch<32, false>(g, mfold, st);
+  return split ? tc::launch<64, true>(g, mfold, st) : tc::launch<64, false>(g, mfold, st);
 }
 
 }  // namespace snop_ops
@@ -350,6 +390,7 @@ extern "C" int snop_internal_gemm_test(int engine, int M, int N, int K, int batc
   g.alpha = alpha;
   g.beta = beta;
   g.act = act;
+  g.ksplit = 0;
   cudaError_t e = engine == 1 ? snop_ops::gemm_tc(g, 0, mfold) : snop_ops::gemm_f32(g, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   return (int)e;

@@ -349,31 +349,54 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
   if (!V || !Vn || !Vh || !U) return cuda_status("FNO workspace", cudaErrorMemoryAllocation);
   fno_lift<<<grid_for(ctx, vsz), 256, 0, ctx.stream>>>(B, n, C, in, op.xc, op.lift_W, op.lift_b, V);
   ctx.launches++;
+  const bool tc_fused = use_tc() && (2 * M) % 32 == 0;
   for (int l = 0; l < op.layers; ++l) {
-    // forward truncated DFT per sample: Vh[b][c][m'] = sum_i V[b][i][c] F[m'][i]
+    // forward truncated DFT: Vh[b][c][m'] = sum_i V[b][i][c] F[m'][i]. Tensor-core engine: one
+    // GEMM over all B*C rows (batch folded into M); FFMA engine: batched per sample.
     GemmArgs f{};
     f.M = C; f.N = 2 * M; f.K = n; f.batch = B;
     f.A = V; f.sam = 1; f.sak = C; f.sab = (int64_t)n * C;
     f.B = op.F; f.sbn = n; f.sbk = 1; f.sbb = 0;
     f.C = Vh; f.scm = 2 * M; f.scn = 1; f.scb = (int64_t)C * 2 * M;
     f.alpha = 1.f; f.act = ACT_NONE;
-    SNOP_TRY(gemm(ctx, f));
+    if (use_tc()) {
+      f.M = B * C;
+      f.batch = 1;
+      SNOP_TRY(gemm(ctx, f, C));
+    } else {
+      SNOP_TRY(gemm(ctx, f));
+    }
     // complex channel mixing per retained mode
     fno_mix<<<dim3((B + 3) / 4 < 1024 ? (B + 3) / 4 : 1024, M), 4 * C, 2 * C * C * sizeof(float), ctx.stream>>>(
         B, C, M, Vh, op.Rr[l], op.Ri[l], U);
     ctx.launches++;
-    // inverse truncated DFT per sample: Vn[b][i][o] = sum_m' Ginv[i][m'] U[b][o][m']
-    GemmArgs iv{};
-    iv.M = n; iv.N = C; iv.K = 2 * M; iv.batch = B;
-    iv.A = op.Ginv; iv.sam = 2 * M; iv.sak = 1; iv.sab = 0;
-    iv.B = U; iv.sbn = 2 * M; iv.sbk = 1; iv.sbb = (int64_t)C * 2 * M;
-    iv.C = Vn; iv.scm = C; iv.scn = 1; iv.scb = (int64_t)n * C;
-    iv.alpha = 1.f; iv.act = ACT_NONE;
-    SNOP_TRY(gemm(ctx, iv));
-    // + W path + bias, activation (accumulating epilogue)
-    GemmArgs wp = rowmajor((int)rowsN, C, C, V, C, op.W[l], C, Vn, C, op.b[l], op.act);
-    wp.beta = 1.f;
-    SNOP_TRY(gemm(ctx, wp));
+    if (tc_fused) {
+      // inverse truncated DFT + W path + bias + activation as ONE contraction per sample:
+      // Vn[b][i][o] = act( [Ginv | V_b](i, :) . [U_b | W](o, :) + b[o] ),  K = 2M + C
+      GemmArgs iv{};
+      iv.M = n; iv.N = C; iv.K = 2 * M + C; iv.batch = B;
+      iv.A = op.Ginv; iv.sam = 2 * M; iv.sak = 1; iv.sab = 0;
+      iv.B = U; iv.sbn = 2 * M; iv.sbk = 1; iv.sbb = (int64_t)C * 2 * M;
+      iv.ksplit = 2 * M;
+      iv.A2 = V; iv.sam2 = C; iv.sak2 = 1; iv.sab2 = (int64_t)n * C;
+      iv.B2 = op.W[l]; iv.sbn2 = C; iv.sbk2 = 1; iv.sbb2 = 0;
+      iv.C = Vn; iv.scm = C; iv.scn = 1; iv.scb = (int64_t)n * C;
+      iv.bias = op.b[l]; iv.alpha = 1.f; iv.act = op.act;
+      SNOP_TRY(gemm(ctx, iv));
+    } else {
+      // inverse truncated DFT per sample: Vn[b][i][o] = sum_m' Ginv[i][m'] U[b][o][m']
+      GemmArgs iv{};
+      iv.M = n; iv.N = C; iv.K = 2 * M; iv.batch = B;
+      iv.A = op.Ginv; iv.sam = 2 * M; iv.sak = 1; iv.sab = 0;
+      iv.B = U; iv.sbn = 2 * M; iv.sbk = 1; iv.sbb = (int64_t)C * 2 * M;
+      iv.C = Vn; iv.scm = C; iv.scn = 1; iv.scb = (int64_t)n * C;
+      iv.alpha = 1.f; iv.act = ACT_NONE;
+      SNOP_TRY(gemm(ctx, iv));
+      // + W path + bias, activation (accumulating epilogue)
+      GemmArgs wp = rowmajor((int)rowsN, C, C, V, C, op.W[l], C, Vn, C, op.b[l], op.act);
+      wp.beta = 1.f;
+      SNOP_TRY(gemm(ctx, wp));
+    }
     std::swap(V, Vn);
   }
   // projection 64 -> hidden (act) -> 1, chunked over rows

@@ -109,3 +109,4 @@ snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int 
 }
 
 }  // namespace snop_impl
+

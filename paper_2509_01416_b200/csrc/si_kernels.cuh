@@ -13,9 +13,12 @@ namespace snop_si {
 using namespace snop_dev;
 
 // Register budget: 128 regs/thread (16 resident warps per SM at NT * minBlocks = 512).
+#ifndef SNOP_WARPS_PER_SM
+#define SNOP_WARPS_PER_SM 16
+#endif
 template <int K, int NT>
 constexpr int min_blocks() {
-  return NT <= 128 ? 512 / NT : (NT <= 256 ? 2 : 1);
+  return (SNOP_WARPS_PER_SM * 32) / NT > 0 ? (SNOP_WARPS_PER_SM * 32) / NT : 1;
 }
 
 template <int K, int NT>

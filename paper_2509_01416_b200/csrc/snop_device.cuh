@@ -170,6 +170,7 @@ struct SweepSmem {
   static constexpr int NW = NT / 32;
   double st[K * NT];           // Sigma_t (0 on padding cells)
   double q2[K * NT];           // 2 x isotropic emission: Ss0 phi + S (rebuilt every iteration)
+  double ist[K * NT];          // 1 / Sigma_t (0 on padding), set at solver entry
   double phi[K * NT];          // scalar flux
   // chunk-indexed arrays use spos(): one pad slot per E = NT/32 entries, so the scan warp's
   // lane-strided reads (lane l owns chunks l*E .. l*E+E-1) are bank-conflict free
@@ -264,6 +265,20 @@ struct CellIO {
   const double* __restrict__ ss1;  // P1 moment (ANISO only)
   double* __restrict__ jc;         // cell-average current (ANISO / CUR)
 };
+
+#ifdef SNOP_PHASE_TIMING
+// experiment builds only: per-phase cycle counters (thread 0 and thread 32 of every CTA)
+static __device__ unsigned long long g_phase_cycles[2][8];
+#define SNOP_TSTAMP(var) long long var = clock64()
+#define SNOP_TACC(slot, t0, t1)                                                          \
+  do {                                                                                   \
+    if ((threadIdx.x & 31) == 0 && threadIdx.x < 64)                                     \
+      atomicAdd(&g_phase_cycles[threadIdx.x >> 5][slot], (unsigned long long)((t1) - (t0))); \
+  } while (0)
+#else
+#define SNOP_TSTAMP(var)
+#define SNOP_TACC(slot, t0, t1)
+#endif
 
 struct SweepCtl {
   int t, lane, warp, it, gslot;
@@ -450,12 +465,23 @@ template <int K, int NT, bool ANISO, int NP, bool CL>
 __device__ __forceinline__ void sweep_pair_group(const SweepConsts& sc, SweepSmem<K, NT>& sm, const CellIO& io,
                                                  int p0, SweepCtl& w, double (&Jl)[K], double& Jend) {
   double al[NP][K], bp[NP][K], bm[NP][K];
+  SNOP_TSTAMP(t0);
   maps_phase<K, NT, ANISO, NP>(sc, sm, io, p0, w, al, bp, bm);
+  SNOP_TSTAMP(t1);
   __syncthreads();
+  SNOP_TSTAMP(t2);
   scan_phase<K, NT, NP, CL>(sm, w.lane, w.warp, w.gslot);
+  SNOP_TSTAMP(t3);
   if constexpr (CL) cl_sync();
   else __syncthreads();
+  SNOP_TSTAMP(t4);
   replay_phase<K, NT, NP, CL>(sc, sm, p0, w, al, bp, bm, Jl, Jend);
+  SNOP_TSTAMP(t5);
+  SNOP_TACC(0, t0, t1);
+  SNOP_TACC(1, t1, t2);
+  SNOP_TACC(2, t2, t3);
+  SNOP_TACC(3, t3, t4);
+  SNOP_TACC(4, t4, t5);
   w.gslot ^= 1;
 }
 
@@ -466,7 +492,10 @@ __device__ __forceinline__ void sweep_pair_group(const SweepConsts& sc, SweepSme
 // are the natural-layout global arrays of the instance. On exit sm.phi holds the final flux and
 // io.jc the cell-average current of the last sweep (written when ANISO || CUR). Returns sweeps
 // performed; *converged is uniform across the CTA / cluster.
-template <int K, int NT, bool ANISO, bool CUR, bool CL = false, int NP = (K <= 8 ? 2 : 1)>
+#ifndef SNOP_NP
+#define SNOP_NP 2
+#endif
+template <int K, int NT, bool ANISO, bool CUR, bool CL = false, int NP = SNOP_NP>
 __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem<K, NT>& sm, const CellIO& io,
                         bool* converged) {
   const int t = threadIdx.x;
@@ -489,6 +518,11 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
     sm.lag[0][t] = 0.0;
     sm.lag[1][t] = 0.0;
   }
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const double stj = sm.st[j * NT + t];
+    sm.ist[j * NT + t] = stj > 0.0 ? 1.0 / stj : 0.0;  // iteration-invariant
+  }
   if constexpr (CL) cl_sync();
   else __syncthreads();
 
@@ -506,11 +540,14 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
 #pragma unroll
     for (int j = 0; j < K; ++j) Jl[j] = 0.0;
     double Jend = 0.0;
+    SNOP_TSTAMP(ti0);
     int p = 0;
     if constexpr (NP == 2) {
       for (; p + 1 < P; p += 2) sweep_pair_group<K, NT, ANISO, 2, CL>(sc, sm, io, p, w, Jl, Jend);
     }
     for (; p < P; ++p) sweep_pair_group<K, NT, ANISO, 1, CL>(sc, sm, io, p, w, Jl, Jend);
+    SNOP_TSTAMP(ti1);
+    SNOP_TACC(5, ti0, ti1);
     // edge-current exchange: J at the right edge of own last cell = next thread's first edge
     // (cluster mode: the last thread of a CTA reads the next CTA's first edge through DSMEM)
     sm.jfirst[t] = Jl[0];
@@ -529,7 +566,7 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
         double JR = (j + 1 < K) ? Jl[j + 1] : Jnext;
         if (w.owns_last && j == jlast) JR = Jlastv;
         // balance form of phi = sum_n w_n psi_avg,n
-        const double pn = (sm.q2[j * NT + t] - (JR - Jl[j]) * sc.inv_dx) / sm.st[j * NT + t];
+        const double pn = (sm.q2[j * NT + t] - (JR - Jl[j]) * sc.inv_dx) * sm.ist[j * NT + t];
         if constexpr (ANISO || CUR) io.jc[c0 + j] = 0.5 * (Jl[j] + JR);
         const double d = pn - sm.phi[j * NT + t];
         if (cfg.norm == 0) {
@@ -543,6 +580,8 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
       }
     }
     reduce2<NT, CL>(num, den, cfg.norm == 0, sm.red, sm.cred, rphase++, sm);
+    SNOP_TSTAMP(ti2);
+    SNOP_TACC(6, ti1, ti2);
     const double rel = rel_change(num, den, cfg.norm);
     if (!(rel == rel)) break;  // NaN: stop, reported non-converged
     if (rel < cfg.tol) {
