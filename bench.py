@@ -226,6 +226,42 @@ def run_gpu(args):
     h2d = 3 * p.batch * p.n_cells * 8
     d2h = p.batch * p.n_cells * 8 + p.batch * 4 + p.batch
 
+    # MD-PNOP warm-start arm (BASELINE C2): random-init DeepONet (branch 2000->128x4, trunk 1->128x4,
+    # tanh) on the recast source, then the model-based solve from phi_NO.
+    warm = None
+    if not args.no_warm_start:
+        from paper_2509_01416_b200 import operators as OPS
+        don = snop.SolutionOperator.deeponet(g, OPS.deeponet_init(p.n_cells), p.ref_params, ctx=ctx)
+        snop.precondition_fixed_source(don, p.order, st, ss, src, cfg, recast_max_iterations=args.recast_max)
+        wt = []
+        for _ in range(max(1, args.steps // 4)):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rw = snop.precondition_fixed_source(don, p.order, st, ss, src, cfg, recast_max_iterations=args.recast_max)
+            e1.record(stream)
+            ctx.synchronize()
+            wt.append(e0.elapsed_time(e1) / 1e3)
+        tp = []
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            don.predict(src, sync=False)
+            e1.record(stream)
+            ctx.synchronize()
+            tp.append(e0.elapsed_time(e1) / 1e3)
+        ri = rw.refine_iterations.to(torch.int64)
+        warm = {"operator": "DeepONet 2000->128x4 / 1->128x4, p=128, tanh, random-init (seeded Xavier), fp32 "
+                            "on tcgen05 (3xTF32)",
+                "recast_max_iterations": args.recast_max,
+                "solves_per_sec": p.batch / float(np.mean(wt)), "ms_per_step": 1e3 * float(np.mean(wt)),
+                "operator_ms": 1e3 * float(np.min(tp)),
+                "refine_iterations_mean": float(ri.float().mean().item()),
+                "recast_iterations_mean": float(rw.precond_iterations.float().mean().item()),
+                "recast_status_counts": [int((rw.recast_status == k).sum().item()) for k in range(3)],
+                "zero_guess_iterations_mean": float(iters.float().mean().item()),
+                "note": "random-init operator: the warm start does not reduce iterations (DESIGN.md §5)"}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -253,6 +289,8 @@ def run_gpu(args):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if warm is not None:
+        line["warm_start"] = warm
     if not args.no_cpu_baseline and world == 1:
         from tests import oracle_lib as O
         th = O.hardware_threads()
@@ -275,6 +313,8 @@ def main():
     ap.add_argument("--batch", type=int, default=2048)
     ap.add_argument("--cpu-sample", type=int, default=2048)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-warm-start", action="store_true")
+    ap.add_argument("--recast-max", type=int, default=1)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
