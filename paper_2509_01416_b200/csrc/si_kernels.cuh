@@ -48,12 +48,13 @@ si_fixed_source_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
                        const double* __restrict__ ss1_g, const double* __restrict__ src_g,
                        const double* __restrict__ phi0_g, double* __restrict__ phi_g,
                        double* __restrict__ jc_g, int32_t* __restrict__ iters, uint8_t* __restrict__ conv,
-                       int* __restrict__ flags) {
+                       int* __restrict__ flags, const int* __restrict__ order) {
   extern __shared__ __align__(32) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<SweepSmem<K, NT>*>(smem_raw);
   const int t = threadIdx.x, Nc = sc.n_cells;
   int b, rank;
   instance_of_block<CL>(b, rank);
+  if (order) b = order[b];  // longest-expected-first dispatch (see launch_si_t)
   const size_t base = (size_t)b * Nc;
   const int c0 = rank * NT * K + t * K;
   CellIO io;
@@ -285,6 +286,67 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   if constexpr (CL) cl_sync();
 }
 
+// ---------------------------------------------------------------------------------------------
+// Dispatch order for K1: instances with a larger scattering ratio need more source iterations
+// (the iteration matrix has spectral radius ~ max sigma_s0/sigma_t), so launching them first
+// shortens the tail of the batch. Any permutation gives identical per-instance results.
+// key_b = max_i Ss0_i / St_i, quantised into NBUCKET buckets, bucket sort (descending).
+// ---------------------------------------------------------------------------------------------
+constexpr int NBUCKET = 1024;
+
+static __global__ void order_keys_kernel(int Nc, const double* __restrict__ st, const double* __restrict__ ss,
+                                  int* __restrict__ bucket, int* __restrict__ hist) {
+  const int b = blockIdx.x;
+  double m = 0.0;
+  for (int i = threadIdx.x; i < Nc; i += blockDim.x) {
+    const double t = st[(size_t)b * Nc + i];
+    if (t > 0.0) m = fmax(m, ss[(size_t)b * Nc + i] / t);
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ double sh[32];
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, sh[w]);
+    m = fmin(fmax(m, 0.0), 1.0);
+    const int k = NBUCKET - 1 - (int)fmin(m * (NBUCKET - 1), (double)(NBUCKET - 1));  // descending
+    bucket[b] = k;
+    atomicAdd(&hist[k], 1);
+  }
+}
+
+static __global__ void order_scan_kernel(int* __restrict__ hist) {  // exclusive scan, one block of NBUCKET
+  __shared__ int s[NBUCKET];
+  const int t = threadIdx.x;
+  s[t] = hist[t];
+  __syncthreads();
+  for (int o = 1; o < NBUCKET; o <<= 1) {
+    const int v = t >= o ? s[t - o] : 0;
+    __syncthreads();
+    s[t] += v;
+    __syncthreads();
+  }
+  hist[t] = t > 0 ? s[t - 1] : 0;
+}
+
+static __global__ void order_scatter_kernel(int B, const int* __restrict__ bucket, int* __restrict__ cursor,
+                                     int* __restrict__ order) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) order[atomicAdd(&cursor[bucket[b]], 1)] = b;
+}
+
+static inline const int* make_order(snop_impl::Ctx& ctx, int batch, int Nc, const double* st, const double* ss) {
+  int* buf = static_cast<int*>(ctx.slot(23, ((size_t)2 * batch + NBUCKET) * sizeof(int)));
+  if (!buf) return nullptr;
+  int *bucket = buf, *order = buf + batch, *hist = buf + 2 * batch;
+  cudaMemsetAsync(hist, 0, NBUCKET * sizeof(int), ctx.stream);
+  order_keys_kernel<<<batch, 128, 0, ctx.stream>>>(Nc, st, ss, bucket, hist);
+  order_scan_kernel<<<1, NBUCKET, 0, ctx.stream>>>(hist);
+  order_scatter_kernel<<<(batch + 255) / 256, 256, 0, ctx.stream>>>(batch, bucket, hist, order);
+  ctx.launches += 3;
+  return cudaGetLastError() == cudaSuccess ? order : nullptr;
+}
+
 // Launch helper: plain launch for CS = 1, cluster launch (CS CTAs per instance) otherwise.
 template <class Kern, class... Args>
 inline cudaError_t launch_k(Kern kern, int batch, int cs, int nt, size_t smem, cudaStream_t s, Args... args) {
@@ -325,8 +387,10 @@ inline snop_status launch_si_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
       return SNOP_CUDA_ERROR;
     }
   }
+  // longest-expected-first order pays off once the batch spans several waves of CTAs
+  const int* order = (!CL && batch > 4 * ctx.sm_count) ? make_order(ctx, batch, sc.n_cells, st, ss0) : nullptr;
   const cudaError_t e = launch_k(kern, batch, CL ? cs : 1, NT, smem, ctx.stream, sc, cfg, st, ss0, ss1, src, phi0,
-                                 phi, jc, iters, conv, ctx.d_flags);
+                                 phi, jc, iters, conv, ctx.d_flags, order);
   ctx.launches++;
   if (e != cudaSuccess) {
     snop_impl::set_error(std::string("si_fixed_source_kernel launch: ") + cudaGetErrorString(e));
