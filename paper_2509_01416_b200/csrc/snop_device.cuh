@@ -397,7 +397,7 @@ __device__ __forceinline__ void scan_phase(SweepSmem<K, NT>& sm, int lane, int w
 template <int K, int NT, int NP, bool CL>
 __device__ __forceinline__ void replay_phase(const SweepConsts& sc, SweepSmem<K, NT>& sm, int p0, const SweepCtl& w,
                                              const double (&al)[NP][K], const double (&bp)[NP][K],
-                                             const double (&bm)[NP][K], double (&Jl)[K], double& Jend) {
+                                             const double (&bm)[NP][K], double (&Jl)[K], double& Jr) {
   const int t = w.t;
 #pragma unroll
   for (int q = 0; q < NP; ++q) {
@@ -457,13 +457,13 @@ __device__ __forceinline__ void replay_phase(const SweepConsts& sc, SweepSmem<K,
       psib = fma(al[q][K - 1 - j], psib, bm[q][K - 1 - j]);
       Jl[K - 1 - j] = fma(-wm, psib, Jl[K - 1 - j]);
     }
-    if (w.owns_last) Jend = fma(wm, psi - psib_in, Jend);  // J at x = L
+    Jr = fma(wm, psi - psib_in, Jr);  // J at this thread's right chunk edge (no neighbour exchange)
   }
 }
 
 template <int K, int NT, bool ANISO, int NP, bool CL>
 __device__ __forceinline__ void sweep_pair_group(const SweepConsts& sc, SweepSmem<K, NT>& sm, const CellIO& io,
-                                                 int p0, SweepCtl& w, double (&Jl)[K], double& Jend) {
+                                                 int p0, SweepCtl& w, double (&Jl)[K], double& Jr) {
   double al[NP][K], bp[NP][K], bm[NP][K];
   SNOP_TSTAMP(t0);
   maps_phase<K, NT, ANISO, NP>(sc, sm, io, p0, w, al, bp, bm);
@@ -475,7 +475,7 @@ __device__ __forceinline__ void sweep_pair_group(const SweepConsts& sc, SweepSme
   if constexpr (CL) cl_sync();
   else __syncthreads();
   SNOP_TSTAMP(t4);
-  replay_phase<K, NT, NP, CL>(sc, sm, p0, w, al, bp, bm, Jl, Jend);
+  replay_phase<K, NT, NP, CL>(sc, sm, p0, w, al, bp, bm, Jl, Jr);
   SNOP_TSTAMP(t5);
   SNOP_TACC(0, t0, t1);
   SNOP_TACC(1, t1, t2);
@@ -512,7 +512,6 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
   w.owns_last = (c0 <= Nc - 1) && (Nc - 1 < c0 + K);
   w.rl = cfg.bc_left == 1;
   w.rr = cfg.bc_right == 1;
-  const int jlast = Nc - 1 - c0;
 
   if (t < kMaxPairs) {
     sm.lag[0][t] = 0.0;
@@ -539,32 +538,22 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
     double Jl[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) Jl[j] = 0.0;
-    double Jend = 0.0;
+    double Jr = 0.0;
     SNOP_TSTAMP(ti0);
     int p = 0;
     if constexpr (NP == 2) {
-      for (; p + 1 < P; p += 2) sweep_pair_group<K, NT, ANISO, 2, CL>(sc, sm, io, p, w, Jl, Jend);
+      for (; p + 1 < P; p += 2) sweep_pair_group<K, NT, ANISO, 2, CL>(sc, sm, io, p, w, Jl, Jr);
     }
-    for (; p < P; ++p) sweep_pair_group<K, NT, ANISO, 1, CL>(sc, sm, io, p, w, Jl, Jend);
+    for (; p < P; ++p) sweep_pair_group<K, NT, ANISO, 1, CL>(sc, sm, io, p, w, Jl, Jr);
     SNOP_TSTAMP(ti1);
     SNOP_TACC(5, ti0, ti1);
-    // edge-current exchange: J at the right edge of own last cell = next thread's first edge
-    // (cluster mode: the last thread of a CTA reads the next CTA's first edge through DSMEM)
-    sm.jfirst[t] = Jl[0];
-    if (w.owns_last) sm.jfirst[NT] = Jend;
-    if constexpr (CL) cl_sync();
-    else __syncthreads();
-    double Jnext;
-    if (t + 1 < NT) Jnext = sm.jfirst[t + 1];
-    else if (CL && w.crank + 1 < w.csz) Jnext = *cl_map(&sm.jfirst[0], w.crank + 1);
-    else Jnext = sm.jfirst[NT];
-    const double Jlastv = sm.jfirst[NT];
+    // J at the right edge of the own last cell was accumulated locally (Jr); padding cells after
+    // the global last cell are identity maps, so Jl[j+1] of a padding cell is J at x = L.
     double num = 0.0, den = 0.0;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       if (c0 + j < Nc) {
-        double JR = (j + 1 < K) ? Jl[j + 1] : Jnext;
-        if (w.owns_last && j == jlast) JR = Jlastv;
+        const double JR = (j + 1 < K) ? Jl[j + 1] : Jr;
         // balance form of phi = sum_n w_n psi_avg,n
         const double pn = (sm.q2[j * NT + t] - (JR - Jl[j]) * sc.inv_dx) * sm.ist[j * NT + t];
         if constexpr (ANISO || CUR) io.jc[c0 + j] = 0.5 * (Jl[j] + JR);
