@@ -41,6 +41,12 @@ struct GemmArgs {
   int64_t sam2, sak2, sab2;
   const float* B2;
   int64_t sbn2, sbk2, sbb2;
+  // optional row-dot epilogue (tensor-core engine; requires N <= 128): instead of storing C,
+  // rowdot_out[row] = sum_n act(alpha*acc + bias[n]) * rowdot_w[n] + rowdot_b  (fp64 output),
+  // row = b * scb + m * scm. Fuses the FNO projection 64 -> hidden -> 1.
+  const float* rowdot_w;
+  float rowdot_b;
+  double* rowdot_out;
 };
 
 __device__ __forceinline__ float gemm_a(const GemmArgs& a, int b, int64_t m, int k) {

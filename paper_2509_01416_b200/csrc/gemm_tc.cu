@@ -116,48 +116,75 @@ constexpr int SPLIT_K = 4 * KC;
 // One operand's staging for a chunk: ROWS x KC fp32 = ROWS * KC / 4 float4 groups; thread tid
 // handles groups tid + i * THREADS, group -> (row = g % ROWS, kq = g / ROWS): consecutive lanes
 // take consecutive rows, so the float4 stores into the core-matrix layout are bank-conflict free
-// (8 lanes fill one 128 B core matrix) and MN-contiguous operands load coalesced.
+// (8 lanes fill one 128 B core matrix) and MN-contiguous operands load coalesced. Because
+// THREADS is a multiple of ROWS, every group of a thread lies in the same row (row = tid % ROWS):
+// the row's base pointers are resolved once per tile (RowPtr) and a chunk only adds k offsets.
 template <int ROWS>
 struct Stage {
   static constexpr int G = ROWS * KC / 4 / THREADS;
   float4 v[G];
 };
 
+struct RowPtr {
+  const float* p1;  // row base in the first K segment (nullptr: row out of range)
+  const float* p2;  // row base in the second K segment (ksplit > 0)
+  int64_t sk1, sk2;
+};
+
 template <int ROWS, bool IS_A>
-__device__ __forceinline__ void load_chunk(Stage<ROWS>& st, const GemmArgs& g, int b, int64_t row0, int k0,
-                                           int64_t mfold, int tid) {
+__device__ __forceinline__ RowPtr row_ptr(const GemmArgs& g, int b, int64_t row0, int64_t mfold, int tid) {
+  RowPtr rp;
+  const int64_t gr = row0 + (tid % ROWS);
   const int64_t nrows = IS_A ? (int64_t)g.M : (int64_t)g.N;
+  if (gr >= nrows) {
+    rp.p1 = rp.p2 = nullptr;
+    rp.sk1 = rp.sk2 = 0;
+    return rp;
+  }
+  if (IS_A) {
+    int64_t r1, r2;
+    if (mfold > 0) {
+      const int64_t q = gr / mfold, r = gr - q * mfold;
+      r1 = q * g.sab + r * g.sam;
+      r2 = q * g.sab2 + r * g.sam2;
+    } else {
+      r1 = (int64_t)b * g.sab + gr * g.sam;
+      r2 = (int64_t)b * g.sab2 + gr * g.sam2;
+    }
+    rp.p1 = g.A + r1;
+    rp.p2 = g.ksplit > 0 ? g.A2 + r2 : nullptr;
+    rp.sk1 = g.sak;
+    rp.sk2 = g.sak2;
+  } else {
+    rp.p1 = g.B + (int64_t)b * g.sbb + gr * g.sbn;
+    rp.p2 = g.ksplit > 0 ? g.B2 + (int64_t)b * g.sbb2 + gr * g.sbn2 : nullptr;
+    rp.sk1 = g.sbk;
+    rp.sk2 = g.sbk2;
+  }
+  return rp;
+}
+
+template <int ROWS>
+__device__ __forceinline__ void load_chunk(Stage<ROWS>& st, const GemmArgs& g, const RowPtr& rp, int k0, int tid) {
+  const bool seg2 = g.ksplit > 0 && k0 >= g.ksplit;  // ksplit is a multiple of KC: whole chunk
+  const float* base = seg2 ? rp.p2 : rp.p1;
+  const int64_t sk = seg2 ? rp.sk2 : rp.sk1;
+  const int kofs = seg2 ? k0 - g.ksplit : k0;
+  const bool vec = base && sk == 1 && k0 + KC <= g.K &&
+                   ((reinterpret_cast<uintptr_t>(base + kofs) & 15) == 0);
 #pragma unroll
   for (int i = 0; i < Stage<ROWS>::G; ++i) {
-    const int grp = tid + i * THREADS;
-    const int r = grp % ROWS, kq = grp / ROWS;
-    const int64_t gr = row0 + r;
-    const int kg = k0 + kq * 4;
+    const int kq = (tid + i * THREADS) / ROWS;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (gr < nrows && kg < g.K) {
-      const bool seg2 = g.ksplit > 0 && kg >= g.ksplit;
-      const int kk = seg2 ? kg - g.ksplit : kg;
-      const float* base;
-      int64_t sk;
-      if (IS_A) {
-        const int64_t sam = seg2 ? g.sam2 : g.sam, sab = seg2 ? g.sab2 : g.sab;
-        sk = seg2 ? g.sak2 : g.sak;
-        const int64_t roff = mfold > 0 ? (gr / mfold) * sab + (gr % mfold) * sam : (int64_t)b * sab + gr * sam;
-        base = (seg2 ? g.A2 : g.A) + roff;
-      } else {
-        const int64_t sbn = seg2 ? g.sbn2 : g.sbn, sbb = seg2 ? g.sbb2 : g.sbb;
-        sk = seg2 ? g.sbk2 : g.sbk;
-        base = (seg2 ? g.B2 : g.B) + (int64_t)b * sbb + gr * sbn;
-      }
-      const float* p = base + (int64_t)kk * sk;
-      if (sk == 1 && kg + 3 < g.K && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
-        v = __ldg(reinterpret_cast<const float4*>(p));
-      } else {
-        v.x = __ldg(p);
-        if (kg + 1 < g.K) v.y = __ldg(p + sk);
-        if (kg + 2 < g.K) v.z = __ldg(p + 2 * sk);
-        if (kg + 3 < g.K) v.w = __ldg(p + 3 * sk);
-      }
+    if (vec) {
+      v = __ldg(reinterpret_cast<const float4*>(base + kofs + kq * 4));
+    } else if (base) {
+      const int kg = k0 + kq * 4;
+      const float* p = base + (int64_t)(kofs + kq * 4) * sk;
+      if (kg < g.K) v.x = __ldg(p);
+      if (kg + 1 < g.K) v.y = __ldg(p + sk);
+      if (kg + 2 < g.K) v.z = __ldg(p + 2 * sk);
+      if (kg + 3 < g.K) v.w = __ldg(p + 3 * sk);
     }
     st.v[i] = v;
   }
@@ -179,13 +206,11 @@ __device__ __forceinline__ void store_chunk(const Stage<ROWS>& st, float* hi, fl
 }
 
 template <int N, bool SPLIT>
-__global__ void __launch_bounds__(THREADS, 2) gemm_tc_kernel(const GemmArgs g, int64_t mfold) {
+__global__ void __launch_bounds__(THREADS, (N <= 64 ? 2 : 1))
+    gemm_tc_kernel(const GemmArgs g, int64_t mfold, int64_t m_tiles, int64_t n_tiles, int64_t n_total) {
   extern __shared__ __align__(1024) unsigned char raw[];
   auto& s = *reinterpret_cast<Smem<N>*>(raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int b = blockIdx.z;
-  const int64_t m0 = (int64_t)blockIdx.x * TM;
-  const int n0 = blockIdx.y * N;
   constexpr uint32_t NACC = SPLIT ? 2 : 1;
   constexpr uint32_t TCOLS = (N * NACC) <= 32 ? 32 : (N * NACC) <= 64 ? 64 : (N * NACC) <= 128 ? 128 : 256;
 
@@ -209,13 +234,9 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_tc_kernel(const GemmArgs g, i
 
   const int nchunks = (g.K + KC - 1) / KC;
   uint32_t phase[2] = {0u, 0u}, aphase[2] = {0u, 0u};
+  int64_t cg = 0;  // chunk counter across the tiles of this persistent CTA (buffer parity)
   constexpr uint32_t idesc = make_idesc(N);
   float sum[SPLIT ? N : 1];
-  if constexpr (SPLIT) {
-#pragma unroll
-    for (int j = 0; j < N; ++j) sum[j] = 0.f;
-  }
-  // drain TMEM accumulator slot `slot` (chunk finished) into the register sums
   auto drain = [&](int slot) {
     mbar_wait(&s.accbar[slot], aphase[slot]);
     aphase[slot] ^= 1u;
@@ -239,96 +260,172 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_tc_kernel(const GemmArgs g, i
 
   Stage<TM> sa;
   Stage<N> sb;
-  load_chunk<TM, true>(sa, g, b, m0, 0, mfold, tid);
-  load_chunk<N, false>(sb, g, b, n0, 0, 0, tid);
-  for (int c = 0; c < nchunks; ++c) {
-    const int buf = c & 1;
-    if (c >= 2) {  // buffer reuse: wait for the MMAs issued on it two chunks ago
-      mbar_wait(&s.bar[buf], phase[buf]);
-      phase[buf] ^= 1u;
+  // persistent loop over output tiles (n fastest, then m, then batch)
+  for (int64_t tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
+    const int nt = (int)(tile % n_tiles);
+    const int64_t mt = (tile / n_tiles) % m_tiles;
+    const int b = (int)(tile / (n_tiles * m_tiles));
+    const int64_t m0 = mt * TM;
+    const int n0 = nt * N;
+    if constexpr (SPLIT) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) sum[j] = 0.f;
     }
-    store_chunk<TM>(sa, s.a_hi[buf], s.a_lo[buf], tid);
-    store_chunk<N>(sb, s.b_hi[buf], s.b_lo[buf], tid);
-    if (c + 1 < nchunks) {  // prefetch the next chunk: global latency overlaps this chunk's MMAs
-      load_chunk<TM, true>(sa, g, b, m0, (c + 1) * KC, mfold, tid);
-      load_chunk<N, false>(sb, g, b, n0, (c + 1) * KC, 0, tid);
+    const RowPtr ra = row_ptr<TM, true>(g, b, m0, mfold, tid);
+    const RowPtr rb = row_ptr<N, false>(g, b, n0, 0, tid);
+    load_chunk<TM>(sa, g, ra, 0, tid);
+    load_chunk<N>(sb, g, rb, 0, tid);
+    int last_buf = 0;
+    for (int c = 0; c < nchunks; ++c, ++cg) {
+      const int buf = (int)(cg & 1);
+      if (cg >= 2) {  // buffer reuse: wait for the MMAs issued on it two chunks ago
+        mbar_wait(&s.bar[buf], phase[buf]);
+        phase[buf] ^= 1u;
+      }
+      store_chunk<TM>(sa, s.a_hi[buf], s.a_lo[buf], tid);
+      store_chunk<N>(sb, s.b_hi[buf], s.b_lo[buf], tid);
+      if (c + 1 < nchunks) {  // prefetch the next chunk: global latency overlaps this chunk's MMAs
+        load_chunk<TM>(sa, g, ra, (c + 1) * KC, tid);
+        load_chunk<N>(sb, g, rb, (c + 1) * KC, tid);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> async proxy
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int slot = SPLIT ? (c & 1) : 0;
+      if (tid == 0) {
+        const uint32_t ah = smem_u32(s.a_hi[buf]), al = smem_u32(s.a_lo[buf]);
+        const uint32_t bh = smem_u32(s.b_hi[buf]), bl = smem_u32(s.b_lo[buf]);
+        const uint32_t td = tmem + (uint32_t)(slot * N);
+#pragma unroll
+        for (int ks = 0; ks < KC / 8; ++ks) {
+          const uint32_t off = ks * 2 * 128;  // two core matrices along K per k-step
+          const uint64_t dah = make_sdesc(ah + off, LBO_BYTES, SBO_BYTES);
+          const uint64_t dal = make_sdesc(al + off, LBO_BYTES, SBO_BYTES);
+          const uint64_t dbh = make_sdesc(bh + off, LBO_BYTES, SBO_BYTES);
+          const uint64_t dbl = make_sdesc(bl + off, LBO_BYTES, SBO_BYTES);
+          const uint32_t first = (SPLIT ? ks == 0 : (c == 0 && ks == 0)) ? 0u : 1u;
+          if (SPLIT) mma_tf32(td, dal, dbl, idesc, first);  // 4xTF32 on the long-K path
+          mma_tf32(td, dal, dbh, idesc, SPLIT ? 1u : first);  // small terms first
+          mma_tf32(td, dah, dbl, idesc, 1u);
+          mma_tf32(td, dah, dbh, idesc, 1u);
+        }
+        mma_commit(&s.bar[buf]);
+        if (SPLIT) mma_commit(&s.accbar[slot]);
+      }
+      __syncwarp();
+      if constexpr (SPLIT) {
+        if (c > 0) drain((c - 1) & 1);
+      }
+      last_buf = buf;
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> async proxy
+    if constexpr (SPLIT) {
+      drain((nchunks - 1) & 1);
+    } else {
+      // the tile's last commit covers all its MMAs; consume that completion so the buffer
+      // parity bookkeeping stays exact across tiles
+      mbar_wait(&s.bar[last_buf], phase[last_buf]);
+      phase[last_buf] ^= 1u;
+      // the other buffer's last commit (if any this tile) completed before; consume it too
+      if (nchunks >= 2) {
+        const int ob = last_buf ^ 1;
+        mbar_wait(&s.bar[ob], phase[ob]);
+        phase[ob] ^= 1u;
+      }
+      cg = 0;  // both buffers drained: restart parity at the next tile
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    if constexpr (SPLIT) {
+      // drain() consumed the accumulator barriers; the chunk-buffer barriers still hold up to two
+      // pending completions — consume them before reusing the buffers on the next tile
+      const int lb = (int)((cg - 1) & 1);
+      mbar_wait(&s.bar[lb], phase[lb]);
+      phase[lb] ^= 1u;
+      if (nchunks >= 2) {
+        mbar_wait(&s.bar[lb ^ 1], phase[lb ^ 1]);
+        phase[lb ^ 1] ^= 1u;
+      }
+      cg = 0;
+    }
+
+    // epilogue: warp w owns TMEM lanes (rows) 32w..32w+31
+    const int64_t gm = m0 + warp * 32 + lane;
+    const int64_t row = mfold > 0 ? (gm / mfold) * g.scb + (gm % mfold) * g.scm : (int64_t)b * g.scb + gm * g.scm;
+    double rdot = 0.0;
+#pragma unroll
+    for (int c0 = 0; c0 < N; c0 += 16) {
+      float x16[16];
+      if constexpr (SPLIT) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) x16[j] = sum[c0 + j];
+      } else {
+        uint32_t v[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(tlane + (uint32_t)c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) x16[j] = __uint_as_float(v[j]);
+      }
+      if (gm < g.M) {
+        const bool full = (n0 + c0 + 16 <= g.N);
+        if (g.rowdot_w) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int gn = n0 + c0 + j;
+            if (gn >= g.N) continue;
+            float x = g.alpha * x16[j];
+            if (g.bias) x += g.bias[gn];
+            rdot += (double)(act_f(x, g.act) * g.rowdot_w[gn]);
+          }
+        } else if (full && g.scn == 1 && !g.Cd && ((row + n0 + c0) & 3) == 0 &&
+                   ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0)) {
+          // vectorised path: 16 contiguous fp32 of this row -> 4 x 16 B
+          float4* dst = reinterpret_cast<float4*>(g.C + row + n0 + c0);
+#pragma unroll
+          for (int v4 = 0; v4 < 4; ++v4) {
+            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (g.beta != 0.f) o = dst[v4];
+            float* op = reinterpret_cast<float*>(&o);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int j = v4 * 4 + e;
+              float x = g.alpha * x16[j] + (g.beta != 0.f ? g.beta * op[e] : 0.f);
+              if (g.bias) x += g.bias[n0 + c0 + j];
+              op[e] = act_f(x, g.act);
+            }
+            dst[v4] = o;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int gn = n0 + c0 + j;
+            if (gn >= g.N) continue;
+            const int64_t off = row + (int64_t)gn * g.scn;
+            float x = g.alpha * x16[j];
+            if (g.beta != 0.f) x += g.beta * g.C[off];
+            if (g.bias) x += g.bias[gn];
+            x = act_f(x, g.act);
+            if (g.Cd) g.Cd[off] = (double)x;
+            else g.C[off] = x;
+          }
+        }
+      }
+    }
+    if (g.rowdot_w && gm < g.M) {
+      // N split over at most two 64-wide tiles: two addends onto a zeroed output commute exactly
+      // in IEEE arithmetic (0 + a + b == 0 + b + a), so the atomic accumulation is deterministic
+      const double part = rdot + (nt == 0 ? (double)g.rowdot_b : 0.0);
+      if (n_tiles == 1) g.rowdot_out[row] = part;
+      else atomicAdd(&g.rowdot_out[row], part);
+    }
+    // all warps finished reading TMEM before the next tile's first MMA overwrites it
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int slot = SPLIT ? (c & 1) : 0;
-    if (tid == 0) {
-      const uint32_t ah = smem_u32(s.a_hi[buf]), al = smem_u32(s.a_lo[buf]);
-      const uint32_t bh = smem_u32(s.b_hi[buf]), bl = smem_u32(s.b_lo[buf]);
-      const uint32_t td = tmem + (uint32_t)(slot * N);
-#pragma unroll
-      for (int ks = 0; ks < KC / 8; ++ks) {
-        const uint32_t off = ks * 2 * 128;  // two core matrices along K per k-step
-        const uint64_t dah = make_sdesc(ah + off, LBO_BYTES, SBO_BYTES);
-        const uint64_t dal = make_sdesc(al + off, LBO_BYTES, SBO_BYTES);
-        const uint64_t dbh = make_sdesc(bh + off, LBO_BYTES, SBO_BYTES);
-        const uint64_t dbl = make_sdesc(bl + off, LBO_BYTES, SBO_BYTES);
-        const uint32_t first = (SPLIT ? ks == 0 : (c == 0 && ks == 0)) ? 0u : 1u;
-        if (SPLIT) mma_tf32(td, dal, dbl, idesc, first);  // 4xTF32 on the long-K path
-        mma_tf32(td, dal, dbh, idesc, SPLIT ? 1u : first);  // small terms first
-        mma_tf32(td, dah, dbl, idesc, 1u);
-        mma_tf32(td, dah, dbh, idesc, 1u);
-      }
-      mma_commit(&s.bar[buf]);
-      if (SPLIT) mma_commit(&s.accbar[slot]);
-    }
-    __syncwarp();
-    // split mode: once chunk c is queued on the tensor core, drain chunk c-1's accumulator
-    if constexpr (SPLIT) {
-      if (c > 0) drain((c - 1) & 1);
-    }
   }
-  if constexpr (SPLIT) {
-    drain((nchunks - 1) & 1);
-  } else {
-    const int last = (nchunks - 1) & 1;
-    mbar_wait(&s.bar[last], phase[last]);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  }
-
-  // epilogue: warp w owns TMEM lanes (rows) 32w..32w+31
-  const int64_t gm = m0 + warp * 32 + lane;
-  const int64_t row = mfold > 0 ? (gm / mfold) * g.scb + (gm % mfold) * g.scm : (int64_t)b * g.scb + gm * g.scm;
-#pragma unroll
-  for (int c0 = 0; c0 < N; c0 += 16) {
-    float x16[16];
-    if constexpr (SPLIT) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) x16[j] = sum[c0 + j];
-    } else {
-      uint32_t v[16];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-          : "r"(tlane + (uint32_t)c0));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-      for (int j = 0; j < 16; ++j) x16[j] = __uint_as_float(v[j]);
-    }
-    if (gm < g.M) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int gn = n0 + c0 + j;
-        if (gn >= g.N) continue;
-        const int64_t off = row + (int64_t)gn * g.scn;
-        float x = g.alpha * x16[j];
-        if (g.beta != 0.f) x += g.beta * g.C[off];
-        if (g.bias) x += g.bias[gn];
-        x = act_f(x, g.act);
-        if (g.Cd) g.Cd[off] = (double)x;
-        else g.C[off] = x;
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
 }
 
@@ -336,15 +433,22 @@ template <int N, bool SPLIT>
 cudaError_t launch(const GemmArgs& g, int64_t mfold, cudaStream_t st) {
   const size_t smem = sizeof(Smem<N>);
   static bool attr = false;
+  static int sms = 148;
   if (!attr) {
     const cudaError_t e =
         cudaFuncSetAttribute(gemm_tc_kernel<N, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     attr = true;
   }
-  const int64_t mt = (g.M + TM - 1) / TM;
-  dim3 grid((unsigned)mt, (unsigned)((g.N + N - 1) / N), (unsigned)(mfold > 0 ? 1 : g.batch));
-  gemm_tc_kernel<N, SPLIT><<<grid, THREADS, smem, st>>>(g, mfold);
+  const int64_t m_tiles = (g.M + TM - 1) / TM;
+  const int64_t n_tiles = (g.N + N - 1) / N;
+  const int64_t total = m_tiles * n_tiles * (mfold > 0 ? 1 : g.batch);
+  const int per_sm = N <= 64 ? 2 : 1;
+  const int64_t grid = total < (int64_t)sms * per_sm ? total : (int64_t)sms * per_sm;
+  gemm_tc_kernel<N, SPLIT><<<(unsigned)grid, THREADS, smem, st>>>(g, mfold, m_tiles, n_tiles, total);
   return cudaGetLastError();
 }
 
@@ -357,6 +461,10 @@ cudaError_t gemm_tc(const GemmArgs& g, cudaStream_t st, int64_t mfold) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
   if (g.ksplit > 0 && g.ksplit % tc::KC != 0) return cudaErrorInvalidValue;  // segment = whole chunks
   const bool split = g.K > tc::SPLIT_K;  // long K: chunk-wise drained accumulation
+  if (g.rowdot_w) {  // row-dot epilogue: N <= 128 as one or two 64-wide tiles (caller zeroes out)
+    if (g.N > 128 || split) return cudaErrorInvalidValue;
+    return tc::launch<64, false>(g, mfold, st);
+  }
   if (g.N <= 32) return split ? tc::launch<32, true>(g, mfold, st) : tc::launch<32, false>(g, mfold, st);
   return split ? tc::launch<64, true>(g, mfold, st) : tc::launch<64, false>(g, mfold, st);
 }

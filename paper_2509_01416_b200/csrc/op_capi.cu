@@ -32,6 +32,7 @@ struct snop_op {
   float *lift_W = nullptr, *lift_b = nullptr, *xc = nullptr;
   std::vector<float*> Rr, Ri, W, b;
   float *P1W = nullptr, *P1b = nullptr, *P2W = nullptr, *P2b = nullptr;
+  float p2b_host = 0.f;
   float *F = nullptr, *Ginv = nullptr;  // forward [2M][n] and inverse [n][2M] truncated DFT
   // exact operator
   int order = 16;
@@ -399,15 +400,26 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
     }
     std::swap(V, Vn);
   }
-  // projection 64 -> hidden (act) -> 1, chunked over rows
-  const size_t chunk = (size_t)1 << 18;
-  float* h = static_cast<float*>(ctx.slot(49, chunk * H * sizeof(float)));
-  if (!h) return cuda_status("FNO projection workspace", cudaErrorMemoryAllocation);
-  for (size_t r0 = 0; r0 < rowsN; r0 += chunk) {
-    const int rows = (int)std::min(chunk, rowsN - r0);
-    SNOP_TRY(gemm(ctx, rowmajor(rows, H, C, V + r0 * C, C, op.P1W, C, h, H, op.P1b, op.act)));
-    rowdot<<<grid_for(ctx, (size_t)rows * 32), 256, 0, ctx.stream>>>(rows, H, h, op.P2W, op.P2b, out + r0);
-    ctx.launches++;
+  // projection 64 -> hidden (act) -> 1. Tensor-core engine: one GEMM whose epilogue does the
+  // second layer as a row-dot (no hidden tensor in HBM); FFMA engine: chunked GEMM + rowdot.
+  if (use_tc() && H <= 128) {
+    GemmArgs pj = rowmajor((int)rowsN, H, C, V, C, op.P1W, C, nullptr, 1, op.P1b, op.act);
+    pj.scm = 1;
+    pj.rowdot_w = op.P2W;
+    pj.rowdot_out = out;
+    pj.rowdot_b = op.p2b_host;
+    if (H > 64) SNOP_TRY(cuda_status("zero", cudaMemsetAsync(out, 0, rowsN * sizeof(double), ctx.stream)));
+    SNOP_TRY(gemm(ctx, pj));
+  } else {
+    const size_t chunk = (size_t)1 << 18;
+    float* h = static_cast<float*>(ctx.slot(49, chunk * H * sizeof(float)));
+    if (!h) return cuda_status("FNO projection workspace", cudaErrorMemoryAllocation);
+    for (size_t r0 = 0; r0 < rowsN; r0 += chunk) {
+      const int rows = (int)std::min(chunk, rowsN - r0);
+      SNOP_TRY(gemm(ctx, rowmajor(rows, H, C, V + r0 * C, C, op.P1W, C, h, H, op.P1b, op.act)));
+      rowdot<<<grid_for(ctx, (size_t)rows * 32), 256, 0, ctx.stream>>>(rows, H, h, op.P2W, op.P2b, out + r0);
+      ctx.launches++;
+    }
   }
   return cuda_status("FNO forward", cudaGetLastError());
 }
@@ -603,6 +615,7 @@ snop_status snop_fno_create(snop_ctx* ctx, const snop_grid* grid, double tstar, 
   p += hidden;
   op->P2W = op->upload(p, hidden);
   p += hidden;
+  op->p2b_host = p[0];
   op->P2b = op->upload(p, 1);
   // truncated real DFT matrices (exact index reduction), SURVEY §9 #9 conventions
   std::vector<float> F(2 * M * n), G((size_t)n * 2 * M), xs(n);
