@@ -94,12 +94,18 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-template <int N>
+// Shared-memory chunk buffers: the non-split kernels use ONE stage (48 KB at N = 64 -> four
+// CTAs per SM; the register prefetch of the next chunk still overlaps the MMAs), the split
+// (long-K) kernels keep two stages (their register sums leave room for two CTAs per SM only).
+template <bool SPLIT>
+constexpr int stages() { return SPLIT ? 2 : 1; }
+
+template <int N, int STAGES>
 struct Smem {
-  float a_hi[2][TM * KC];
-  float a_lo[2][TM * KC];
-  float b_hi[2][N * KC];
-  float b_lo[2][N * KC];
+  float a_hi[STAGES][TM * KC];
+  float a_lo[STAGES][TM * KC];
+  float b_hi[STAGES][N * KC];
+  float b_lo[STAGES][N * KC];
   uint64_t bar[2];     // chunk buffers: MMAs reading the buffer have completed
   uint64_t accbar[2];  // split mode: all MMAs of the chunk accumulating into TMEM slot s are done
   uint32_t tmem_base;
@@ -206,10 +212,11 @@ __device__ __forceinline__ void store_chunk(const Stage<ROWS>& st, float* hi, fl
 }
 
 template <int N, bool SPLIT>
-__global__ void __launch_bounds__(THREADS, (N <= 64 ? 2 : 1))
+__global__ void __launch_bounds__(THREADS, (N <= 64 ? (SPLIT ? 2 : 4) : 1))
     gemm_tc_kernel(const GemmArgs g, int64_t mfold, int64_t m_tiles, int64_t n_tiles, int64_t n_total) {
+  constexpr int STAGES = stages<SPLIT>();
   extern __shared__ __align__(1024) unsigned char raw[];
-  auto& s = *reinterpret_cast<Smem<N>*>(raw);
+  auto& s = *reinterpret_cast<Smem<N, STAGES>*>(raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr uint32_t NACC = SPLIT ? 2 : 1;
   constexpr uint32_t TCOLS = (N * NACC) <= 32 ? 32 : (N * NACC) <= 64 ? 64 : (N * NACC) <= 128 ? 128 : 256;
@@ -277,8 +284,8 @@ __global__ void __launch_bounds__(THREADS, (N <= 64 ? 2 : 1))
     load_chunk<N>(sb, g, rb, 0, tid);
     int last_buf = 0;
     for (int c = 0; c < nchunks; ++c, ++cg) {
-      const int buf = (int)(cg & 1);
-      if (cg >= 2) {  // buffer reuse: wait for the MMAs issued on it two chunks ago
+      const int buf = (int)(cg % STAGES);
+      if (cg >= STAGES) {  // buffer reuse: wait for the MMAs issued on it STAGES chunks ago
         mbar_wait(&s.bar[buf], phase[buf]);
         phase[buf] ^= 1u;
       }
@@ -327,7 +334,7 @@ __global__ void __launch_bounds__(THREADS, (N <= 64 ? 2 : 1))
       mbar_wait(&s.bar[last_buf], phase[last_buf]);
       phase[last_buf] ^= 1u;
       // the other buffer's last commit (if any this tile) completed before; consume it too
-      if (nchunks >= 2) {
+      if (STAGES == 2 && nchunks >= 2) {
         const int ob = last_buf ^ 1;
         mbar_wait(&s.bar[ob], phase[ob]);
         phase[ob] ^= 1u;
@@ -338,10 +345,10 @@ __global__ void __launch_bounds__(THREADS, (N <= 64 ? 2 : 1))
     if constexpr (SPLIT) {
       // drain() consumed the accumulator barriers; the chunk-buffer barriers still hold up to two
       // pending completions — consume them before reusing the buffers on the next tile
-      const int lb = (int)((cg - 1) & 1);
+      const int lb = (int)((cg - 1) % STAGES);
       mbar_wait(&s.bar[lb], phase[lb]);
       phase[lb] ^= 1u;
-      if (nchunks >= 2) {
+      if (STAGES == 2 && nchunks >= 2) {
         mbar_wait(&s.bar[lb ^ 1], phase[lb ^ 1]);
         phase[lb ^ 1] ^= 1u;
       }
@@ -431,7 +438,7 @@ __global__ void __launch_bounds__(THREADS, (N <= 64 ? 2 : 1))
 
 template <int N, bool SPLIT>
 cudaError_t launch(const GemmArgs& g, int64_t mfold, cudaStream_t st) {
-  const size_t smem = sizeof(Smem<N>);
+  const size_t smem = sizeof(Smem<N, stages<SPLIT>()>);
   static bool attr = false;
   static int sms = 148;
   if (!attr) {
@@ -446,7 +453,7 @@ cudaError_t launch(const GemmArgs& g, int64_t mfold, cudaStream_t st) {
   const int64_t m_tiles = (g.M + TM - 1) / TM;
   const int64_t n_tiles = (g.N + N - 1) / N;
   const int64_t total = m_tiles * n_tiles * (mfold > 0 ? 1 : g.batch);
-  const int per_sm = N <= 64 ? 2 : 1;
+  const int per_sm = N <= 64 ? (SPLIT ? 2 : 4) : 1;
   const int64_t grid = total < (int64_t)sms * per_sm ? total : (int64_t)sms * per_sm;
   gemm_tc_kernel<N, SPLIT><<<(unsigned)grid, THREADS, smem, st>>>(g, mfold, m_tiles, n_tiles, total);
   return cudaGetLastError();
