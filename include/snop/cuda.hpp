@@ -254,5 +254,43 @@ inline RecastResult recast_fixed_point(const SolutionOperator& op, const std::ve
   return r;
 }
 
+struct HybridEigenSolution : EigenSolution {  // EigenSolution + stage diagnostics
+  std::vector<double> stage1_k;
+  std::vector<int32_t> stage1_outer;
+  std::vector<int64_t> stage1_inner;
+  std::vector<uint8_t> fallback;
+};
+
+enum class HybridAlgorithm { SP, CP };
+
+// sp_eigen / cp_eigen: stage 1 with the operator as the within-group solver,
+// stage 2 model-based from (k_NO, phi_NO); divergence falls back to the cold start.
+inline HybridEigenSolution hybrid_eigen(HybridAlgorithm alg, const SolutionOperator& op, int order,
+                                        const MultiGroupMaterials& m, const SolverConfig& cfg,
+                                        double recast_tolerance = 1e-4, int recast_max_iterations = 50) {
+  const size_t n = (size_t)m.batch * m.groups * op.n_cells();
+  if (m.sigma_t.size() != n || m.nu_sigma_f.size() != n || m.sigma_s0.size() != n * m.groups ||
+      m.chi.size() != (size_t)m.batch * m.groups || (!m.sigma_s1.empty() && m.sigma_s1.size() != n))
+    throw InvalidArgument("hybrid_eigen: array sizes do not match batch/groups/n_cells");
+  HybridEigenSolution e;
+  e.k.resize(m.batch);
+  e.phi.resize(n);
+  e.stage1_k.resize(m.batch);
+  e.stage1_outer.resize(m.batch);
+  e.stage1_inner.resize(m.batch);
+  e.outer_iterations.resize(m.batch);
+  e.total_inner_iterations.resize(m.batch);
+  e.converged.resize(m.batch);
+  e.fallback.resize(m.batch);
+  const snop_solver_config c = cfg.c();
+  auto fn = alg == HybridAlgorithm::SP ? snop_sp_eigen_batched : snop_cp_eigen_batched;
+  check(fn(op.context().get(), op.get(), SNOP_MEM_HOST, order, m.batch, m.groups, m.sigma_t.data(),
+           m.sigma_s0.data(), m.sigma_s1.empty() ? nullptr : m.sigma_s1.data(), m.nu_sigma_f.data(), m.chi.data(), &c,
+           recast_tolerance, recast_max_iterations, e.k.data(), e.phi.data(), e.stage1_k.data(),
+           e.stage1_outer.data(), e.stage1_inner.data(), e.outer_iterations.data(), e.total_inner_iterations.data(),
+           e.converged.data(), e.fallback.data()));
+  return e;
+}
+
 }  // namespace cuda
 }  // namespace snop

@@ -164,6 +164,31 @@ snop_status snop_precondition_fixed_source(
     double* phi_out, int32_t* precond_iterations, int32_t* recast_status,
     int32_t* refine_iterations, uint8_t* converged);
 
+/* sp_eigen / cp_eigen (paper Appendix A2 Eqs. A5-A8), batched over instances.
+ * Stage 1: power iteration whose within-group solve is the operator -- SP: recast fixed point
+ * (against the operator's p*, within-group Sigma_t,g / Sigma_s0(g->g) recast, inter-group scatter
+ * and fission as external source) warm-started from the current group flux, to recast_tolerance
+ * or recast_max_iterations; CP: that prediction refined by a model-based source iteration.
+ * Stage 2: model-based power iteration (as snop_power_iteration_batched) from (k_NO, phi_NO).
+ * An instance whose stage 1 diverged or degenerated restarts stage 2 cold; fallback[b] = 1.
+ * Layouts as snop_power_iteration_batched; the operator's grid is the problem grid. stage1_k =
+ * k_NO; stage*_inner count recast iterations (+ refinement sweeps for CP) / sweeps. */
+snop_status snop_sp_eigen_batched(
+    snop_ctx* ctx, snop_op* op, int32_t memspace, int32_t order, int32_t batch, int32_t n_groups,
+    const double* sigma_t, const double* sigma_s0, const double* sigma_s1, const double* nu_sigma_f,
+    const double* chi, const snop_solver_config* cfg, double recast_tolerance,
+    int32_t recast_max_iterations, double* k_out, double* phi_out, double* stage1_k,
+    int32_t* stage1_outer, int64_t* stage1_inner, int32_t* stage2_outer, int64_t* stage2_inner,
+    uint8_t* converged, uint8_t* fallback);
+
+snop_status snop_cp_eigen_batched(
+    snop_ctx* ctx, snop_op* op, int32_t memspace, int32_t order, int32_t batch, int32_t n_groups,
+    const double* sigma_t, const double* sigma_s0, const double* sigma_s1, const double* nu_sigma_f,
+    const double* chi, const snop_solver_config* cfg, double recast_tolerance,
+    int32_t recast_max_iterations, double* k_out, double* phi_out, double* stage1_k,
+    int32_t* stage1_outer, int64_t* stage1_inner, int32_t* stage2_outer, int64_t* stage2_inner,
+    uint8_t* converged, uint8_t* fallback);
+
 #ifdef __cplusplus
 }
 #endif

@@ -347,6 +347,89 @@ int oracle_precondition_fixed_source(void* vop, int32_t order, int32_t batch, co
   }
 }
 
+// SPEC.md:423-441 (paper Eqs. A5-A8). Stage 1: power iteration whose inner solver is the
+// operator through the recast fixed point, warm-started from the current group flux (SP), or
+// that prediction refined by a model-based source iteration (CP). Stage 2: model-based power
+// iteration from (k_NO, phi_NO); stage-1 divergence falls back to the cold start.
+int oracle_sp_cp_eigen_batched(void* vop, int32_t algorithm, int32_t order, int32_t batch, int32_t G,
+                               const double* st, const double* ss0, const double* ss1, const double* nsf,
+                               const double* chi, const snop_solver_config* ccfg, double rtol, int32_t rmax,
+                               double* k_out, double* phi_out, double* s1_k, int32_t* s1_outer, int64_t* s1_inner,
+                               int32_t* s2_outer, int64_t* s2_inner, uint8_t* conv, uint8_t* fallback,
+                               int32_t n_threads) {
+  try {
+    const auto* op = static_cast<const OracleOp*>(vop);
+    const Grid1D g = op->grid;
+    const Quadrature q = gauss_legendre(order);
+    const SolverConfig cfg = to_cfg(ccfg);
+    const std::size_t Nc = g.n_cells, GN = (std::size_t)G * Nc;
+    std::string err;
+    int code = 0;
+    std::mutex mu;
+    parallel_chunks(batch, batch, [&](std::size_t, std::size_t b0, std::size_t b1) {
+      for (std::size_t b = b0; b < b1; ++b) {
+        try {
+          MGView m;
+          m.G = G;
+          m.sigma_t = st + b * GN;
+          m.sigma_s0 = ss0 + b * GN * G;
+          m.sigma_s1 = ss1 ? ss1 + b * GN : nullptr;
+          m.nu_sigma_f = nsf + b * GN;
+          m.chi = chi + b * G;
+          double* phi = phi_out + b * GN;
+          std::fill(phi, phi + GN, 1.0);
+          bool diverged = false;
+          InnerSolver stage1 = [&](int gg, const double* qe, double* phig) -> int {
+            const double* stg = m.sigma_t + (std::size_t)gg * Nc;
+            const double* ssg = m.sigma_s0 + ((std::size_t)gg * G + gg) * Nc;
+            std::vector<double> pred(Nc);
+            const RecastResult r = recast_fixed_point(
+                (int)Nc, qe, stg, ssg, op->tstar, op->sstar, [&](const double* s, double* o) { op->predict(s, o); },
+                rtol, rmax, cfg.norm, phig, pred.data());
+            if (r.status == RecastStatus::Diverged) diverged = true;
+            int count = r.iterations;
+            if (algorithm == 1) {  // CP: model-based refinement of the prediction (Eq. A8)
+              SolverConfig icfg = cfg;
+              std::copy(pred.begin(), pred.end(), phig);
+              const double* s1g = m.sigma_s1 ? m.sigma_s1 + (std::size_t)gg * Nc : nullptr;
+              count += source_iteration(g, q, stg, ssg, s1g, qe, icfg, phig, nullptr).iterations;
+            } else {
+              std::copy(pred.begin(), pred.end(), phig);
+            }
+            return count;
+          };
+          EigenResult r1;
+          bool fb = false;
+          try {
+            r1 = power_iteration(g, q, m, cfg, phi, true, 1.0, &stage1);
+            if (diverged || !std::isfinite(r1.k) || !(r1.k > 0.0)) fb = true;
+          } catch (const DegenerateProblem&) {
+            fb = true;
+          }
+          if (fb) std::fill(phi, phi + GN, 1.0);
+          const EigenResult r2 = power_iteration(g, q, m, cfg, phi, true, fb ? 1.0 : r1.k, nullptr);
+          k_out[b] = r2.k;
+          s1_k[b] = r1.k;
+          s1_outer[b] = r1.outer;
+          s1_inner[b] = r1.inner;
+          s2_outer[b] = r2.outer;
+          s2_inner[b] = r2.inner;
+          conv[b] = r2.converged ? 1 : 0;
+          fallback[b] = fb ? 1 : 0;
+        } catch (...) {
+          std::lock_guard<std::mutex> lk(mu);
+          code = map_exc();
+          err = g_err;
+        }
+      }
+    }, n_threads);
+    if (code) { g_err = err; return code; }
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
 int oracle_balance_residual(const snop_grid* grid, const double* st, const double* ss0, const double* src,
                             const double* phi, double leak_left, double leak_right, double* out) {
   try {

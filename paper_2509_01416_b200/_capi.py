@@ -22,7 +22,7 @@ EXPORTS = [
     "snop_ctx_launch_count", "snop_ctx_stream", "snop_gauss_legendre", "snop_source_iteration_batched",
     "snop_power_iteration_batched", "snop_recast_source", "snop_deeponet_create", "snop_fno_create",
     "snop_exact_operator_create", "snop_op_destroy", "snop_op_predict", "snop_recast_fixed_point",
-    "snop_precondition_fixed_source",
+    "snop_precondition_fixed_source", "snop_sp_eigen_batched", "snop_cp_eigen_batched",
 ]
 
 _lib = None
@@ -68,6 +68,9 @@ def load():
     lib.snop_recast_fixed_point.argtypes = [vp, vp, i32, i32, vp, vp, vp, dbl, i32, i32, vp, vp, vp, vp]
     lib.snop_precondition_fixed_source.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp, vp, dbl, i32,
                                                    C.POINTER(SnopSolverConfig), vp, vp, vp, vp, vp]
+    for fn in ("snop_sp_eigen_batched", "snop_cp_eigen_batched"):
+        getattr(lib, fn).argtypes = [vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, C.POINTER(SnopSolverConfig), dbl,
+                                     i32, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     _lib = lib
     return lib
 

@@ -429,9 +429,15 @@ snop_status drain(Ctx& ctx) {
   cudaError_t e = cudaMemcpyAsync(&flags, ctx.d_flags, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx.stream);
   if (e != cudaSuccess) return cuda_status("synchronize", e);
-  if (flags) {
-    cudaMemsetAsync(ctx.d_flags, 0, sizeof(int), ctx.stream);
-    return invalid("nonpositive sigma_t in at least one instance");
+  if (flags) cudaMemsetAsync(ctx.d_flags, 0, sizeof(int), ctx.stream);
+  if (flags & FLAG_BAD_SIGMA_T) return invalid("nonpositive sigma_t in at least one instance");
+  if (flags & FLAG_DEGENERATE) {
+    set_error("zero fission integral in at least one instance");
+    return SNOP_DEGENERATE_PROBLEM;
+  }
+  if (flags & FLAG_NONFINITE) {
+    set_error("non-finite values produced");
+    return SNOP_NUMERICAL_ERROR;
   }
   return SNOP_OK;
 }
@@ -495,6 +501,265 @@ snop_status unstage(Ctx& ctx, T* h, const T* d, size_t n) {
 }
 
 bool valid_act(int a) { return a == ACT_RELU || a == ACT_TANH || a == ACT_GELU; }
+
+
+// ---- SP / CP hybrid eigenvalue solve (paper Eqs. A5-A8) -----------------------
+// Stage 1 is a power iteration whose within-group solve is the operator: SP = recast fixed point
+// warm-started from the current group flux (Eq. A5); CP = that prediction refined by a
+// model-based source iteration (Eqs. A7-A8). Stage 2 is the fused model-based power iteration
+// (K2) started from (k_NO, phi_NO), or from the cold start where stage 1 diverged.
+// The outer loop is host-orchestrated because the operator is a multi-kernel pipeline; the
+// per-instance bookkeeping (fission density, group source, k update, convergence, freeze) is in
+// the one-CTA-per-instance kernels below.
+constexpr int HY_THREADS = 256;
+
+__device__ double hy_block_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x / 32] = v;
+  __syncthreads();
+  double r = 0.0;
+  for (int u = 0; u < HY_THREADS / 32; ++u) r += sh[u];
+  return r;
+}
+
+__device__ double hy_block_max(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x / 32] = v;
+  __syncthreads();
+  double r = 0.0;
+  for (int u = 0; u < HY_THREADS / 32; ++u) r = fmax(r, sh[u]);
+  return r;
+}
+
+// dx * sum_i sum_g nuSf_g,i phi_g,i for instance b
+__device__ double hy_fission_integral(int G, int Nc, double dx, const double* nsf, const double* phi, double* sh) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < Nc; i += HY_THREADS) {
+    double f = 0.0;
+    for (int g = 0; g < G; ++g) f = fma(nsf[(size_t)g * Nc + i], phi[(size_t)g * Nc + i], f);
+    s += f;
+  }
+  return hy_block_sum(s, sh) * dx;
+}
+
+__global__ void __launch_bounds__(HY_THREADS) hy_init(int G, int Nc, double dx, const double* __restrict__ st,
+                                                      const double* __restrict__ nsf, double* __restrict__ phi,
+                                                      double* __restrict__ k, uint8_t* __restrict__ active,
+                                                      uint8_t* __restrict__ fb, uint8_t* __restrict__ div,
+                                                      int32_t* __restrict__ outer, int64_t* __restrict__ inner,
+                                                      int* __restrict__ flags) {
+  __shared__ double sh[HY_THREADS / 32];
+  const int b = blockIdx.x;
+  const size_t GN = (size_t)G * Nc;
+  double* p = phi + b * GN;
+  int bad = 0;
+  for (size_t i = threadIdx.x; i < GN; i += HY_THREADS) {
+    p[i] = 1.0;
+    bad |= !(st[b * GN + i] > 0.0);
+  }
+  bad = __syncthreads_or(bad);
+  const double F = hy_fission_integral(G, Nc, dx, nsf + b * GN, p, sh);
+  const bool ok = !bad && F != 0.0 && isfinite(F);
+  if (ok)
+    for (size_t i = threadIdx.x; i < GN; i += HY_THREADS) p[i] /= F;
+  if (threadIdx.x == 0) {
+    if (bad) atomicOr(flags, FLAG_BAD_SIGMA_T);
+    k[b] = 1.0;
+    active[b] = ok ? 1 : 0;
+    fb[b] = ok ? 0 : 1;
+    div[b] = 0;
+    outer[b] = 0;
+    inner[b] = 0;
+  }
+}
+
+// old = phi; fiss_i = sum_g nuSf_g,i phi_g,i (frozen for the Gauss-Seidel pass)
+__global__ void hy_outer_begin(int G, int Nc, const double* __restrict__ nsf, const double* __restrict__ phi,
+                               double* __restrict__ old, double* __restrict__ fiss, const uint8_t* __restrict__ active) {
+  const int b = blockIdx.x;
+  if (!active[b]) return;
+  const size_t GN = (size_t)G * Nc;
+  for (int i = threadIdx.x; i < Nc; i += blockDim.x) {
+    double f = 0.0;
+    for (int g = 0; g < G; ++g) {
+      const double v = phi[b * GN + (size_t)g * Nc + i];
+      old[b * GN + (size_t)g * Nc + i] = v;
+      f = fma(nsf[b * GN + (size_t)g * Nc + i], v, f);
+    }
+    fiss[(size_t)b * Nc + i] = f;
+  }
+}
+
+// Group-g inputs, gathered contiguous [B][Nc]: q_ext = chi_g fiss / k + sum_{g'!=g} Ss0(g'->g) phi_g',
+// Sigma_t,g, Sigma_s0(g->g), Sigma_s1,g and the warm-start flux phi_g.
+__global__ void hy_group_in(int g, int G, int Nc, const double* __restrict__ chi, const double* __restrict__ k,
+                            const double* __restrict__ st, const double* __restrict__ ss0,
+                            const double* __restrict__ ss1, const double* __restrict__ phi,
+                            const double* __restrict__ fiss, double* __restrict__ qext, double* __restrict__ stg,
+                            double* __restrict__ ssg, double* __restrict__ s1g, double* __restrict__ phig) {
+  const int b = blockIdx.x;
+  const size_t GN = (size_t)G * Nc;
+  const double chig = chi[(size_t)b * G + g] / k[b];
+  for (int i = threadIdx.x; i < Nc; i += blockDim.x) {
+    const size_t o = (size_t)b * Nc + i;
+    double q = chig * fiss[o];
+    for (int gp = 0; gp < G; ++gp)
+      if (gp != g) q = fma(ss0[b * GN * G + ((size_t)gp * G + g) * Nc + i], phi[b * GN + (size_t)gp * Nc + i], q);
+    qext[o] = q;
+    stg[o] = st[b * GN + (size_t)g * Nc + i];
+    ssg[o] = ss0[b * GN * G + ((size_t)g * G + g) * Nc + i];
+    if (ss1) s1g[o] = ss1[b * GN + (size_t)g * Nc + i];
+    phig[o] = phi[b * GN + (size_t)g * Nc + i];
+  }
+}
+
+__global__ void hy_group_out(int g, int G, int Nc, const double* __restrict__ phig, double* __restrict__ phi,
+                             const uint8_t* __restrict__ active, const int32_t* __restrict__ it_a,
+                             const int32_t* __restrict__ it_b, const int32_t* __restrict__ rstatus,
+                             int64_t* __restrict__ inner, uint8_t* __restrict__ div) {
+  const int b = blockIdx.x;
+  if (!active[b]) return;
+  const size_t GN = (size_t)G * Nc;
+  for (int i = threadIdx.x; i < Nc; i += blockDim.x) phi[b * GN + (size_t)g * Nc + i] = phig[(size_t)b * Nc + i];
+  if (threadIdx.x == 0) {
+    inner[b] += it_a[b] + (it_b ? it_b[b] : 0);
+    if (rstatus[b] == SNOP_RECAST_DIVERGED) div[b] = 1;
+  }
+}
+
+// k_new = k F1 (old flux had unit fission integral), phi /= F1, convergence on dk and dphi.
+__global__ void __launch_bounds__(HY_THREADS) hy_outer_end(int G, int Nc, double dx, int outer_it, double tol_k,
+                                                           double tol_phi, int norm, const double* __restrict__ nsf,
+                                                           double* __restrict__ phi, const double* __restrict__ old,
+                                                           double* __restrict__ k, uint8_t* __restrict__ active,
+                                                           uint8_t* __restrict__ fb, int32_t* __restrict__ outer,
+                                                           int* __restrict__ n_active) {
+  __shared__ double sh[HY_THREADS / 32];
+  const int b = blockIdx.x;
+  if (!active[b]) return;
+  const size_t GN = (size_t)G * Nc;
+  double* p = phi + b * GN;
+  const double F1 = hy_fission_integral(G, Nc, dx, nsf + b * GN, p, sh);
+  if (!(F1 != 0.0) || !isfinite(F1)) {  // degenerate stage 1 -> cold-start fallback
+    if (threadIdx.x == 0) {
+      active[b] = 0;
+      fb[b] = 1;
+      outer[b] = outer_it;
+    }
+    return;
+  }
+  const double kb = k[b], k_new = kb * F1;
+  double num = 0.0, den = 0.0;
+  for (size_t i = threadIdx.x; i < GN; i += HY_THREADS) {
+    const double pn = p[i] / F1;
+    p[i] = pn;
+    const double d = pn - old[b * GN + i];
+    if (norm == 0) {
+      num = fmax(num, fabs(d));
+      den = fmax(den, fabs(pn));
+    } else {
+      num = fma(d, d, num);
+      den = fma(pn, pn, den);
+    }
+  }
+  if (norm == 0) {
+    num = hy_block_max(num, sh);
+    den = hy_block_max(den, sh);
+  } else {
+    num = hy_block_sum(num, sh);
+    den = hy_block_sum(den, sh);
+  }
+  if (threadIdx.x == 0) {
+    const double dphi = snop_dev::rel_change(num, den, norm);
+    const double dk = fabs(k_new - kb) / fabs(k_new);
+    k[b] = k_new;
+    outer[b] = outer_it;
+    if (dk < tol_k && dphi < tol_phi) active[b] = 0;
+    else atomicAdd(n_active, 1);
+  }
+}
+
+// Stage-2 start: (k_NO, phi_NO), or the flat cold start where stage 1 diverged.
+__global__ void hy_stage2_init(int G, int Nc, double* __restrict__ phi, const double* __restrict__ k1,
+                               double* __restrict__ k0, uint8_t* __restrict__ fb, const uint8_t* __restrict__ div) {
+  const int b = blockIdx.x;
+  const double kb = k1[b];
+  const bool f = fb[b] || div[b] || !isfinite(kb) || !(kb > 0.0);
+  if (f) {
+    const size_t GN = (size_t)G * Nc;
+    for (size_t i = threadIdx.x; i < GN; i += blockDim.x) phi[b * GN + i] = 1.0;
+  }
+  if (threadIdx.x == 0) {
+    fb[b] = f ? 1 : 0;
+    k0[b] = f ? 1.0 : kb;
+  }
+}
+
+struct HybridOut {
+  double *k, *phi, *k1;
+  int32_t *outer1, *outer2;
+  int64_t *inner1, *inner2;
+  uint8_t *conv, *fb;
+};
+
+snop_status hybrid_eigen_dev(Ctx& ctx, snop_op& op, int algorithm, int order, int B, int G, const double* st,
+                             const double* ss0, const double* ss1, const double* nsf, const double* chi,
+                             const snop_solver_config& cfg, double rtol, int rmax, const HybridOut& o) {
+  const int Nc = op.grid.n_cells;
+  const size_t N = (size_t)B * Nc, GNB = N * G;
+  const double dx = op.grid.length_cm / Nc;
+  auto dslot = [&](int i, size_t n) { return static_cast<double*>(ctx.slot(i, n * sizeof(double))); };
+  double *phi1 = dslot(80, GNB), *old = dslot(81, GNB), *fiss = dslot(82, N), *qext = dslot(83, N);
+  double *stg = dslot(84, N), *ssg = dslot(85, N), *s1g = ss1 ? dslot(86, N) : nullptr, *phig = dslot(87, N);
+  double *pred = dslot(88, N), *refined = dslot(89, N), *k0 = dslot(90, B);
+  uint8_t* active = static_cast<uint8_t*>(ctx.slot(91, (size_t)B));
+  uint8_t* div = static_cast<uint8_t*>(ctx.slot(92, (size_t)B));
+  int32_t* rit = static_cast<int32_t*>(ctx.slot(93, (size_t)B * sizeof(int32_t)));
+  int32_t* rst = static_cast<int32_t*>(ctx.slot(94, (size_t)B * sizeof(int32_t)));
+  int32_t* sit = static_cast<int32_t*>(ctx.slot(95, (size_t)B * sizeof(int32_t)));
+  uint8_t* scv = static_cast<uint8_t*>(ctx.slot(96, (size_t)B));
+  int* n_active = static_cast<int*>(ctx.slot(97, sizeof(int)));
+  double* pi_old = dslot(98, GNB);
+  if (!phi1 || !old || !fiss || !qext || !stg || !ssg || (ss1 && !s1g) || !phig || !pred || !refined || !k0 ||
+      !active || !div || !rit || !rst || !sit || !scv || !n_active || !pi_old)
+    return cuda_status("workspace", cudaErrorMemoryAllocation);
+  cudaStream_t s = ctx.stream;
+  hy_init<<<B, HY_THREADS, 0, s>>>(G, Nc, dx, st, nsf, phi1, o.k1, active, o.fb, div, o.outer1, o.inner1,
+                                   ctx.d_flags);
+  ctx.launches++;
+  for (int outer = 1; outer <= cfg.max_outer; ++outer) {
+    hy_outer_begin<<<B, HY_THREADS, 0, s>>>(G, Nc, nsf, phi1, old, fiss, active);
+    ctx.launches++;
+    for (int g = 0; g < G; ++g) {
+      hy_group_in<<<B, HY_THREADS, 0, s>>>(g, G, Nc, chi, o.k1, st, ss0, ss1, phi1, fiss, qext, stg, ssg, s1g, phig);
+      ctx.launches++;
+      SNOP_TRY(recast_fp_dev(ctx, op, B, qext, stg, ssg, rtol, rmax, cfg.norm, phig, pred, rit, rst));
+      const double* result = pred;
+      if (algorithm == 1) {
+        SNOP_TRY(launch_source_iteration(ctx, op.grid, order, B, stg, ssg, s1g, qext, cfg, pred, refined, nullptr,
+                                         sit, scv));
+        result = refined;
+      }
+      hy_group_out<<<B, HY_THREADS, 0, s>>>(g, G, Nc, result, phi1, active, rit, algorithm == 1 ? sit : nullptr,
+                                            rst, o.inner1, div);
+      ctx.launches++;
+    }
+    cudaMemsetAsync(n_active, 0, sizeof(int), s);
+    hy_outer_end<<<B, HY_THREADS, 0, s>>>(G, Nc, dx, outer, cfg.tolerance_k, cfg.tolerance_phi, cfg.norm, nsf, phi1,
+                                          old, o.k1, active, o.fb, o.outer1, n_active);
+    ctx.launches++;
+    int h_active = 0;
+    cudaMemcpyAsync(&h_active, n_active, sizeof(int), cudaMemcpyDeviceToHost, s);
+    SNOP_TRY(cuda_status("hybrid stage 1", cudaStreamSynchronize(s)));
+    if (h_active == 0) break;
+  }
+  hy_stage2_init<<<B, HY_THREADS, 0, s>>>(G, Nc, phi1, o.k1, k0, o.fb, div);
+  ctx.launches++;
+  return launch_power_iteration(ctx, op.grid, order, B, G, st, ss0, ss1, nsf, chi, cfg, k0, phi1, o.k, o.phi,
+                                pi_old, o.outer2, o.inner2, o.conv);
+}
 
 }  // namespace
 
@@ -775,5 +1040,78 @@ snop_status snop_precondition_fixed_source(snop_ctx* ctx, snop_op* op, int32_t m
   }
   return SNOP_OK;
 }
+
+static snop_status hybrid_eigen(snop_ctx* ctx, snop_op* op, int algorithm, int32_t memspace, int32_t order,
+                                int32_t batch, int32_t G, const double* sigma_t, const double* sigma_s0,
+                                const double* sigma_s1, const double* nu_sigma_f, const double* chi,
+                                const snop_solver_config* cfg, double rtol, int32_t rmax, double* k_out,
+                                double* phi_out, double* stage1_k, int32_t* stage1_outer, int64_t* stage1_inner,
+                                int32_t* stage2_outer, int64_t* stage2_inner, uint8_t* converged, uint8_t* fallback) {
+  SNOP_TRY(check_op(ctx, op));
+  if (!cfg) return invalid("config is NULL");
+  if (order < 2 || order > 128 || order % 2) return invalid("quadrature order must be even in [2,128]");
+  if (!(cfg->tolerance > 0.0) || !(cfg->tolerance_k > 0.0) || !(cfg->tolerance_phi > 0.0) || cfg->max_inner < 1 ||
+      cfg->max_outer < 1)
+    return invalid("config: tolerances must be positive and iteration limits >= 1");
+  if (batch < 0 || rmax < 0 || !(rtol > 0.0)) return invalid("bad batch / recast settings");
+  if (G < 1 || G > 64) return invalid("n_groups must be in [1,64]");
+  if (op->grid.n_cells > kMaxCells) return invalid("n_cells exceeds the per-CTA sweep limit");
+  if (batch == 0) return SNOP_OK;
+  if (!sigma_t || !sigma_s0 || !nu_sigma_f || !chi || !k_out || !phi_out || !stage1_k || !stage1_outer ||
+      !stage1_inner || !stage2_outer || !stage2_inner || !converged || !fallback)
+    return invalid("NULL array");
+  const bool host = memspace == SNOP_MEM_HOST;
+  if (!host && memspace != SNOP_MEM_DEVICE) return invalid("memspace must be HOST(0) or DEVICE(1)");
+  cudaSetDevice(ctx->device);
+  const size_t B = batch, n = B * G * op->grid.n_cells;
+  const double *st = sigma_t, *ss = sigma_s0, *s1 = sigma_s1, *nsf = nu_sigma_f, *ch = chi;
+  HybridOut o{k_out, phi_out, stage1_k, stage1_outer, stage2_outer, stage1_inner, stage2_inner, converged, fallback};
+  if (host) {
+    double *a, *b, *c, *d, *e;
+    SNOP_TRY(stage(*ctx, 100, sigma_t, n, &a));
+    SNOP_TRY(stage(*ctx, 101, sigma_s0, n * G, &b));
+    SNOP_TRY(stage(*ctx, 102, sigma_s1, n, &c));
+    SNOP_TRY(stage(*ctx, 103, nu_sigma_f, n, &d));
+    SNOP_TRY(stage(*ctx, 104, chi, B * G, &e));
+    st = a; ss = b; s1 = c; nsf = d; ch = e;
+    o.k = static_cast<double*>(ctx->slot(105, B * sizeof(double)));
+    o.phi = static_cast<double*>(ctx->slot(106, n * sizeof(double)));
+    o.k1 = static_cast<double*>(ctx->slot(107, B * sizeof(double)));
+    o.outer1 = static_cast<int32_t*>(ctx->slot(108, B * sizeof(int32_t)));
+    o.outer2 = static_cast<int32_t*>(ctx->slot(109, B * sizeof(int32_t)));
+    o.inner1 = static_cast<int64_t*>(ctx->slot(110, B * sizeof(int64_t)));
+    o.inner2 = static_cast<int64_t*>(ctx->slot(111, B * sizeof(int64_t)));
+    o.conv = static_cast<uint8_t*>(ctx->slot(112, B));
+    o.fb = static_cast<uint8_t*>(ctx->slot(113, B));
+    if (!o.k || !o.phi || !o.k1 || !o.outer1 || !o.outer2 || !o.inner1 || !o.inner2 || !o.conv || !o.fb)
+      return cuda_status("cudaMalloc", cudaErrorMemoryAllocation);
+  }
+  SNOP_TRY(hybrid_eigen_dev(*ctx, *op, algorithm, order, batch, G, st, ss, s1, nsf, ch, *cfg, rtol, rmax, o));
+  if (!host) return SNOP_OK;
+  SNOP_TRY(unstage(*ctx, k_out, o.k, B));
+  SNOP_TRY(unstage(*ctx, phi_out, o.phi, n));
+  SNOP_TRY(unstage(*ctx, stage1_k, o.k1, B));
+  SNOP_TRY(unstage(*ctx, stage1_outer, o.outer1, B));
+  SNOP_TRY(unstage(*ctx, stage1_inner, o.inner1, B));
+  SNOP_TRY(unstage(*ctx, stage2_outer, o.outer2, B));
+  SNOP_TRY(unstage(*ctx, stage2_inner, o.inner2, B));
+  SNOP_TRY(unstage(*ctx, converged, o.conv, B));
+  SNOP_TRY(unstage(*ctx, fallback, o.fb, B));
+  return drain(*ctx);
+}
+
+#define SNOP_HYBRID_ARGS                                                                                          \
+  snop_ctx *ctx, snop_op *op, int32_t memspace, int32_t order, int32_t batch, int32_t n_groups,                   \
+      const double *sigma_t, const double *sigma_s0, const double *sigma_s1, const double *nu_sigma_f,           \
+      const double *chi, const snop_solver_config *cfg, double recast_tolerance, int32_t recast_max_iterations,   \
+      double *k_out, double *phi_out, double *stage1_k, int32_t *stage1_outer, int64_t *stage1_inner,            \
+      int32_t *stage2_outer, int64_t *stage2_inner, uint8_t *converged, uint8_t *fallback
+#define SNOP_HYBRID_FWD                                                                                          \
+  memspace, order, batch, n_groups, sigma_t, sigma_s0, sigma_s1, nu_sigma_f, chi, cfg, recast_tolerance,         \
+      recast_max_iterations, k_out, phi_out, stage1_k, stage1_outer, stage1_inner, stage2_outer, stage2_inner,    \
+      converged, fallback
+
+snop_status snop_sp_eigen_batched(SNOP_HYBRID_ARGS) { return hybrid_eigen(ctx, op, 0, SNOP_HYBRID_FWD); }
+snop_status snop_cp_eigen_batched(SNOP_HYBRID_ARGS) { return hybrid_eigen(ctx, op, 1, SNOP_HYBRID_FWD); }
 
 }  // extern "C"

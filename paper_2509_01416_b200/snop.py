@@ -392,3 +392,62 @@ def precondition_fixed_source(op: SolutionOperator, order: int, sigma_t, sigma_s
     if a.device:
         op.ctx.synchronize()
     return PreconditionedResult(phi, pit, rst, rit, cv)
+
+
+@dataclass
+class HybridEigenSolution:
+    """EigenSolution + stage diagnostics."""
+    k: object
+    phi: object
+    stage1_k: object
+    stage1_outer: object
+    stage1_inner: object
+    stage2_outer: object
+    stage2_inner: object
+    converged: object
+    fallback: object
+
+
+def _hybrid_eigen(fn: str, op: SolutionOperator, order: int, sigma_t, sigma_s0, nu_sigma_f, chi,
+                  config: SolverConfig | None, recast_tolerance: float, recast_max_iterations: int,
+                  sigma_s1) -> HybridEigenSolution:
+    config = config or SolverConfig()
+    a = _Args(sigma_t, sigma_s0, nu_sigma_f, chi, sigma_s1)
+    B, G, n = (int(x) for x in sigma_t.shape)
+    if n != op.grid.n_cells:
+        raise ValueError("sigma_t last dim must equal the operator grid's n_cells")
+    st = a.inp(sigma_t, shape=(B, G, n))
+    ss = a.inp(sigma_s0, shape=(B, G, G, n))
+    nsf = a.inp(nu_sigma_f, shape=(B, G, n))
+    ch = a.inp(chi, shape=(B, G))
+    s1 = a.inp(sigma_s1, shape=(B, G, n))
+    k, k_p = a.out((B,))
+    phi, phi_p = a.out((B, G, n))
+    k1, k1_p = a.out((B,))
+    o1, o1_p = a.out((B,), np.int32)
+    i1, i1_p = a.out((B,), np.int64)
+    o2, o2_p = a.out((B,), np.int32)
+    i2, i2_p = a.out((B,), np.int64)
+    cv, cv_p = a.out((B,), np.uint8)
+    fb, fb_p = a.out((B,), np.uint8)
+    cfg = config.c()
+    _capi.check(getattr(op.ctx._lib, fn)(
+        op.ctx.h, op.h, a.memspace, int(order), B, G, st, ss, s1, nsf, ch, C.byref(cfg), float(recast_tolerance),
+        int(recast_max_iterations), k_p, phi_p, k1_p, o1_p, i1_p, o2_p, i2_p, cv_p, fb_p))
+    if a.device:
+        op.ctx.synchronize()
+    return HybridEigenSolution(k, phi, k1, o1, i1, o2, i2, cv, fb)
+
+
+def sp_eigen(op: SolutionOperator, order: int, sigma_t, sigma_s0, nu_sigma_f, chi, config: SolverConfig | None = None,
+             recast_tolerance: float = 1e-4, recast_max_iterations: int = 50, sigma_s1=None) -> HybridEigenSolution:
+    """SP eigen solve (paper Eq. A5-A6), batched; layouts as power_iteration."""
+    return _hybrid_eigen("snop_sp_eigen_batched", op, order, sigma_t, sigma_s0, nu_sigma_f, chi, config,
+                         recast_tolerance, recast_max_iterations, sigma_s1)
+
+
+def cp_eigen(op: SolutionOperator, order: int, sigma_t, sigma_s0, nu_sigma_f, chi, config: SolverConfig | None = None,
+             recast_tolerance: float = 1e-4, recast_max_iterations: int = 50, sigma_s1=None) -> HybridEigenSolution:
+    """CP eigen solve (paper Eq. A7-A8), batched; layouts as power_iteration."""
+    return _hybrid_eigen("snop_cp_eigen_batched", op, order, sigma_t, sigma_s0, nu_sigma_f, chi, config,
+                         recast_tolerance, recast_max_iterations, sigma_s1)

@@ -71,6 +71,15 @@ int main() {
   ec.tolerance_phi = 1e-7;
   auto e = power_iteration(ctx, g, 32, mg, ec);
   EXPECT(std::fabs(e.k[0] - 1.30621) < 5e-5 && e.converged[0] == 1);
+  // CP eigen with the exact operator at p* = (1.0, 0.5): stage 2 reproduces the
+  // model-based k; CP stage 1 already sits at it.
+  {
+    SolverConfig oc = ec;
+    auto xop = SolutionOperator::exact(ctx, g, 32, 1.0, 0.5, oc);
+    auto h = hybrid_eigen(HybridAlgorithm::CP, xop, 32, mg, ec);
+    EXPECT(std::fabs(h.k[0] - e.k[0]) < 1e-6 && h.converged[0] == 1 && h.fallback[0] == 0);
+    EXPECT(std::fabs(h.stage1_k[0] - e.k[0]) < 1e-5);
+  }
   // zero fission -> DegenerateProblem
   mg.nu_sigma_f.assign(300, 0.0);
   try {

@@ -238,6 +238,29 @@ class OracleOperator:
         return {"phi": phi, "precond_iterations": pit, "recast_status": rst, "refine_iterations": rit,
                 "converged": cv.astype(bool)}
 
+    def hybrid_eigen(self, algorithm, order, sigma_t, sigma_s0, nu_sigma_f, chi, cfg, rtol=1e-4, rmax=50,
+                     sigma_s1=None, n_threads=0):
+        """SP (algorithm 0) / CP (1) eigen solve."""
+        st = np.ascontiguousarray(sigma_t, dtype=np.float64)
+        B, G, n = st.shape
+        k = np.empty(B)
+        phi = np.empty((B, G, n))
+        k1 = np.empty(B)
+        o1 = np.empty(B, dtype=np.int32)
+        i1 = np.empty(B, dtype=np.int64)
+        o2 = np.empty(B, dtype=np.int32)
+        i2 = np.empty(B, dtype=np.int64)
+        cv = np.empty(B, dtype=np.uint8)
+        fb = np.empty(B, dtype=np.uint8)
+        _check(lib().oracle_sp_cp_eigen_batched(
+            self.h, C.c_int32(algorithm), C.c_int32(order), C.c_int32(B), C.c_int32(G), _p(st),
+            _p(np.ascontiguousarray(sigma_s0, dtype=np.float64)), _opt(sigma_s1),
+            _p(np.ascontiguousarray(nu_sigma_f, dtype=np.float64)), _p(np.ascontiguousarray(chi, dtype=np.float64)),
+            C.byref(cfg), C.c_double(rtol), C.c_int32(rmax), _p(k), _p(phi), _p(k1), _p(o1), _p(i1), _p(o2),
+            _p(i2), _p(cv), _p(fb), C.c_int32(n_threads)))
+        return {"k": k, "phi": phi, "stage1_k": k1, "stage1_outer": o1, "stage1_inner": i1, "stage2_outer": o2,
+                "stage2_inner": i2, "converged": cv.astype(bool), "fallback": fb.astype(bool)}
+
 
 __all__ = ["lib", "gauss_legendre", "source_iteration", "power_iteration", "infinite_medium_k", "recast_source",
            "OracleOperator", "make_config", "make_grid", "SnopSolverConfig", "SnopGrid", "balance_residual",
