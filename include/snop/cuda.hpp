@@ -225,6 +225,16 @@ class SolutionOperator {
     return SolutionOperator(ctx, op, grid.n_cells);
   }
 
+  // load_model / save_model: DeepONet or FNO model files.
+  static SolutionOperator load(Context& ctx, const std::string& path) {
+    snop_model_info info{};
+    check(snop_model_inspect(path.c_str(), &info));
+    snop_op* op = nullptr;
+    check(snop_op_load(ctx.get(), path.c_str(), &op));
+    return SolutionOperator(ctx, op, info.grid.n_cells);
+  }
+  void save(const std::string& path) const { check(snop_op_save(op_, path.c_str())); }
+
   SolutionOperator(SolutionOperator&& o) noexcept : ctx_(o.ctx_), op_(o.op_), n_(o.n_) { o.op_ = nullptr; }
 
  private:

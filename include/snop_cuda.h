@@ -67,6 +67,20 @@ typedef struct {
   int32_t reserved;
 } snop_solver_config;
 
+/* Model-file architecture tags and header summary (snop_model_inspect). */
+typedef enum { SNOP_ARCH_DEEPONET = 0, SNOP_ARCH_FNO = 1 } snop_arch;
+typedef struct {
+  int32_t arch;              /* snop_arch */
+  snop_grid grid;            /* grid provenance */
+  double sigma_t_star;       /* p* */
+  double sigma_s0_star;
+  int32_t activation;        /* snop_activation */
+  int64_t n_params;
+  int32_t n_branch, n_trunk, latent, has_bias0;  /* DeepONet */
+  float bias0;
+  int32_t width, modes, layers, hidden;          /* FNO */
+} snop_model_info;
+
 typedef struct snop_ctx snop_ctx;  /* owns one CUDA stream + device workspace */
 typedef struct snop_op snop_op;    /* SolutionOperator handle */
 
@@ -142,6 +156,26 @@ snop_status snop_exact_operator_create(
     const snop_solver_config* cfg, snop_op** out);
 
 snop_status snop_op_destroy(snop_op* op);
+
+/* save_model / load_model (file format SPEC.md:373): versioned little-endian
+ * record + trailing FNV-1a-64 digest in the reference's binary container
+ * (proj/core/include/snop/binary_io.hpp:12-62); record layout in csrc/model_io.h. Load errors
+ * (missing file, bad magic, version mismatch, truncation, checksum failure) -> SNOP_IO_ERROR.
+ * save -> load -> predict is bit-identical to predict before save. The exact operator has no
+ * weights and cannot be saved (SNOP_INVALID_ARGUMENT). */
+snop_status snop_op_save(const snop_op* op, const char* path);
+snop_status snop_op_load(snop_ctx* ctx, const char* path, snop_op** out);
+/* Host-only (no GPU needed): write a model file from parameters laid out as for
+ * snop_deeponet_create / snop_fno_create, and read + validate a file's header. */
+snop_status snop_model_write_deeponet(const char* path, const snop_grid* grid, double sigma_t_star,
+                                      double sigma_s0_star, int32_t activation, int32_t n_branch,
+                                      const int32_t* branch_sizes, const float* branch_params,
+                                      int32_t n_trunk, const int32_t* trunk_sizes,
+                                      const float* trunk_params, int32_t has_bias0, float bias0);
+snop_status snop_model_write_fno(const char* path, const snop_grid* grid, double sigma_t_star,
+                                 double sigma_s0_star, int32_t activation, int32_t width, int32_t modes,
+                                 int32_t layers, int32_t hidden, const float* params);
+snop_status snop_model_inspect(const char* path, snop_model_info* info);
 
 /* predict(model, source) for a batch [B][Nc]; fp64 in/out, the neural
  * operators compute in fp32. */

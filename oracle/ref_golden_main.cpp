@@ -61,7 +61,63 @@ int main(int argc, char** argv) {
     int ch;
     while ((ch = std::fgetc(f)) != EOF) std::printf("%02x", ch);
     std::fclose(f);
-    std::printf("\"}\n}\n");
+    std::printf("\"},\n");
   }
+  // Model files written through the reference's own BinaryWriter with the
+  // record of paper_2509_01416_b200/csrc/model_io.h; tiny fixed architectures, parameters
+  // exactly representable in fp32 (tests/test_model_io.py regenerates them the same way).
+  {
+    auto hex_of = [&](const char* label, bool last) {
+      std::FILE* f = std::fopen(tmpfile, "rb");
+      std::printf("  \"%s\": \"", label);
+      int ch;
+      while ((ch = std::fgetc(f)) != EOF) std::printf("%02x", ch);
+      std::fclose(f);
+      std::printf("\"%s\n", last ? "" : ",");
+    };
+    {
+      snop::BinaryWriter w(tmpfile);
+      w.write_string("SNOP-MODEL");
+      w.write_u32(1);
+      w.write_string("deeponet");
+      w.write_f64(10.0);
+      w.write_u64(4);
+      w.write_f64(1.0);
+      w.write_f64(0.5);
+      w.write_u32(1);  // tanh
+      const unsigned long long bs[3] = {4, 3, 2}, ts[3] = {1, 3, 2};
+      w.write_u32(3);
+      for (auto v : bs) w.write_u64(v);
+      w.write_u32(3);
+      for (auto v : ts) w.write_u64(v);
+      w.write_u8(1);
+      w.write_f64(0.125);
+      const int nbp = 4 * 3 + 3 + 3 * 2 + 2, ntp = 1 * 3 + 3 + 3 * 2 + 2;
+      w.write_u64(nbp + ntp);
+      for (int i = 0; i < nbp; ++i) w.write_f64((double)(((i % 7) - 3) * 0.125f));
+      for (int i = 0; i < ntp; ++i) w.write_f64((double)(((i % 5) - 2) * 0.25f));
+      w.finish();
+      hex_of("model_deeponet_hex", false);
+    }
+    {
+      snop::BinaryWriter w(tmpfile);
+      w.write_string("SNOP-MODEL");
+      w.write_u32(1);
+      w.write_string("fno");
+      w.write_f64(10.0);
+      w.write_u64(8);
+      w.write_f64(1.0);
+      w.write_f64(0.8);
+      w.write_u32(2);  // gelu
+      const unsigned long long dims[4] = {2, 2, 1, 3};  // width, modes, layers, hidden
+      for (auto v : dims) w.write_u64(v);
+      const int np = 3 * 2 + 1 * (2 * 2 * 2 * 2 + 2 * 2 + 2) + 3 * 2 + 2 * 3 + 1;
+      w.write_u64(np);
+      for (int i = 0; i < np; ++i) w.write_f64((double)((float)(((i * 3) % 11) - 5) / 16.0f));
+      w.finish();
+      hex_of("model_fno_hex", true);
+    }
+  }
+  std::printf("}\n");
   return 0;
 }

@@ -3,7 +3,9 @@
 // host pointers only. Batched entry points parallelise over instances with the restated
 // parallel_chunks (proj/core/include/snop/parallel.hpp:17-48): one chunk per instance, so
 // results are bit-identical at any thread count.
+#include <cstdio>
 #include <cstring>
+#include <stdexcept>
 #include <memory>
 #include <mutex>
 #include <thread>
@@ -264,6 +266,107 @@ void* oracle_fno_create(const snop_grid* grid, double tstar, double sstar, int32
   f.P2_W = take(hidden);
   f.P2_b = take(1);
   return op;
+}
+
+// load_model: streaming restatement of the reader side of the reference's
+// binary container (binary_io.cpp:12-17 FNV-1a-64 running hash; :88-141 little-endian reads,
+// truncation error, trailing-digest verify) over the record of csrc/model_io.h.
+namespace {
+struct IoFail : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct StreamReader {
+  std::FILE* f = nullptr;
+  std::uint64_t h = 0xcbf29ce484222325ull;
+  ~StreamReader() { if (f) std::fclose(f); }
+  void bytes(unsigned char* p, std::size_t n) {
+    if (std::fread(p, 1, n, f) != n) throw IoFail("unexpected end of file (truncated?)");
+    for (std::size_t i = 0; i < n; ++i) h = (h ^ p[i]) * 0x100000001b3ull;
+  }
+  std::uint64_t uint(int n) {
+    unsigned char b[8];
+    bytes(b, n);
+    std::uint64_t v = 0;
+    for (int i = n - 1; i >= 0; --i) v = (v << 8) | b[i];
+    return v;
+  }
+  double f64() {
+    const std::uint64_t u = uint(8);
+    double d;
+    std::memcpy(&d, &u, 8);
+    return d;
+  }
+  std::string str() {
+    const std::uint64_t n = uint(4);
+    if (n > 4096) throw IoFail("string length implausible");
+    std::string s(n, '\0');
+    bytes(reinterpret_cast<unsigned char*>(s.data()), n);
+    return s;
+  }
+  void verify() {
+    const std::uint64_t expect = h;
+    unsigned char b[8];
+    if (std::fread(b, 1, 8, f) != 8) throw IoFail("checksum missing (truncated file)");
+    std::uint64_t v = 0;
+    for (int i = 7; i >= 0; --i) v = (v << 8) | b[i];
+    if (v != expect) throw IoFail("checksum mismatch");
+    if (std::fgetc(f) != EOF) throw IoFail("trailing bytes after checksum");
+  }
+};
+}  // namespace
+
+int oracle_model_load(const char* path, void** out) {
+  *out = nullptr;
+  try {
+    StreamReader r;
+    r.f = std::fopen(path, "rb");
+    if (!r.f) throw IoFail("cannot open");
+    if (r.str() != "SNOP-MODEL") throw IoFail("bad magic");
+    if (r.uint(4) != 1) throw IoFail("version mismatch");
+    const std::string arch = r.str();
+    snop_grid g{};
+    g.length_cm = r.f64();
+    g.n_cells = (int32_t)r.uint(8);
+    const double tstar = r.f64(), sstar = r.f64();
+    const int act = (int)r.uint(4);
+    std::vector<int32_t> bs, ts;
+    bool hb = false;
+    double b0 = 0.0;
+    std::uint64_t arch_dims[4] = {0, 0, 0, 0};
+    if (arch == "deeponet") {
+      for (auto* v : {&bs, &ts}) {
+        const std::uint64_t n = r.uint(4);
+        if (n > 64) throw IoFail("implausible layer count");
+        for (std::uint64_t i = 0; i < n; ++i) v->push_back((int32_t)r.uint(8));
+      }
+      hb = r.uint(1) != 0;
+      b0 = r.f64();
+    } else if (arch == "fno") {
+      for (auto& d : arch_dims) d = r.uint(8);
+    } else {
+      throw IoFail("unknown architecture");
+    }
+    const std::uint64_t np = r.uint(8);
+    if (np > (1ull << 32)) throw IoFail("implausible parameter count");
+    std::vector<float> prm(np);
+    for (auto& x : prm) x = (float)r.f64();
+    r.verify();
+    if (arch == "deeponet") {
+      std::size_t nbp = 0;
+      for (std::size_t l = 0; l + 1 < bs.size(); ++l) nbp += (std::size_t)bs[l] * bs[l + 1] + bs[l + 1];
+      *out = oracle_deeponet_create(&g, tstar, sstar, act, (int32_t)bs.size(), bs.data(), prm.data(),
+                                    (int32_t)ts.size(), ts.data(), prm.data() + nbp, hb ? 1 : 0, (float)b0);
+    } else {
+      *out = oracle_fno_create(&g, tstar, sstar, act, (int32_t)arch_dims[0], (int32_t)arch_dims[1],
+                               (int32_t)arch_dims[2], (int32_t)arch_dims[3], prm.data());
+    }
+    return 0;
+  } catch (const IoFail& e) {
+    g_err = std::string("model load: ") + e.what();
+    return SNOP_IO_ERROR;
+  } catch (...) {
+    return map_exc();
+  }
 }
 
 void* oracle_exact_operator_create(const snop_grid* grid, int32_t order, double tstar, double sstar,

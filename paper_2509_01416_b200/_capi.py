@@ -10,7 +10,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-from ._types import STATUS_NAMES, SnopGrid, SnopSolverConfig
+from ._types import STATUS_NAMES, SnopGrid, SnopModelInfo, SnopSolverConfig
 from .errors import raise_for_status
 
 PKG = Path(__file__).resolve().parent
@@ -23,6 +23,7 @@ EXPORTS = [
     "snop_power_iteration_batched", "snop_recast_source", "snop_deeponet_create", "snop_fno_create",
     "snop_exact_operator_create", "snop_op_destroy", "snop_op_predict", "snop_recast_fixed_point",
     "snop_precondition_fixed_source", "snop_sp_eigen_batched", "snop_cp_eigen_batched",
+    "snop_op_save", "snop_op_load", "snop_model_write_deeponet", "snop_model_write_fno", "snop_model_inspect",
 ]
 
 _lib = None
@@ -71,6 +72,12 @@ def load():
     for fn in ("snop_sp_eigen_batched", "snop_cp_eigen_batched"):
         getattr(lib, fn).argtypes = [vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, C.POINTER(SnopSolverConfig), dbl,
                                      i32, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    lib.snop_op_save.argtypes = [vp, C.c_char_p]
+    lib.snop_op_load.argtypes = [vp, C.c_char_p, C.POINTER(vp)]
+    lib.snop_model_write_deeponet.argtypes = [C.c_char_p, C.POINTER(SnopGrid), dbl, dbl, i32, i32, vp, vp, i32, vp,
+                                              vp, i32, C.c_float]
+    lib.snop_model_write_fno.argtypes = [C.c_char_p, C.POINTER(SnopGrid), dbl, dbl, i32, i32, i32, i32, i32, vp]
+    lib.snop_model_inspect.argtypes = [C.c_char_p, C.POINTER(SnopModelInfo)]
     _lib = lib
     return lib
 

@@ -23,6 +23,26 @@ class SnopSolverConfig(C.Structure):
     ]
 
 
+class SnopModelInfo(C.Structure):
+    _fields_ = [
+        ("arch", C.c_int32),
+        ("grid", SnopGrid),
+        ("sigma_t_star", C.c_double),
+        ("sigma_s0_star", C.c_double),
+        ("activation", C.c_int32),
+        ("n_params", C.c_int64),
+        ("n_branch", C.c_int32),
+        ("n_trunk", C.c_int32),
+        ("latent", C.c_int32),
+        ("has_bias0", C.c_int32),
+        ("bias0", C.c_float),
+        ("width", C.c_int32),
+        ("modes", C.c_int32),
+        ("layers", C.c_int32),
+        ("hidden", C.c_int32),
+    ]
+
+
 def make_grid(length: float, n_cells: int) -> SnopGrid:
     return SnopGrid(float(length), int(n_cells), 0)
 

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "gemm.cuh"
+#include "model_io.h"
 #include "snop_internal.h"
 
 using namespace snop_impl;
@@ -27,6 +28,9 @@ struct snop_op {
   std::vector<float*> bW, bb;  // device, per branch layer
   float* trunk_out = nullptr;  // [Nc][p] trunk evaluated at the cell centres (once)
   float* bias0_vec = nullptr;  // [Nc] filled with bias0 (or nullptr)
+  bool has_bias0 = false;
+  float bias0 = 0.f;
+  std::vector<float> host_params;  // as created (save_model); DeepONet: branch then trunk
   // FNO
   int width = 64, modes = 16, layers = 4, hidden = 128;
   float *lift_W = nullptr, *lift_b = nullptr, *xc = nullptr;
@@ -789,6 +793,14 @@ snop_status snop_deeponet_create(snop_ctx* ctx, const snop_grid* grid, double ts
   op->act = act;
   op->bsizes.assign(bs, bs + nb);
   op->tsizes.assign(ts, ts + nt);
+  op->has_bias0 = has_bias0 != 0;
+  op->bias0 = bias0;
+  {
+    const size_t nbp = dense_param_count(std::vector<int32_t>(bs, bs + nb));
+    const size_t ntp = dense_param_count(std::vector<int32_t>(ts, ts + nt));
+    op->host_params.assign(bp, bp + nbp);
+    op->host_params.insert(op->host_params.end(), tp, tp + ntp);
+  }
   size_t off = 0;
   for (int l = 0; l + 1 < nb; ++l) {
     const size_t nw = (size_t)bs[l] * bs[l + 1];
@@ -859,6 +871,7 @@ snop_status snop_fno_create(snop_ctx* ctx, const snop_grid* grid, double tstar, 
   op->modes = modes;
   op->layers = layers;
   op->hidden = hidden;
+  op->host_params.assign(p, p + fno_param_count(width, modes, layers, hidden));
   const size_t C = width, M = modes;
   op->lift_W = op->upload(p, C * 2);
   p += C * 2;
@@ -926,6 +939,48 @@ snop_status snop_exact_operator_create(snop_ctx* ctx, const snop_grid* grid, int
   op->cfg = *cfg;
   *out = op;
   return SNOP_OK;
+}
+
+snop_status snop_op_save(const snop_op* op, const char* path) {
+  if (!op) return invalid("op is NULL");
+  ModelFile m;
+  m.grid = op->grid;
+  m.tstar = op->tstar;
+  m.sstar = op->sstar;
+  m.act = op->act;
+  m.params = op->host_params;
+  if (op->kind == 0) {
+    m.arch = SNOP_ARCH_DEEPONET;
+    m.bs.assign(op->bsizes.begin(), op->bsizes.end());
+    m.ts.assign(op->tsizes.begin(), op->tsizes.end());
+    m.has_bias0 = op->has_bias0;
+    m.bias0 = op->bias0;
+  } else if (op->kind == 1) {
+    m.arch = SNOP_ARCH_FNO;
+    m.width = op->width;
+    m.modes = op->modes;
+    m.layers = op->layers;
+    m.hidden = op->hidden;
+  } else {
+    return invalid("the exact operator has no weights to save");
+  }
+  return write_model(path, m);
+}
+
+snop_status snop_op_load(snop_ctx* ctx, const char* path, snop_op** out) {
+  if (!out) return invalid("out is NULL");
+  *out = nullptr;
+  if (!ctx) return invalid("ctx is NULL");
+  ModelFile m;
+  SNOP_TRY(read_model(path, m));
+  if (m.arch == SNOP_ARCH_DEEPONET) {
+    const size_t nbp = dense_param_count(m.bs);
+    return snop_deeponet_create(ctx, &m.grid, m.tstar, m.sstar, m.act, (int32_t)m.bs.size(), m.bs.data(),
+                                m.params.data(), (int32_t)m.ts.size(), m.ts.data(), m.params.data() + nbp,
+                                m.has_bias0 ? 1 : 0, m.bias0, out);
+  }
+  return snop_fno_create(ctx, &m.grid, m.tstar, m.sstar, m.act, m.width, m.modes, m.layers, m.hidden,
+                         m.params.data(), out);
 }
 
 snop_status snop_op_destroy(snop_op* op) {

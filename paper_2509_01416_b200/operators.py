@@ -104,3 +104,47 @@ def fno_init(width: int = 64, modes: int = 16, layers: int = 4, hidden: int = 12
     P2_W = _xavier(r, hidden, 1)
     return FNOParams(width, modes, layers, hidden, activation, lift_W, lift_b, R_re, R_im, W, b, P1_W,
                      np.zeros(hidden, np.float32), P2_W.reshape(-1), np.zeros(1, np.float32))
+
+
+def dense_from_packed(sizes, flat) -> DenseParams:
+    """Inverse of DenseParams.packed(): per layer W[n_out][n_in] then b[n_out]."""
+    flat = np.asarray(flat, dtype=np.float32)
+    Ws, bs, off = [], [], 0
+    for i in range(len(sizes) - 1):
+        n_in, n_out = int(sizes[i]), int(sizes[i + 1])
+        Ws.append(flat[off:off + n_in * n_out].reshape(n_out, n_in).copy())
+        off += n_in * n_out
+        bs.append(flat[off:off + n_out].copy())
+        off += n_out
+    if off != flat.size:
+        raise ValueError("parameter vector length does not match the layer sizes")
+    return DenseParams(list(int(s) for s in sizes), Ws, bs)
+
+
+def fno_from_packed(width, modes, layers, hidden, activation, flat) -> FNOParams:
+    """Inverse of FNOParams.packed()."""
+    flat = np.asarray(flat, dtype=np.float32)
+    C, M, H = int(width), int(modes), int(hidden)
+    off = 0
+
+    def take(n, shape=None):
+        nonlocal off
+        v = flat[off:off + n].copy()
+        off += n
+        return v.reshape(shape) if shape else v
+
+    lift_W = take(2 * C, (C, 2))
+    lift_b = take(C)
+    R_re, R_im, W, b = [], [], [], []
+    for _ in range(int(layers)):
+        R_re.append(take(M * C * C, (M, C, C)))
+        R_im.append(take(M * C * C, (M, C, C)))
+        W.append(take(C * C, (C, C)))
+        b.append(take(C))
+    P1_W = take(H * C, (H, C))
+    P1_b = take(H)
+    P2_W = take(H)
+    P2_b = take(1)
+    if off != flat.size:
+        raise ValueError("parameter vector length does not match the FNO architecture")
+    return FNOParams(C, M, int(layers), H, int(activation), lift_W, lift_b, R_re, R_im, W, b, P1_W, P1_b, P2_W, P2_b)

@@ -12,16 +12,19 @@ in PyTorch. Arrays may be numpy (host memory: the call stages H2D/D2H) or CUDA t
   predict
   recast_fixed_point
   precondition_fixed_source SPEC.md:413-421
+  sp_eigen / cp_eigen
+  save_model / load_model
 """
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _capi
-from ._types import SnopGrid, SnopSolverConfig, make_grid
+from ._types import SnopGrid, SnopModelInfo, SnopSolverConfig, make_grid
 
 VACUUM, REFLECTIVE = 0, 1
 REL_LINF, REL_L2 = 0, 1
@@ -323,6 +326,20 @@ class SolutionOperator:
                                                         float(reference_params[1]), C.byref(cfg), C.byref(h)))
         return cls(h, grid, reference_params, ctx)
 
+    @classmethod
+    def load(cls, path, ctx: Context | None = None):
+        """load_model(path): DeepONet or FNO from a model file."""
+        ctx = ctx or default_context()
+        info = inspect_model(path)
+        h = C.c_void_p()
+        _capi.check(ctx._lib.snop_op_load(ctx.h, os.fsencode(path), C.byref(h)))
+        grid = Grid1D(info.grid.length_cm, info.grid.n_cells)
+        return cls(h, grid, (info.sigma_t_star, info.sigma_s0_star), ctx)
+
+    def save(self, path) -> None:
+        """save_model(model, path) (SPEC.md:349-357)."""
+        _capi.check(self.ctx._lib.snop_op_save(self.h, os.fsencode(path)))
+
     def predict(self, source, sync: bool = True):
         """predict(model, source) (SPEC.md:319-322), batched [B][Nc]."""
         a = _Args(source)
@@ -451,3 +468,34 @@ def cp_eigen(op: SolutionOperator, order: int, sigma_t, sigma_s0, nu_sigma_f, ch
     """CP eigen solve (paper Eq. A7-A8), batched; layouts as power_iteration."""
     return _hybrid_eigen("snop_cp_eigen_batched", op, order, sigma_t, sigma_s0, nu_sigma_f, chi, config,
                          recast_tolerance, recast_max_iterations, sigma_s1)
+
+
+# ---- model files (host-only; no GPU needed) -----------------------------------------------------
+def write_deeponet_file(path, grid: Grid1D, params, reference_params=(1.0, 0.5)) -> None:
+    """Write a DeepONet model file (record layout csrc/model_io.h)."""
+    lib = _capi.load()
+    bs = np.ascontiguousarray(params.branch.sizes, dtype=np.int32)
+    ts = np.ascontiguousarray(params.trunk.sizes, dtype=np.int32)
+    bp, tp = params.branch.packed(), params.trunk.packed()
+    g = grid.c()
+    _capi.check(lib.snop_model_write_deeponet(
+        os.fsencode(path), C.byref(g), float(reference_params[0]), float(reference_params[1]), int(params.activation),
+        len(bs), bs.ctypes.data, bp.ctypes.data, len(ts), ts.ctypes.data, tp.ctypes.data,
+        int(params.bias0 is not None), float(params.bias0 or 0.0)))
+
+
+def write_fno_file(path, grid: Grid1D, params, reference_params=(1.0, 0.8)) -> None:
+    """Write an FNO model file (record layout csrc/model_io.h)."""
+    lib = _capi.load()
+    p = params.packed()
+    g = grid.c()
+    _capi.check(lib.snop_model_write_fno(os.fsencode(path), C.byref(g), float(reference_params[0]),
+                                         float(reference_params[1]), int(params.activation), int(params.width),
+                                         int(params.modes), int(params.layers), int(params.hidden), p.ctypes.data))
+
+
+def inspect_model(path) -> SnopModelInfo:
+    """Read and validate a model file (magic, version, record, FNV-1a-64 digest); header summary."""
+    info = SnopModelInfo()
+    _capi.check(_capi.load().snop_model_inspect(os.fsencode(path), C.byref(info)))
+    return info

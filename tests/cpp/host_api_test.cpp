@@ -97,6 +97,14 @@ int main() {
   auto rf = recast_fixed_point(op, std::vector<double>(100, 0.1), std::vector<double>(100, 1.0),
                                std::vector<double>(100, 0.5));
   EXPECT(rf.status[0] == SNOP_RECAST_CONVERGED && rf.iterations[0] <= 2);
+  {  // save_model -> load_model -> predict bit-identical is covered in Python; here the
+    // exact operator must refuse to save (no weights)
+    try {
+      op.save("/tmp/snop_host_api_exact.bin");
+      EXPECT(false);
+    } catch (const snop::InvalidArgument&) {
+    }
+  }
   std::printf("host_api_test: all passed (Table-9 k = %.6f)\n", e.k[0]);
   return 0;
 }
