@@ -81,6 +81,26 @@ typedef struct {
   int32_t width, modes, layers, hidden;          /* FNO */
 } snop_model_info;
 
+/* GrfSpec: paper Appendix A1 defaults mean 0.07, variance 3e-4, length
+ * scale 1.2 cm, jitter 1e-10; sample s of a stream draws from Rng(seed + s). */
+typedef struct {
+  double mean;
+  double variance;
+  double length_scale_cm;
+  double jitter;
+  uint64_t seed;
+} snop_grf_spec;
+
+/* Training-dataset provenance. */
+typedef struct {
+  int64_t n_samples;
+  snop_grid grid;
+  int32_t order;
+  int32_t reserved;
+  snop_grf_spec spec;
+  double sigma_t_star, sigma_s0_star, tolerance;
+} snop_dataset_info;
+
 typedef struct snop_ctx snop_ctx;  /* owns one CUDA stream + device workspace */
 typedef struct snop_op snop_op;    /* SolutionOperator handle */
 
@@ -222,6 +242,36 @@ snop_status snop_cp_eigen_batched(
     int32_t recast_max_iterations, double* k_out, double* phi_out, double* stage1_k,
     int32_t* stage1_outer, int64_t* stage1_inner, int32_t* stage2_outer, int64_t* stage2_inner,
     uint8_t* converged, uint8_t* fallback);
+
+/* sample_grf: field[s][i] = mean + (L z_s)_i, L L^T = C + jitter variance I
+ * (squared-exponential kernel at the cell centres; jitter relative to the variance, escalated x10
+ * up to 1e-6), z_s = the first n_cells
+ * normals of snop::Rng(seed + first_sample + s) (rng.hpp:17-49). negatives[s] (nullable) counts
+ * negative entries (reported, never clipped). n_cells >= 2. */
+snop_status snop_grf_sample(snop_ctx* ctx, int32_t memspace, const snop_grid* grid, const snop_grf_spec* spec,
+                            int64_t first_sample, int32_t n_samples, double* field_out, int64_t* negatives);
+
+/* normalize_source (paper Eq. 13): out = raw / (dx sum raw) per sample;
+ * SNOP_INVALID_ARGUMENT naming the first sample whose integral is <= 0. */
+snop_status snop_normalize_source(snop_ctx* ctx, int32_t memspace, const snop_grid* grid, int32_t n_samples,
+                                  const double* raw, double* out);
+
+/* generate_dataset: sample s = normalize(sample_grf(seed + s)) and its flux from
+ * the source iteration at p* = (sigma_t*, sigma_s0*) (vacuum, zero initial guess, tolerance).
+ * Any non-convergent sample -> SNOP_NUMERICAL_ERROR naming the sample index. */
+snop_status snop_generate_dataset(snop_ctx* ctx, int32_t memspace, const snop_grid* grid, int32_t order,
+                                  const snop_grf_spec* spec, int32_t n_samples, double sigma_t_star,
+                                  double sigma_s0_star, double tolerance, double* sources, double* fluxes,
+                                  int32_t* iterations);
+
+/* Dataset file, host-only: versioned header (format version, n_samples, n_cells,
+ * grid, GRF spec, p*, solver tolerance), sources then fluxes as row-major little-endian f64, and
+ * a trailing FNV-1a-64 digest (the reference container, binary_io.hpp:12-62); a text manifest is
+ * written alongside at "<path>.txt". snop_dataset_read fills info and, when non-NULL, the
+ * [n_samples][n_cells] arrays (call once with NULL arrays to size them). */
+snop_status snop_dataset_write(const char* path, const snop_dataset_info* info, const double* sources,
+                               const double* fluxes);
+snop_status snop_dataset_read(const char* path, snop_dataset_info* info, double* sources, double* fluxes);
 
 #ifdef __cplusplus
 }

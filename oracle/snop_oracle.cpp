@@ -471,4 +471,60 @@ RecastResult recast_fixed_point(int n, const double* S, const double* st, const 
   return r;
 }
 
+// --- grf -----------------------------------------------------------------------
+std::vector<double> grf_cholesky(const Grid1D& g, const GrfSpec& spec, double* jitter_used) {
+  if (!(spec.variance > 0.0) || !(spec.length_scale > 0.0) || !(spec.jitter > 0.0))
+    throw InvalidArgument("grf: variance, length scale and jitter must be positive");
+  if (g.n_cells < 2) throw InvalidArgument("grf: n_cells must be >= 2");
+  const int n = g.n_cells;
+  const double inv2l2 = 1.0 / (2.0 * spec.length_scale * spec.length_scale);
+  std::vector<double> L((std::size_t)n * n);
+  for (double jitter = spec.jitter; jitter <= 1e-6 * (1.0 + 1e-12); jitter *= 10.0) {
+    std::fill(L.begin(), L.end(), 0.0);
+    bool ok = true;
+    for (int i = 0; i < n && ok; ++i) {
+      for (int j = 0; j <= i; ++j) {
+        const double d = g.center(i) - g.center(j);
+        double s = spec.variance * (std::exp(-d * d * inv2l2) + (i == j ? jitter : 0.0));
+        for (int k = 0; k < j; ++k) s -= L[(std::size_t)i * n + k] * L[(std::size_t)j * n + k];
+        if (i == j) {
+          if (!(s > 0.0)) { ok = false; break; }
+          L[(std::size_t)i * n + i] = std::sqrt(s);
+        } else {
+          L[(std::size_t)i * n + j] = s / L[(std::size_t)j * n + j];
+        }
+      }
+    }
+    if (ok) {
+      if (jitter_used) *jitter_used = jitter;
+      return L;
+    }
+  }
+  throw NumericalError("grf: covariance factorization failed after jitter escalation to 1e-6");
+}
+
+long long sample_grf(const Grid1D& g, const GrfSpec& spec, const std::vector<double>& L, std::uint64_t sample,
+                     double* out) {
+  const int n = g.n_cells;
+  Rng r(spec.seed + sample);
+  std::vector<double> z(n);
+  for (int j = 0; j < n; ++j) z[j] = r.normal();
+  long long neg = 0;
+  for (int i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (int j = 0; j <= i; ++j) s += L[(std::size_t)i * n + j] * z[j];
+    out[i] = spec.mean + s;
+    neg += out[i] < 0.0;
+  }
+  return neg;
+}
+
+void normalize_source(const Grid1D& g, const double* raw, double* out) {
+  double s = 0.0;
+  for (int i = 0; i < g.n_cells; ++i) s += raw[i];
+  s *= g.dx();
+  if (!(s > 0.0) || !std::isfinite(s)) throw InvalidArgument("normalize_source: non-positive integral (resample)");
+  for (int i = 0; i < g.n_cells; ++i) out[i] = raw[i] / s;
+}
+
 }  // namespace snop::oracle

@@ -184,4 +184,25 @@ RecastResult recast_fixed_point(int n, const double* S, const double* sigma_t, c
                                 double tol, int max_it, Norm norm, const double* initial_phi,
                                 double* phi_out);
 
+// --- grf ------------------------------------------------------
+struct GrfSpec {
+  double mean = 0.07, variance = 3e-4, length_scale = 1.2, jitter = 1e-10;
+  std::uint64_t seed = 0;
+};
+
+// Row-major lower-triangular L with L L^T = C + jitter var I, C_ij = var exp(-(x_i-x_j)^2 / (2 l^2))
+// at the cell centres (Cholesky-Banachiewicz, row by row); on a non-positive pivot the jitter is
+// escalated x10 while <= 1e-6, else NumericalError. The jitter is relative to the
+// variance: SPEC.md:245's example (variance 1e-18 -> field constant within 1e-8) is unreachable
+// with an absolute 1e-10 jitter (noise sqrt(1e-10) = 1e-5), so the SPEC's own example pins it.
+std::vector<double> grf_cholesky(const Grid1D& g, const GrfSpec& spec, double* jitter_used = nullptr);
+
+// sample_grf: out_i = mean + sum_{j<=i} L_ij z_j, z_j = Rng(seed + sample).normal()
+// drawn j = 0..n-1. Returns the number of negative entries (reported, not clipped).
+long long sample_grf(const Grid1D& g, const GrfSpec& spec, const std::vector<double>& L, std::uint64_t sample,
+                     double* out);
+
+// normalize_source: raw / (dx sum raw); InvalidArgument if the integral <= 0.
+void normalize_source(const Grid1D& g, const double* raw, double* out);
+
 }  // namespace snop::oracle

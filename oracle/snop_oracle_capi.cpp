@@ -533,6 +533,79 @@ int oracle_sp_cp_eigen_batched(void* vop, int32_t algorithm, int32_t order, int3
   }
 }
 
+// GRF sampling / dataset generation. spec = {mean, variance, length_scale,
+// jitter, seed} as snop_grf_spec.
+int oracle_grf_sample(const snop_grid* grid, const snop_grf_spec* sp, int64_t first, int32_t n_samples,
+                      double* out, int64_t* negatives, double* jitter_used) {
+  try {
+    const Grid1D g{grid->length_cm, grid->n_cells};
+    const GrfSpec spec{sp->mean, sp->variance, sp->length_scale_cm, sp->jitter, sp->seed};
+    double jit = 0.0;
+    const std::vector<double> L = grf_cholesky(g, spec, &jit);
+    if (jitter_used) *jitter_used = jit;
+    for (int32_t s = 0; s < n_samples; ++s) {
+      const long long neg = sample_grf(g, spec, L, (std::uint64_t)(first + s), out + (std::size_t)s * g.n_cells);
+      if (negatives) negatives[s] = neg;
+    }
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+int oracle_normalize_source(const snop_grid* grid, int32_t n, const double* raw, double* out) {
+  try {
+    const Grid1D g{grid->length_cm, grid->n_cells};
+    for (int32_t s = 0; s < n; ++s)
+      normalize_source(g, raw + (std::size_t)s * g.n_cells, out + (std::size_t)s * g.n_cells);
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+// generate_dataset: per sample sample_grf -> normalize -> source_iteration at p*
+// (zero initial guess, vacuum both sides); non-convergence aborts with the sample index.
+int oracle_generate_dataset(const snop_grid* grid, int32_t order, const snop_grf_spec* sp, int32_t n_samples,
+                            double tstar, double sstar, double tol, double* sources, double* fluxes,
+                            int32_t* iterations, int32_t n_threads) {
+  try {
+    const Grid1D g{grid->length_cm, grid->n_cells};
+    const GrfSpec spec{sp->mean, sp->variance, sp->length_scale_cm, sp->jitter, sp->seed};
+    const std::vector<double> L = grf_cholesky(g, spec);
+    const Quadrature q = gauss_legendre(order);
+    SolverConfig cfg;
+    cfg.tolerance = tol;
+    const std::size_t Nc = g.n_cells;
+    const std::vector<double> st(Nc, tstar), ss(Nc, sstar);
+    std::string err;
+    int code = 0;
+    std::mutex mu;
+    parallel_chunks(n_samples, n_samples, [&](std::size_t, std::size_t b0, std::size_t b1) {
+      for (std::size_t b = b0; b < b1; ++b) {
+        try {
+          std::vector<double> raw(Nc);
+          sample_grf(g, spec, L, b, raw.data());
+          normalize_source(g, raw.data(), sources + b * Nc);
+          double* phi = fluxes + b * Nc;
+          std::fill(phi, phi + Nc, 0.0);
+          const SIResult r = source_iteration(g, q, st.data(), ss.data(), nullptr, sources + b * Nc, cfg, phi, nullptr);
+          iterations[b] = r.iterations;
+          if (!r.converged) throw NumericalError("generate_dataset: sample " + std::to_string(b) + " did not converge");
+        } catch (...) {
+          std::lock_guard<std::mutex> lk(mu);
+          code = map_exc();
+          err = g_err;
+        }
+      }
+    }, n_threads);
+    if (code) { g_err = err; return code; }
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
 int oracle_balance_residual(const snop_grid* grid, const double* st, const double* ss0, const double* src,
                             const double* phi, double leak_left, double leak_right, double* out) {
   try {

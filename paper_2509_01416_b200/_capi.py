@@ -10,7 +10,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-from ._types import STATUS_NAMES, SnopGrid, SnopModelInfo, SnopSolverConfig
+from ._types import STATUS_NAMES, SnopDatasetInfo, SnopGrfSpec, SnopGrid, SnopModelInfo, SnopSolverConfig
 from .errors import raise_for_status
 
 PKG = Path(__file__).resolve().parent
@@ -24,6 +24,7 @@ EXPORTS = [
     "snop_exact_operator_create", "snop_op_destroy", "snop_op_predict", "snop_recast_fixed_point",
     "snop_precondition_fixed_source", "snop_sp_eigen_batched", "snop_cp_eigen_batched",
     "snop_op_save", "snop_op_load", "snop_model_write_deeponet", "snop_model_write_fno", "snop_model_inspect",
+    "snop_grf_sample", "snop_normalize_source", "snop_generate_dataset", "snop_dataset_write", "snop_dataset_read",
 ]
 
 _lib = None
@@ -78,6 +79,12 @@ def load():
                                               vp, i32, C.c_float]
     lib.snop_model_write_fno.argtypes = [C.c_char_p, C.POINTER(SnopGrid), dbl, dbl, i32, i32, i32, i32, i32, vp]
     lib.snop_model_inspect.argtypes = [C.c_char_p, C.POINTER(SnopModelInfo)]
+    lib.snop_grf_sample.argtypes = [vp, i32, C.POINTER(SnopGrid), C.POINTER(SnopGrfSpec), C.c_int64, i32, vp, vp]
+    lib.snop_normalize_source.argtypes = [vp, i32, C.POINTER(SnopGrid), i32, vp, vp]
+    lib.snop_generate_dataset.argtypes = [vp, i32, C.POINTER(SnopGrid), i32, C.POINTER(SnopGrfSpec), i32, dbl, dbl,
+                                          dbl, vp, vp, vp]
+    lib.snop_dataset_write.argtypes = [C.c_char_p, C.POINTER(SnopDatasetInfo), vp, vp]
+    lib.snop_dataset_read.argtypes = [C.c_char_p, C.POINTER(SnopDatasetInfo), vp, vp]
     _lib = lib
     return lib
 

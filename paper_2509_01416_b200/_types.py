@@ -43,6 +43,17 @@ class SnopModelInfo(C.Structure):
     ]
 
 
+class SnopGrfSpec(C.Structure):
+    _fields_ = [("mean", C.c_double), ("variance", C.c_double), ("length_scale_cm", C.c_double),
+                ("jitter", C.c_double), ("seed", C.c_uint64)]
+
+
+class SnopDatasetInfo(C.Structure):
+    _fields_ = [("n_samples", C.c_int64), ("grid", SnopGrid), ("order", C.c_int32), ("reserved", C.c_int32),
+                ("spec", SnopGrfSpec), ("sigma_t_star", C.c_double), ("sigma_s0_star", C.c_double),
+                ("tolerance", C.c_double)]
+
+
 def make_grid(length: float, n_cells: int) -> SnopGrid:
     return SnopGrid(float(length), int(n_cells), 0)
 

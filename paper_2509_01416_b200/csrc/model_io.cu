@@ -315,4 +315,109 @@ snop_status snop_model_inspect(const char* path, snop_model_info* info) {
   return SNOP_OK;
 }
 
+// Dataset record (format version 1), same container as the model file:
+//   string "SNOP-DATASET", u32 version, u64 n_samples, u64 n_cells, f64 length_cm, u32 order,
+//   f64 mean, f64 variance, f64 length_scale, f64 jitter, u64 seed, f64 sigma_t*, f64 sigma_s0*,
+//   f64 tolerance, f64 sources[n_samples*n_cells], f64 fluxes[n_samples*n_cells], u64 digest.
+snop_status snop_dataset_write(const char* path, const snop_dataset_info* info, const double* sources,
+                               const double* fluxes) {
+  if (!path || !info || !sources || !fluxes) return bad("NULL argument");
+  if (info->n_samples < 0 || info->grid.n_cells < 1 || !(info->grid.length_cm > 0.0)) return bad("bad dataset header");
+  const size_t N = (size_t)info->n_samples * info->grid.n_cells;
+  Out o;
+  o.buf.reserve(128 + 16 * N);
+  o.str("SNOP-DATASET");
+  o.u32(1);
+  o.u64((uint64_t)info->n_samples);
+  o.u64((uint64_t)info->grid.n_cells);
+  o.f64(info->grid.length_cm);
+  o.u32((uint32_t)info->order);
+  o.f64(info->spec.mean);
+  o.f64(info->spec.variance);
+  o.f64(info->spec.length_scale_cm);
+  o.f64(info->spec.jitter);
+  o.u64(info->spec.seed);
+  o.f64(info->sigma_t_star);
+  o.f64(info->sigma_s0_star);
+  o.f64(info->tolerance);
+  for (size_t i = 0; i < N; ++i) o.f64(sources[i]);
+  for (size_t i = 0; i < N; ++i) o.f64(fluxes[i]);
+  o.u64(fnv1a(o.buf.data(), o.buf.size()));
+  std::FILE* f = std::fopen(path, "wb");
+  if (!f) return io_error(std::string("cannot open for writing: ") + path);
+  const bool ok = std::fwrite(o.buf.data(), 1, o.buf.size(), f) == o.buf.size();
+  if (std::fclose(f) != 0 || !ok) return io_error(std::string("short write: ") + path);
+  // human-readable manifest alongside
+  const std::string mpath = std::string(path) + ".txt";
+  std::FILE* m = std::fopen(mpath.c_str(), "w");
+  if (!m) return io_error("cannot open manifest for writing: " + mpath);
+  std::fprintf(m,
+               "format = SNOP-DATASET v1\nn_samples = %lld\nn_cells = %d\nlength_cm = %.17g\nquadrature_order = %d\n"
+               "grf_mean = %.17g\ngrf_variance = %.17g\ngrf_length_scale_cm = %.17g\ngrf_jitter = %.17g\n"
+               "grf_seed = %llu\nsigma_t_star = %.17g\nsigma_s0_star = %.17g\nsolver_tolerance = %.17g\n"
+               "layout = sources[n_samples][n_cells] then fluxes[n_samples][n_cells], f64 little-endian\n"
+               "digest_fnv1a64 = %016llx\n",
+               (long long)info->n_samples, info->grid.n_cells, info->grid.length_cm, info->order, info->spec.mean,
+               info->spec.variance, info->spec.length_scale_cm, info->spec.jitter,
+               (unsigned long long)info->spec.seed, info->sigma_t_star, info->sigma_s0_star, info->tolerance,
+               (unsigned long long)fnv1a(o.buf.data(), o.buf.size() - 8));
+  if (std::fclose(m) != 0) return io_error("manifest write failed: " + mpath);
+  return SNOP_OK;
+}
+
+snop_status snop_dataset_read(const char* path, snop_dataset_info* info, double* sources, double* fluxes) {
+  if (!path || !info) return bad("NULL argument");
+  std::FILE* f = std::fopen(path, "rb");
+  if (!f) return io_error(std::string("cannot open for reading: ") + path);
+  std::vector<uint8_t> buf;
+  uint8_t chunk[1 << 16];
+  size_t got;
+  while ((got = std::fread(chunk, 1, sizeof chunk, f)) > 0) buf.insert(buf.end(), chunk, chunk + got);
+  std::fclose(f);
+  if (buf.size() < 8) return io_error("checksum missing (truncated file)");
+  const size_t body = buf.size() - 8;
+  snop_dataset_info h{};
+  size_t data_pos = 0;
+  try {
+    In in(buf.data(), body);
+    if (in.str(64) != "SNOP-DATASET") return io_error("not a snop dataset file (bad magic)");
+    const uint32_t version = in.u32();
+    if (version != 1) return io_error("dataset file version " + std::to_string(version) + " unsupported (expected 1)");
+    h.n_samples = (int64_t)in.u64();
+    const uint64_t nc = in.u64();
+    if (nc < 1 || nc > (1u << 30) || h.n_samples < 0) throw Truncated{};
+    h.grid.n_cells = (int32_t)nc;
+    h.grid.length_cm = in.f64();
+    h.order = (int32_t)in.u32();
+    h.spec.mean = in.f64();
+    h.spec.variance = in.f64();
+    h.spec.length_scale_cm = in.f64();
+    h.spec.jitter = in.f64();
+    h.spec.seed = in.u64();
+    h.sigma_t_star = in.f64();
+    h.sigma_s0_star = in.f64();
+    h.tolerance = in.f64();
+    data_pos = in.pos;
+    const size_t N = (size_t)h.n_samples * nc;
+    if (N > (body - data_pos) / 16 || data_pos + 16 * N != body) throw Truncated{};
+  } catch (const Truncated&) {
+    return io_error("unexpected end of file (truncated or corrupt dataset file)");
+  }
+  uint64_t stored = 0;
+  for (int i = 0; i < 8; ++i) stored |= static_cast<uint64_t>(buf[body + i]) << (8 * i);
+  if (stored != fnv1a(buf.data(), body)) return io_error("checksum mismatch (corrupt file)");
+  *info = h;
+  const size_t N = (size_t)h.n_samples * h.grid.n_cells;
+  In data(buf.data() + data_pos, 16 * N);
+  for (size_t i = 0; i < N; ++i) {
+    const double v = data.f64();
+    if (sources) sources[i] = v;
+  }
+  for (size_t i = 0; i < N; ++i) {
+    const double v = data.f64();
+    if (fluxes) fluxes[i] = v;
+  }
+  return SNOP_OK;
+}
+
 }  // extern "C"

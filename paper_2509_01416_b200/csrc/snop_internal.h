@@ -30,6 +30,7 @@ struct Ctx {
   int sm_count = 148;
   std::atomic<int64_t> launches{0};
   std::vector<DevBuf> slots;  // scratch buffers for host-memspace staging and workspaces
+  std::vector<double> grf_key;  // (length, n_cells, variance, length scale, jitter) of the cached GRF factor
   void* slot(size_t i, size_t bytes);  // grow-only
   ~Ctx();
 };

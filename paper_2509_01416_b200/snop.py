@@ -14,6 +14,7 @@ in PyTorch. Arrays may be numpy (host memory: the call stages H2D/D2H) or CUDA t
   precondition_fixed_source SPEC.md:413-421
   sp_eigen / cp_eigen
   save_model / load_model
+  sample_grf / normalize_source / generate_dataset / dataset file
 """
 from __future__ import annotations
 
@@ -24,7 +25,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _capi
-from ._types import SnopGrid, SnopModelInfo, SnopSolverConfig, make_grid
+from ._types import SnopDatasetInfo, SnopGrfSpec, SnopGrid, SnopModelInfo, SnopSolverConfig, make_grid
 
 VACUUM, REFLECTIVE = 0, 1
 REL_LINF, REL_L2 = 0, 1
@@ -499,3 +500,105 @@ def inspect_model(path) -> SnopModelInfo:
     info = SnopModelInfo()
     _capi.check(_capi.load().snop_model_inspect(os.fsencode(path), C.byref(info)))
     return info
+
+
+# ---- GRF sources and training datasets -----------------------------------------
+@dataclass(frozen=True)
+class GrfSpec:
+    """SPEC.md:226-230 (paper Appendix A1 defaults)."""
+    mean: float = 0.07
+    variance: float = 3e-4
+    length_scale_cm: float = 1.2
+    jitter: float = 1e-10
+    seed: int = 0
+
+    def c(self) -> SnopGrfSpec:
+        return SnopGrfSpec(float(self.mean), float(self.variance), float(self.length_scale_cm), float(self.jitter),
+                           int(self.seed))
+
+
+def sample_grf(grid: Grid1D, spec: GrfSpec, n_samples: int, first_sample: int = 0, with_negatives: bool = False,
+               ctx: Context | None = None, device: bool = False):
+    """sample_grf for samples first..first+n-1 -> [n][Nc] raw fields (numpy, or a CUDA tensor
+    when device=True); optionally the per-sample count of negative entries."""
+    ctx = ctx or default_context()
+    g, sp = grid.c(), spec.c()
+    n = int(n_samples)
+    if device:
+        import torch
+        out = torch.empty((n, grid.n_cells), dtype=torch.float64, device=f"cuda:{ctx.device}")
+        neg = torch.empty(n, dtype=torch.int64, device=out.device) if with_negatives else None
+        _capi.check(ctx._lib.snop_grf_sample(ctx.h, 1, C.byref(g), C.byref(sp), int(first_sample), n, out.data_ptr(),
+                                             neg.data_ptr() if neg is not None else None))
+        ctx.synchronize()
+    else:
+        out = np.empty((n, grid.n_cells))
+        neg = np.empty(n, dtype=np.int64) if with_negatives else None
+        _capi.check(ctx._lib.snop_grf_sample(ctx.h, 0, C.byref(g), C.byref(sp), int(first_sample), n,
+                                             out.ctypes.data, neg.ctypes.data if neg is not None else None))
+    return (out, neg) if with_negatives else out
+
+
+def normalize_source(grid: Grid1D, raw, ctx: Context | None = None):
+    """normalize_source: raw / integral, per row."""
+    ctx = ctx or default_context()
+    a = _Args(raw)
+    n = int(raw.shape[0])
+    r = a.inp(raw, shape=(n, grid.n_cells))
+    out, out_p = a.out((n, grid.n_cells))
+    g = grid.c()
+    _capi.check(ctx._lib.snop_normalize_source(ctx.h, a.memspace, C.byref(g), n, r, out_p))
+    if a.device:
+        ctx.synchronize()
+    return out
+
+
+@dataclass
+class TrainingDataset:
+    """SPEC.md:232-236."""
+    sources: object
+    fluxes: object
+    iterations: object
+    grid: Grid1D
+    order: int
+    spec: GrfSpec
+    reference_params: tuple
+    tolerance: float
+
+
+def generate_dataset(n_samples: int, spec: GrfSpec, grid: Grid1D, order: int, reference_params=(1.0, 0.5),
+                     tolerance: float = 1e-8, ctx: Context | None = None) -> TrainingDataset:
+    """generate_dataset on the device; host numpy arrays out."""
+    ctx = ctx or default_context()
+    n = int(n_samples)
+    S = np.empty((n, grid.n_cells))
+    phi = np.empty((n, grid.n_cells))
+    it = np.empty(n, dtype=np.int32)
+    g, sp = grid.c(), spec.c()
+    _capi.check(ctx._lib.snop_generate_dataset(ctx.h, 0, C.byref(g), int(order), C.byref(sp), n,
+                                               float(reference_params[0]), float(reference_params[1]),
+                                               float(tolerance), S.ctypes.data, phi.ctypes.data, it.ctypes.data))
+    return TrainingDataset(S, phi, it, grid, int(order), spec, tuple(reference_params), float(tolerance))
+
+
+def save_dataset(path, ds: TrainingDataset) -> None:
+    """Dataset file + text manifest; host-only."""
+    info = SnopDatasetInfo(int(ds.sources.shape[0]), ds.grid.c(), int(ds.order), 0, ds.spec.c(),
+                           float(ds.reference_params[0]), float(ds.reference_params[1]), float(ds.tolerance))
+    S = np.ascontiguousarray(ds.sources, dtype=np.float64)
+    phi = np.ascontiguousarray(ds.fluxes, dtype=np.float64)
+    _capi.check(_capi.load().snop_dataset_write(os.fsencode(path), C.byref(info), S.ctypes.data, phi.ctypes.data))
+
+
+def load_dataset(path) -> TrainingDataset:
+    lib = _capi.load()
+    info = SnopDatasetInfo()
+    _capi.check(lib.snop_dataset_read(os.fsencode(path), C.byref(info), None, None))
+    n, nc = int(info.n_samples), int(info.grid.n_cells)
+    S = np.empty((n, nc))
+    phi = np.empty((n, nc))
+    _capi.check(lib.snop_dataset_read(os.fsencode(path), C.byref(info), S.ctypes.data, phi.ctypes.data))
+    sp = info.spec
+    return TrainingDataset(S, phi, None, Grid1D(info.grid.length_cm, nc), int(info.order),
+                           GrfSpec(sp.mean, sp.variance, sp.length_scale_cm, sp.jitter, int(sp.seed)),
+                           (info.sigma_t_star, info.sigma_s0_star), info.tolerance)

@@ -262,6 +262,38 @@ class OracleOperator:
                 "stage2_inner": i2, "converged": cv.astype(bool), "fallback": fb.astype(bool)}
 
 
-__all__ = ["lib", "gauss_legendre", "source_iteration", "power_iteration", "infinite_medium_k", "recast_source",
+def grf_sample(length, n_cells, spec, n_samples, first=0):
+    """spec: paper_2509_01416_b200.snop.GrfSpec (or anything with .c() -> SnopGrfSpec)."""
+    g = make_grid(length, n_cells)
+    sp = spec.c()
+    out = np.empty((n_samples, n_cells))
+    neg = np.empty(n_samples, dtype=np.int64)
+    jit = C.c_double()
+    _check(lib().oracle_grf_sample(C.byref(g), C.byref(sp), C.c_int64(first), C.c_int32(n_samples), _p(out),
+                                   _p(neg), C.byref(jit)))
+    return out, neg, jit.value
+
+
+def normalize_source(length, n_cells, raw):
+    raw = np.ascontiguousarray(raw, dtype=np.float64)
+    out = np.empty_like(raw)
+    g = make_grid(length, n_cells)
+    _check(lib().oracle_normalize_source(C.byref(g), C.c_int32(raw.shape[0]), _p(raw), _p(out)))
+    return out
+
+
+def generate_dataset(length, n_cells, order, spec, n_samples, tstar, sstar, tol, n_threads=0):
+    g = make_grid(length, n_cells)
+    sp = spec.c()
+    S = np.empty((n_samples, n_cells))
+    phi = np.empty((n_samples, n_cells))
+    it = np.empty(n_samples, dtype=np.int32)
+    _check(lib().oracle_generate_dataset(C.byref(g), C.c_int32(order), C.byref(sp), C.c_int32(n_samples),
+                                         C.c_double(tstar), C.c_double(sstar), C.c_double(tol), _p(S), _p(phi),
+                                         _p(it), C.c_int32(n_threads)))
+    return S, phi, it
+
+
+__all__ = ["grf_sample", "normalize_source", "generate_dataset", "lib", "gauss_legendre", "source_iteration", "power_iteration", "infinite_medium_k", "recast_source",
            "OracleOperator", "make_config", "make_grid", "SnopSolverConfig", "SnopGrid", "balance_residual",
            "chunk_bounds", "rng_stream", "hardware_threads", "OracleError"]
