@@ -131,6 +131,22 @@ snop_status snop_source_iteration_batched(
     const snop_solver_config* cfg, const double* initial_phi,
     double* phi_out, double* current_out, int32_t* iterations, uint8_t* converged);
 
+/* source_iteration + balance diagnostic: as snop_source_iteration_batched,
+ * plus leakage_out[b][2] = the NET outflows (outgoing minus incoming partial currents) at x = 0 and
+ * x = L of the last sweep -- the quantities the balance report needs. */
+snop_status snop_source_iteration_leakage_batched(
+    snop_ctx* ctx, int32_t memspace, const snop_grid* grid, int32_t order, int32_t batch,
+    const double* sigma_t, const double* sigma_s0, const double* sigma_s1, const double* source,
+    const snop_solver_config* cfg, const double* initial_phi, double* phi_out, double* current_out,
+    int32_t* iterations, uint8_t* converged, double* leakage_out);
+
+/* balance_report, batched: residual[b] = |leak_l + leak_r + absorption -
+ * production| / production, absorption = dx sum (Sigma_t - Sigma_s0,total-out) phi, production =
+ * dx sum S. production == 0 -> SNOP_NUMERICAL_ERROR (division guard). */
+snop_status snop_balance_report(snop_ctx* ctx, int32_t memspace, const snop_grid* grid, int32_t batch,
+                                const double* sigma_t, const double* sigma_s0_out, const double* source,
+                                const double* phi, const double* leakage, double* residual_out);
+
 /*
  * Batched k-eigenvalue power iteration — replaces
  *   power_iteration(grid, quadrature, materials, config, inner_solver, initial)

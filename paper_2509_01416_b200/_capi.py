@@ -25,6 +25,7 @@ EXPORTS = [
     "snop_precondition_fixed_source", "snop_sp_eigen_batched", "snop_cp_eigen_batched",
     "snop_op_save", "snop_op_load", "snop_model_write_deeponet", "snop_model_write_fno", "snop_model_inspect",
     "snop_grf_sample", "snop_normalize_source", "snop_generate_dataset", "snop_dataset_write", "snop_dataset_read",
+    "snop_source_iteration_leakage_batched", "snop_balance_report",
 ]
 
 _lib = None
@@ -85,6 +86,9 @@ def load():
                                           dbl, vp, vp, vp]
     lib.snop_dataset_write.argtypes = [C.c_char_p, C.POINTER(SnopDatasetInfo), vp, vp]
     lib.snop_dataset_read.argtypes = [C.c_char_p, C.POINTER(SnopDatasetInfo), vp, vp]
+    lib.snop_source_iteration_leakage_batched.argtypes = [
+        vp, i32, C.POINTER(SnopGrid), i32, i32, vp, vp, vp, vp, C.POINTER(SnopSolverConfig), vp, vp, vp, vp, vp, vp]
+    lib.snop_balance_report.argtypes = [vp, i32, C.POINTER(SnopGrid), i32, vp, vp, vp, vp, vp, vp]
     _lib = lib
     return lib
 

@@ -147,6 +147,10 @@ snop_status drain_flags(Ctx& ctx) {
     set_error("non-finite values produced");
     return SNOP_NUMERICAL_ERROR;
   }
+  if (flags & FLAG_ZERO_PRODUCTION) {
+    set_error("balance_report: zero production (division guard)");
+    return SNOP_NUMERICAL_ERROR;
+  }
   return SNOP_OK;
 }
 
@@ -249,12 +253,11 @@ snop_status snop_gauss_legendre(int32_t order, double* mu, double* w) {
   return SNOP_OK;
 }
 
-snop_status snop_source_iteration_batched(snop_ctx* ctx, int32_t memspace, const snop_grid* grid, int32_t order,
-                                          int32_t batch, const double* sigma_t, const double* sigma_s0,
-                                          const double* sigma_s1, const double* source,
-                                          const snop_solver_config* cfg, const double* initial_phi,
-                                          double* phi_out, double* current_out, int32_t* iterations,
-                                          uint8_t* converged) {
+static snop_status si_entry(snop_ctx* ctx, int32_t memspace, const snop_grid* grid, int32_t order, int32_t batch,
+                            const double* sigma_t, const double* sigma_s0, const double* sigma_s1,
+                            const double* source, const snop_solver_config* cfg, const double* initial_phi,
+                            double* phi_out, double* current_out, int32_t* iterations, uint8_t* converged,
+                            double* leakage_out) {
   if (!ctx) return invalid("ctx is NULL");
   SNOP_TRY(check_grid(grid, order));
   SNOP_TRY(check_cfg(cfg));
@@ -266,7 +269,7 @@ snop_status snop_source_iteration_batched(snop_ctx* ctx, int32_t memspace, const
   const size_t n = (size_t)batch * grid->n_cells;
   if (memspace == SNOP_MEM_DEVICE) {
     return launch_source_iteration(*ctx, *grid, order, batch, sigma_t, sigma_s0, sigma_s1, source, *cfg,
-                                   initial_phi, phi_out, current_out, iterations, converged);
+                                   initial_phi, phi_out, current_out, iterations, converged, leakage_out);
   }
   if (memspace != SNOP_MEM_HOST) return invalid("memspace must be HOST(0) or DEVICE(1)");
   const double *st, *ss, *s1, *src, *p0;
@@ -282,11 +285,60 @@ snop_status snop_source_iteration_batched(snop_ctx* ctx, int32_t memspace, const
   SNOP_TRY(stage_out_alloc(*ctx, 6, current_out, n, &cur));
   SNOP_TRY(stage_out_alloc(*ctx, 7, iterations, (size_t)batch, &it));
   SNOP_TRY(stage_out_alloc(*ctx, 8, converged, (size_t)batch, &cv));
-  SNOP_TRY(launch_source_iteration(*ctx, *grid, order, batch, st, ss, s1, src, *cfg, p0, phi, cur, it, cv));
+  double* lk;
+  SNOP_TRY(stage_out_alloc(*ctx, 9, leakage_out, 2 * (size_t)batch, &lk));
+  SNOP_TRY(launch_source_iteration(*ctx, *grid, order, batch, st, ss, s1, src, *cfg, p0, phi, cur, it, cv, lk));
   SNOP_TRY(copy_out(*ctx, phi_out, phi, n));
   SNOP_TRY(copy_out(*ctx, current_out, cur, n));
   SNOP_TRY(copy_out(*ctx, iterations, it, (size_t)batch));
   SNOP_TRY(copy_out(*ctx, converged, cv, (size_t)batch));
+  SNOP_TRY(copy_out(*ctx, leakage_out, lk, 2 * (size_t)batch));
+  return drain_flags(*ctx);
+}
+
+snop_status snop_source_iteration_batched(snop_ctx* ctx, int32_t memspace, const snop_grid* grid, int32_t order,
+                                          int32_t batch, const double* sigma_t, const double* sigma_s0,
+                                          const double* sigma_s1, const double* source,
+                                          const snop_solver_config* cfg, const double* initial_phi,
+                                          double* phi_out, double* current_out, int32_t* iterations,
+                                          uint8_t* converged) {
+  return si_entry(ctx, memspace, grid, order, batch, sigma_t, sigma_s0, sigma_s1, source, cfg, initial_phi, phi_out,
+                  current_out, iterations, converged, nullptr);
+}
+
+snop_status snop_source_iteration_leakage_batched(snop_ctx* ctx, int32_t memspace, const snop_grid* grid,
+                                                  int32_t order, int32_t batch, const double* sigma_t,
+                                                  const double* sigma_s0, const double* sigma_s1,
+                                                  const double* source, const snop_solver_config* cfg,
+                                                  const double* initial_phi, double* phi_out, double* current_out,
+                                                  int32_t* iterations, uint8_t* converged, double* leakage_out) {
+  if (!leakage_out) return invalid("leakage_out is NULL");
+  return si_entry(ctx, memspace, grid, order, batch, sigma_t, sigma_s0, sigma_s1, source, cfg, initial_phi, phi_out,
+                  current_out, iterations, converged, leakage_out);
+}
+
+snop_status snop_balance_report(snop_ctx* ctx, int32_t memspace, const snop_grid* grid, int32_t batch,
+                                const double* sigma_t, const double* sigma_s0_out, const double* source,
+                                const double* phi, const double* leakage, double* residual_out) {
+  if (!ctx || !grid) return invalid("ctx/grid is NULL");
+  if (!(grid->length_cm > 0.0) || grid->n_cells < 1 || batch < 0) return invalid("bad grid / batch");
+  if (batch == 0) return SNOP_OK;
+  if (!sigma_t || !sigma_s0_out || !source || !phi || !leakage || !residual_out) return invalid("NULL array");
+  cudaSetDevice(ctx->device);
+  const size_t n = (size_t)batch * grid->n_cells;
+  if (memspace == SNOP_MEM_DEVICE)
+    return launch_balance(*ctx, *grid, batch, sigma_t, sigma_s0_out, source, phi, leakage, residual_out);
+  if (memspace != SNOP_MEM_HOST) return invalid("memspace must be HOST(0) or DEVICE(1)");
+  const double *st, *ss, *src, *p, *lk;
+  double* res;
+  SNOP_TRY(stage_in(*ctx, 0, sigma_t, n, &st));
+  SNOP_TRY(stage_in(*ctx, 1, sigma_s0_out, n, &ss));
+  SNOP_TRY(stage_in(*ctx, 3, source, n, &src));
+  SNOP_TRY(stage_in(*ctx, 4, phi, n, &p));
+  SNOP_TRY(stage_in(*ctx, 10, leakage, 2 * (size_t)batch, &lk));
+  SNOP_TRY(stage_out_alloc(*ctx, 11, residual_out, (size_t)batch, &res));
+  SNOP_TRY(launch_balance(*ctx, *grid, batch, st, ss, src, p, lk, res));
+  SNOP_TRY(copy_out(*ctx, residual_out, res, (size_t)batch));
   return drain_flags(*ctx);
 }
 

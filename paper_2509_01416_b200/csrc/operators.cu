@@ -34,9 +34,62 @@ __global__ void recast_source_kernel(size_t n, const double* __restrict__ S, con
   }
 }
 
+// balance_report, one CTA per instance.
+__global__ void __launch_bounds__(256) balance_kernel(int n, double dx, const double* __restrict__ st,
+                                                      const double* __restrict__ ss, const double* __restrict__ src,
+                                                      const double* __restrict__ phi, const double* __restrict__ leak,
+                                                      double* __restrict__ residual, int* __restrict__ flags) {
+  __shared__ double sh[2][8];
+  const int b = blockIdx.x;
+  const size_t o = (size_t)b * n;
+  double ab = 0.0, pr = 0.0;
+  for (int i = threadIdx.x; i < n; i += 256) {
+    ab = fma(st[o + i] - ss[o + i], phi[o + i], ab);
+    pr += src[o + i];
+  }
+  for (int k = 16; k > 0; k >>= 1) {
+    ab += __shfl_xor_sync(0xffffffffu, ab, k);
+    pr += __shfl_xor_sync(0xffffffffu, pr, k);
+  }
+  if (threadIdx.x % 32 == 0) {
+    sh[0][threadIdx.x / 32] = ab;
+    sh[1][threadIdx.x / 32] = pr;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, p = 0.0;
+    for (int u = 0; u < 8; ++u) {
+      a += sh[0][u];
+      p += sh[1][u];
+    }
+    a *= dx;
+    p *= dx;
+    if (p == 0.0) {
+      atomicOr(flags, FLAG_ZERO_PRODUCTION);
+      residual[b] = __longlong_as_double(0x7ff8000000000000ll);
+    } else {
+      residual[b] = fabs(leak[2 * b] + leak[2 * b + 1] + a - p) / fabs(p);
+    }
+  }
+}
+
 }  // namespace
 
 namespace snop_impl {
+
+snop_status launch_balance(Ctx& ctx, const snop_grid& g, int batch, const double* st, const double* ss_out,
+                           const double* src, const double* phi, const double* leak, double* residual) {
+  if (batch == 0) return SNOP_OK;
+  balance_kernel<<<batch, 256, 0, ctx.stream>>>(g.n_cells, g.length_cm / g.n_cells, st, ss_out, src, phi, leak,
+                                                 residual, ctx.d_flags);
+  ctx.launches++;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("balance_kernel: ") + cudaGetErrorString(e));
+    return SNOP_CUDA_ERROR;
+  }
+  return SNOP_OK;
+}
 
 snop_status launch_recast(Ctx& ctx, size_t n, const double* S, const double* phi, const double* st,
                           const double* ss, double tstar, double sstar, double* out) {

@@ -48,7 +48,7 @@ si_fixed_source_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
                        const double* __restrict__ ss1_g, const double* __restrict__ src_g,
                        const double* __restrict__ phi0_g, double* __restrict__ phi_g,
                        double* __restrict__ jc_g, int32_t* __restrict__ iters, uint8_t* __restrict__ conv,
-                       int* __restrict__ flags, const int* __restrict__ order) {
+                       int* __restrict__ flags, const int* __restrict__ order, double* __restrict__ leak_g) {
   extern __shared__ __align__(32) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<SweepSmem<K, NT>*>(smem_raw);
   const int t = threadIdx.x, Nc = sc.n_cells;
@@ -62,6 +62,7 @@ si_fixed_source_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   io.src = src_g + base;
   io.ss1 = ANISO ? ss1_g + base : nullptr;
   io.jc = (ANISO || CUR) ? jc_g + base : nullptr;
+  io.leak = leak_g ? leak_g + 2 * (size_t)b : nullptr;
   bool bad = false;
 #pragma unroll
   for (int j = 0; j < K; ++j) {
@@ -373,7 +374,8 @@ inline cudaError_t launch_k(Kern kern, int batch, int cs, int nt, size_t smem, c
 template <int K, int NT, bool CL>
 inline snop_status launch_si_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveConfig& cfg, int batch, int cs,
                                const double* st, const double* ss0, const double* ss1, const double* src,
-                               const double* phi0, double* phi, double* cur, int32_t* iters, uint8_t* conv) {
+                               const double* phi0, double* phi, double* cur, int32_t* iters, uint8_t* conv,
+                               double* leak) {
   const bool aniso = ss1 != nullptr;
   const size_t smem = smem_bytes<K, NT>();
   auto kern = aniso ? si_fixed_source_kernel<K, NT, true, true, CL>
@@ -390,7 +392,7 @@ inline snop_status launch_si_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
   // longest-expected-first order pays off once the batch spans several waves of CTAs
   const int* order = (!CL && batch > 4 * ctx.sm_count) ? make_order(ctx, batch, sc.n_cells, st, ss0) : nullptr;
   const cudaError_t e = launch_k(kern, batch, CL ? cs : 1, NT, smem, ctx.stream, sc, cfg, st, ss0, ss1, src, phi0,
-                                 phi, jc, iters, conv, ctx.d_flags, order);
+                                 phi, jc, iters, conv, ctx.d_flags, order, leak);
   ctx.launches++;
   if (e != cudaSuccess) {
     snop_impl::set_error(std::string("si_fixed_source_kernel launch: ") + cudaGetErrorString(e));
@@ -428,7 +430,7 @@ inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
 // Explicitly instantiated in si_k8_{fixed,eigen}{,_cl}.cu (one TU per variant, parallel build).
 #define SNOP_SI_ARGS                                                                                          \
   snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, int, int, const double*, const double*, const double*, \
-      const double*, const double*, double*, double*, int32_t*, uint8_t*
+      const double*, const double*, double*, double*, int32_t*, uint8_t*, double*
 #define SNOP_PI_ARGS                                                                                          \
   snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, const EigenParams&, int, int, const double*,          \
       const double*, const double*, const double*, const double*, const double*, const double*, double*, double*, \

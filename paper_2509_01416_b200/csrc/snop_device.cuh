@@ -180,7 +180,7 @@ struct SweepSmem {
   double agg[2][3][NP_PAD];    // chunk maps of the current pair group: [q][{A, Bfwd, Bbwd}][chunk]
   double xmap[2][4][NP_PAD];   // exclusive maps entering each chunk: [q][{Af, Bf, Ab, Bb}][chunk]
   double total[2][4];          // whole-domain maps [q][{Af, Bf, Ab, Bb}]
-  double jfirst[NT + 1];       // J at each thread's first edge (+ J at the last edge, slot NT)
+  double leak[2];              // net face currents of the latest sweep (written by the face owners)
   double red[4 * NW];          // reductions inside si_solve
   double red2[4 * NW];         // reductions of the enclosing (eigen) kernel
   double lag[2][kMaxPairs];    // both-reflective: lagged mu>0 outflow at x=L, by iteration parity
@@ -264,6 +264,7 @@ struct CellIO {
   const double* __restrict__ src;  // external isotropic source
   const double* __restrict__ ss1;  // P1 moment (ANISO only)
   double* __restrict__ jc;         // cell-average current (ANISO / CUR)
+  double* leak = nullptr;          // [2] net outflow at x=0 / x=L of the last sweep (nullable)
 };
 
 #ifdef SNOP_PHASE_TIMING
@@ -557,6 +558,8 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
         // balance form of phi = sum_n w_n psi_avg,n
         const double pn = (sm.q2[j * NT + t] - (JR - Jl[j]) * sc.inv_dx) * sm.ist[j * NT + t];
         if constexpr (ANISO || CUR) io.jc[c0 + j] = 0.5 * (Jl[j] + JR);
+        if (j == 0 && c0 == 0) sm.leak[0] = -Jl[0];  // J(0) = in - out at the left face
+        if (c0 + j == Nc - 1) sm.leak[1] = JR;       // J(L) = out - in at the right face
         const double d = pn - sm.phi[j * NT + t];
         if (cfg.norm == 0) {
           num = fmax(num, fabs(d));
@@ -577,6 +580,10 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
       conv = true;
       break;
     }
+  }
+  if (io.leak) {  // balance diagnostic: net leakages of the last sweep
+    if (c0 == 0) io.leak[0] = sm.leak[0];  // written by this same thread: no barrier needed
+    if (w.owns_last) io.leak[1] = sm.leak[1];
   }
   if constexpr (CL) cl_sync();  // keep shared memory alive until every remote read is done
   *converged = conv;

@@ -14,7 +14,7 @@
 namespace snop_impl {
 
 // Error flags written by kernels into ctx->d_flags (bitwise OR).
-enum : int { FLAG_BAD_SIGMA_T = 1, FLAG_DEGENERATE = 2, FLAG_NONFINITE = 4 };
+enum : int { FLAG_BAD_SIGMA_T = 1, FLAG_DEGENERATE = 2, FLAG_NONFINITE = 4, FLAG_ZERO_PRODUCTION = 8 };
 
 void set_error(const std::string& msg);
 
@@ -42,13 +42,18 @@ snop_dev::SweepConsts make_consts(const snop_grid& g, int order);
 snop_status launch_source_iteration(Ctx& ctx, const snop_grid& g, int order, int batch, const double* st,
                                     const double* ss0, const double* ss1, const double* src,
                                     const snop_solver_config& cfg, const double* phi0, double* phi,
-                                    double* cur, int32_t* iters, uint8_t* conv);
+                                    double* cur, int32_t* iters, uint8_t* conv, double* leak = nullptr);
 
 snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int batch, int G, const double* st,
                                    const double* ss0, const double* ss1, const double* nsf, const double* chi,
                                    const snop_solver_config& cfg, const double* k0, const double* phi0,
                                    double* k, double* phi, double* phi_old_ws, int32_t* outer, int64_t* inner,
                                    uint8_t* conv);
+
+// balance_report, batched: residual[b] = |leak_l + leak_r + absorption - production|
+// / production with absorption = dx sum (Sigma_t - Sigma_s0,out) phi, production = dx sum S.
+snop_status launch_balance(Ctx& ctx, const snop_grid& g, int batch, const double* st, const double* ss_out,
+                           const double* src, const double* phi, const double* leak, double* residual);
 
 snop_status launch_recast(Ctx& ctx, size_t n, const double* S, const double* phi, const double* st,
                           const double* ss, double tstar, double sstar, double* out);

@@ -7,6 +7,7 @@ in PyTorch. Arrays may be numpy (host memory: the call stages H2D/D2H) or CUDA t
 
   gauss_legendre
   source_iteration          SPEC.md:125-134 (sweep :115-123)
+  balance_report
   power_iteration           SPEC.md:179-189 (+ decisions :206-209)
   recast_source
   predict
@@ -185,10 +186,11 @@ class FixedSourceResult:
     iterations: object
     converged: object
     current: object = None
+    leakage: object = None  # [B][2] net outflow at x=0, x=L of the last sweep (want_leakage)
 
 
 def source_iteration(grid: Grid1D, order: int, sigma_t, sigma_s0, source, config: SolverConfig | None = None,
-                     initial_phi=None, sigma_s1=None, want_current: bool = False,
+                     initial_phi=None, sigma_s1=None, want_current: bool = False, want_leakage: bool = False,
                      ctx: Context | None = None, sync: bool = True) -> FixedSourceResult:
     """Batched single-group fixed-source solve. Arrays are [B][Nc].
     Device (torch CUDA) arrays: enqueued on ctx's stream; with sync=False the caller must call
@@ -205,11 +207,34 @@ def source_iteration(grid: Grid1D, order: int, sigma_t, sigma_s0, source, config
     it, it_p = a.out((B,), np.int32)
     cv, cv_p = a.out((B,), np.uint8)
     g, cfg = grid.c(), config.c()
-    _capi.check(ctx._lib.snop_source_iteration_batched(ctx.h, a.memspace, C.byref(g), int(order), B, st, ss, s1,
-                                                       src, C.byref(cfg), p0, phi_p, cur_p, it_p, cv_p))
+    if want_leakage:
+        lk, lk_p = a.out((B, 2))
+        _capi.check(ctx._lib.snop_source_iteration_leakage_batched(
+            ctx.h, a.memspace, C.byref(g), int(order), B, st, ss, s1, src, C.byref(cfg), p0, phi_p, cur_p, it_p, cv_p,
+            lk_p))
+    else:
+        lk = None
+        _capi.check(ctx._lib.snop_source_iteration_batched(ctx.h, a.memspace, C.byref(g), int(order), B, st, ss, s1,
+                                                           src, C.byref(cfg), p0, phi_p, cur_p, it_p, cv_p))
     if a.device and sync:
         ctx.synchronize()
-    return FixedSourceResult(phi, it, cv, cur)
+    return FixedSourceResult(phi, it, cv, cur, lk)
+
+
+def balance_report(grid: Grid1D, sigma_t, sigma_s0_out, source, phi, leakage, ctx: Context | None = None):
+    """balance_report (SPEC.md:136-148), batched [B][Nc]; leakage [B][2] from source_iteration."""
+    ctx = ctx or default_context()
+    a = _Args(sigma_t, sigma_s0_out, source, phi, leakage)
+    B = int(sigma_t.shape[0])
+    n = grid.n_cells
+    st, ss, S, p = (a.inp(x, shape=(B, n)) for x in (sigma_t, sigma_s0_out, source, phi))
+    lk = a.inp(leakage, shape=(B, 2))
+    res, res_p = a.out((B,))
+    g = grid.c()
+    _capi.check(ctx._lib.snop_balance_report(ctx.h, a.memspace, C.byref(g), B, st, ss, S, p, lk, res_p))
+    if a.device:
+        ctx.synchronize()
+    return res
 
 
 @dataclass
