@@ -7,7 +7,7 @@ sinusoidal Sigma_t, vacuum, source iteration to rel-Linf < 1e-8 from a zero gues
 
   value      cell.angle.group sweep updates/s (sum over instances of iterations x N x Nc),
              inputs resident in HBM, device time (CUDA events on the solver stream).
-  e2e        same metric through the public host API (numpy arrays in pinned host memory,
+  e2e        same metric through the public host API (numpy arrays in pinned host memory, in and out;
              H2D of the inputs + D2H of flux/iterations inside the timed region).
   roofline   algorithmic bytes per launch (40 B per cell per source iteration)
              / average launch time, vs the measured HBM copy bandwidth.
@@ -212,13 +212,16 @@ def run_gpu(args):
     # e2e through the public host API: pinned host arrays, H2D + D2H inside the timed region
     pin = [torch.from_numpy(a).pin_memory() for a in (p.sigma_t, p.sigma_s0, p.source)]
     host = [x.numpy() for x in pin]
-    snop.source_iteration(g, p.order, *host, cfg, ctx=ctx)  # warm the staging buffers
+    outs = (torch.empty((p.batch, p.n_cells), dtype=torch.float64).pin_memory().numpy(),
+            torch.empty(p.batch, dtype=torch.int32).pin_memory().numpy(),
+            torch.empty(p.batch, dtype=torch.uint8).pin_memory().numpy())
+    snop.source_iteration(g, p.order, *host, cfg, ctx=ctx, out=outs)  # warm the staging buffers
     e2e_times = []
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        rh = snop.source_iteration(g, p.order, *host, cfg, ctx=ctx)
+        rh = snop.source_iteration(g, p.order, *host, cfg, ctx=ctx, out=outs)
         e2e_times.append(time.perf_counter() - t0)
     upd_h = int(np.asarray(rh.iterations, dtype=np.int64).sum()) * p.n_cells * p.order
     e2e_t = reduce_max(float(np.sum(e2e_times)), dev)

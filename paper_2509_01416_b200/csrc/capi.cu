@@ -1,7 +1,9 @@
 // capi.cu — the extern "C" boundary (include/snop_cuda.h): argument validation, host<->device
 // staging for SNOP_MEM_HOST calls, error mapping onto the reference's exception classes
 // (proj/core/include/snop/errors.hpp:8-41) and the per-context stream/workspace.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -32,7 +34,29 @@ void* Ctx::slot(size_t i, size_t bytes) {
   return b.ptr;
 }
 
+Ctx* Ctx::sub(size_t i) {
+  while (subs.size() <= i) {
+    Ctx* c = new (std::nothrow) Ctx;
+    if (!c) return nullptr;
+    c->device = device;
+    c->sm_count = sm_count;
+    // later sub-contexts get higher stream priority: in the chunked host pipeline the last chunk's
+    // data arrives last, so its CTAs must be dispatched ahead of earlier chunks' remaining ones
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    const int prio = std::max(greatest, least - (int)subs.size());
+    if (cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio) != cudaSuccess ||
+        cudaMalloc(&c->d_flags, sizeof(int)) != cudaSuccess || cudaMemset(c->d_flags, 0, sizeof(int)) != cudaSuccess) {
+      delete c;
+      return nullptr;
+    }
+    subs.push_back(c);
+  }
+  return subs[i];
+}
+
 Ctx::~Ctx() {
+  for (Ctx* c : subs) delete c;
   for (auto& b : slots)
     if (b.ptr) cudaFree(b.ptr);
   if (d_flags) cudaFree(d_flags);
@@ -189,6 +213,25 @@ snop_status copy_out(Ctx& ctx, T* host, const T* dev, size_t n) {
   return SNOP_OK;
 }
 
+// Pinned (page-locked, UVA-mapped) host memory can be addressed by kernels directly.
+bool pinned(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost && a.devicePointer != nullptr;
+}
+
+template <class T>
+T* dev_ptr(T* p) {
+  if (!p) return nullptr;
+  cudaPointerAttributes a{};
+  cudaPointerGetAttributes(&a, p);
+  return static_cast<T*>(a.devicePointer);
+}
+
 }  // namespace
 
 namespace snop_impl {
@@ -253,6 +296,95 @@ snop_status snop_gauss_legendre(int32_t order, double* mu, double* w) {
   return SNOP_OK;
 }
 
+// Host-memspace source iteration over a large batch: the instances are independent, so the batch
+// is cut into NCH chunks, each with its own stream (sub-context): H2D of chunk c+1 overlaps the
+// solve of chunk c, chunk kernels run concurrently (later chunks back-fill SMs while earlier ones
+// drain their longest instances), and every chunk's D2H starts as soon as its solve ends.
+static snop_status si_host_pipelined(Ctx& ctx, const snop_grid& grid, int order, int batch, const double* sigma_t,
+                                     const double* sigma_s0, const double* sigma_s1, const double* source,
+                                     const snop_solver_config& cfg, const double* initial_phi, double* phi_out,
+                                     double* current_out, int32_t* iterations, uint8_t* converged,
+                                     double* leakage_out) {
+  static const int NCH = [] {  // experiment override: SNOP_HOST_CHUNKS (1..8)
+    const char* e = std::getenv("SNOP_HOST_CHUNKS");
+    const int v = e ? std::atoi(e) : 4;
+    return v < 1 ? 1 : (v > 8 ? 8 : v);
+  }();
+  const size_t Nc = grid.n_cells, n = (size_t)batch * Nc;
+  auto dbuf = [&](size_t i, size_t count) { return static_cast<double*>(ctx.slot(i, count * sizeof(double))); };
+  double* st = dbuf(0, n);
+  double* ss = dbuf(1, n);
+  double* s1 = sigma_s1 ? dbuf(2, n) : nullptr;
+  double* src = dbuf(3, n);
+  double* p0 = initial_phi ? dbuf(4, n) : nullptr;
+  double* phi = dbuf(5, n);
+  double* cur = current_out ? dbuf(6, n) : nullptr;
+  int32_t* it = static_cast<int32_t*>(ctx.slot(7, (size_t)batch * sizeof(int32_t)));
+  uint8_t* cv = static_cast<uint8_t*>(ctx.slot(8, (size_t)batch));
+  double* lk = leakage_out ? dbuf(9, 2 * (size_t)batch) : nullptr;
+  if (!st || !ss || (sigma_s1 && !s1) || !src || (initial_phi && !p0) || !phi || (current_out && !cur) || !it ||
+      !cv || (leakage_out && !lk))
+    return cuda_fail("cudaMalloc", cudaErrorMemoryAllocation);
+  cudaEvent_t ready;
+  cudaError_t e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+  if (e != cudaSuccess) return cuda_fail("cudaEventCreate", e);
+  cudaEventRecord(ready, ctx.stream);  // earlier work on the context's stream may still use the slots
+  Ctx* subs[8];
+  for (int c = 0; c < NCH; ++c) {
+    subs[c] = ctx.sub(c);
+    if (!subs[c]) {
+      cudaEventDestroy(ready);
+      return cuda_fail("sub-context", cudaErrorMemoryAllocation);
+    }
+    cudaStreamWaitEvent(subs[c]->stream, ready, 0);
+  }
+  cudaEventDestroy(ready);
+  auto h2d = [&](double* d, const double* h, size_t b0, size_t nb, cudaStream_t s) {
+    return h ? cudaMemcpyAsync(d + b0 * Nc, h + b0 * Nc, nb * Nc * sizeof(double), cudaMemcpyHostToDevice, s)
+             : cudaSuccess;
+  };
+  snop_status st_out = SNOP_OK;
+  size_t bounds[9];
+  for (int c = 0; c <= NCH; ++c) bounds[c] = (size_t)batch * c / NCH;
+  for (int c = 0; c < NCH && st_out == SNOP_OK; ++c) {
+    const size_t b0 = bounds[c], nb = bounds[c + 1] - b0;
+    Ctx& sc = *subs[c];
+    cudaError_t ce = h2d(st, sigma_t, b0, nb, sc.stream);
+    if (ce == cudaSuccess) ce = h2d(ss, sigma_s0, b0, nb, sc.stream);
+    if (ce == cudaSuccess) ce = h2d(s1, sigma_s1, b0, nb, sc.stream);
+    if (ce == cudaSuccess) ce = h2d(src, source, b0, nb, sc.stream);
+    if (ce == cudaSuccess) ce = h2d(p0, initial_phi, b0, nb, sc.stream);
+    if (ce != cudaSuccess) {
+      st_out = cuda_fail("H2D copy", ce);
+      break;
+    }
+    const size_t o = b0 * Nc;
+    st_out = launch_source_iteration(sc, grid, order, (int)nb, st + o, ss + o, s1 ? s1 + o : nullptr, src + o, cfg,
+                                     p0 ? p0 + o : nullptr, phi + o, cur ? cur + o : nullptr, it + b0, cv + b0,
+                                     lk ? lk + 2 * b0 : nullptr);
+  }
+  for (int c = 0; c < NCH && st_out == SNOP_OK; ++c) {
+    const size_t b0 = bounds[c], nb = bounds[c + 1] - b0;
+    const cudaStream_t s = subs[c]->stream;
+    cudaError_t ce = cudaMemcpyAsync(phi_out + b0 * Nc, phi + b0 * Nc, nb * Nc * sizeof(double),
+                                     cudaMemcpyDeviceToHost, s);
+    if (ce == cudaSuccess && current_out)
+      ce = cudaMemcpyAsync(current_out + b0 * Nc, cur + b0 * Nc, nb * Nc * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(iterations + b0, it + b0, nb * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(converged + b0, cv + b0, nb, cudaMemcpyDeviceToHost, s);
+    if (ce == cudaSuccess && leakage_out)
+      ce = cudaMemcpyAsync(leakage_out + 2 * b0, lk + 2 * b0, 2 * nb * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (ce != cudaSuccess) st_out = cuda_fail("D2H copy", ce);
+  }
+  snop_status drained = SNOP_OK;
+  for (int c = 0; c < NCH; ++c) {  // always synchronise every chunk stream, even after an error
+    const snop_status d = drain_flags(*subs[c]);
+    if (drained == SNOP_OK) drained = d;
+    ctx.launches += subs[c]->launches.exchange(0);
+  }
+  return st_out != SNOP_OK ? st_out : drained;
+}
+
 static snop_status si_entry(snop_ctx* ctx, int32_t memspace, const snop_grid* grid, int32_t order, int32_t batch,
                             const double* sigma_t, const double* sigma_s0, const double* sigma_s1,
                             const double* source, const snop_solver_config* cfg, const double* initial_phi,
@@ -272,6 +404,21 @@ static snop_status si_entry(snop_ctx* ctx, int32_t memspace, const snop_grid* gr
                                    initial_phi, phi_out, current_out, iterations, converged, leakage_out);
   }
   if (memspace != SNOP_MEM_HOST) return invalid("memspace must be HOST(0) or DEVICE(1)");
+  if (!current_out && pinned(sigma_t) && pinned(sigma_s0) && pinned(source) && (!sigma_s1 || pinned(sigma_s1)) &&
+      (!initial_phi || pinned(initial_phi)) && pinned(phi_out) && pinned(iterations) && pinned(converged) &&
+      (!leakage_out || pinned(leakage_out))) {
+    // zero-copy: the kernel reads its instance's inputs over the bus and writes its results back
+    // as it finishes, so transfers overlap the solves of other instances (no staging copies)
+    double* stage = static_cast<double*>(ctx->slot(24, n * (sigma_s1 ? 3 : 2) * sizeof(double)));
+    if (!stage) return cuda_fail("cudaMalloc", cudaErrorMemoryAllocation);
+    SNOP_TRY(launch_source_iteration(*ctx, *grid, order, batch, dev_ptr(sigma_t), dev_ptr(sigma_s0),
+                                     dev_ptr(sigma_s1), dev_ptr(source), *cfg, dev_ptr(initial_phi), dev_ptr(phi_out),
+                                     nullptr, dev_ptr(iterations), dev_ptr(converged), dev_ptr(leakage_out), stage));
+    return drain_flags(*ctx);
+  }
+  if (batch >= 4 * ctx->sm_count)
+    return si_host_pipelined(*ctx, *grid, order, batch, sigma_t, sigma_s0, sigma_s1, source, *cfg, initial_phi,
+                             phi_out, current_out, iterations, converged, leakage_out);
   const double *st, *ss, *s1, *src, *p0;
   double *phi, *cur;
   int32_t* it;

@@ -69,14 +69,19 @@ namespace snop_impl {
 snop_status launch_source_iteration(Ctx& ctx, const snop_grid& g, int order, int batch, const double* st,
                                     const double* ss0, const double* ss1, const double* src,
                                     const snop_solver_config& cfg, const double* phi0, double* phi, double* cur,
-                                    int32_t* iters, uint8_t* conv, double* leak) {
+                                    int32_t* iters, uint8_t* conv, double* leak, double* stage) {
   if (batch == 0) return SNOP_OK;
   const SweepConsts sc = make_consts(g, order);
   const SolveConfig c = inner_cfg(cfg);
   const Shape s = pick_shape(g.n_cells, batch, ctx.sm_count);
+  if (stage && s.cs > 1) {
+    set_error("host-resident inputs need the one-CTA-per-instance kernel (unset SNOP_CLUSTER)");
+    return SNOP_INVALID_ARGUMENT;
+  }
 #define SNOP_SI(NN, CC)                       \
   if (s.nt == NN && (s.cs > 1) == CC)         \
-    return launch_si_t<K, NN, CC>(ctx, sc, c, batch, s.cs, st, ss0, ss1, src, phi0, phi, cur, iters, conv, leak);
+    return launch_si_t<K, NN, CC>(ctx, sc, c, batch, s.cs, st, ss0, ss1, src, phi0, phi, cur, iters, conv, leak, \
+                                  stage);
   SNOP_SI(32, false) SNOP_SI(64, false) SNOP_SI(128, false) SNOP_SI(256, false) SNOP_SI(512, false)
   SNOP_SI(32, true) SNOP_SI(64, true) SNOP_SI(128, true) SNOP_SI(256, true)
 #undef SNOP_SI

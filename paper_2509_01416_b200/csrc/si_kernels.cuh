@@ -48,7 +48,8 @@ si_fixed_source_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
                        const double* __restrict__ ss1_g, const double* __restrict__ src_g,
                        const double* __restrict__ phi0_g, double* __restrict__ phi_g,
                        double* __restrict__ jc_g, int32_t* __restrict__ iters, uint8_t* __restrict__ conv,
-                       int* __restrict__ flags, const int* __restrict__ order, double* __restrict__ leak_g) {
+                       int* __restrict__ flags, const int* __restrict__ order, double* __restrict__ leak_g,
+                       double* __restrict__ stage_g) {
   extern __shared__ __align__(32) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<SweepSmem<K, NT>*>(smem_raw);
   const int t = threadIdx.x, Nc = sc.n_cells;
@@ -64,18 +65,50 @@ si_fixed_source_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   io.jc = (ANISO || CUR) ? jc_g + base : nullptr;
   io.leak = leak_g ? leak_g + 2 * (size_t)b : nullptr;
   bool bad = false;
+  if (!CL && stage_g) {
+    // Inputs (and outputs) in pinned host memory, read over the bus by the kernel itself: one
+    // coalesced pass copies the per-iteration operands (Ss0, S, Ss1) into this instance's rows of
+    // a device workspace and Sigma_t / phi0 into shared memory, so the transfer of later
+    // instances overlaps the solves of earlier ones.
+    constexpr int R = ANISO ? 3 : 2;
+    double* ws = stage_g + (size_t)b * R * Nc;
+    for (int i = t; i < NT * K; i += NT) {
+      const int owner = i / K, j = i - owner * K;
+      double stv = 0.0, p0 = 0.0;  // padding: identity map (see maps_phase)
+      if (i < Nc) {
+        ws[i] = ss0_g[base + i];
+        ws[Nc + i] = src_g[base + i];
+        if constexpr (ANISO) ws[2 * Nc + i] = ss1_g[base + i];
+        stv = st_g[base + i];
+        bad |= !(stv > 0.0);
+        p0 = phi0_g ? phi0_g[base + i] : 0.0;
+      }
+      sm.st[j * NT + owner] = stv;
+      sm.phi[j * NT + owner] = p0;
+    }
+    io.ss0 = ws;
+    io.src = ws + Nc;
+    if constexpr (ANISO) io.ss1 = ws + 2 * Nc;
+    if constexpr (ANISO) {
 #pragma unroll
-  for (int j = 0; j < K; ++j) {
-    const int i = c0 + j;
-    if (i < Nc) {
-      const double stv = st_g[base + i];
-      sm.st[j * NT + t] = stv;
-      bad |= !(stv > 0.0);
-      sm.phi[j * NT + t] = phi0_g ? phi0_g[base + i] : 0.0;
-      if constexpr (ANISO) io.jc[i] = 0.0;
-    } else {
-      sm.st[j * NT + t] = 0.0;  // padding: identity map (see maps_phase)
-      sm.phi[j * NT + t] = 0.0;
+      for (int j = 0; j < K; ++j)
+        if (c0 + j < Nc) io.jc[c0 + j] = 0.0;
+    }
+    __syncthreads();
+  } else {
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int i = c0 + j;
+      if (i < Nc) {
+        const double stv = st_g[base + i];
+        sm.st[j * NT + t] = stv;
+        bad |= !(stv > 0.0);
+        sm.phi[j * NT + t] = phi0_g ? phi0_g[base + i] : 0.0;
+        if constexpr (ANISO) io.jc[i] = 0.0;
+      } else {
+        sm.st[j * NT + t] = 0.0;  // padding: identity map (see maps_phase)
+        sm.phi[j * NT + t] = 0.0;
+      }
     }
   }
   if (cluster_any<NT, CL>(bad, sm)) {  // nonpositive Sigma_t -> invalid argument
@@ -88,10 +121,15 @@ si_fixed_source_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   }
   bool converged = false;
   const int it = si_solve<K, NT, ANISO, CUR, CL>(sc, cfg, sm, io, &converged);
+  if (!CL && stage_g) {  // coalesced write-back (host memory: full bus transactions)
+    __syncthreads();
+    for (int i = t; i < Nc; i += NT) phi_g[base + i] = sm.phi[(i % K) * NT + i / K];
+  } else {
 #pragma unroll
-  for (int j = 0; j < K; ++j) {
-    const int i = c0 + j;
-    if (i < Nc) phi_g[base + i] = sm.phi[j * NT + t];
+    for (int j = 0; j < K; ++j) {
+      const int i = c0 + j;
+      if (i < Nc) phi_g[base + i] = sm.phi[j * NT + t];
+    }
   }
   if (t == 0 && rank == 0) {
     iters[b] = it;
@@ -296,12 +334,21 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
 constexpr int NBUCKET = 1024;
 
 static __global__ void order_keys_kernel(int Nc, const double* __restrict__ st, const double* __restrict__ ss,
-                                  int* __restrict__ bucket, int* __restrict__ hist) {
+                                  int* __restrict__ bucket, int* __restrict__ hist, int sampled) {
   const int b = blockIdx.x;
   double m = 0.0;
-  for (int i = threadIdx.x; i < Nc; i += blockDim.x) {
+  if (sampled && Nc > (int)blockDim.x) {
+    // host-resident inputs: 4 contiguous runs of blockDim/4 cells spread over the slab (whole bus
+    // transactions instead of one per strided cell)
+    const int run = blockDim.x / 4, r = threadIdx.x / run;
+    const int i = (int)((long long)r * (Nc - run) / 3) + (int)(threadIdx.x % run);
     const double t = st[(size_t)b * Nc + i];
     if (t > 0.0) m = fmax(m, ss[(size_t)b * Nc + i] / t);
+  } else {
+    for (int i = threadIdx.x; i < Nc; i += blockDim.x) {
+      const double t = st[(size_t)b * Nc + i];
+      if (t > 0.0) m = fmax(m, ss[(size_t)b * Nc + i] / t);
+    }
   }
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   __shared__ double sh[32];
@@ -336,12 +383,15 @@ static __global__ void order_scatter_kernel(int B, const int* __restrict__ bucke
   if (b < B) order[atomicAdd(&cursor[bucket[b]], 1)] = b;
 }
 
-static inline const int* make_order(snop_impl::Ctx& ctx, int batch, int Nc, const double* st, const double* ss) {
+// sampled = true when st / ss live in host memory: the key is taken over 128 sampled cells
+// (it only steers dispatch order; results do not depend on it)
+static inline const int* make_order(snop_impl::Ctx& ctx, int batch, int Nc, const double* st, const double* ss,
+                                    bool sampled = false) {
   int* buf = static_cast<int*>(ctx.slot(23, ((size_t)2 * batch + NBUCKET) * sizeof(int)));
   if (!buf) return nullptr;
   int *bucket = buf, *order = buf + batch, *hist = buf + 2 * batch;
   cudaMemsetAsync(hist, 0, NBUCKET * sizeof(int), ctx.stream);
-  order_keys_kernel<<<batch, 128, 0, ctx.stream>>>(Nc, st, ss, bucket, hist);
+  order_keys_kernel<<<batch, 128, 0, ctx.stream>>>(Nc, st, ss, bucket, hist, sampled ? 1 : 0);
   order_scan_kernel<<<1, NBUCKET, 0, ctx.stream>>>(hist);
   order_scatter_kernel<<<(batch + 255) / 256, 256, 0, ctx.stream>>>(batch, bucket, hist, order);
   ctx.launches += 3;
@@ -375,7 +425,7 @@ template <int K, int NT, bool CL>
 inline snop_status launch_si_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveConfig& cfg, int batch, int cs,
                                const double* st, const double* ss0, const double* ss1, const double* src,
                                const double* phi0, double* phi, double* cur, int32_t* iters, uint8_t* conv,
-                               double* leak) {
+                               double* leak, double* stage) {
   const bool aniso = ss1 != nullptr;
   const size_t smem = smem_bytes<K, NT>();
   auto kern = aniso ? si_fixed_source_kernel<K, NT, true, true, CL>
@@ -390,9 +440,10 @@ inline snop_status launch_si_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
     }
   }
   // longest-expected-first order pays off once the batch spans several waves of CTAs
-  const int* order = (!CL && batch > 4 * ctx.sm_count) ? make_order(ctx, batch, sc.n_cells, st, ss0) : nullptr;
+  const int* order =
+      (!CL && batch > 4 * ctx.sm_count) ? make_order(ctx, batch, sc.n_cells, st, ss0, stage != nullptr) : nullptr;
   const cudaError_t e = launch_k(kern, batch, CL ? cs : 1, NT, smem, ctx.stream, sc, cfg, st, ss0, ss1, src, phi0,
-                                 phi, jc, iters, conv, ctx.d_flags, order, leak);
+                                 phi, jc, iters, conv, ctx.d_flags, order, leak, CL ? nullptr : stage);
   ctx.launches++;
   if (e != cudaSuccess) {
     snop_impl::set_error(std::string("si_fixed_source_kernel launch: ") + cudaGetErrorString(e));
@@ -430,7 +481,7 @@ inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
 // Explicitly instantiated in si_k8_{fixed,eigen}{,_cl}.cu (one TU per variant, parallel build).
 #define SNOP_SI_ARGS                                                                                          \
   snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, int, int, const double*, const double*, const double*, \
-      const double*, const double*, double*, double*, int32_t*, uint8_t*, double*
+      const double*, const double*, double*, double*, int32_t*, uint8_t*, double*, double*
 #define SNOP_PI_ARGS                                                                                          \
   snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, const EigenParams&, int, int, const double*,          \
       const double*, const double*, const double*, const double*, const double*, const double*, double*, double*, \

@@ -339,56 +339,126 @@ __device__ __forceinline__ void maps_phase(const SweepConsts& sc, SweepSmem<K, N
 // gets the exclusive map that carries the CTA's inflow to its first edge. Forward = prefix (left
 // to right), backward = suffix (right to left). In cluster mode the CTA totals are also
 // published (ctot) for the other CTAs of the cluster.
-template <int K, int NT, int NP, bool CL>
-__device__ __forceinline__ void scan_phase(SweepSmem<K, NT>& sm, int lane, int warp, int gslot) {
-  constexpr int NW = NT / 32, E = NT / 32;
-  for (int s = warp; s < 2 * NP; s += NW) {
-    const int q = s >> 1;
-    const bool fwd = (s & 1) == 0;
-    const double* Ag = sm.agg[q][0];
-    const double* Bg = sm.agg[q][fwd ? 1 : 2];
-    // lane order = sweep order; operands are re-read from shared memory in the second pass so
-    // the scan adds no register pressure on top of the live per-cell maps
-    auto at = [&](int e) { return SweepSmem<K, NT>::spos(fwd ? lane * E + e : NT - 1 - (lane * E + e)); };
-    double A = Ag[at(0)], B = Bg[at(0)];
-#pragma unroll 4
-    for (int e = 1; e < E; ++e) {
-      const double ae = Ag[at(e)];
-      B = fma(ae, B, Bg[at(e)]);
-      A *= ae;
+// One (pair, direction) scan by one warp. Lane l owns chunks l*E .. l*E+E-1 in sweep order; with
+// the padded layout those E chunk maps are contiguous in shared memory (ascending for the forward
+// sweep, descending for the backward one), so every access is base + compile-time offset.
+//   1. serial inclusive prefix over the lane's E chunks, written to the exclusive-map array as
+//      scratch (stores are fire-and-forget: the chain is E-1 dependent DFMA/DMUL pairs);
+//   2. 5-step shuffle scan of the lane totals -> the lane's exclusive entry map (Ax, Bx);
+//   3. exclusive map of chunk e = (Ax, Bx) composed with prefix e-1: E-1 independent
+//      compositions, processed in descending e so each reads its prefix before it is replaced.
+template <int K, int NT, bool FWD, bool CL>
+__device__ __forceinline__ void scan_one(SweepSmem<K, NT>& sm, int q, int lane, int gslot) {
+  constexpr int E = NT / 32;
+  constexpr int S = E > 1 ? E + 1 : 1;  // padded stride between consecutive lanes' chunk runs
+  constexpr int D = FWD ? 1 : -1;
+  const int base = FWD ? lane * S : (31 - lane) * S + (E - 1);
+  const double* a = sm.agg[q][0] + base;
+  const double* b = sm.agg[q][FWD ? 1 : 2] + base;
+  double* XA = sm.xmap[q][FWD ? 0 : 2] + base;
+  double* XB = sm.xmap[q][FWD ? 1 : 3] + base;
+  // Loads are batched ahead of the dependent chain in runs of H chunks: stores to the xmap
+  // scratch may alias later agg loads as far as the compiler knows, so without batching every
+  // step would pay a full shared-memory round trip.
+  constexpr int H = E < 4 ? E : 4;
+  double A = 1.0, B = 0.0;
+#pragma unroll
+  for (int e0 = 0; e0 < E; e0 += H) {
+    double av[H], bv[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      av[h] = a[D * (e0 + h)];
+      bv[h] = b[D * (e0 + h)];
     }
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double ap = __shfl_up_sync(0xffffffffu, A, o), bq = __shfl_up_sync(0xffffffffu, B, o);
-      if (lane >= o) {
-        B = fma(A, bq, B);
-        A *= ap;
+    for (int h = 0; h < H; ++h) {
+      if (e0 + h == 0) {
+        A = av[0];
+        B = bv[0];
+      } else {
+        B = fma(av[h], B, bv[h]);
+        A *= av[h];
+      }
+      XA[D * (e0 + h)] = A;
+      XB[D * (e0 + h)] = B;
+    }
+  }
+#ifdef SNOP_SCAN_R4
+  // experiment (opt-in, measured slower than radix 2 on B200): radix-4 Kogge-Stone over the 32
+  // lane totals, strides 1, 4, 16, each step composing lanes L-3o, L-2o, L-o, L as a 2-level tree
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 2) {
+    double a1 = __shfl_up_sync(0xffffffffu, A, o), b1 = __shfl_up_sync(0xffffffffu, B, o);
+    double a2 = __shfl_up_sync(0xffffffffu, A, 2 * o), b2 = __shfl_up_sync(0xffffffffu, B, 2 * o);
+    double a3 = __shfl_up_sync(0xffffffffu, A, 3 * o), b3 = __shfl_up_sync(0xffffffffu, B, 3 * o);
+    if (lane < o) { a1 = 1.0; b1 = 0.0; }
+    if (lane < 2 * o) { a2 = 1.0; b2 = 0.0; }
+    if (lane < 3 * o) { a3 = 1.0; b3 = 0.0; }
+    // (3 then 2) and (1 then own), then combine: f then g = (Af Ag, Ag Bf + Bg)
+    const double ax = a3 * a2, bx = fma(a2, b3, b2);
+    const double ay = a1 * A, by = fma(A, b1, B);
+    B = fma(ay, bx, by);
+    A = ax * ay;
+  }
+#else
+  // radix-2 Kogge-Stone over the 32 lane totals (5 dependent shuffle rounds)
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double ap = __shfl_up_sync(0xffffffffu, A, o), bq = __shfl_up_sync(0xffffffffu, B, o);
+    if (lane >= o) {
+      B = fma(A, bq, B);
+      A *= ap;
+    }
+  }
+#endif
+  double Ax = __shfl_up_sync(0xffffffffu, A, 1), Bx = __shfl_up_sync(0xffffffffu, B, 1);
+  if (lane == 0) {
+    Ax = 1.0;
+    Bx = 0.0;
+  }
+  if (lane == 31) {
+    sm.total[q][FWD ? 0 : 2] = A;
+    sm.total[q][FWD ? 1 : 3] = B;
+    if constexpr (CL) {
+      sm.ctot[gslot][q][FWD ? 0 : 2] = A;
+      sm.ctot[gslot][q][FWD ? 1 : 3] = B;
+    }
+  }
+  // exclusive maps, descending in runs of H: each run reads its prefixes before replacing them
+#pragma unroll
+  for (int e1 = E - 1; e1 >= 1; e1 -= H) {
+    double pa[H], pb[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int e = e1 - h;
+      if (e >= 1) {
+        pa[h] = XA[D * (e - 1)];
+        pb[h] = XB[D * (e - 1)];
       }
     }
-    double Ax = __shfl_up_sync(0xffffffffu, A, 1), Bx = __shfl_up_sync(0xffffffffu, B, 1);
-    if (lane == 0) {
-      Ax = 1.0;
-      Bx = 0.0;
-    }
-    if (lane == 31) {
-      sm.total[q][fwd ? 0 : 2] = A;
-      sm.total[q][fwd ? 1 : 3] = B;
-      if constexpr (CL) {
-        sm.ctot[gslot][q][fwd ? 0 : 2] = A;
-        sm.ctot[gslot][q][fwd ? 1 : 3] = B;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int e = e1 - h;
+      if (e >= 1) {
+        XA[D * e] = Ax * pa[h];
+        XB[D * e] = fma(pa[h], Bx, pb[h]);
       }
     }
-    double* XA = sm.xmap[q][fwd ? 0 : 2];
-    double* XB = sm.xmap[q][fwd ? 1 : 3];
-#pragma unroll 4
-    for (int e = 0; e < E; ++e) {
-      const int idx = at(e);
-      const double ae = Ag[idx], be = Bg[idx];
-      XA[idx] = Ax;
-      XB[idx] = Bx;
-      Bx = fma(ae, Bx, be);
-      Ax *= ae;
-    }
+  }
+  XA[0] = Ax;
+  XB[0] = Bx;
+}
+
+// Phase B: one warp per (pair, direction) scans the NT chunk maps of the CTA into the exclusive
+// maps that carry the CTA's inflow to each chunk's first edge. Forward = prefix (left to right),
+// backward = suffix (right to left). In cluster mode the CTA totals are also published (ctot)
+// for the other CTAs of the cluster.
+template <int K, int NT, int NP, bool CL>
+__device__ __forceinline__ void scan_phase(SweepSmem<K, NT>& sm, int lane, int warp, int gslot) {
+  constexpr int NW = NT / 32;
+  for (int s = warp; s < 2 * NP; s += NW) {
+    if ((s & 1) == 0) scan_one<K, NT, true, CL>(sm, s >> 1, lane, gslot);
+    else scan_one<K, NT, false, CL>(sm, s >> 1, lane, gslot);
   }
 }
 
@@ -529,13 +599,15 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
   int it = 0;
   bool conv = false;
   int rphase = 0;
+  // emission (x2): q2 = Ss0 phi + S ; angular q_n = q2/2 + 3/2 Ss1 mu_n J. Built
+  // here for the first sweep and then in each flux update for the next one, so the L2 loads of
+  // Ss0 and S overlap the flux update and the convergence reduction.
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+    sm.q2[j * NT + t] = (c0 + j < Nc) ? fma(io.ss0[c0 + j], sm.phi[j * NT + t], io.src[c0 + j]) : 0.0;
   while (it < cfg.max_it) {
     ++it;
     w.it = it;
-    // emission (x2): q2 = Ss0 phi + S ; angular q_n = q2/2 + 3/2 Ss1 mu_n J
-#pragma unroll
-    for (int j = 0; j < K; ++j)
-      sm.q2[j * NT + t] = (c0 + j < Nc) ? fma(io.ss0[c0 + j], sm.phi[j * NT + t], io.src[c0 + j]) : 0.0;
     double Jl[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) Jl[j] = 0.0;
@@ -550,6 +622,12 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
     SNOP_TACC(5, ti0, ti1);
     // J at the right edge of the own last cell was accumulated locally (Jr); padding cells after
     // the global last cell are identity maps, so Jl[j+1] of a padding cell is J at x = L.
+    double ssv[K], srcv[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      ssv[j] = (c0 + j < Nc) ? io.ss0[c0 + j] : 0.0;
+      srcv[j] = (c0 + j < Nc) ? io.src[c0 + j] : 0.0;
+    }
     double num = 0.0, den = 0.0;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
@@ -569,6 +647,7 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
           den = fma(pn, pn, den);
         }
         sm.phi[j * NT + t] = pn;
+        sm.q2[j * NT + t] = fma(ssv[j], pn, srcv[j]);  // emission of the next sweep
       }
     }
     reduce2<NT, CL>(num, den, cfg.norm == 0, sm.red, sm.cred, rphase++, sm);

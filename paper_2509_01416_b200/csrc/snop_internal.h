@@ -32,6 +32,10 @@ struct Ctx {
   std::vector<DevBuf> slots;  // scratch buffers for host-memspace staging and workspaces
   std::vector<double> grf_key;  // (length, n_cells, variance, length scale, jitter) of the cached GRF factor
   void* slot(size_t i, size_t bytes);  // grow-only
+  // Sub-contexts (own stream, flag word and workspace) for host-memspace calls that pipeline
+  // H2D / compute / D2H over chunks of the batch; created on first use, owned by this context.
+  std::vector<Ctx*> subs;
+  Ctx* sub(size_t i);
   ~Ctx();
 };
 
@@ -42,7 +46,11 @@ snop_dev::SweepConsts make_consts(const snop_grid& g, int order);
 snop_status launch_source_iteration(Ctx& ctx, const snop_grid& g, int order, int batch, const double* st,
                                     const double* ss0, const double* ss1, const double* src,
                                     const snop_solver_config& cfg, const double* phi0, double* phi,
-                                    double* cur, int32_t* iters, uint8_t* conv, double* leak = nullptr);
+                                    double* cur, int32_t* iters, uint8_t* conv, double* leak = nullptr,
+                                    double* stage = nullptr);
+// stage != nullptr: st/ss0/ss1/src/phi0 and phi/iters/conv/leak may be pinned host memory (read
+// and written by the kernel over the bus); stage is a device workspace of batch * (ss1 ? 3 : 2) *
+// n_cells doubles. cur must then be device memory or null.
 
 snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int batch, int G, const double* st,
                                    const double* ss0, const double* ss1, const double* nsf, const double* chi,

@@ -168,7 +168,23 @@ class _Args:
         self.keep.append(a)
         return a.ctypes.data
 
-    def out(self, shape, dtype=np.float64):
+    def out(self, shape, dtype=np.float64, into=None):
+        """A fresh output array, or the caller's ``into`` (checked: same memory space, dtype, shape,
+        contiguous) so results can land directly in e.g. pinned host memory."""
+        if into is not None:
+            if self.device != _is_dev(into):
+                raise ValueError("output array is in the wrong memory space")
+            if self.device:
+                import torch
+                tdt = {np.float64: torch.float64, np.int32: torch.int32, np.uint8: torch.uint8}[dtype]
+                ok = into.dtype == tdt and into.is_contiguous() and tuple(into.shape) == tuple(shape)
+                ptr = into.data_ptr()
+            else:
+                ok = into.dtype == dtype and into.flags.c_contiguous and into.shape == tuple(shape)
+                ptr = into.ctypes.data
+            if not ok:
+                raise ValueError(f"output array must be contiguous {np.dtype(dtype).name} of shape {tuple(shape)}")
+            return into, ptr
         if self.device:
             import torch
             tdt = {np.float64: torch.float64, np.float32: torch.float32, np.int32: torch.int32,
@@ -191,21 +207,23 @@ class FixedSourceResult:
 
 def source_iteration(grid: Grid1D, order: int, sigma_t, sigma_s0, source, config: SolverConfig | None = None,
                      initial_phi=None, sigma_s1=None, want_current: bool = False, want_leakage: bool = False,
-                     ctx: Context | None = None, sync: bool = True) -> FixedSourceResult:
+                     ctx: Context | None = None, sync: bool = True, out=None) -> FixedSourceResult:
     """Batched single-group fixed-source solve. Arrays are [B][Nc].
     Device (torch CUDA) arrays: enqueued on ctx's stream; with sync=False the caller must call
-    ctx.synchronize() (which also reports kernel-raised argument errors) before using results."""
+    ctx.synchronize() (which also reports kernel-raised argument errors) before using results.
+    ``out`` = optional (phi, iterations, converged) arrays to write into (e.g. pinned host memory)."""
     ctx = ctx or default_context()
     config = config or SolverConfig()
     a = _Args(sigma_t, sigma_s0, source, initial_phi, sigma_s1)
+    o_phi, o_it, o_cv = out if out is not None else (None, None, None)
     B = int(sigma_t.shape[0])
     n = grid.n_cells
     st, ss, src = a.inp(sigma_t, shape=(B, n)), a.inp(sigma_s0, shape=(B, n)), a.inp(source, shape=(B, n))
     s1, p0 = a.inp(sigma_s1, shape=(B, n)), a.inp(initial_phi, shape=(B, n))
-    phi, phi_p = a.out((B, n))
+    phi, phi_p = a.out((B, n), into=o_phi)
     cur, cur_p = a.out((B, n)) if want_current else (None, None)
-    it, it_p = a.out((B,), np.int32)
-    cv, cv_p = a.out((B,), np.uint8)
+    it, it_p = a.out((B,), np.int32, into=o_it)
+    cv, cv_p = a.out((B,), np.uint8, into=o_cv)
     g, cfg = grid.c(), config.c()
     if want_leakage:
         lk, lk_p = a.out((B, 2))

@@ -153,6 +153,64 @@ def test_device_memspace_matches_host():
     assert np.array_equal(h.iterations, d.iterations.cpu().numpy())
 
 
+@pytest.mark.parametrize("aniso", [False, True])
+def test_host_pipelined_path_matches_device(aniso):
+    """batch >= 4 x SMs takes the chunked H2D / solve / D2H pipeline on the host path (4 streams);
+    every output must equal the single-launch device-memspace result bit for bit."""
+    import torch
+    B, n = 700, 300
+    p = W.config2(batch=B, n_cells=n)
+    rng = np.random.default_rng(3)
+    s1 = 0.2 * p.sigma_s0 if aniso else None
+    phi0 = rng.uniform(0.0, 1.0, (B, n))
+    cfg = snop.SolverConfig(tolerance=1e-9)
+    g = snop.Grid1D(p.length, n)
+    pinned = (torch.empty((B, n), dtype=torch.float64).pin_memory().numpy(),
+              torch.empty(B, dtype=torch.int32).pin_memory().numpy(),
+              torch.empty(B, dtype=torch.uint8).pin_memory().numpy())
+    h = snop.source_iteration(g, p.order, p.sigma_t, p.sigma_s0, p.source, cfg, initial_phi=phi0, sigma_s1=s1,
+                              want_current=True, want_leakage=True, out=pinned)
+    dv = [torch.from_numpy(x).cuda() for x in (p.sigma_t, p.sigma_s0, p.source, phi0)]
+    d = snop.source_iteration(g, p.order, dv[0], dv[1], dv[2], cfg, initial_phi=dv[3],
+                              sigma_s1=None if s1 is None else torch.from_numpy(s1).cuda(), want_current=True,
+                              want_leakage=True)
+    assert h.phi is pinned[0]
+    assert np.array_equal(h.phi, d.phi.cpu().numpy())
+    assert np.array_equal(h.current, d.current.cpu().numpy())
+    assert np.array_equal(h.iterations, d.iterations.cpu().numpy())
+    assert np.array_equal(h.converged, d.converged.cpu().numpy())
+    assert np.array_equal(h.leakage, d.leakage.cpu().numpy())
+
+
+@pytest.mark.parametrize("B,aniso,warm", [(37, False, False), (700, False, True), (64, True, True)])
+def test_host_zero_copy_path_matches_device(B, aniso, warm):
+    """All host arrays pinned -> the kernel reads inputs / writes results over the bus itself
+    (device staging workspace for the per-iteration operands); must equal the device path bit for bit."""
+    import torch
+    n = 300
+    p = W.config2(batch=B, n_cells=n)
+    rng = np.random.default_rng(4)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    st, ss, src = pin(p.sigma_t), pin(p.sigma_s0), pin(p.source)
+    s1 = pin(0.2 * p.sigma_s0) if aniso else None
+    phi0 = pin(rng.uniform(0.0, 1.0, (B, n))) if warm else None
+    cfg = snop.SolverConfig(tolerance=1e-9)
+    g = snop.Grid1D(p.length, n)
+    outs = (pin(np.empty((B, n))), pin(np.empty(B, dtype=np.int32)), pin(np.empty(B, dtype=np.uint8)))
+    # leakage output is allocated by the wrapper (pageable) -> zero-copy needs it pinned too, so
+    # exercise both: without leakage (zero-copy) and with it (staged path)
+    h = snop.source_iteration(g, p.order, st, ss, src, cfg, initial_phi=phi0, sigma_s1=s1, out=outs)
+    dv = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    d = snop.source_iteration(g, p.order, dv(st), dv(ss), dv(src), cfg, initial_phi=dv(phi0), sigma_s1=dv(s1))
+    assert np.array_equal(h.phi, d.phi.cpu().numpy())
+    assert np.array_equal(h.iterations, d.iterations.cpu().numpy())
+    assert np.array_equal(h.converged, d.converged.cpu().numpy())
+    bad = st.copy()
+    bad[B // 2, 5] = 0.0
+    with pytest.raises(InvalidArgument):
+        snop.source_iteration(g, p.order, pin(bad), ss, src, cfg, out=outs)
+
+
 def test_deterministic_repeat():
     p = W.config2(batch=8, n_cells=2000)
     cfg = snop.SolverConfig(tolerance=1e-8)

@@ -1,4 +1,5 @@
-"""Experiment: per-phase cycle breakdown of K1 (needs a -DSNOP_PHASE_TIMING build via SNOP_LIB)."""
+"""Experiment: per-phase cycle breakdown of K1 (needs a -DSNOP_PHASE_TIMING build via SNOP_LIB).
+Usage: SNOP_LIB=tmp_exp/timing.so python tools/phase_timing.py [batch ...]"""
 import ctypes as C, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -8,18 +9,20 @@ lib = _capi.load()
 f = lib.snop_internal_phase_cycles
 f.argtypes = [C.c_void_p, C.c_int]
 buf = np.zeros(16, dtype=np.uint64)
-for name, p in (("C2", W.config2(batch=int(sys.argv[1]) if len(sys.argv) > 1 else 2048)), ("C5", W.config5())):
-    g = snop.Grid1D(p.length, p.n_cells)
-    args = [torch.from_numpy(a).cuda() for a in (p.sigma_t, p.sigma_s0, p.source)]
-    snop.source_iteration(g, p.order, *args, snop.SolverConfig(tolerance=p.tolerance))
-    f(buf.ctypes.data, 1)
-    r = snop.source_iteration(g, p.order, *args, snop.SolverConfig(tolerance=p.tolerance))
-    torch.cuda.synchronize()
-    f(buf.ctypes.data, 1)
-    it = int(r.iterations.to(torch.int64).sum())
-    ngroups = it * (p.order // 2 // 2)
-    labels = ["A maps", "bar1", "B scan", "bar2", "C replay", "pairs total", "phi+norm"]
-    for w in range(2):
-        row = buf[w * 8: w * 8 + 8]
-        print(name, "warp", w, " | ".join(f"{labels[k]} {row[k] / (ngroups if k < 5 else it):8.0f}" for k in range(7)),
-              "(cycles per group / per iteration)")
+labels = ["A maps", "bar1", "B scan", "bar2", "C replay", "pairs total", "phi+norm"]
+for batch in [int(a) for a in sys.argv[1:]] or [2048]:
+    for name, p in (("C2", W.config2(batch=batch)),):
+        g = snop.Grid1D(p.length, p.n_cells)
+        args = [torch.from_numpy(a).cuda() for a in (p.sigma_t, p.sigma_s0, p.source)]
+        snop.source_iteration(g, p.order, *args, snop.SolverConfig(tolerance=p.tolerance))
+        torch.cuda.synchronize()
+        f(buf.ctypes.data, 1)
+        r = snop.source_iteration(g, p.order, *args, snop.SolverConfig(tolerance=p.tolerance))
+        torch.cuda.synchronize()
+        f(buf.ctypes.data, 1)
+        it = int(np.asarray(r.iterations.cpu() if hasattr(r.iterations, "cpu") else r.iterations).astype(np.int64).sum())
+        ngroups = it * (p.order // 2 // 2)
+        for w in range(2):
+            row = buf[w * 8: w * 8 + 8].astype(np.float64)
+            print(name, "B", batch, "warp", w, " | ".join(f"{labels[k]} {row[k] / (ngroups if k < 5 else it):7.0f}"
+                                                         for k in range(7)), "(cycles per group / per iteration)")
