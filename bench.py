@@ -49,6 +49,53 @@ def peaks():
     return 6650.0, "fallback"
 
 
+def c5_arm(snop, ctx, stream, args):
+    """BASELINE configs[4] (C5): FNO (4 layers, width 64, 16 modes, lift 2->64, proj 64->128->1, GELU,
+    random-init) on the recast source of 4096 x 1024-cell instances -> warm-started S16 solve, against
+    the zero-guess solve. Device-resident inputs, CUDA-event timing on the solver stream."""
+    import torch
+    from paper_2509_01416_b200 import operators as OPS, workloads as W
+    p = W.config5()
+    g = snop.Grid1D(p.length, p.n_cells)
+    cfg = snop.SolverConfig(tolerance=p.tolerance)
+    st, ss, src = (torch.from_numpy(a).cuda() for a in (p.sigma_t, p.sigma_s0, p.source))
+    fno = snop.SolutionOperator.fno(g, OPS.fno_init(64, 16, 4, 128, OPS.GELU), p.ref_params, ctx=ctx)
+
+    def timed(fn, reps=2):
+        fn()
+        ts = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            out = fn()
+            e1.record(stream)
+            ctx.synchronize()
+            ts.append(e0.elapsed_time(e1) / 1e3)
+        return out, float(np.min(ts))
+
+    cold, t_cold = timed(lambda: snop.source_iteration(g, p.order, st, ss, src, cfg, ctx=ctx, sync=False))
+    _, t_op = timed(lambda: fno.predict(src, sync=False))
+    warm, t_warm = timed(lambda: snop.precondition_fixed_source(fno, p.order, st, ss, src, cfg,
+                                                                recast_max_iterations=args.recast_max))
+    it_cold = cold.iterations.to(torch.int64)
+    it_warm = warm.refine_iterations.to(torch.int64)
+    return {"workload": "C5 4096x1024 S16, p*=(1.0,0.8), tol 1e-8; FNO random-init (seeded), fp32 on tcgen05",
+            "operator_ms": 1e3 * t_op, "zero_guess_ms": 1e3 * t_cold, "warm_start_ms": 1e3 * t_warm,
+            "solves_per_sec_zero_guess": p.batch / t_cold, "solves_per_sec_warm_start": p.batch / t_warm,
+            "iterations_mean_zero_guess": float(it_cold.float().mean().item()),
+            "iterations_mean_warm_start": float(it_warm.float().mean().item()),
+            "recast_max_iterations": args.recast_max}
+
+
+def fp64_peak():
+    p = ROOT / "profiles" / "fp64_peak.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    return float(d["dfma_per_clk_per_sm"]), float(d["k1_fp64_thread_ops_per_update"])
+
+
 def dist_env():
     from paper_2509_01416_b200.distributed import env
     return env()
@@ -237,7 +284,7 @@ def run_gpu(args):
         don = snop.SolutionOperator.deeponet(g, OPS.deeponet_init(p.n_cells), p.ref_params, ctx=ctx)
         snop.precondition_fixed_source(don, p.order, st, ss, src, cfg, recast_max_iterations=args.recast_max)
         wt = []
-        for _ in range(max(1, args.steps // 4)):
+        for _ in range(max(3, args.steps // 4)):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -245,6 +292,8 @@ def run_gpu(args):
             e1.record(stream)
             ctx.synchronize()
             wt.append(e0.elapsed_time(e1) / 1e3)
+        if os.environ.get("SNOP_BENCH_DEBUG"):
+            print("warm step times (ms):", [round(1e3 * x, 3) for x in wt], file=sys.stderr)
         tp = []
         for _ in range(3):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -257,13 +306,16 @@ def run_gpu(args):
         warm = {"operator": "DeepONet 2000->128x4 / 1->128x4, p=128, tanh, random-init (seeded Xavier), fp32 "
                             "on tcgen05 (3xTF32)",
                 "recast_max_iterations": args.recast_max,
-                "solves_per_sec": p.batch / float(np.mean(wt)), "ms_per_step": 1e3 * float(np.mean(wt)),
+                "solves_per_sec": p.batch / float(np.median(wt)), "ms_per_step": 1e3 * float(np.median(wt)),
+                "timing": f"median of {len(wt)} device-timed steps",
                 "operator_ms": 1e3 * float(np.min(tp)),
                 "refine_iterations_mean": float(ri.float().mean().item()),
                 "recast_iterations_mean": float(rw.precond_iterations.float().mean().item()),
                 "recast_status_counts": [int((rw.recast_status == k).sum().item()) for k in range(3)],
                 "zero_guess_iterations_mean": float(iters.float().mean().item()),
                 "note": "random-init operator: the warm start does not reduce iterations (DESIGN.md §5)"}
+
+    c5 = None if (args.no_c5 or world > 1) else c5_arm(snop, ctx, stream, args)
 
     if rank != 0:
         if world > 1:
@@ -292,8 +344,20 @@ def run_gpu(args):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    fp = fp64_peak()
+    if fp is not None:  # the kernel's binding ceiling (report both, name the binding one)
+        per_sm_clk, ops_per_update = fp
+        sm_mhz = (line["clocks"] or {}).get("sm_mhz") or 1965.0
+        peak_ops = per_sm_clk * torch.cuda.get_device_properties(dev).multi_processor_count * sm_mhz * 1e6
+        ach = value / world * ops_per_update
+        line["roofline_fp64"] = {"bound": "fp64-issue", "achieved": ach / 1e12, "peak": peak_ops / 1e12,
+                                 "unit": "T fp64-ops/s", "frac": ach / peak_ops,
+                                 "note": "fp64 pipe instructions per update from ncu (profiles/fp64_peak.json); "
+                                         "peak = measured DFMA rate per SM x SMs x sampled SM clock"}
     if warm is not None:
         line["warm_start"] = warm
+    if c5 is not None:
+        line["c5_fno_warm_start"] = c5
     if not args.no_cpu_baseline and world == 1:
         from tests import oracle_lib as O
         th = O.hardware_threads()
@@ -317,6 +381,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=2048)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-warm-start", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 FNO warm-start arm")
     ap.add_argument("--recast-max", type=int, default=1)
     args = ap.parse_args()
     if args.impl == "reference":
