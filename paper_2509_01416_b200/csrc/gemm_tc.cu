@@ -109,6 +109,8 @@ struct Smem {
   uint64_t bar[2];     // chunk buffers: MMAs reading the buffer have completed
   uint64_t accbar[2];  // split mode: all MMAs of the chunk accumulating into TMEM slot s are done
   uint32_t tmem_base;
+  float ep_bias[N];    // this tile's bias[n0 .. n0 + N) (0 beyond N / without bias)
+  float ep_rw[N];      // this tile's row-dot weights (fused FNO projection)
 };
 
 // Long-K contractions (K > SPLIT_K: DeepONet branch K = 2000, FNO forward DFT K = 1024) use split
@@ -187,10 +189,17 @@ __device__ __forceinline__ void load_chunk(Stage<ROWS>& st, const GemmArgs& g, c
     } else if (base) {
       const int kg = k0 + kq * 4;
       const float* p = base + (int64_t)(kofs + kq * 4) * sk;
-      if (kg < g.K) v.x = __ldg(p);
-      if (kg + 1 < g.K) v.y = __ldg(p + sk);
-      if (kg + 2 < g.K) v.z = __ldg(p + 2 * sk);
-      if (kg + 3 < g.K) v.w = __ldg(p + 3 * sk);
+      if (k0 + KC <= g.K) {  // interior chunk: no per-element bounds checks
+        v.x = __ldg(p);
+        v.y = __ldg(p + sk);
+        v.z = __ldg(p + 2 * sk);
+        v.w = __ldg(p + 3 * sk);
+      } else {
+        if (kg < g.K) v.x = __ldg(p);
+        if (kg + 1 < g.K) v.y = __ldg(p + sk);
+        if (kg + 2 < g.K) v.z = __ldg(p + 2 * sk);
+        if (kg + 3 < g.K) v.w = __ldg(p + 3 * sk);
+      }
     }
     st.v[i] = v;
   }
@@ -280,6 +289,11 @@ __global__ void __launch_bounds__(THREADS, (N <= 64 ? (SPLIT ? 2 : 4) : 1))
     }
     const RowPtr ra = row_ptr<TM, true>(g, b, m0, mfold, tid);
     const RowPtr rb = row_ptr<N, false>(g, b, n0, 0, tid);
+    for (int j = tid; j < N; j += THREADS) {  // visible to the epilogue through the chunk barriers
+      const int gn = n0 + j;
+      s.ep_bias[j] = (g.bias && gn < g.N) ? g.bias[gn] : 0.f;
+      s.ep_rw[j] = (g.rowdot_w && gn < g.N) ? g.rowdot_w[gn] : 0.f;
+    }
     load_chunk<TM>(sa, g, ra, 0, tid);
     load_chunk<N>(sb, g, rb, 0, tid);
     int last_buf = 0;
@@ -379,14 +393,14 @@ __global__ void __launch_bounds__(THREADS, (N <= 64 ? (SPLIT ? 2 : 4) : 1))
       if (gm < g.M) {
         const bool full = (n0 + c0 + 16 <= g.N);
         if (g.rowdot_w) {
+          float part = 0.f;  // 16 products in fp32, then one fp64 accumulate per 16 columns
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            const int gn = n0 + c0 + j;
-            if (gn >= g.N) continue;
-            float x = g.alpha * x16[j];
-            if (g.bias) x += g.bias[gn];
-            rdot += (double)(act_f(x, g.act) * g.rowdot_w[gn]);
+            if (!full && n0 + c0 + j >= g.N) continue;
+            const float x = fmaf(g.alpha, x16[j], s.ep_bias[c0 + j]);
+            part = fmaf(act_f(x, g.act), s.ep_rw[c0 + j], part);
           }
+          rdot += (double)part;
         } else if (full && g.scn == 1 && !g.Cd && ((row + n0 + c0) & 3) == 0 &&
                    ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0)) {
           // vectorised path: 16 contiguous fp32 of this row -> 4 x 16 B
@@ -400,7 +414,7 @@ __global__ void __launch_bounds__(THREADS, (N <= 64 ? (SPLIT ? 2 : 4) : 1))
             for (int e = 0; e < 4; ++e) {
               const int j = v4 * 4 + e;
               float x = g.alpha * x16[j] + (g.beta != 0.f ? g.beta * op[e] : 0.f);
-              if (g.bias) x += g.bias[n0 + c0 + j];
+              x += s.ep_bias[c0 + j];
               op[e] = act_f(x, g.act);
             }
             dst[v4] = o;
@@ -413,7 +427,7 @@ __global__ void __launch_bounds__(THREADS, (N <= 64 ? (SPLIT ? 2 : 4) : 1))
             const int64_t off = row + (int64_t)gn * g.scn;
             float x = g.alpha * x16[j];
             if (g.beta != 0.f) x += g.beta * g.C[off];
-            if (g.bias) x += g.bias[gn];
+            x += s.ep_bias[c0 + j];
             x = act_f(x, g.act);
             if (g.Cd) g.Cd[off] = (double)x;
             else g.C[off] = x;
