@@ -8,6 +8,7 @@
 #include <new>
 #include <string>
 
+#define SNOP_PHASE_SYM g_phase_cycles_capi
 #include "snop_internal.h"
 
 namespace snop_impl {

@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#define SNOP_PHASE_SYM g_phase_cycles_grf
 #include "snop_internal.h"
 
 namespace snop_impl {

@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#define SNOP_PHASE_SYM g_phase_cycles_op
 #include "gemm.cuh"
 #include "model_io.h"
 #include "snop_internal.h"

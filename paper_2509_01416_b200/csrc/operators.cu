@@ -1,6 +1,7 @@
 // operators.cu — K3 recast-source kernel and the SolutionOperator entry points.
 #include <string>
 
+#define SNOP_PHASE_SYM g_phase_cycles_ops
 #include "snop_internal.h"
 
 using namespace snop_impl;

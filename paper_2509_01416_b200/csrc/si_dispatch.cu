@@ -2,6 +2,7 @@
 // size (CS CTAs per instance) of K1/K2 for a launch.
 #include <cstdlib>
 
+#define SNOP_PHASE_SYM g_phase_cycles_disp
 #include "si_kernels.cuh"
 
 namespace snop_si {

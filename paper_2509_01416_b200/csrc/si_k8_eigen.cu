@@ -1,4 +1,5 @@
 // Explicit instantiations: K2 power-iteration kernels, K = 8, cluster mode = false.
+#define SNOP_PHASE_SYM g_phase_cycles_eigen
 #include "si_kernels.cuh"
 
 namespace snop_si {
@@ -8,3 +9,14 @@ SNOP_INST_PI(8, 128, false)
 SNOP_INST_PI(8, 256, false)
 SNOP_INST_PI(8, 512, false)
 }  // namespace snop_si
+
+#ifdef SNOP_PHASE_TIMING
+extern "C" int snop_internal_phase_cycles_eigen(unsigned long long* out /* [2][10] */, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, snop_dev::g_phase_cycles_eigen, sizeof(unsigned long long) * 20);
+  if (reset) {
+    unsigned long long z[20] = {};
+    cudaMemcpyToSymbol(snop_dev::g_phase_cycles_eigen, z, sizeof(z));
+  }
+  return (int)e;
+}
+#endif

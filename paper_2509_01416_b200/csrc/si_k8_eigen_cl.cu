@@ -1,4 +1,5 @@
 // Explicit instantiations: K2 power-iteration kernels, K = 8, cluster mode = true.
+#define SNOP_PHASE_SYM g_phase_cycles_ecl
 #include "si_kernels.cuh"
 
 namespace snop_si {

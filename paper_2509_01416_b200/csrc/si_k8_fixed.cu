@@ -10,10 +10,10 @@ SNOP_INST_SI(8, 512, false)
 }  // namespace snop_si
 
 #ifdef SNOP_PHASE_TIMING
-extern "C" int snop_internal_phase_cycles(unsigned long long* out /* [2][8] */, int reset) {
-  cudaError_t e = cudaMemcpyFromSymbol(out, snop_dev::g_phase_cycles, sizeof(unsigned long long) * 16);
+extern "C" int snop_internal_phase_cycles(unsigned long long* out /* [2][10] */, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, snop_dev::g_phase_cycles, sizeof(unsigned long long) * 20);
   if (reset) {
-    unsigned long long z[16] = {};
+    unsigned long long z[20] = {};
     cudaMemcpyToSymbol(snop_dev::g_phase_cycles, z, sizeof(z));
   }
   return (int)e;

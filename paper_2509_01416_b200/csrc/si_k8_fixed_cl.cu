@@ -1,4 +1,5 @@
 // Explicit instantiations: K1 fixed-source kernels, K = 8, cluster mode = true.
+#define SNOP_PHASE_SYM g_phase_cycles_fcl
 #include "si_kernels.cuh"
 
 namespace snop_si {

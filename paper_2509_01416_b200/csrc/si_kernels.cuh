@@ -199,16 +199,23 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   }
   double k = k0_g ? k0_g[b] : 1.0;
   int rphase = 0;
+  // Loops over groups are outermost and the thread's K cells innermost (unrolled) throughout: the
+  // per-group global loads of all K cells are then independent and in flight together, instead of
+  // one dependent L2 round trip per (cell, group). Per-cell summation order is unchanged (g ascending).
   auto fission_integral = [&]() {
+    double f[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) f[j] = 0.0;
+#pragma unroll 2
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (c0 + j < Nc) f[j] = fma(nsf_b[cell(g, j)], phi_b[cell(g, j)], f[j]);
+    }
     double s = 0.0, dummy = 0.0;
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      if (c0 + j < Nc) {
-        double f = 0.0;
-        for (int g = 0; g < G; ++g) f = fma(nsf_b[cell(g, j)], phi_b[cell(g, j)], f);
-        s += f;
-      }
-    }
+    for (int j = 0; j < K; ++j)
+      if (c0 + j < Nc) s += f[j];
     reduce2<NT, CL>(s, dummy, false, sm.red2, sm.cred2, rphase++, sm);
     return s * sc.dx;
   };
@@ -239,15 +246,18 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   int64_t inner_total = 0;
   int outer = 0;
   bool converged = false;
+  SNOP_TSTAMP(tpi0);
   while (outer < ep.max_outer) {
     ++outer;
     // fission density from the flux at the start of the outer (frozen during the GS pass)
     double fiss[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      fiss[j] = 0.0;
-      if (c0 + j < Nc) {
-        for (int g = 0; g < G; ++g) {
+    for (int j = 0; j < K; ++j) fiss[j] = 0.0;
+#pragma unroll 2
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (c0 + j < Nc) {
           const double v = phi_b[cell(g, j)];
           old_b[cell(g, j)] = v;
           fiss[j] = fma(nsf_b[cell(g, j)], v, fiss[j]);
@@ -257,14 +267,22 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
     const double inv_k = 1.0 / k;
     for (int g = 0; g < G; ++g) {
       const double chig = chi_g[(size_t)b * G + g] * inv_k;
+      double q[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) q[j] = chig * fiss[j];
+#pragma unroll 2
+      for (int gp = 0; gp < G; ++gp) {
+        if (gp == g) continue;
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+          if (c0 + j < Nc)
+            q[j] = fma(ss_b[((size_t)gp * G + g) * Nc + c0 + j], phi_b[(size_t)gp * Nc + c0 + j], q[j]);
+      }
 #pragma unroll
       for (int j = 0; j < K; ++j) {
         if (c0 + j < Nc) {
           const size_t i = (size_t)c0 + j;
-          double q = chig * fiss[j];
-          for (int gp = 0; gp < G; ++gp)
-            if (gp != g) q = fma(ss_b[((size_t)gp * G + g) * Nc + i], phi_b[(size_t)gp * Nc + i], q);
-          qext_b[i] = q;
+          qext_b[i] = q[j];
           if constexpr (ANISO) jc_b[i] = 0.0;
           sm.st[j * NT + t] = st_b[(size_t)g * Nc + i];
           sm.phi[j * NT + t] = phi_b[(size_t)g * Nc + i];
@@ -278,7 +296,10 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
       io.src = qext_b;
       io.ss1 = ANISO ? ss1_g + (size_t)b * GN + (size_t)g * Nc : nullptr;
       io.jc = jc_b;
+      SNOP_TSTAMP(tsol0);
       inner_total += si_solve_call<K, NT, ANISO, CL>(sc, icfg, sm, io);
+      SNOP_TSTAMP(tsol1);
+      SNOP_TACC(7, tsol0, tsol1);
 #pragma unroll
       for (int j = 0; j < K; ++j)
         if (c0 + j < Nc) phi_b[cell(g, j)] = sm.phi[j * NT + t];
@@ -316,6 +337,8 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
       break;
     }
   }
+  SNOP_TSTAMP(tpi1);
+  SNOP_TACC(8, tpi0, tpi1);
   if (t == 0 && rank == 0) {
     k_g[b] = k;
     outer_g[b] = outer;

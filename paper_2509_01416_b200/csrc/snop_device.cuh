@@ -269,12 +269,15 @@ struct CellIO {
 
 #ifdef SNOP_PHASE_TIMING
 // experiment builds only: per-phase cycle counters (thread 0 and thread 32 of every CTA)
-static __device__ unsigned long long g_phase_cycles[2][8];
+#ifndef SNOP_PHASE_SYM
+#define SNOP_PHASE_SYM g_phase_cycles
+#endif
+static __device__ unsigned long long SNOP_PHASE_SYM[2][10];  // distinct name per translation unit
 #define SNOP_TSTAMP(var) long long var = clock64()
 #define SNOP_TACC(slot, t0, t1)                                                          \
   do {                                                                                   \
     if ((threadIdx.x & 31) == 0 && threadIdx.x < 64)                                     \
-      atomicAdd(&g_phase_cycles[threadIdx.x >> 5][slot], (unsigned long long)((t1) - (t0))); \
+      atomicAdd(&SNOP_PHASE_SYM[threadIdx.x >> 5][slot], (unsigned long long)((t1) - (t0))); \
   } while (0)
 #else
 #define SNOP_TSTAMP(var)

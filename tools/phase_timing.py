@@ -8,7 +8,7 @@ from paper_2509_01416_b200 import snop, workloads as W, _capi
 lib = _capi.load()
 f = lib.snop_internal_phase_cycles
 f.argtypes = [C.c_void_p, C.c_int]
-buf = np.zeros(16, dtype=np.uint64)
+buf = np.zeros(20, dtype=np.uint64)
 labels = ["A maps", "bar1", "B scan", "bar2", "C replay", "pairs total", "phi+norm"]
 for batch in [int(a) for a in sys.argv[1:]] or [2048]:
     for name, p in (("C2", W.config2(batch=batch)),):
@@ -23,6 +23,6 @@ for batch in [int(a) for a in sys.argv[1:]] or [2048]:
         it = int(np.asarray(r.iterations.cpu() if hasattr(r.iterations, "cpu") else r.iterations).astype(np.int64).sum())
         ngroups = it * (p.order // 2 // 2)
         for w in range(2):
-            row = buf[w * 8: w * 8 + 8].astype(np.float64)
+            row = buf[w * 10: w * 10 + 10].astype(np.float64)
             print(name, "B", batch, "warp", w, " | ".join(f"{labels[k]} {row[k] / (ngroups if k < 5 else it):7.0f}"
                                                          for k in range(7)), "(cycles per group / per iteration)")
