@@ -185,6 +185,11 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   double* qext_b = qext_g + (size_t)b * Nc;
   double* jc_b = ANISO ? jc_g + (size_t)b * Nc : nullptr;
   auto cell = [&](int g, int j) -> size_t { return (size_t)g * Nc + c0 + j; };
+  // Coalesced mapping for the per-cell outer-loop work (fission density, in-scatter source,
+  // renormalisation): r-th cell of thread t = cb + r * NT + t, so a warp touches 256 contiguous
+  // bytes per load; the thread-owned chunk mapping (c0 + j) is kept for shared-memory staging.
+  const int cb = rank * NT * K;
+  auto cc = [&](int r) -> int { return cb + r * NT + t; };
 
   // validation + initial flux (flat) and k
   bool bad = false;
@@ -205,17 +210,17 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   auto fission_integral = [&]() {
     double f[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) f[j] = 0.0;
+    for (int r = 0; r < K; ++r) f[r] = 0.0;
 #pragma unroll 2
     for (int g = 0; g < G; ++g) {
 #pragma unroll
-      for (int j = 0; j < K; ++j)
-        if (c0 + j < Nc) f[j] = fma(nsf_b[cell(g, j)], phi_b[cell(g, j)], f[j]);
+      for (int r = 0; r < K; ++r)
+        if (cc(r) < Nc) f[r] = fma(nsf_b[(size_t)g * Nc + cc(r)], phi_b[(size_t)g * Nc + cc(r)], f[r]);
     }
     double s = 0.0, dummy = 0.0;
 #pragma unroll
-    for (int j = 0; j < K; ++j)
-      if (c0 + j < Nc) s += f[j];
+    for (int r = 0; r < K; ++r)
+      if (cc(r) < Nc) s += f[r];
     reduce2<NT, CL>(s, dummy, false, sm.red2, sm.cred2, rphase++, sm);
     return s * sc.dx;
   };
@@ -240,8 +245,8 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   }
   for (int g = 0; g < G; ++g)
 #pragma unroll
-    for (int j = 0; j < K; ++j)
-      if (c0 + j < Nc) phi_b[cell(g, j)] /= F;
+    for (int r = 0; r < K; ++r)
+      if (cc(r) < Nc) phi_b[(size_t)g * Nc + cc(r)] /= F;
 
   int64_t inner_total = 0;
   int outer = 0;
@@ -256,16 +261,18 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
 #pragma unroll 2
     for (int g = 0; g < G; ++g) {
 #pragma unroll
-      for (int j = 0; j < K; ++j) {
-        if (c0 + j < Nc) {
-          const double v = phi_b[cell(g, j)];
-          old_b[cell(g, j)] = v;
-          fiss[j] = fma(nsf_b[cell(g, j)], v, fiss[j]);
+      for (int r = 0; r < K; ++r) {
+        if (cc(r) < Nc) {
+          const size_t i = (size_t)g * Nc + cc(r);
+          const double v = phi_b[i];
+          old_b[i] = v;
+          fiss[r] = fma(nsf_b[i], v, fiss[r]);
         }
       }
     }
     const double inv_k = 1.0 / k;
     for (int g = 0; g < G; ++g) {
+      SNOP_TSTAMP(tq0);
       const double chig = chi_g[(size_t)b * G + g] * inv_k;
       double q[K];
 #pragma unroll
@@ -274,16 +281,22 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
       for (int gp = 0; gp < G; ++gp) {
         if (gp == g) continue;
 #pragma unroll
-        for (int j = 0; j < K; ++j)
-          if (c0 + j < Nc)
-            q[j] = fma(ss_b[((size_t)gp * G + g) * Nc + c0 + j], phi_b[(size_t)gp * Nc + c0 + j], q[j]);
+        for (int r = 0; r < K; ++r)
+          if (cc(r) < Nc)
+            q[r] = fma(ss_b[((size_t)gp * G + g) * Nc + cc(r)], phi_b[(size_t)gp * Nc + cc(r)], q[r]);
       }
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        if (cc(r) < Nc) {
+          qext_b[cc(r)] = q[r];
+          if constexpr (ANISO) jc_b[cc(r)] = 0.0;
+        }
+      }
+      // (si_solve's entry barrier orders these coalesced writes before the owner-mapped reads)
 #pragma unroll
       for (int j = 0; j < K; ++j) {
         if (c0 + j < Nc) {
           const size_t i = (size_t)c0 + j;
-          qext_b[i] = q[j];
-          if constexpr (ANISO) jc_b[i] = 0.0;
           sm.st[j * NT + t] = st_b[(size_t)g * Nc + i];
           sm.phi[j * NT + t] = phi_b[(size_t)g * Nc + i];
         } else {
@@ -297,12 +310,14 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
       io.ss1 = ANISO ? ss1_g + (size_t)b * GN + (size_t)g * Nc : nullptr;
       io.jc = jc_b;
       SNOP_TSTAMP(tsol0);
+      SNOP_TACC(9, tq0, tsol0);
       inner_total += si_solve_call<K, NT, ANISO, CL>(sc, icfg, sm, io);
       SNOP_TSTAMP(tsol1);
       SNOP_TACC(7, tsol0, tsol1);
 #pragma unroll
       for (int j = 0; j < K; ++j)
         if (c0 + j < Nc) phi_b[cell(g, j)] = sm.phi[j * NT + t];
+      __syncthreads();  // owner-mapped writes -> coalesced reads of the next group / the update
     }
     const double F1 = fission_integral();
     if (!(F1 != 0.0) || !isfinite(F1)) {
@@ -311,13 +326,15 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
     }
     const double k_new = k * F1;
     double num = 0.0, den = 0.0;
+#pragma unroll 2
     for (int g = 0; g < G; ++g) {
 #pragma unroll
-      for (int j = 0; j < K; ++j) {
-        if (c0 + j < Nc) {
-          const double pn = phi_b[cell(g, j)] / F1;
-          phi_b[cell(g, j)] = pn;
-          const double d = pn - old_b[cell(g, j)];
+      for (int r = 0; r < K; ++r) {
+        if (cc(r) < Nc) {
+          const size_t i = (size_t)g * Nc + cc(r);
+          const double pn = phi_b[i] / F1;
+          phi_b[i] = pn;
+          const double d = pn - old_b[i];
           if (ep.norm == 0) {
             num = fmax(num, fabs(d));
             den = fmax(den, fabs(pn));

@@ -22,4 +22,6 @@ row = buf[:10].astype(np.float64)
 groups = sweeps * (p.order // 4)
 print(f"sweeps {sweeps} outer {outer}: per pair group maps {row[0]/groups:.0f} bar1 {row[1]/groups:.0f} scan {row[2]/groups:.0f} "
       f"bar2 {row[3]/groups:.0f} replay {row[4]/groups:.0f} | per sweep pairs {row[5]/sweeps:.0f} phi {row[6]/sweeps:.0f} | "
-      f"in solve calls per sweep {row[7]/sweeps:.0f} | whole loop per sweep {row[8]/sweeps:.0f} cycles")
+      f"in solve calls per sweep {row[7]/sweeps:.0f} | whole loop per sweep {row[8]/sweeps:.0f} cycles | "
+      f"group-source build per group solve {row[9]/(outer*p.n_groups):.0f} | outer-loop rest per outer "
+      f"{(row[8]-row[7]-row[9])/outer:.0f}")
