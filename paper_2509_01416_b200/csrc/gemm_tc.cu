@@ -520,7 +520,12 @@ extern "C" int snop_internal_gemm_test(int engine, int M, int N, int K, int batc
   g.beta = beta;
   g.act = act;
   g.ksplit = 0;
-  cudaError_t e = engine == 1 ? snop_ops::gemm_tc(g, 0, mfold) : snop_ops::gemm_f32(g, 0);
+  cudaError_t e = cudaSuccess;
+  if (engine == 2) {  // TMA-fed warp-specialised engine; -1 when the shape does not fit it
+    if (!snop_ops::gemm_tc2(g, 0, mfold, &e)) return -1;
+  } else {
+    e = engine == 1 ? snop_ops::gemm_tc(g, 0, mfold) : snop_ops::gemm_f32(g, 0);
+  }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   return (int)e;
 }

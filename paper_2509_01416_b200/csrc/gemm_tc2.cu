@@ -1,0 +1,424 @@
+// gemm_tc2.cu — warp-specialised, TMA-fed tcgen05 GEMM (3xTF32) for K-contiguous operands with
+// K <= 128 (the FNO inverse-DFT + W contraction, the FNO projection head, the DeepONet hidden
+// layers and combine). Same contract and accuracy as gemm_tc.cu's non-split kernel:
+//
+//   C(b, m, n) = act( alpha * sum_k A(b, m, k) B(b, n, k) + bias[n] )   (or the fused row-dot)
+//
+// Roles (one persistent CTA per SM, 14 warps):
+//   warp 0      TMA producer: 2-D tensor-map loads of the raw fp32 A (128 x 32) and B (N x 32)
+//               chunks into a 128-byte-swizzled K-major stage (cp.async.bulk.tensor, mbarrier tx)
+//   warps 2-5   converters: per stage, hi = tf32_round(x) in place and lo = x - hi into the lo
+//               buffer — an element-wise pass, so the swizzled layout is preserved
+//   warp 1      MMA issuer: 4 k-steps x 3 tcgen05.mma.kind::tf32 (lo*hi, hi*lo, hi*hi) per chunk
+//               into one of two TMEM accumulators, commits free the stage / publish the tile
+//   warps 6-13  epilogue: tcgen05.ld of the finished accumulator (warp w reads TMEM lanes
+//               32 (w % 4) .., one of two column halves), bias / activation (compile-time) /
+//               fp32-fp64 store or the fused row-dot; the other accumulator is meanwhile filled
+//               by the next tile's MMAs
+// Stages are recycled through full (TMA) -> conv (converters) -> empty (MMA commit) mbarriers,
+// so global loads, the split, the tensor core and the epilogue all overlap.
+#include <cuda.h>
+
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+
+#include "gemm.cuh"
+
+namespace snop_ops {
+namespace tc2 {
+
+constexpr int TM = 128;
+constexpr int KC = 32;  // fp32 per 128-byte swizzle row
+constexpr int NWARPS = 14;
+constexpr int THREADS = NWARPS * 32;
+constexpr int CONV0 = 2, EPI0 = 6, NEPI = 8;  // epilogue: 2 warps per TMEM lane quarter (column halves)
+
+template <int N>
+constexpr int stages() { return N <= 64 ? 4 : 3; }
+
+template <int N>
+struct alignas(1024) Stage {
+  float a_hi[TM * KC];  // 16 KB, 1024-B aligned (swizzle atom = 8 rows x 128 B)
+  float a_lo[TM * KC];
+  float b_hi[N * KC];
+  float b_lo[N * KC];
+};
+
+template <int N>
+struct Smem {
+  Stage<N> st[stages<N>()];
+  uint64_t full[stages<N>()], conv[stages<N>()], empty[stages<N>()];
+  uint64_t acc_full[2], acc_empty[2];
+  uint32_t tmem_base;
+  float ep_bias[2][N];  // per accumulator: this tile's bias / row-dot weights
+  float ep_rw[2][N];
+};
+
+struct Args {
+  GemmArgs g;
+  int64_t a1_brows, a2_brows, b1_brows, b2_brows;  // batch stride in rows of each 2-D view
+  int64_t m_tiles, n_tiles, total;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(su32(b)), "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
+      : "memory");
+}
+
+// K-major, 128-byte swizzle: 8-row groups 1024 B apart (SBO), LBO unused (1), version 1, type 2.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__host__ __device__ constexpr uint32_t idesc(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+}
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(
+          d),
+      "l"(a), "l"(b), "r"(id), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ float tf32_round(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+template <int ACT>
+__device__ __forceinline__ float act_c(float x) {
+  if constexpr (ACT == ACT_RELU) return x > 0.f ? x : 0.f;
+  else if constexpr (ACT == ACT_TANH) return tanhf(x);
+  else if constexpr (ACT == ACT_GELU) return 0.5f * x * (1.f + erff(x * 0.70710678118654752440f));
+  else return x;
+}
+
+template <int N, int ACT>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tA1, const __grid_constant__ CUtensorMap tA2,
+                    const __grid_constant__ CUtensorMap tB1, const __grid_constant__ CUtensorMap tB2,
+                    const __grid_constant__ Args a) {
+  constexpr int S = stages<N>();
+  constexpr uint32_t TCOLS = 2 * N;
+  extern __shared__ __align__(1024) unsigned char raw[];
+  // the 128-B swizzle atoms need 1024-B aligned stages: align the dynamic window explicitly
+  const uint32_t pad = (1024u - (su32(raw) & 1023u)) & 1023u;
+  auto& s = *reinterpret_cast<Smem<N>*>(raw + pad);
+  const GemmArgs& g = a.g;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nchunks = (g.K + KC - 1) / KC;
+
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&s.tmem_base)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      bar_init(&s.full[i], 1);
+      bar_init(&s.conv[i], 4);
+      bar_init(&s.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      bar_init(&s.acc_full[i], 1);
+      bar_init(&s.acc_empty[i], NEPI);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s.tmem_base;
+
+  auto tile_coords = [&](int64_t tile, int& b, int64_t& m0, int& n0) {
+    const int nt = (int)(tile % a.n_tiles);
+    const int64_t mt = (tile / a.n_tiles) % a.m_tiles;
+    b = (int)(tile / (a.n_tiles * a.m_tiles));
+    m0 = mt * TM;
+    n0 = nt * N;
+  };
+
+  if (warp == 0) {
+    // ---------------- TMA producer (one lane; the rest of the warp waits at the final barrier) --
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t tile = blockIdx.x; tile < a.total; tile += gridDim.x) {
+        int b, n0;
+        int64_t m0;
+        tile_coords(tile, b, m0, n0);
+        for (int c = 0; c < nchunks; ++c, ++it) {
+          const int st = (int)(it % S);
+          bar_wait(&s.empty[st], ((it / S) & 1) ^ 1);
+          bar_expect_tx(&s.full[st], (uint32_t)((TM + N) * KC * sizeof(float)));
+          const int k0 = c * KC;
+          const bool seg2 = g.ksplit > 0 && k0 >= g.ksplit;
+          const int kk = seg2 ? k0 - g.ksplit : k0;
+          tma_2d(s.st[st].a_hi, seg2 ? &tA2 : &tA1, kk, (int)(b * (seg2 ? a.a2_brows : a.a1_brows) + m0), &s.full[st]);
+          tma_2d(s.st[st].b_hi, seg2 ? &tB2 : &tB1, kk, (int)(b * (seg2 ? a.b2_brows : a.b1_brows) + n0), &s.full[st]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      uint32_t it = 0, tcount = 0;
+      constexpr uint32_t id = idesc(N);
+      for (int64_t tile = blockIdx.x; tile < a.total; tile += gridDim.x, ++tcount) {
+        const uint32_t acc = tcount & 1;
+        bar_wait(&s.acc_empty[acc], ((tcount >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + acc * N;
+        for (int c = 0; c < nchunks; ++c, ++it) {
+          const int st = (int)(it % S);
+          bar_wait(&s.conv[st], (it / S) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t ah = su32(s.st[st].a_hi), al = su32(s.st[st].a_lo);
+          const uint32_t bh = su32(s.st[st].b_hi), bl = su32(s.st[st].b_lo);
+#pragma unroll
+          for (int ks = 0; ks < KC / 8; ++ks) {
+            const uint32_t off = ks * 32;  // 8 tf32 = 32 B along K inside the swizzle row
+            const uint32_t first = (c == 0 && ks == 0) ? 0u : 1u;
+            mma(d, sw128_desc(al + off), sw128_desc(bh + off), id, first);  // small terms first
+            mma(d, sw128_desc(ah + off), sw128_desc(bl + off), id, 1u);
+            mma(d, sw128_desc(ah + off), sw128_desc(bh + off), id, 1u);
+          }
+          commit(&s.empty[st]);
+        }
+        commit(&s.acc_full[acc]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= CONV0 && warp < CONV0 + 4) {
+    // ---------------- converters: hi = round(x) in place, lo = x - hi ----------------
+    const int ct = tid - CONV0 * 32;  // 0..127
+    uint32_t it = 0;
+    for (int64_t tile = blockIdx.x; tile < a.total; tile += gridDim.x) {
+      for (int c = 0; c < nchunks; ++c, ++it) {
+        const int st = (int)(it % S);
+        bar_wait(&s.full[st], (it / S) & 1);
+        float4* ah = reinterpret_cast<float4*>(s.st[st].a_hi);
+        float4* al = reinterpret_cast<float4*>(s.st[st].a_lo);
+#pragma unroll
+        for (int i = 0; i < TM * KC / 4 / 128; ++i) {
+          const float4 x = ah[ct + i * 128];
+          const float4 h = make_float4(tf32_round(x.x), tf32_round(x.y), tf32_round(x.z), tf32_round(x.w));
+          ah[ct + i * 128] = h;
+          al[ct + i * 128] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+        }
+        float4* bh = reinterpret_cast<float4*>(s.st[st].b_hi);
+        float4* bl = reinterpret_cast<float4*>(s.st[st].b_lo);
+#pragma unroll
+        for (int i = 0; i < N * KC / 4 / 128; ++i) {
+          const float4 x = bh[ct + i * 128];
+          const float4 h = make_float4(tf32_round(x.x), tf32_round(x.y), tf32_round(x.z), tf32_round(x.w));
+          bh[ct + i * 128] = h;
+          bl[ct + i * 128] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+        __syncwarp();
+        if (lane == 0) bar_arrive(&s.conv[st]);
+      }
+    }
+  } else if (warp >= EPI0) {
+    // ---------------- epilogue ----------------
+    const int e = warp - EPI0;             // 0..7
+    const int et = tid - EPI0 * 32;        // 0..255
+    const int q = warp & 3;                // TMEM lane quarter this warp may access
+    constexpr int NH = N / 2;              // columns per epilogue warp
+    const int cbeg = (e >> 2) * NH;
+    uint32_t tcount = 0;
+    for (int64_t tile = blockIdx.x; tile < a.total; tile += gridDim.x, ++tcount) {
+      const uint32_t acc = tcount & 1;
+      int b, n0;
+      int64_t m0;
+      tile_coords(tile, b, m0, n0);
+      // this tile's bias / row-dot weights (epilogue warps only; named barrier 1)
+      for (int j = et; j < N; j += NEPI * 32) {
+        const int gn = n0 + j;
+        s.ep_bias[acc][j] = (g.bias && gn < g.N) ? g.bias[gn] : 0.f;
+        s.ep_rw[acc][j] = (g.rowdot_w && gn < g.N) ? g.rowdot_w[gn] : 0.f;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(NEPI * 32) : "memory");
+      bar_wait(&s.acc_full[acc], (tcount >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t gm = m0 + q * 32 + lane;
+      const int64_t row = (int64_t)b * g.scb + gm * g.scm;
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * N + cbeg;
+      float rpart = 0.f;
+#pragma unroll 1
+      for (int c0 = 0; c0 < NH; c0 += 16) {
+        uint32_t v[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr + (uint32_t)c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (gm >= g.M) continue;
+        const int cc = cbeg + c0;  // column within the tile
+        const bool full = n0 + cc + 16 <= g.N;
+        float o[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) o[j] = act_c<ACT>(fmaf(g.alpha, __uint_as_float(v[j]), s.ep_bias[acc][cc + j]));
+        if (g.rowdot_w) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (full || n0 + cc + j < g.N) rpart = fmaf(o[j], s.ep_rw[acc][cc + j], rpart);
+        } else if (full && g.scn == 1 && !g.Cd && ((row + n0 + cc) & 3) == 0) {
+          float4* dst = reinterpret_cast<float4*>(g.C + row + n0 + cc);
+#pragma unroll
+          for (int v4 = 0; v4 < 4; ++v4) dst[v4] = make_float4(o[4 * v4], o[4 * v4 + 1], o[4 * v4 + 2], o[4 * v4 + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int gn = n0 + cc + j;
+            if (gn >= g.N) continue;
+            const int64_t off = row + (int64_t)gn * g.scn;
+            if (g.Cd) g.Cd[off] = (double)o[j];
+            else g.C[off] = o[j];
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) bar_arrive(&s.acc_empty[acc]);
+      if (g.rowdot_w) {  // the two column halves of a row meet in shared memory (fixed order)
+        __shared__ float rsum[128];
+        if (e >= 4 && gm < g.M) rsum[q * 32 + lane] = rpart;
+        asm volatile("bar.sync 2, %0;" ::"r"(NEPI * 32) : "memory");
+        if (e < 4 && gm < g.M) g.rowdot_out[row] = (double)rpart + (double)rsum[q * 32 + lane] + (double)g.rowdot_b;
+        asm volatile("bar.sync 2, %0;" ::"r"(NEPI * 32) : "memory");
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+}
+
+// ---- host side ------------------------------------------------------------------------------
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encoder() {
+  static EncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (EncodeFn) nullptr;
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  return fn;
+}
+
+// 2-D view [rows][cols] of fp32 with row stride `ld` elements, box [box_rows][32], 128-B swizzle.
+bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  EncodeFn enc = encoder();
+  if (!enc || !base || rows <= 0 || cols <= 0) return false;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * 4) & 15)) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  const cuuint32_t box[2] = {(cuuint32_t)KC, (cuuint32_t)box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int N, int ACT>
+cudaError_t launch(const Args& a, const CUtensorMap* maps, cudaStream_t st) {
+  const size_t smem = sizeof(Smem<N>) + 1024;  // + alignment slack
+  static bool attr = false;
+  static int sms = 148;
+  if (!attr) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(gemm_tc2_kernel<N, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    attr = true;
+  }
+  const int64_t grid = a.total < sms ? a.total : sms;
+  gemm_tc2_kernel<N, ACT><<<(unsigned)grid, THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], a);
+  return cudaGetLastError();
+}
+
+}  // namespace tc2
+
+// Returns true (and launches) when the contraction fits this engine: K-contiguous operands,
+// K <= 128 in whole 32-wide chunks per segment, N <= 128, no batch folding, beta = 0, aligned
+// strides. Otherwise false and the caller uses gemm_tc.
+bool gemm_tc2(const GemmArgs& g, cudaStream_t st, int64_t mfold, cudaError_t* err) {
+  using namespace tc2;
+  *err = cudaSuccess;
+  if (std::getenv("SNOP_GEMM_V1")) return false;
+  if (mfold > 0 || g.beta != 0.f || g.K > 128 || g.N > 128 || g.sak != 1 || g.sbk != 1) return false;
+  if (g.ksplit > 0 && (g.ksplit % KC != 0 || g.sak2 != 1 || g.sbk2 != 1)) return false;
+  if (g.rowdot_w && g.N > 128) return false;
+  const int K1 = g.ksplit > 0 ? g.ksplit : g.K, K2 = g.ksplit > 0 ? g.K - g.ksplit : 0;
+  auto brows = [](int64_t sb, int64_t sr, int64_t* out) {
+    if (sb == 0) { *out = 0; return true; }
+    if (sr <= 0 || sb % sr != 0) return false;
+    *out = sb / sr;
+    return true;
+  };
+  Args a{};
+  a.g = g;
+  if (!brows(g.sab, g.sam, &a.a1_brows) || !brows(g.sbb, g.sbn, &a.b1_brows)) return false;
+  if (g.ksplit > 0 && (!brows(g.sab2, g.sam2, &a.a2_brows) || !brows(g.sbb2, g.sbn2, &a.b2_brows))) return false;
+  const int NT = g.N <= 64 ? 64 : 128;
+  CUtensorMap maps[4];
+  std::memset(maps, 0, sizeof(maps));
+  const int64_t rowsA1 = (g.batch - 1) * a.a1_brows + g.M, rowsB1 = (g.batch - 1) * a.b1_brows + g.N;
+  if (!make_map(&maps[0], g.A, rowsA1, K1, g.sam, TM) || !make_map(&maps[2], g.B, rowsB1, K1, g.sbn, NT)) return false;
+  if (g.ksplit > 0) {
+    const int64_t rowsA2 = (g.batch - 1) * a.a2_brows + g.M, rowsB2 = (g.batch - 1) * a.b2_brows + g.N;
+    if (!make_map(&maps[1], g.A2, rowsA2, K2, g.sam2, TM) || !make_map(&maps[3], g.B2, rowsB2, K2, g.sbn2, NT))
+      return false;
+  } else {
+    maps[1] = maps[0];
+    maps[3] = maps[2];
+  }
+  a.m_tiles = (g.M + TM - 1) / TM;
+  a.n_tiles = (g.N + NT - 1) / NT;
+  a.total = a.m_tiles * a.n_tiles * g.batch;
+  if (a.total == 0) return true;
+  switch (g.act) {
+    case ACT_RELU: *err = NT == 64 ? launch<64, ACT_RELU>(a, maps, st) : launch<128, ACT_RELU>(a, maps, st); break;
+    case ACT_TANH: *err = NT == 64 ? launch<64, ACT_TANH>(a, maps, st) : launch<128, ACT_TANH>(a, maps, st); break;
+    case ACT_GELU: *err = NT == 64 ? launch<64, ACT_GELU>(a, maps, st) : launch<128, ACT_GELU>(a, maps, st); break;
+    default: *err = NT == 64 ? launch<64, ACT_NONE>(a, maps, st) : launch<128, ACT_NONE>(a, maps, st); break;
+  }
+  return true;
+}
+
+}  // namespace snop_ops

@@ -262,7 +262,11 @@ bool use_tc() {
 
 snop_status gemm(Ctx& ctx, const GemmArgs& a, int64_t mfold = 0) {
   ctx.launches++;
-  if (use_tc()) return cuda_status("gemm_tc", gemm_tc(a, ctx.stream, mfold));
+  if (use_tc()) {
+    cudaError_t e = cudaSuccess;
+    if (gemm_tc2(a, ctx.stream, mfold, &e)) return cuda_status("gemm_tc2", e);
+    return cuda_status("gemm_tc", gemm_tc(a, ctx.stream, mfold));
+  }
   if (mfold > 0) return invalid("batch-folded GEMM requires the tensor-core engine");
   return cuda_status("gemm", gemm_f32(a, ctx.stream));
 }
