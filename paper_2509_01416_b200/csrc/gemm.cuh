@@ -47,6 +47,13 @@ struct GemmArgs {
   const float* rowdot_w;
   float rowdot_b;
   double* rowdot_out;
+  // optional rank-2 epilogue term (TMA engine only): + r2_a[n] * r2_s[b * r2_sb + m] + r2_b[n] * r2_x[m]
+  // (the FNO's affine lift folded through layer 0's W path)
+  const float* r2_a;
+  const float* r2_b;
+  const float* r2_s;
+  int64_t r2_sb;
+  const float* r2_x;
 };
 
 __device__ __forceinline__ float gemm_a(const GemmArgs& a, int b, int64_t m, int k) {

@@ -480,6 +480,7 @@ cudaError_t launch(const GemmArgs& g, int64_t mfold, cudaStream_t st) {
 // (r / mfold) * scb + (r % mfold) * scm (used for the FNO forward DFT over B x C rows).
 cudaError_t gemm_tc(const GemmArgs& g, cudaStream_t st, int64_t mfold) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
+  if (g.r2_a) return cudaErrorInvalidValue;  // rank-2 epilogue: TMA engine only
   if (g.ksplit > 0 && g.ksplit % tc::KC != 0) return cudaErrorInvalidValue;  // segment = whole chunks
   const bool split = g.K > tc::SPLIT_K;  // long K: chunk-wise drained accumulation
   if (g.rowdot_w) {  // row-dot epilogue: N <= 128 as one or two 64-wide tiles (caller zeroes out)

@@ -51,8 +51,10 @@ struct Smem {
   uint64_t full[stages<N>()], conv[stages<N>()], empty[stages<N>()];
   uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem_base;
-  float ep_bias[2][N];  // per accumulator: this tile's bias / row-dot weights
+  float ep_bias[2][N];  // per accumulator: this tile's bias / row-dot weights / rank-2 columns
   float ep_rw[2][N];
+  float ep_ra[2][N];
+  float ep_rb[2][N];
 };
 
 struct Args {
@@ -264,6 +266,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int gn = n0 + j;
         s.ep_bias[acc][j] = (g.bias && gn < g.N) ? g.bias[gn] : 0.f;
         s.ep_rw[acc][j] = (g.rowdot_w && gn < g.N) ? g.rowdot_w[gn] : 0.f;
+        s.ep_ra[acc][j] = (g.r2_a && gn < g.N) ? g.r2_a[gn] : 0.f;
+        s.ep_rb[acc][j] = (g.r2_b && gn < g.N) ? g.r2_b[gn] : 0.f;
       }
       asm volatile("bar.sync 1, %0;" ::"r"(NEPI * 32) : "memory");
       bar_wait(&s.acc_full[acc], (tcount >> 1) & 1);
@@ -272,6 +276,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int64_t row = (int64_t)b * g.scb + gm * g.scm;
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * N + cbeg;
       float rpart = 0.f;
+      const bool r2 = g.r2_a != nullptr;
+      const float rs = (r2 && gm < g.M) ? g.r2_s[(int64_t)b * g.r2_sb + gm] : 0.f;
+      const float rx = (r2 && gm < g.M) ? g.r2_x[gm] : 0.f;
 #pragma unroll 1
       for (int c0 = 0; c0 < NH; c0 += 16) {
         uint32_t v[16];
@@ -286,7 +293,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         const bool full = n0 + cc + 16 <= g.N;
         float o[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) o[j] = act_c<ACT>(fmaf(g.alpha, __uint_as_float(v[j]), s.ep_bias[acc][cc + j]));
+        for (int j = 0; j < 16; ++j) {
+          float x = fmaf(g.alpha, __uint_as_float(v[j]), s.ep_bias[acc][cc + j]);
+          if (r2) x = fmaf(s.ep_ra[acc][cc + j], rs, fmaf(s.ep_rb[acc][cc + j], rx, x));
+          o[j] = act_c<ACT>(x);
+        }
         if (g.rowdot_w) {
 #pragma unroll
           for (int j = 0; j < 16; ++j)

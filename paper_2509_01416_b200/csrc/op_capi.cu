@@ -38,6 +38,9 @@ struct snop_op {
   std::vector<float*> Rr, Ri, W, b;
   float *P1W = nullptr, *P1b = nullptr, *P2W = nullptr, *P2b = nullptr;
   float p2b_host = 0.f;
+  // layer 0 folded through the affine lift: U0 = S^ (x) P + Q, W-path rank-2 terms
+  float *l0_P = nullptr, *l0_Q = nullptr;         // [2][M][C] (re, im)
+  float *l0_A = nullptr, *l0_B = nullptr, *l0_C = nullptr;  // [C]
   float *F = nullptr, *Ginv = nullptr;  // forward [2M][n] and inverse [n][2M] truncated DFT
   // exact operator
   int order = 16;
@@ -126,6 +129,23 @@ __global__ void fno_mix(int B, int C, int M, const float* __restrict__ Vh, const
     }
     U[(size_t)b * C * 2 * M + (size_t)o * 2 * M + m] = re;
     U[(size_t)b * C * 2 * M + (size_t)o * 2 * M + M + m] = im;
+  }
+}
+
+// Layer-0 spectral mixing from the source spectrum (affine-lift folding): U[b][o][m] + i U[b][o][M+m]
+// = (Sh[b][m] + i Sh[b][M+m]) (P[m][o] + i P[M+m][o]) + Q[m][o] + i Q[M+m][o].
+__global__ void fno_mix_l0(int B, int C, int M, const float* __restrict__ Sh, const float* __restrict__ P,
+                           const float* __restrict__ Q, float* __restrict__ U) {
+  const size_t total = (size_t)B * C * M;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int m = (int)(e % M);
+    const size_t bo = e / M;
+    const int o = (int)(bo % C);
+    const size_t b = bo / C;
+    const float sr = Sh[b * 2 * M + m], si = Sh[b * 2 * M + M + m];
+    const float pr = P[(size_t)m * C + o], pi = P[(size_t)(M + m) * C + o];
+    U[bo * 2 * M + m] = fmaf(sr, pr, fmaf(-si, pi, Q[(size_t)m * C + o]));
+    U[bo * 2 * M + M + m] = fmaf(sr, pi, fmaf(si, pr, Q[(size_t)(M + m) * C + o]));
   }
 }
 
@@ -357,10 +377,30 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
   float* Vh = static_cast<float*>(ctx.slot(47, (size_t)B * C * 2 * M * sizeof(float)));
   float* U = static_cast<float*>(ctx.slot(48, (size_t)B * C * 2 * M * sizeof(float)));
   if (!V || !Vn || !Vh || !U) return cuda_status("FNO workspace", cudaErrorMemoryAllocation);
-  fno_lift<<<grid_for(ctx, vsz), 256, 0, ctx.stream>>>(B, n, C, in, op.xc, op.lift_W, op.lift_b, V);
-  ctx.launches++;
   const bool tc_fused = use_tc() && (2 * M) % 32 == 0;
-  for (int l = 0; l < op.layers; ++l) {
+  // layer 0 without materialising the lifted field (TMA engine with the rank-2 epilogue)
+  const bool l0 = tc_fused && op.layers >= 1 && op.l0_P && 2 * M <= 128 && C <= 128 && !std::getenv("SNOP_GEMM_V1");
+  if (l0) {
+    cast_f64_to_f32<<<grid_for(ctx, rowsN), 256, 0, ctx.stream>>>(rowsN, in, X);
+    ctx.launches++;
+    // source spectrum S^[b][m'] = sum_i S[b][i] F[m'][i]  (B x 2M x n)
+    GemmArgs fs = rowmajor(B, 2 * M, n, X, n, op.F, n, Vh, 2 * M, nullptr, ACT_NONE);
+    SNOP_TRY(gemm(ctx, fs));
+    fno_mix_l0<<<grid_for(ctx, (size_t)B * C * M), 256, 0, ctx.stream>>>(B, C, M, Vh, op.l0_P, op.l0_Q, U);
+    ctx.launches++;
+    GemmArgs iv{};
+    iv.M = n; iv.N = C; iv.K = 2 * M; iv.batch = B;
+    iv.A = op.Ginv; iv.sam = 2 * M; iv.sak = 1; iv.sab = 0;
+    iv.B = U; iv.sbn = 2 * M; iv.sbk = 1; iv.sbb = (int64_t)C * 2 * M;
+    iv.C = V; iv.scm = C; iv.scn = 1; iv.scb = (int64_t)n * C;
+    iv.bias = op.l0_C; iv.alpha = 1.f; iv.act = op.act;
+    iv.r2_a = op.l0_A; iv.r2_b = op.l0_B; iv.r2_s = X; iv.r2_sb = n; iv.r2_x = op.xc;
+    SNOP_TRY(gemm(ctx, iv));
+  } else {
+    fno_lift<<<grid_for(ctx, vsz), 256, 0, ctx.stream>>>(B, n, C, in, op.xc, op.lift_W, op.lift_b, V);
+    ctx.launches++;
+  }
+  for (int l = l0 ? 1 : 0; l < op.layers; ++l) {
     // forward truncated DFT: Vh[b][c][m'] = sum_i V[b][i][c] F[m'][i]. Tensor-core engine: one
     // GEMM over all B*C rows (batch folded into M); FFMA engine: batched per sample.
     GemmArgs f{};
@@ -918,7 +958,55 @@ snop_status snop_fno_create(snop_ctx* ctx, const snop_grid* grid, double tstar, 
   op->F = op->upload(F.data(), F.size());
   op->Ginv = op->upload(G.data(), G.size());
   op->xc = op->upload(xs.data(), n);
-  if (!op->F || !op->Ginv || !op->xc || !op->P2b) {
+  if (layers >= 1) {
+    // Layer 0 acts on V = lift(S, x) = Wl0 S + Wl1 x + bl, which is affine in the source, so its
+    // forward DFT is Wl0 S^ + Wl1 x^ + bl 1^ and (by linearity) its spectral mixing is
+    // U0 = S^ P + Q and its W path is Aw S + Bw x + Cw. Constants in fp64 from the fp32 parameters.
+    const float* hp = op->host_params.data();
+    const float *Wl = hp, *bl = hp + 2 * C, *R0r = bl + C, *R0i = R0r + M * C * C;
+    const float *W0 = R0i + M * C * C, *b0 = W0 + C * C;
+    std::vector<double> xh(2 * M, 0.0), oh(2 * M, 0.0);
+    for (size_t m = 0; m < 2 * M; ++m)
+      for (int i = 0; i < n; ++i) {
+        xh[m] += (double)F[m * n + i] * (double)xs[i];
+        oh[m] += (double)F[m * n + i];
+      }
+    std::vector<float> P(2 * M * C), Q(2 * M * C), Aw(C), Bw(C), Cw(C);
+    for (size_t m = 0; m < M; ++m)
+      for (size_t o = 0; o < C; ++o) {
+        double pr = 0, pi = 0, qr = 0, qi = 0;
+        for (size_t c = 0; c < C; ++c) {
+          const double rr = R0r[(m * C + c) * C + o], ri = R0i[(m * C + c) * C + o];
+          const double w0 = Wl[2 * c], w1 = Wl[2 * c + 1], bc = bl[c];
+          const double zr = w1 * xh[m] + bc * oh[m], zi = w1 * xh[M + m] + bc * oh[M + m];
+          pr += rr * w0;
+          pi += ri * w0;
+          qr += rr * zr - ri * zi;
+          qi += rr * zi + ri * zr;
+        }
+        P[m * C + o] = (float)pr;
+        P[(M + m) * C + o] = (float)pi;
+        Q[m * C + o] = (float)qr;
+        Q[(M + m) * C + o] = (float)qi;
+      }
+    for (size_t o = 0; o < C; ++o) {
+      double a = 0, bb = 0, cc = b0[o];
+      for (size_t c = 0; c < C; ++c) {
+        a += (double)W0[o * C + c] * Wl[2 * c];
+        bb += (double)W0[o * C + c] * Wl[2 * c + 1];
+        cc += (double)W0[o * C + c] * bl[c];
+      }
+      Aw[o] = (float)a;
+      Bw[o] = (float)bb;
+      Cw[o] = (float)cc;
+    }
+    op->l0_P = op->upload(P.data(), P.size());
+    op->l0_Q = op->upload(Q.data(), Q.size());
+    op->l0_A = op->upload(Aw.data(), C);
+    op->l0_B = op->upload(Bw.data(), C);
+    op->l0_C = op->upload(Cw.data(), C);
+  }
+  if (!op->F || !op->Ginv || !op->xc || !op->P2b || (layers >= 1 && (!op->l0_P || !op->l0_Q || !op->l0_C))) {
     delete op;
     return cuda_status("FNO upload", cudaErrorMemoryAllocation);
   }
