@@ -1,0 +1,26 @@
+"""Experiment: K2 phase split for the slowest C3 instance (needs a -DSNOP_PHASE_TIMING build via SNOP_LIB)."""
+import ctypes as C, sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np, torch
+from paper_2509_01416_b200 import snop, workloads as W, _capi
+lib = _capi.load()
+f = lib.snop_internal_phase_cycles_eigen
+f.argtypes = [C.c_void_p, C.c_int]
+buf = np.zeros(20, dtype=np.uint64)
+p = W.config3()
+cfg = snop.SolverConfig(tolerance=p.tolerance_inner, tolerance_k=p.tolerance_k, tolerance_phi=p.tolerance_phi,
+                        boundary_left=p.bc_left, boundary_right=p.bc_right)
+g = snop.Grid1D(p.length, p.n_cells)
+q = p.subset([int(sys.argv[1]) if len(sys.argv) > 1 else 491])
+args = [torch.from_numpy(a).cuda() for a in (q.sigma_t, q.sigma_s0, q.nu_sigma_f, q.chi)]
+snop.power_iteration(g, p.order, *args, cfg); torch.cuda.synchronize()
+f(buf.ctypes.data, 1)
+r = snop.power_iteration(g, p.order, *args, cfg); torch.cuda.synchronize()
+f(buf.ctypes.data, 1)
+sweeps = int(r.total_inner_iterations[0]); outer = int(r.outer_iterations[0])
+row = buf[:10].astype(np.float64)
+groups = sweeps * (p.order // 4)
+print(f"C3 inst: sweeps {sweeps} outer {outer}: per pair group maps {row[0]/groups:.0f} bar1 {row[1]/groups:.0f} "
+      f"scan {row[2]/groups:.0f} bar2 {row[3]/groups:.0f} replay {row[4]/groups:.0f} | per sweep pairs {row[5]/sweeps:.0f} "
+      f"phi {row[6]/sweeps:.0f} | in solve per sweep {row[7]/sweeps:.0f} | loop per sweep {row[8]/sweeps:.0f}")
