@@ -120,7 +120,15 @@ class ClockSampler:
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.p = None
-        time.sleep(0.05)
+        # nvidia-smi takes a few hundred ms to start: wait for its first row so the whole (short)
+        # timed region is sampled
+        t0 = time.perf_counter()
+        while self.p is not None and time.perf_counter() - t0 < 10.0:
+            self.f.flush()
+            if Path(self.f.name).read_text().strip():
+                break
+            time.sleep(0.02)
+        self.n0 = len([r for r in Path(self.f.name).read_text().splitlines() if r.strip()])
         return self
 
     def __exit__(self, *a):
@@ -134,6 +142,7 @@ class ClockSampler:
     def summary(self):
         self.f.flush()
         rows = [r.split(",") for r in Path(self.f.name).read_text().splitlines() if r.strip()]
+        rows = rows[getattr(self, "n0", 0):]  # rows taken before the timed region started
         os.unlink(self.f.name)
         sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
         mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
