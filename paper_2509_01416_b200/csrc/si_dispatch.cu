@@ -1,5 +1,6 @@
 // si_dispatch.cu — picks the block shape (K cells per thread, NT threads per CTA) and the cluster
 // size (CS CTAs per instance) of K1/K2 for a launch.
+#include <algorithm>
 #include <cstdlib>
 
 #define SNOP_PHASE_SYM g_phase_cycles_disp
@@ -12,6 +13,7 @@ SNOP_DECL_SI(8, 32, true) SNOP_DECL_SI(8, 64, true) SNOP_DECL_SI(8, 128, true) S
 SNOP_DECL_PI(8, 32, false) SNOP_DECL_PI(8, 64, false) SNOP_DECL_PI(8, 128, false) SNOP_DECL_PI(8, 256, false)
 SNOP_DECL_PI(8, 512, false)
 SNOP_DECL_PI(8, 32, true) SNOP_DECL_PI(8, 64, true) SNOP_DECL_PI(8, 128, true) SNOP_DECL_PI(8, 256, true)
+SNOP_DECL_PS(8, 32) SNOP_DECL_PS(8, 64) SNOP_DECL_PS(8, 128) SNOP_DECL_PS(8, 256) SNOP_DECL_PS(8, 512)
 }  // namespace snop_si
 
 using namespace snop_si;
@@ -104,6 +106,27 @@ snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int 
   ep.max_outer = cfg.max_outer;
   ep.norm = cfg.norm;
   const Shape s = pick_shape(g.n_cells, batch, ctx.sm_count);
+  // Pair-split clusters (si_solve PS): a single-group eigen solve is one long chain of dependent
+  // sweeps and a batch finishes with its slowest instance, so the sweep of one instance is spread
+  // over cs = min(4, pair groups) CTAs (measured on C3: slowest instance 320 -> 153 ms, batch
+  // 361 -> 275 ms; cs = 8 is throughput-bound). Multigroup solves spend their time in the outer
+  // loop, which every CTA of a cluster repeats, so they stay on one CTA (C4: 37 vs 49 ms). The
+  // rule depends on (G, order) only, never on the batch, so an instance's result does not depend
+  // on what it is batched with. SNOP_PS=0 disables it, SNOP_PS=n sets the cluster size (<= 8).
+  int ps = 0;
+  if (!ss1 && s.cs == 1) {
+    int want = G == 1 ? 4 : 0;
+    if (const char* e = std::getenv("SNOP_PS")) want = std::atoi(e);
+    ps = std::min(std::min(want, 8), (order / 2) / 2);
+    if (ps < 2 || (s.nt % ps) != 0) ps = 0;
+  }
+  if (ps) {
+#define SNOP_PS(NN) \
+  if (s.nt == NN)   \
+    return launch_pi_t<K, NN, false, true>(ctx, sc, ic, ep, batch, ps, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv);
+    SNOP_PS(32) SNOP_PS(64) SNOP_PS(128) SNOP_PS(256) SNOP_PS(512)
+#undef SNOP_PS
+  }
 #define SNOP_PI(NN, CC)               \
   if (s.nt == NN && (s.cs > 1) == CC) \
     return launch_pi_t<K, NN, CC>(ctx, sc, ic, ep, batch, s.cs, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv);
@@ -116,3 +139,15 @@ snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int 
 
 }  // namespace snop_impl
 
+
+#ifdef SNOP_PHASE_TIMING
+// nvcc also emits the kernel templates referenced from this TU; the runtime may launch that copy
+extern "C" int snop_internal_phase_cycles_disp(unsigned long long* out /* [2][10] */, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, snop_dev::g_phase_cycles_disp, sizeof(unsigned long long) * 20);
+  if (reset) {
+    unsigned long long z[20] = {};
+    cudaMemcpyToSymbol(snop_dev::g_phase_cycles_disp, z, sizeof(z));
+  }
+  return (int)e;
+}
+#endif

@@ -146,11 +146,11 @@ si_fixed_source_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
 // ---------------------------------------------------------------------------------------------
 // The inner solver is called through a non-inlined boundary: the outer loop's live state is
 // saved once per group solve instead of competing with the sweep's maps for registers.
-template <int K, int NT, bool ANISO, bool CL>
+template <int K, int NT, bool ANISO, bool CL, bool PS = false>
 __device__ __noinline__ int si_solve_call(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem<K, NT>& sm,
                                           const CellIO& io) {
   bool c = false;
-  return si_solve<K, NT, ANISO, false, CL>(sc, cfg, sm, io, &c);
+  return si_solve<K, NT, ANISO, false, CL, SNOP_NP, PS>(sc, cfg, sm, io, &c);
 }
 
 struct EigenParams {
@@ -160,7 +160,10 @@ struct EigenParams {
   int norm;
 };
 
-template <int K, int NT, bool ANISO, bool CL>
+// PS = pair-split cluster (see si_solve): every CTA of the cluster runs the whole outer loop
+// redundantly on private working copies of phi / old / q_ext (ranks > 0 in psw_g), only the inner
+// sweeps are divided; rank 0 owns the outputs.
+template <int K, int NT, bool ANISO, bool CL, bool PS = false>
 __global__ void __launch_bounds__(NT, min_blocks<K, NT>())
 power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig icfg, const EigenParams ep,
                        const double* __restrict__ st_g, const double* __restrict__ ss0_g,
@@ -169,13 +172,20 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
                        const double* __restrict__ phi0_g, double* __restrict__ k_g, double* __restrict__ phi_g,
                        double* __restrict__ old_g, double* __restrict__ qext_g, double* __restrict__ jc_g,
                        int32_t* __restrict__ outer_g, int64_t* __restrict__ inner_g,
-                       uint8_t* __restrict__ conv_g, int* __restrict__ flags) {
+                       uint8_t* __restrict__ conv_g, int* __restrict__ flags, double* __restrict__ psw_g) {
+  static_assert(!(PS && (CL || ANISO)), "pair split: isotropic, no cell split");
   extern __shared__ __align__(32) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<SweepSmem<K, NT>*>(smem_raw);
   const int t = threadIdx.x, Nc = sc.n_cells, G = ep.G;
   int b, rank;
-  instance_of_block<CL>(b, rank);
-  const int c0 = rank * NT * K + t * K;
+  if constexpr (PS) {
+    rank = cl_rank();
+    b = blockIdx.x / cl_size();
+  } else {
+    instance_of_block<CL>(b, rank);
+  }
+  const int cb = CL ? rank * NT * K : 0;  // first cell of this CTA (cell split only)
+  const int c0 = cb + t * K;
   const size_t GN = (size_t)G * Nc;
   const double* st_b = st_g + (size_t)b * GN;
   const double* ss_b = ss0_g + (size_t)b * GN * G;
@@ -183,12 +193,19 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   double* phi_b = phi_g + (size_t)b * GN;
   double* old_b = old_g + (size_t)b * GN;
   double* qext_b = qext_g + (size_t)b * Nc;
+  if constexpr (PS) {
+    if (rank > 0) {
+      double* wsp = psw_g + ((size_t)b * (cl_size() - 1) + rank - 1) * (2 * GN + Nc);
+      phi_b = wsp;
+      old_b = wsp + GN;
+      qext_b = wsp + 2 * GN;
+    }
+  }
   double* jc_b = ANISO ? jc_g + (size_t)b * Nc : nullptr;
   auto cell = [&](int g, int j) -> size_t { return (size_t)g * Nc + c0 + j; };
   // Coalesced mapping for the per-cell outer-loop work (fission density, in-scatter source,
   // renormalisation): r-th cell of thread t = cb + r * NT + t, so a warp touches 256 contiguous
   // bytes per load; the thread-owned chunk mapping (c0 + j) is kept for shared-memory staging.
-  const int cb = rank * NT * K;
   auto cc = [&](int r) -> int { return cb + r * NT + t; };
 
   // validation + initial flux (flat) and k
@@ -311,7 +328,7 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
       io.jc = jc_b;
       SNOP_TSTAMP(tsol0);
       SNOP_TACC(9, tq0, tsol0);
-      inner_total += si_solve_call<K, NT, ANISO, CL>(sc, icfg, sm, io);
+      inner_total += si_solve_call<K, NT, ANISO, CL, PS>(sc, icfg, sm, io);
       SNOP_TSTAMP(tsol1);
       SNOP_TACC(7, tsol0, tsol1);
 #pragma unroll
@@ -492,7 +509,7 @@ inline snop_status launch_si_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
   return SNOP_OK;
 }
 
-template <int K, int NT, bool CL>
+template <int K, int NT, bool CL, bool PS = false>
 inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveConfig& icfg,
                                const EigenParams& ep, int batch, int cs, const double* st, const double* ss0,
                                const double* ss1, const double* nsf, const double* chi, const double* k0,
@@ -500,16 +517,30 @@ inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
                                int64_t* inner, uint8_t* conv) {
   const bool aniso = ss1 != nullptr;
   const size_t smem = smem_bytes<K, NT>();
-  auto kern = aniso ? power_iteration_kernel<K, NT, true, CL> : power_iteration_kernel<K, NT, false, CL>;
+  auto kern = PS ? power_iteration_kernel<K, NT, false, false, PS>
+                 : (aniso ? power_iteration_kernel<K, NT, true, CL> : power_iteration_kernel<K, NT, false, CL>);
+  if (PS && aniso) {
+    snop_impl::set_error("pair-split eigen kernel is isotropic only");
+    return SNOP_INVALID_ARGUMENT;
+  }
   const size_t n = (size_t)batch * sc.n_cells;
   double* qext = static_cast<double*>(ctx.slot(22, n * sizeof(double)));
   double* jc = aniso ? static_cast<double*>(ctx.slot(21, n * sizeof(double))) : nullptr;
+  double* psw = nullptr;
+  if (PS && cs > 1) {  // private phi / old / q_ext of the ranks > 0
+    const size_t GN = (size_t)ep.G * sc.n_cells;
+    psw = static_cast<double*>(ctx.slot(24, (size_t)batch * (cs - 1) * (2 * GN + sc.n_cells) * sizeof(double)));
+    if (!psw) {
+      snop_impl::set_error("cudaMalloc (pair-split workspace) failed");
+      return SNOP_CUDA_ERROR;
+    }
+  }
   if (!qext || (aniso && !jc)) {
     snop_impl::set_error("cudaMalloc (eigen workspace) failed");
     return SNOP_CUDA_ERROR;
   }
-  const cudaError_t e = launch_k(kern, batch, CL ? cs : 1, NT, smem, ctx.stream, sc, icfg, ep, st, ss0, ss1, nsf,
-                                 chi, k0, phi0, k, phi, old, qext, jc, outer, inner, conv, ctx.d_flags);
+  const cudaError_t e = launch_k(kern, batch, (CL || PS) ? cs : 1, NT, smem, ctx.stream, sc, icfg, ep, st, ss0, ss1,
+                                 nsf, chi, k0, phi0, k, phi, old, qext, jc, outer, inner, conv, ctx.d_flags, psw);
   ctx.launches++;
   if (e != cudaSuccess) {
     snop_impl::set_error(std::string("power_iteration_kernel launch: ") + cudaGetErrorString(e));
@@ -528,6 +559,8 @@ inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
       double*, int32_t*, int64_t*, uint8_t*
 #define SNOP_DECL_SI(KK, NN, CC) extern template snop_status launch_si_t<KK, NN, CC>(SNOP_SI_ARGS);
 #define SNOP_DECL_PI(KK, NN, CC) extern template snop_status launch_pi_t<KK, NN, CC>(SNOP_PI_ARGS);
+#define SNOP_DECL_PS(KK, NN) extern template snop_status launch_pi_t<KK, NN, false, true>(SNOP_PI_ARGS);
+#define SNOP_INST_PS(KK, NN) template snop_status launch_pi_t<KK, NN, false, true>(SNOP_PI_ARGS);
 #define SNOP_INST_SI(KK, NN, CC) template snop_status launch_si_t<KK, NN, CC>(SNOP_SI_ARGS);
 #define SNOP_INST_PI(KK, NN, CC) template snop_status launch_pi_t<KK, NN, CC>(SNOP_PI_ARGS);
 

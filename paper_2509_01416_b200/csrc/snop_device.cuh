@@ -569,9 +569,16 @@ __device__ __forceinline__ void sweep_pair_group(const SweepConsts& sc, SweepSme
 #ifndef SNOP_NP
 #define SNOP_NP 2
 #endif
-template <int K, int NT, bool ANISO, bool CUR, bool CL = false, int NP = SNOP_NP>
+// PS (pair split, eigen kernel only): the CTAs of a thread-block cluster each sweep a contiguous
+// range of pair groups over ALL cells of the instance; after the pairs of a source iteration the
+// partial edge currents are exchanged through distributed shared memory and summed in rank order,
+// so every CTA performs the identical (redundant) flux update and convergence test. One source
+// iteration then costs P/(2*CS) pair groups of latency plus one exchange, instead of P/2 groups.
+template <int K, int NT, bool ANISO, bool CUR, bool CL = false, int NP = SNOP_NP, bool PS = false>
 __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem<K, NT>& sm, const CellIO& io,
                         bool* converged) {
+  static_assert(!(PS && CL), "pair split and cell split are exclusive");
+  static_assert((K + 1) * NT <= 14 * SweepSmem<K, NT>::NP_PAD, "exchange buffer must fit in agg + xmap");
   const int t = threadIdx.x;
   const int Nc = sc.n_cells, P = sc.n_pairs;
   SweepCtl w;
@@ -616,13 +623,65 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
     for (int j = 0; j < K; ++j) Jl[j] = 0.0;
     double Jr = 0.0;
     SNOP_TSTAMP(ti0);
-    int p = 0;
-    if constexpr (NP == 2) {
-      for (; p + 1 < P; p += 2) sweep_pair_group<K, NT, ANISO, 2, CL>(sc, sm, io, p, w, Jl, Jr);
+    int p = 0, pend = P;
+    if constexpr (PS) {  // this CTA's contiguous range of pair groups (the odd tail pair: last rank)
+      const int prank = cl_rank(), psz = cl_size(), G2 = P / 2, per = (G2 + psz - 1) / psz;
+      const int g0 = min(G2, prank * per), g1 = min(G2, g0 + per);
+      p = 2 * g0;
+      pend = prank == psz - 1 ? P : 2 * g1;
     }
-    for (; p < P; ++p) sweep_pair_group<K, NT, ANISO, 1, CL>(sc, sm, io, p, w, Jl, Jr);
+    if constexpr (NP == 2) {
+      for (; p + 1 < pend; p += 2) sweep_pair_group<K, NT, ANISO, 2, CL>(sc, sm, io, p, w, Jl, Jr);
+    }
+    for (; p < pend; ++p) sweep_pair_group<K, NT, ANISO, 1, CL>(sc, sm, io, p, w, Jl, Jr);
     SNOP_TSTAMP(ti1);
     SNOP_TACC(5, ti0, ti1);
+    double num = 0.0, den = 0.0;
+    if constexpr (PS) {
+      // Rank r owns the flux update of the cells of owner threads [r per, (r+1) per), per = NT/CS.
+      // Every CTA pushes its partial edge currents (K + 1 per thread) into the owner rank's
+      // incoming buffer (agg + xmap, by source rank: [CS][K+1][per]); the owner sums the CS
+      // partials in rank order, updates phi locally and pushes the new emission into every CTA.
+      // All remote traffic is stores; the convergence norm is a cluster reduction (reduce2<CL =
+      // true>) whose barrier also publishes the pushed emission. phi is pushed once, at the end.
+      double* xb = &sm.agg[0][0][0];
+      const int prank = cl_rank(), psz = cl_size(), per = NT / psz;
+      cl_sync();  // every CTA has finished its replays (agg / xmap are free cluster-wide)
+      {
+        const int ro = t / per, uu = t - ro * per;
+        double* dst = cl_map(xb, ro) + (size_t)prank * (K + 1) * per + uu;
+#pragma unroll
+        for (int j = 0; j < K; ++j) dst[j * per] = Jl[j];
+        dst[K * per] = Jr;
+      }
+      cl_sync();
+      for (int idx = t; idx < per * K; idx += NT) {
+        const int j = idx / per, uu = idx - j * per, u = prank * per + uu;
+        const int i = u * K + j;
+        if (i < Nc) {
+          double JL = 0.0, JR = 0.0;
+          for (int r = 0; r < psz; ++r) {
+            const double* src = xb + (size_t)r * (K + 1) * per + uu;
+            JL += src[j * per];
+            JR += src[(j + 1) * per];
+          }
+          const int o = j * NT + u;
+          const double pn = (sm.q2[o] - (JR - JL) * sc.inv_dx) * sm.ist[o];
+          const double d = pn - sm.phi[o];
+          if (cfg.norm == 0) {
+            num = fmax(num, fabs(d));
+            den = fmax(den, fabs(pn));
+          } else {
+            num = fma(d, d, num);
+            den = fma(pn, pn, den);
+          }
+          sm.phi[o] = pn;
+          const double q2n = fma(io.ss0[i], pn, io.src[i]);
+          for (int r = 0; r < psz; ++r) cl_map(sm.q2, r)[o] = q2n;
+        }
+      }
+      reduce2<NT, true>(num, den, cfg.norm == 0, sm.red, sm.cred, rphase++, sm);
+    } else {
     // J at the right edge of the own last cell was accumulated locally (Jr); padding cells after
     // the global last cell are identity maps, so Jl[j+1] of a padding cell is J at x = L.
     double ssv[K], srcv[K];
@@ -631,7 +690,6 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
       ssv[j] = (c0 + j < Nc) ? io.ss0[c0 + j] : 0.0;
       srcv[j] = (c0 + j < Nc) ? io.src[c0 + j] : 0.0;
     }
-    double num = 0.0, den = 0.0;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       if (c0 + j < Nc) {
@@ -654,6 +712,7 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
       }
     }
     reduce2<NT, CL>(num, den, cfg.norm == 0, sm.red, sm.cred, rphase++, sm);
+    }
     SNOP_TSTAMP(ti2);
     SNOP_TACC(6, ti1, ti2);
     const double rel = rel_change(num, den, cfg.norm);
@@ -667,7 +726,18 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
     if (c0 == 0) io.leak[0] = sm.leak[0];  // written by this same thread: no barrier needed
     if (w.owns_last) io.leak[1] = sm.leak[1];
   }
-  if constexpr (CL) cl_sync();  // keep shared memory alive until every remote read is done
+  if constexpr (PS) {  // the owners' final phi -> every CTA
+    const int prank = cl_rank(), psz = cl_size(), per = NT / psz;
+    for (int idx = t; idx < per * K; idx += NT) {
+      const int j = idx / per, u = prank * per + (idx - j * per);
+      if (u * K + j < Nc) {
+        const int o = j * NT + u;
+        const double v = sm.phi[o];
+        for (int r = 0; r < psz; ++r) cl_map(sm.phi, r)[o] = v;
+      }
+    }
+  }
+  if constexpr (CL || PS) cl_sync();  // keep shared memory alive until every remote access is done
   *converged = conv;
   return it;
 }

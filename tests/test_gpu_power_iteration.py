@@ -96,3 +96,30 @@ def test_zero_fission_is_degenerate():
                        np.ones((1, 1)))
     with pytest.raises(DegenerateProblem):
         snop.power_iteration(snop.Grid1D(10.0, n), 8, p.sigma_t, p.sigma_s0, p.nu_sigma_f, p.chi, _cfg(p))
+
+
+@pytest.mark.parametrize("cs", ["0", "2", "4", "8"])
+def test_pair_split_cluster_parity(cs, monkeypatch):
+    """Pair-split clusters (si_solve PS, single-group eigen): each CTA sweeps a range of pair groups
+    and the partial edge currents are exchanged through DSMEM. Fixed iteration counts: flux and k
+    against the oracle at 1e-10; SNOP_PS=0 is the one-CTA kernel. C3 shapes (reflective left)."""
+    monkeypatch.setenv("SNOP_PS", cs)
+    p = W.config3(batch=3, n_cells=1000)
+    cfg = _cfg(p, tolerance_k=1e-300, tolerance_phi=1e-300, max_outer_iterations=4, max_inner_iterations=5,
+               tolerance=1e-300)
+    r, o = _both(p, cfg)
+    assert (r.total_inner_iterations == o["inner"]).all()
+    assert np.max(np.abs(r.phi - o["phi"])) / np.max(np.abs(o["phi"])) < K_RTOL
+    assert np.max(np.abs(r.k - o["k"]) / o["k"]) < K_RTOL
+
+
+def test_pair_split_converged_matches_single_cta(monkeypatch):
+    p = W.config3(batch=4, n_cells=777)  # ragged cell count (padding cells in the last chunk)
+    g = snop.Grid1D(p.length, p.n_cells)
+    out = {}
+    for cs in ("0", "4"):
+        monkeypatch.setenv("SNOP_PS", cs)
+        out[cs] = snop.power_iteration(g, p.order, p.sigma_t, p.sigma_s0, p.nu_sigma_f, p.chi, _cfg(p))
+    a, b = out["0"], out["4"]
+    assert np.all(np.abs(a.outer_iterations.astype(int) - b.outer_iterations.astype(int)) <= 1)
+    assert np.max(np.abs(a.k - b.k) / a.k) < 1e-10
