@@ -88,6 +88,58 @@ def c5_arm(snop, ctx, stream, args):
             "recast_max_iterations": args.recast_max}
 
 
+def eigen_arms(snop, ctx, stream, args):
+    """BASELINE configs[2] (C3: 512 x 4096 S32 single-group, reflective-left / vacuum-right) and
+    configs[3] (C4: 128 x 2000 S16, G = 7 with upscatter, Gauss-Seidel over groups): one batched
+    power iteration (fused K2) per step, device-resident inputs, CUDA-event timing; beside it the
+    CPU oracle on a bounded sample of the same instances (all host threads), and the k parity of
+    that sample."""
+    import torch
+    from paper_2509_01416_b200 import workloads as W
+    from tests import oracle_lib as O
+    th = O.hardware_threads()
+    out = {}
+    for name, p, n_cpu in (("c3_eigen", W.config3(), args.cpu_eigen_sample), ("c4_multigroup", W.config4(),
+                                                                               args.cpu_eigen_sample)):
+        g = snop.Grid1D(p.length, p.n_cells)
+        cfg = snop.SolverConfig(tolerance=p.tolerance_inner, tolerance_k=p.tolerance_k, tolerance_phi=p.tolerance_phi,
+                                boundary_left=p.bc_left, boundary_right=p.bc_right)
+        dev = [torch.from_numpy(a).cuda() for a in (p.sigma_t, p.sigma_s0, p.nu_sigma_f, p.chi)]
+        r = snop.power_iteration(g, p.order, *dev, cfg, ctx=ctx)
+        ts = []
+        for _ in range(2):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = snop.power_iteration(g, p.order, *dev, cfg, ctx=ctx, sync=False)
+            e1.record(stream)
+            ctx.synchronize()
+            ts.append(e0.elapsed_time(e1) / 1e3)
+        t = float(np.min(ts))
+        inner = r.total_inner_iterations.to(torch.int64)
+        outer = r.outer_iterations.to(torch.int64)
+        upd = int(inner.sum().item()) * p.n_cells * p.order
+        k_gpu = r.k.cpu().numpy()
+        q = p.subset(np.arange(n_cpu))
+        t0 = time.perf_counter()
+        o = O.power_iteration(q.length, q.n_cells, q.order, q.n_groups, q.sigma_t, q.sigma_s0, q.nu_sigma_f, q.chi,
+                              cfg.c(), n_threads=th)
+        tc = time.perf_counter() - t0
+        upd_cpu = int(o["inner"].astype(np.int64).sum()) * q.n_cells * q.order
+        out[name] = {
+            "workload": f"{p.name} {p.batch}x{p.n_cells} S{p.order} G={p.n_groups}, power iteration tol_k "
+                        f"{p.tolerance_k:g} tol_phi {p.tolerance_phi:g}",
+            "ms_per_solve_batch": 1e3 * t, "solves_per_sec": p.batch / t, "updates_per_sec": upd / t,
+            "outer_mean": float(outer.float().mean().item()), "outer_max": int(outer.max().item()),
+            "inner_sweeps_total": int(inner.sum().item()),
+            "cpu_baseline": {"solves_per_sec": n_cpu / tc, "updates_per_sec": upd_cpu / tc, "cores": th,
+                             "kind": "port", "sample": f"first {n_cpu} of the {p.batch} instances, full solve, "
+                                                       f"{tc:.1f} s"},
+            "k_parity_vs_oracle_sample": float(np.max(np.abs(k_gpu[:n_cpu] - o["k"]) / np.abs(o["k"]))),
+        }
+    return out
+
+
 def fp64_peak():
     p = ROOT / "profiles" / "fp64_peak.json"
     if not p.exists():
@@ -325,6 +377,7 @@ def run_gpu(args):
                 "note": "random-init operator: the warm start does not reduce iterations (DESIGN.md §5)"}
 
     c5 = None if (args.no_c5 or world > 1) else c5_arm(snop, ctx, stream, args)
+    eig = None if (args.no_eigen or world > 1) else eigen_arms(snop, ctx, stream, args)
 
     if rank != 0:
         if world > 1:
@@ -367,6 +420,8 @@ def run_gpu(args):
         line["warm_start"] = warm
     if c5 is not None:
         line["c5_fno_warm_start"] = c5
+    if eig is not None:
+        line.update(eig)
     if not args.no_cpu_baseline and world == 1:
         from tests import oracle_lib as O
         th = O.hardware_threads()
@@ -388,6 +443,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--batch", type=int, default=2048)
     ap.add_argument("--cpu-sample", type=int, default=2048)
+    ap.add_argument("--cpu-eigen-sample", type=int, default=16)
+    ap.add_argument("--no-eigen", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-warm-start", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 FNO warm-start arm")

@@ -267,9 +267,10 @@ class EigenSolution:
 
 def power_iteration(grid: Grid1D, order: int, sigma_t, sigma_s0, nu_sigma_f, chi,
                     config: SolverConfig | None = None, initial_k=None, initial_phi=None, sigma_s1=None,
-                    ctx: Context | None = None) -> EigenSolution:
+                    ctx: Context | None = None, sync: bool = True) -> EigenSolution:
     """Batched k-eigenvalue power iteration. sigma_t/nu_sigma_f/sigma_s1:
-    [B][G][Nc]; sigma_s0: [B][G][G][Nc] ([g'][g] = g'->g); chi: [B][G]."""
+    [B][G][Nc]; sigma_s0: [B][G][G][Nc] ([g'][g] = g'->g); chi: [B][G]. Device (torch CUDA) arrays:
+    enqueued on ctx's stream; with sync=False the caller must call ctx.synchronize() before reading."""
     ctx = ctx or default_context()
     config = config or SolverConfig()
     a = _Args(sigma_t, sigma_s0, nu_sigma_f, chi, initial_k, initial_phi, sigma_s1)
@@ -291,7 +292,7 @@ def power_iteration(grid: Grid1D, order: int, sigma_t, sigma_s0, nu_sigma_f, chi
     g, cfg = grid.c(), config.c()
     _capi.check(ctx._lib.snop_power_iteration_batched(ctx.h, a.memspace, C.byref(g), int(order), B, G, st, ss, s1,
                                                       nsf, ch, C.byref(cfg), k0, p0, k_p, phi_p, o_p, i_p, cv_p))
-    if a.device:
+    if a.device and sync:
         ctx.synchronize()
     return EigenSolution(k, phi, outer, inner, cv)
 
