@@ -7,7 +7,7 @@
 // Roles (one persistent CTA per SM, 14 warps):
 //   warp 0      TMA producer: 2-D tensor-map loads of the raw fp32 A (128 x 32) and B (N x 32)
 //               chunks into a 128-byte-swizzled K-major stage (cp.async.bulk.tensor, mbarrier tx)
-//   warps 2-5   converters: per stage, hi = tf32_round(x) in place and lo = x - hi into the lo
+//   warps 2-5   converters: per stage, hi = x as loaded (read as tf32) and lo = rnd(x - trunc(x)) into the lo
 //               buffer — an element-wise pass, so the swizzled layout is preserved
 //   warp 1      MMA issuer: 4 k-steps x 3 tcgen05.mma.kind::tf32 (lo*hi, hi*lo, hi*hi) per chunk
 //               into one of two TMEM accumulators, commits free the stage / publish the tile
@@ -109,15 +109,22 @@ __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t
 __device__ __forceinline__ void commit(uint64_t* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(b)) : "memory");
 }
-__device__ __forceinline__ float tf32_round(float x) {
-  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+// The tensor core consumes an fp32 operand as tf32 by ignoring its 13 low mantissa bits, so the hi
+// part of the 3xTF32 split is the raw operand already in shared memory (no rewrite) and only the lo
+// part is written to the second buffer: lo = x - trunc_tf32(x) (exact), itself rounded to tf32 so
+// the tensor core's truncation of it loses nothing.
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+__device__ __forceinline__ float tf32_rnd(float x) { return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u); }
+__device__ __forceinline__ float4 split_lo(float4 x) {
+  return make_float4(tf32_rnd(x.x - tf32_trunc(x.x)), tf32_rnd(x.y - tf32_trunc(x.y)), tf32_rnd(x.z - tf32_trunc(x.z)),
+                     tf32_rnd(x.w - tf32_trunc(x.w)));
 }
 
 template <int ACT>
 __device__ __forceinline__ float act_c(float x) {
   if constexpr (ACT == ACT_RELU) return x > 0.f ? x : 0.f;
   else if constexpr (ACT == ACT_TANH) return tanhf(x);
-  else if constexpr (ACT == ACT_GELU) return 0.5f * x * (1.f + erff(x * 0.70710678118654752440f));
+  else if constexpr (ACT == ACT_GELU) return gelu_f(x);
   else return x;
 }
 
@@ -218,7 +225,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     __syncwarp();
   } else if (warp >= CONV0 && warp < CONV0 + 4) {
-    // ---------------- converters: hi = round(x) in place, lo = x - hi ----------------
+    // ---------------- converters: hi = x as loaded, lo = rnd(x - trunc(x)) ----------------
     const int ct = tid - CONV0 * 32;  // 0..127
     uint32_t it = 0;
     for (int64_t tile = blockIdx.x; tile < a.total; tile += gridDim.x) {
@@ -228,21 +235,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         float4* ah = reinterpret_cast<float4*>(s.st[st].a_hi);
         float4* al = reinterpret_cast<float4*>(s.st[st].a_lo);
 #pragma unroll
-        for (int i = 0; i < TM * KC / 4 / 128; ++i) {
-          const float4 x = ah[ct + i * 128];
-          const float4 h = make_float4(tf32_round(x.x), tf32_round(x.y), tf32_round(x.z), tf32_round(x.w));
-          ah[ct + i * 128] = h;
-          al[ct + i * 128] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
-        }
+        for (int i = 0; i < TM * KC / 4 / 128; ++i) al[ct + i * 128] = split_lo(ah[ct + i * 128]);
         float4* bh = reinterpret_cast<float4*>(s.st[st].b_hi);
         float4* bl = reinterpret_cast<float4*>(s.st[st].b_lo);
 #pragma unroll
-        for (int i = 0; i < N * KC / 4 / 128; ++i) {
-          const float4 x = bh[ct + i * 128];
-          const float4 h = make_float4(tf32_round(x.x), tf32_round(x.y), tf32_round(x.z), tf32_round(x.w));
-          bh[ct + i * 128] = h;
-          bl[ct + i * 128] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
-        }
+        for (int i = 0; i < N * KC / 4 / 128; ++i) bl[ct + i * 128] = split_lo(bh[ct + i * 128]);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
         __syncwarp();
         if (lane == 0) bar_arrive(&s.conv[st]);

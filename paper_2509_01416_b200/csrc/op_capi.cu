@@ -107,7 +107,84 @@ __global__ void fno_lift(int B, int n, int C, const double* __restrict__ S, cons
 
 // FNO spectral mixing: U[b][o][m] + i U[b][o][M+m] =
 //   sum_c (Rr[m][c][o] + i Ri[m][c][o]) (Vh[b][c][m] + i Vh[b][c][M+m]).
-// Block = (mode m, 4 samples); R[m] staged in shared memory.
+// Real form per mode: [Ur | Ui] = [Vr | Vi] . [[Rr, Ri], [-Ri, Rr]], a (samples x 2C) x (2C x 2C)
+// product. Block = (mode m, MIX_S samples): the 2C x 2C mode matrix and the samples' (transposed)
+// spectra are staged in shared memory, each thread accumulates a 4-sample x 8-output register tile
+// (three 16-byte shared loads per 32 FFMA). C = 64 (the FNO width) is the tuned shape; other widths
+// use the generic loop below.
+constexpr int MIX_S = 64;
+__global__ void __launch_bounds__(256) fno_mix64(int B, int M, const float* __restrict__ Vh,
+                                                 const float* __restrict__ Rr, const float* __restrict__ Ri,
+                                                 float* __restrict__ U) {
+  constexpr int C = 64, C2 = 128;
+  extern __shared__ __align__(16) float smx[];
+  float* Mx = smx;             // [2C][2C]
+  float* Vt = smx + C2 * C2;   // [2C][MIX_S]: Vt[k][s]
+  const int m = blockIdx.y, b0 = blockIdx.x * MIX_S, t = threadIdx.x;
+  const float* rr = Rr + (size_t)m * C * C;
+  const float* ri = Ri + (size_t)m * C * C;
+  // all global loads of the staging issued before any shared-memory store (independent requests
+  // in flight instead of one L2 round trip per loop trip)
+  constexpr int NR = C * C / 256, NV = MIX_S * C / 256;
+  float ra[NR], rb[NR], va[NV], vb[NV];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    ra[r] = rr[t + 256 * r];
+    rb[r] = ri[t + 256 * r];
+  }
+#pragma unroll
+  for (int r = 0; r < NV; ++r) {  // consecutive threads -> consecutive samples (conflict-free stores)
+    const int e = t + 256 * r, c = e / MIX_S, b = b0 + (e - c * MIX_S);
+    const float* v = Vh + ((size_t)(b < B ? b : B - 1) * C + c) * 2 * M;
+    va[r] = v[m];
+    vb[r] = v[M + m];
+  }
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int e = t + 256 * r, c = e / C, o = e - c * C;
+    Mx[c * C2 + o] = ra[r];
+    Mx[c * C2 + C + o] = rb[r];
+    Mx[(C + c) * C2 + o] = -rb[r];
+    Mx[(C + c) * C2 + C + o] = ra[r];
+  }
+#pragma unroll
+  for (int r = 0; r < NV; ++r) {
+    const int e = t + 256 * r, c = e / MIX_S, sidx = e - c * MIX_S;
+    Vt[c * MIX_S + sidx] = va[r];
+    Vt[(C + c) * MIX_S + sidx] = vb[r];
+  }
+  __syncthreads();
+  const int sg = t & 15, og = t >> 4;  // samples 4 sg .. 4 sg + 3, outputs 8 og .. 8 og + 7
+  float acc[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+#pragma unroll 4
+  for (int k = 0; k < C2; ++k) {
+    const float4 v = *reinterpret_cast<const float4*>(Vt + k * MIX_S + 4 * sg);
+    const float4 w0 = *reinterpret_cast<const float4*>(Mx + k * C2 + 8 * og);
+    const float4 w1 = *reinterpret_cast<const float4*>(Mx + k * C2 + 8 * og + 4);
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+    const float ww[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(vv[i], ww[j], acc[i][j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int b = b0 + 4 * sg + i;
+    if (b >= B) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int q = 8 * og + j;  // 0..63: Ur[o = q]; 64..127: Ui[o = q - 64]
+      const int o = q & (C - 1);
+      U[((size_t)b * C + o) * 2 * M + (q < C ? m : M + m)] = acc[i][j];
+    }
+  }
+}
+
 __global__ void fno_mix(int B, int C, int M, const float* __restrict__ Vh, const float* __restrict__ Rr,
                         const float* __restrict__ Ri, float* __restrict__ U) {
   extern __shared__ float sR[];  // [2][C][C]
@@ -417,8 +494,14 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
       SNOP_TRY(gemm(ctx, f));
     }
     // complex channel mixing per retained mode
-    fno_mix<<<dim3((B + 3) / 4 < 1024 ? (B + 3) / 4 : 1024, M), 4 * C, 2 * C * C * sizeof(float), ctx.stream>>>(
-        B, C, M, Vh, op.Rr[l], op.Ri[l], U);
+    if (C == 64) {
+      const size_t sm = (size_t)(128 * 128 + 128 * MIX_S) * sizeof(float);
+      cudaFuncSetAttribute(fno_mix64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      fno_mix64<<<dim3((B + MIX_S - 1) / MIX_S, M), 256, sm, ctx.stream>>>(B, M, Vh, op.Rr[l], op.Ri[l], U);
+    } else {
+      fno_mix<<<dim3((B + 3) / 4 < 1024 ? (B + 3) / 4 : 1024, M), 4 * C, 2 * C * C * sizeof(float), ctx.stream>>>(
+          B, C, M, Vh, op.Rr[l], op.Ri[l], U);
+    }
     ctx.launches++;
     if (tc_fused) {
       // inverse truncated DFT + W path + bias + activation as ONE contraction per sample:
