@@ -108,17 +108,51 @@ snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int 
   const Shape s = pick_shape(g.n_cells, batch, ctx.sm_count);
   // Pair-split clusters (si_solve PS): a single-group eigen solve is one long chain of dependent
   // sweeps and a batch finishes with its slowest instance, so the sweep of one instance is spread
-  // over cs = min(4, pair groups) CTAs (measured on C3: slowest instance 320 -> 153 ms, batch
-  // 361 -> 275 ms; cs = 8 is throughput-bound). Multigroup solves spend their time in the outer
+  // over cs CTAs (measured on C3, slowest instance alone: 320 ms on one CTA, 153 ms at cs = 4,
+  // 125 ms at cs = 8). cs = 8 for the tail phase below; without it the whole batch runs at cs = 4
+  // (361 -> 275 ms; at cs = 8 the batch becomes throughput-bound). Multigroup solves spend their time in the outer
   // loop, which every CTA of a cluster repeats, so they stay on one CTA (C4: 37 vs 49 ms). The
   // rule depends on (G, order) only, never on the batch, so an instance's result does not depend
   // on what it is batched with. SNOP_PS=0 disables it, SNOP_PS=n sets the cluster size (<= 8).
+  int cap = 48;  // tail split, see below
+  if (const char* e = std::getenv("SNOP_PI_SPLIT")) cap = std::atoi(e);
   int ps = 0;
   if (!ss1 && s.cs == 1) {
-    int want = G == 1 ? 4 : 0;
+    int want = G == 1 ? (cap > 0 ? 8 : 4) : 0;
     if (const char* e = std::getenv("SNOP_PS")) want = std::atoi(e);
     ps = std::min(std::min(want, 8), (order / 2) / 2);
     if (ps < 2 || (s.nt % ps) != 0) ps = 0;
+  }
+  // Tail split (single-group, pair-split eligible): a batch of eigen solves ends with its few
+  // longest instances (C3: outer counts 17 ... 1303). Phase 1 runs every instance on one CTA for at
+  // most `cap` outer iterations; phase 2 continues the unconverged ones from their (k, phi, counts)
+  // on pair-split clusters, so the long tails get cs SMs each once the bulk has drained. The cap is a
+  // constant (SNOP_PI_SPLIT, default 48; 0 disables), so an instance's result depends on its own data
+  // only.
+  if (ps && cap > 0 && cfg.max_outer > cap) {
+    EigenParams e1 = ep, e2 = ep;
+    e1.max_outer = cap;
+    e2.max_outer = cfg.max_outer - cap;
+    int* lst = static_cast<int*>(ctx.slot(25, ((size_t)batch + 1) * sizeof(int)));
+    if (!lst) {
+      set_error("cudaMalloc (tail list) failed");
+      return SNOP_CUDA_ERROR;
+    }
+    int* cnt = lst + batch;
+#define SNOP_P1(NN) \
+  if (s.nt == NN) st1 = launch_pi_t<K, NN, false>(ctx, sc, ic, e1, batch, 1, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv);
+#define SNOP_P2(NN) \
+  if (s.nt == NN) st2 = launch_pi_t<K, NN, false, true>(ctx, sc, ic, e2, batch, ps, st, ss0, ss1, nsf, chi, k, phi, k, phi, old, outer, inner, conv, lst, cnt, 1);
+    snop_status st1 = SNOP_INVALID_ARGUMENT, st2 = SNOP_INVALID_ARGUMENT;
+    SNOP_P1(32) SNOP_P1(64) SNOP_P1(128) SNOP_P1(256) SNOP_P1(512)
+    if (st1 != SNOP_OK) return st1;
+    cudaMemsetAsync(cnt, 0, sizeof(int), ctx.stream);
+    pi_tail_list_kernel<<<(batch + 255) / 256, 256, 0, ctx.stream>>>(batch, cap, outer, conv, lst, cnt);
+    ctx.launches++;
+    SNOP_P2(32) SNOP_P2(64) SNOP_P2(128) SNOP_P2(256) SNOP_P2(512)
+#undef SNOP_P1
+#undef SNOP_P2
+    return st2;
   }
   if (ps) {
 #define SNOP_PS(NN) \

@@ -172,7 +172,8 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
                        const double* __restrict__ phi0_g, double* __restrict__ k_g, double* __restrict__ phi_g,
                        double* __restrict__ old_g, double* __restrict__ qext_g, double* __restrict__ jc_g,
                        int32_t* __restrict__ outer_g, int64_t* __restrict__ inner_g,
-                       uint8_t* __restrict__ conv_g, int* __restrict__ flags, double* __restrict__ psw_g) {
+                       uint8_t* __restrict__ conv_g, int* __restrict__ flags, double* __restrict__ psw_g,
+                       const int* __restrict__ order, const int* __restrict__ order_count, int resume) {
   static_assert(!(PS && (CL || ANISO)), "pair split: isotropic, no cell split");
   extern __shared__ __align__(32) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<SweepSmem<K, NT>*>(smem_raw);
@@ -184,6 +185,13 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   } else {
     instance_of_block<CL>(b, rank);
   }
+  if (order) {  // sub-batch through an instance list (tail phase); the whole cluster leaves together
+    if (b >= *order_count) return;
+    b = order[b];
+  }
+  // resume (tail phase): continue the iteration counts of an earlier launch of the same solve
+  const int outer0 = resume ? outer_g[b] : 0;
+  const int64_t inner0 = resume ? inner_g[b] : 0;
   const int cb = CL ? rank * NT * K : 0;  // first cell of this CTA (cell split only)
   const int c0 = cb + t * K;
   const size_t GN = (size_t)G * Nc;
@@ -220,6 +228,8 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
     }
   }
   double k = k0_g ? k0_g[b] : 1.0;
+  // pair split: phi0 may alias rank 0's working array (resume) -> every rank has its copy first
+  if constexpr (PS) cl_sync();
   int rphase = 0;
   // Loops over groups are outermost and the thread's K cells innermost (unrolled) throughout: the
   // per-group global loads of all K cells are then independent and in flight together, instead of
@@ -375,8 +385,8 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   SNOP_TACC(8, tpi0, tpi1);
   if (t == 0 && rank == 0) {
     k_g[b] = k;
-    outer_g[b] = outer;
-    inner_g[b] = inner_total;
+    outer_g[b] = outer0 + outer;
+    inner_g[b] = inner0 + inner_total;
     conv_g[b] = converged ? 1 : 0;
   }
   if constexpr (CL) cl_sync();
@@ -514,7 +524,8 @@ inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
                                const EigenParams& ep, int batch, int cs, const double* st, const double* ss0,
                                const double* ss1, const double* nsf, const double* chi, const double* k0,
                                const double* phi0, double* k, double* phi, double* old, int32_t* outer,
-                               int64_t* inner, uint8_t* conv) {
+                               int64_t* inner, uint8_t* conv, const int* order = nullptr,
+                               const int* order_count = nullptr, int resume = 0) {
   const bool aniso = ss1 != nullptr;
   const size_t smem = smem_bytes<K, NT>();
   auto kern = PS ? power_iteration_kernel<K, NT, false, false, PS>
@@ -540,13 +551,24 @@ inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
     return SNOP_CUDA_ERROR;
   }
   const cudaError_t e = launch_k(kern, batch, (CL || PS) ? cs : 1, NT, smem, ctx.stream, sc, icfg, ep, st, ss0, ss1,
-                                 nsf, chi, k0, phi0, k, phi, old, qext, jc, outer, inner, conv, ctx.d_flags, psw);
+                                 nsf, chi, k0, phi0, k, phi, old, qext, jc, outer, inner, conv, ctx.d_flags, psw,
+                                 order, order_count, resume);
   ctx.launches++;
   if (e != cudaSuccess) {
     snop_impl::set_error(std::string("power_iteration_kernel launch: ") + cudaGetErrorString(e));
     return SNOP_CUDA_ERROR;
   }
   return SNOP_OK;
+}
+
+// Tail phase of a split power iteration: the instances still iterating after the first launch
+// (not converged, outer count == the phase-1 cap) -> order[0 .. *count). Their position in the list
+// does not affect their results.
+static __global__ void pi_tail_list_kernel(int B, int cap, const int32_t* __restrict__ outer,
+                                           const uint8_t* __restrict__ conv, int* __restrict__ order,
+                                           int* __restrict__ count) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x)
+    if (!conv[b] && outer[b] == cap) order[atomicAdd(count, 1)] = b;
 }
 
 // Explicitly instantiated in si_k8_{fixed,eigen}{,_cl}.cu (one TU per variant, parallel build).
@@ -556,7 +578,7 @@ inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
 #define SNOP_PI_ARGS                                                                                          \
   snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, const EigenParams&, int, int, const double*,          \
       const double*, const double*, const double*, const double*, const double*, const double*, double*, double*, \
-      double*, int32_t*, int64_t*, uint8_t*
+      double*, int32_t*, int64_t*, uint8_t*, const int*, const int*, int
 #define SNOP_DECL_SI(KK, NN, CC) extern template snop_status launch_si_t<KK, NN, CC>(SNOP_SI_ARGS);
 #define SNOP_DECL_PI(KK, NN, CC) extern template snop_status launch_pi_t<KK, NN, CC>(SNOP_PI_ARGS);
 #define SNOP_DECL_PS(KK, NN) extern template snop_status launch_pi_t<KK, NN, false, true>(SNOP_PI_ARGS);

@@ -123,3 +123,34 @@ def test_pair_split_converged_matches_single_cta(monkeypatch):
     a, b = out["0"], out["4"]
     assert np.all(np.abs(a.outer_iterations.astype(int) - b.outer_iterations.astype(int)) <= 1)
     assert np.max(np.abs(a.k - b.k) / a.k) < 1e-10
+
+
+def test_tail_split_resume_parity(monkeypatch):
+    """Tail split: phase 1 (one CTA, outer <= cap) then phase 2 (pair-split clusters) resuming from
+    (k, phi, counts) for the unconverged instances. cap = 3 forces every instance through both
+    phases; converged k against the oracle and against the unsplit single-CTA solve."""
+    p = W.config3(batch=5, n_cells=640)
+    g = snop.Grid1D(p.length, p.n_cells)
+    monkeypatch.setenv("SNOP_PI_SPLIT", "3")
+    r, o = _both(p, _cfg(p))
+    assert np.all(np.abs(r.outer_iterations.astype(int) - o["outer"].astype(int)) <= 1)
+    assert np.max(np.abs(r.k - o["k"]) / o["k"]) < 1e-9
+    monkeypatch.setenv("SNOP_PI_SPLIT", "0")
+    monkeypatch.setenv("SNOP_PS", "0")
+    a = snop.power_iteration(g, p.order, p.sigma_t, p.sigma_s0, p.nu_sigma_f, p.chi, _cfg(p))
+    assert np.all(np.abs(a.outer_iterations.astype(int) - r.outer_iterations.astype(int)) <= 1)
+    assert np.all(np.abs(a.total_inner_iterations - r.total_inner_iterations) <= 2 * a.total_inner_iterations // 100 + 5)
+    assert np.max(np.abs(a.k - r.k) / a.k) < 1e-10
+
+
+def test_tail_split_fixed_iterations(monkeypatch):
+    """Fixed iteration counts across the phase boundary (cap 2 of 5 outers): flux and k at 1e-10."""
+    monkeypatch.setenv("SNOP_PI_SPLIT", "2")
+    p = W.config3(batch=3, n_cells=512)
+    cfg = _cfg(p, tolerance_k=1e-300, tolerance_phi=1e-300, max_outer_iterations=5, max_inner_iterations=4,
+               tolerance=1e-300)
+    r, o = _both(p, cfg)
+    assert (r.outer_iterations == 5).all()
+    assert (r.total_inner_iterations == o["inner"]).all()
+    assert np.max(np.abs(r.phi - o["phi"])) / np.max(np.abs(o["phi"])) < K_RTOL
+    assert np.max(np.abs(r.k - o["k"]) / o["k"]) < K_RTOL
