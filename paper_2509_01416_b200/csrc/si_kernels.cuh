@@ -540,7 +540,7 @@ inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
   double* psw = nullptr;
   if (PS && cs > 1) {  // private phi / old / q_ext of the ranks > 0
     const size_t GN = (size_t)ep.G * sc.n_cells;
-    psw = static_cast<double*>(ctx.slot(24, (size_t)batch * (cs - 1) * (2 * GN + sc.n_cells) * sizeof(double)));
+    psw = static_cast<double*>(ctx.slot(27, (size_t)batch * (cs - 1) * (2 * GN + sc.n_cells) * sizeof(double)));
     if (!psw) {
       snop_impl::set_error("cudaMalloc (pair-split workspace) failed");
       return SNOP_CUDA_ERROR;
