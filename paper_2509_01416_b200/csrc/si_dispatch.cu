@@ -185,3 +185,4 @@ extern "C" int snop_internal_phase_cycles_disp(unsigned long long* out /* [2][10
   return (int)e;
 }
 #endif
+
