@@ -69,7 +69,27 @@ struct GemmArgs {
   const float* r2_s;
   int64_t r2_sb;
   const float* r2_x;
+  // optional pre-split lo parts of constant operands (TMA engine only): lo = rnd_tf32(x - trunc_tf32(x))
+  // with the same layout/strides as A / B / A2 / B2; the engine then loads lo instead of splitting
+  const float* A_lo;
+  const float* B_lo;
+  const float* A2_lo;
+  const float* B2_lo;
 };
+
+// host-side 3xTF32 lo part of a constant operand (matches the engine's in-kernel split)
+inline float tf32_lo_host(float x) {
+  uint32_t u;
+  __builtin_memcpy(&u, &x, 4);
+  uint32_t t = u & 0xFFFFE000u;
+  float h;
+  __builtin_memcpy(&h, &t, 4);
+  float d = x - h;
+  __builtin_memcpy(&u, &d, 4);
+  u = (u + 0x1000u) & 0xFFFFE000u;
+  __builtin_memcpy(&d, &u, 4);
+  return d;
+}
 
 __device__ __forceinline__ float gemm_a(const GemmArgs& a, int b, int64_t m, int k) {
   if (a.ksplit > 0 && k >= a.ksplit)

@@ -61,6 +61,7 @@ struct Args {
   GemmArgs g;
   int64_t a1_brows, a2_brows, b1_brows, b2_brows;  // batch stride in rows of each 2-D view
   int64_t m_tiles, n_tiles, total;
+  int a1_pre, a2_pre, b1_pre, b2_pre;  // operand has a pre-split lo array (loaded, not converted)
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -132,6 +133,8 @@ template <int N, int ACT>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tA1, const __grid_constant__ CUtensorMap tA2,
                     const __grid_constant__ CUtensorMap tB1, const __grid_constant__ CUtensorMap tB2,
+                    const __grid_constant__ CUtensorMap tA1l, const __grid_constant__ CUtensorMap tA2l,
+                    const __grid_constant__ CUtensorMap tB1l, const __grid_constant__ CUtensorMap tB2l,
                     const __grid_constant__ Args a) {
   constexpr int S = stages<N>();
   constexpr uint32_t TCOLS = 2 * N;
@@ -184,12 +187,17 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int c = 0; c < nchunks; ++c, ++it) {
           const int st = (int)(it % S);
           bar_wait(&s.empty[st], ((it / S) & 1) ^ 1);
-          bar_expect_tx(&s.full[st], (uint32_t)((TM + N) * KC * sizeof(float)));
           const int k0 = c * KC;
           const bool seg2 = g.ksplit > 0 && k0 >= g.ksplit;
           const int kk = seg2 ? k0 - g.ksplit : k0;
-          tma_2d(s.st[st].a_hi, seg2 ? &tA2 : &tA1, kk, (int)(b * (seg2 ? a.a2_brows : a.a1_brows) + m0), &s.full[st]);
-          tma_2d(s.st[st].b_hi, seg2 ? &tB2 : &tB1, kk, (int)(b * (seg2 ? a.b2_brows : a.b1_brows) + n0), &s.full[st]);
+          const bool apre = seg2 ? a.a2_pre : a.a1_pre, bpre = seg2 ? a.b2_pre : a.b1_pre;
+          bar_expect_tx(&s.full[st], (uint32_t)(((apre ? 2 : 1) * TM + (bpre ? 2 : 1) * N) * KC * sizeof(float)));
+          const int ar = (int)(b * (seg2 ? a.a2_brows : a.a1_brows) + m0);
+          const int br = (int)(b * (seg2 ? a.b2_brows : a.b1_brows) + n0);
+          tma_2d(s.st[st].a_hi, seg2 ? &tA2 : &tA1, kk, ar, &s.full[st]);
+          tma_2d(s.st[st].b_hi, seg2 ? &tB2 : &tB1, kk, br, &s.full[st]);
+          if (apre) tma_2d(s.st[st].a_lo, seg2 ? &tA2l : &tA1l, kk, ar, &s.full[st]);
+          if (bpre) tma_2d(s.st[st].b_lo, seg2 ? &tB2l : &tB1l, kk, br, &s.full[st]);
         }
       }
     }
@@ -231,15 +239,21 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int64_t tile = blockIdx.x; tile < a.total; tile += gridDim.x) {
       for (int c = 0; c < nchunks; ++c, ++it) {
         const int st = (int)(it % S);
+        const bool seg2 = g.ksplit > 0 && c * KC >= g.ksplit;
+        const bool apre = seg2 ? a.a2_pre : a.a1_pre, bpre = seg2 ? a.b2_pre : a.b1_pre;
         bar_wait(&s.full[st], (it / S) & 1);
-        float4* ah = reinterpret_cast<float4*>(s.st[st].a_hi);
-        float4* al = reinterpret_cast<float4*>(s.st[st].a_lo);
+        if (!apre) {
+          float4* ah = reinterpret_cast<float4*>(s.st[st].a_hi);
+          float4* al = reinterpret_cast<float4*>(s.st[st].a_lo);
 #pragma unroll
-        for (int i = 0; i < TM * KC / 4 / 128; ++i) al[ct + i * 128] = split_lo(ah[ct + i * 128]);
-        float4* bh = reinterpret_cast<float4*>(s.st[st].b_hi);
-        float4* bl = reinterpret_cast<float4*>(s.st[st].b_lo);
+          for (int i = 0; i < TM * KC / 4 / 128; ++i) al[ct + i * 128] = split_lo(ah[ct + i * 128]);
+        }
+        if (!bpre) {
+          float4* bh = reinterpret_cast<float4*>(s.st[st].b_hi);
+          float4* bl = reinterpret_cast<float4*>(s.st[st].b_lo);
 #pragma unroll
-        for (int i = 0; i < N * KC / 4 / 128; ++i) bl[ct + i * 128] = split_lo(bh[ct + i * 128]);
+          for (int i = 0; i < N * KC / 4 / 128; ++i) bl[ct + i * 128] = split_lo(bh[ct + i * 128]);
+        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
         __syncwarp();
         if (lane == 0) bar_arrive(&s.conv[st]);
@@ -376,7 +390,8 @@ cudaError_t launch(const Args& a, const CUtensorMap* maps, cudaStream_t st) {
     attr = true;
   }
   const int64_t grid = a.total < sms ? a.total : sms;
-  gemm_tc2_kernel<N, ACT><<<(unsigned)grid, THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], a);
+  gemm_tc2_kernel<N, ACT><<<(unsigned)grid, THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
+                                                                  maps[6], maps[7], a);
   return cudaGetLastError();
 }
 
@@ -404,18 +419,31 @@ bool gemm_tc2(const GemmArgs& g, cudaStream_t st, int64_t mfold, cudaError_t* er
   if (!brows(g.sab, g.sam, &a.a1_brows) || !brows(g.sbb, g.sbn, &a.b1_brows)) return false;
   if (g.ksplit > 0 && (!brows(g.sab2, g.sam2, &a.a2_brows) || !brows(g.sbb2, g.sbn2, &a.b2_brows))) return false;
   const int NT = g.N <= 64 ? 64 : 128;
-  CUtensorMap maps[4];
+  CUtensorMap maps[8];  // A1 A2 B1 B2, then their pre-split lo parts (copies of the hi maps when absent)
   std::memset(maps, 0, sizeof(maps));
   const int64_t rowsA1 = (g.batch - 1) * a.a1_brows + g.M, rowsB1 = (g.batch - 1) * a.b1_brows + g.N;
   if (!make_map(&maps[0], g.A, rowsA1, K1, g.sam, TM) || !make_map(&maps[2], g.B, rowsB1, K1, g.sbn, NT)) return false;
+  a.a1_pre = g.A_lo && make_map(&maps[4], g.A_lo, rowsA1, K1, g.sam, TM);
+  a.b1_pre = g.B_lo && make_map(&maps[6], g.B_lo, rowsB1, K1, g.sbn, NT);
   if (g.ksplit > 0) {
     const int64_t rowsA2 = (g.batch - 1) * a.a2_brows + g.M, rowsB2 = (g.batch - 1) * a.b2_brows + g.N;
     if (!make_map(&maps[1], g.A2, rowsA2, K2, g.sam2, TM) || !make_map(&maps[3], g.B2, rowsB2, K2, g.sbn2, NT))
       return false;
+    a.a2_pre = g.A2_lo && make_map(&maps[5], g.A2_lo, rowsA2, K2, g.sam2, TM);
+    a.b2_pre = g.B2_lo && make_map(&maps[7], g.B2_lo, rowsB2, K2, g.sbn2, NT);
   } else {
     maps[1] = maps[0];
     maps[3] = maps[2];
+    maps[5] = maps[4];
+    maps[7] = maps[6];
+    a.a2_pre = a.a1_pre;
+    a.b2_pre = a.b1_pre;
   }
+  if (!a.a1_pre) maps[4] = maps[0];
+  if (!a.b1_pre) maps[6] = maps[2];
+  if (!a.a2_pre) maps[5] = maps[1];
+  if (!a.b2_pre) maps[7] = maps[3];
+  if (std::getenv("SNOP_NO_PRESPLIT")) a.a1_pre = a.a2_pre = a.b1_pre = a.b2_pre = 0;
   a.m_tiles = (g.M + TM - 1) / TM;
   a.n_tiles = (g.N + NT - 1) / NT;
   a.total = a.m_tiles * a.n_tiles * g.batch;

@@ -43,6 +43,8 @@ struct snop_op {
   float *l0_A = nullptr, *l0_B = nullptr, *l0_C = nullptr;  // [C]
   float *F = nullptr, *Ginv = nullptr;  // forward [2M][n] and inverse [n][2M] truncated DFT
   float* FT = nullptr;                  // forward DFT transposed, [n][2M] (fno_dft64)
+  // pre-split 3xTF32 lo parts of the constant GEMM operands (TMA engine loads them, no conversion)
+  float *Ginv_lo = nullptr, *P1W_lo = nullptr;
   // exact operator
   int order = 16;
   snop_solver_config cfg{};
@@ -53,6 +55,11 @@ struct snop_op {
     for (void* p : owned) cudaFree(p);
     if (cst) cudaFree(cst);
     if (css) cudaFree(css);
+  }
+  float* upload_lo(const float* h, size_t n) {
+    std::vector<float> lo(n);
+    for (size_t i = 0; i < n; ++i) lo[i] = tf32_lo_host(h[i]);
+    return upload(lo.data(), n);
   }
   template <class T>
   T* upload(const T* h, size_t n) {
@@ -573,6 +580,7 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
     GemmArgs iv{};
     iv.M = n; iv.N = C; iv.K = 2 * M; iv.batch = B;
     iv.A = op.Ginv; iv.sam = 2 * M; iv.sak = 1; iv.sab = 0;
+    iv.A_lo = op.Ginv_lo;
     iv.B = U; iv.sbn = 2 * M; iv.sbk = 1; iv.sbb = (int64_t)C * 2 * M;
     iv.C = V; iv.scm = C; iv.scn = 1; iv.scb = (int64_t)n * C;
     iv.bias = op.l0_C; iv.alpha = 1.f; iv.act = op.act;
@@ -624,6 +632,9 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
       iv.ksplit = 2 * M;
       iv.A2 = V; iv.sam2 = C; iv.sak2 = 1; iv.sab2 = (int64_t)n * C;
       iv.B2 = op.W[l]; iv.sbn2 = C; iv.sbk2 = 1; iv.sbb2 = 0;
+      // (pre-split lo parts measured slower here: the extra lo tiles are re-read for every output
+      // tile and the K = 96 pipeline is not converter-bound; they pay off for layer 0 and the
+      // projection only)
       iv.C = Vn; iv.scm = C; iv.scn = 1; iv.scb = (int64_t)n * C;
       iv.bias = op.b[l]; iv.alpha = 1.f; iv.act = op.act;
       SNOP_TRY(gemm(ctx, iv));
@@ -647,6 +658,7 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
   // second layer as a row-dot (no hidden tensor in HBM); FFMA engine: chunked GEMM + rowdot.
   if (use_tc() && H <= 128) {
     GemmArgs pj = rowmajor((int)rowsN, H, C, V, C, op.P1W, C, nullptr, 1, op.P1b, op.act);
+    pj.B_lo = op.P1W_lo;
     pj.scm = 1;
     pj.rowdot_w = op.P2W;
     pj.rowdot_out = out;
@@ -1127,6 +1139,7 @@ snop_status snop_fno_create(snop_ctx* ctx, const snop_grid* grid, double tstar, 
     p += C;
   }
   op->P1W = op->upload(p, (size_t)hidden * C);
+  op->P1W_lo = op->upload_lo(p, (size_t)hidden * C);
   p += (size_t)hidden * C;
   op->P1b = op->upload(p, hidden);
   p += hidden;
@@ -1151,6 +1164,7 @@ snop_status snop_fno_create(snop_ctx* ctx, const snop_grid* grid, double tstar, 
   for (int i = 0; i < n; ++i) xs[i] = (float)((i + 0.5) * (grid->length_cm / n));
   op->F = op->upload(F.data(), F.size());
   op->Ginv = op->upload(G.data(), G.size());
+  op->Ginv_lo = op->upload_lo(G.data(), G.size());
   {
     std::vector<float> FTh((size_t)n * 2 * M);
     for (size_t m = 0; m < 2 * M; ++m)
