@@ -35,7 +35,10 @@ constexpr int THREADS = NWARPS * 32;
 constexpr int CONV0 = 2, EPI0 = 6, NEPI = 8;  // epilogue: 2 warps per TMEM lane quarter (column halves)
 
 template <int N>
-constexpr int stages() { return N <= 64 ? 4 : 3; }
+constexpr int stages() { return 3; }
+// N = 64 tiles are stored through shared memory by TMA (two 128 x 32 fp32 halves, 128-B swizzle)
+template <int N>
+constexpr int cst_floats() { return N == 64 ? TM * N : 4; }
 
 template <int N>
 struct alignas(1024) Stage {
@@ -48,6 +51,7 @@ struct alignas(1024) Stage {
 template <int N>
 struct Smem {
   Stage<N> st[stages<N>()];
+  alignas(1024) float cst[cst_floats<N>()];  // output tile staging for the TMA store (N = 64)
   uint64_t full[stages<N>()], conv[stages<N>()], empty[stages<N>()];
   uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem_base;
@@ -62,6 +66,7 @@ struct Args {
   int64_t a1_brows, a2_brows, b1_brows, b2_brows;  // batch stride in rows of each 2-D view
   int64_t m_tiles, n_tiles, total;
   int a1_pre, a2_pre, b1_pre, b2_pre;  // operand has a pre-split lo array (loaded, not converted)
+  int tma_store;                       // N = 64, contiguous fp32 rows: epilogue stores by TMA
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -135,7 +140,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     const __grid_constant__ CUtensorMap tB1, const __grid_constant__ CUtensorMap tB2,
                     const __grid_constant__ CUtensorMap tA1l, const __grid_constant__ CUtensorMap tA2l,
                     const __grid_constant__ CUtensorMap tB1l, const __grid_constant__ CUtensorMap tB2l,
-                    const __grid_constant__ Args a) {
+                    const __grid_constant__ CUtensorMap tC, const __grid_constant__ Args a) {
   constexpr int S = stages<N>();
   constexpr uint32_t TCOLS = 2 * N;
   extern __shared__ __align__(1024) unsigned char raw[];
@@ -280,6 +285,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         s.ep_ra[acc][j] = (g.r2_a && gn < g.N) ? g.r2_a[gn] : 0.f;
         s.ep_rb[acc][j] = (g.r2_b && gn < g.N) ? g.r2_b[gn] : 0.f;
       }
+      if (N == 64 && a.tma_store && et == 0)  // the previous tile's TMA store has read the staging
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       asm volatile("bar.sync 1, %0;" ::"r"(NEPI * 32) : "memory");
       bar_wait(&s.acc_full[acc], (tcount >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -313,6 +320,16 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j)
             if (full || n0 + cc + j < g.N) rpart = fmaf(o[j], s.ep_rw[acc][cc + j], rpart);
+        } else if (N == 64 && a.tma_store) {
+          // 128-B swizzled staging: half (cc >> 5), row r, 16-B chunk (c >> 2) ^ (r & 7)
+          const int r = q * 32 + lane, hcol = cc & 31;
+          float* hbase = s.cst + (cc >> 5) * (TM * 32) + r * 32;
+#pragma unroll
+          for (int v4 = 0; v4 < 4; ++v4) {
+            const int chunk = ((hcol >> 2) + v4) ^ (r & 7);
+            *reinterpret_cast<float4*>(hbase + chunk * 4) =
+                make_float4(o[4 * v4], o[4 * v4 + 1], o[4 * v4 + 2], o[4 * v4 + 3]);
+          }
         } else if (full && g.scn == 1 && !g.Cd && ((row + n0 + cc) & 3) == 0) {
           float4* dst = reinterpret_cast<float4*>(g.C + row + n0 + cc);
 #pragma unroll
@@ -331,6 +348,20 @@ __global__ void __launch_bounds__(THREADS, 1)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) bar_arrive(&s.acc_empty[acc]);
+      if (N == 64 && a.tma_store) {  // whole tile staged -> two TMA stores by one thread
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 3, %0;" ::"r"(NEPI * 32) : "memory");
+        if (et == 0) {
+          const int row0 = (int)(b * g.M + m0);
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                             reinterpret_cast<uint64_t>(&tC)),
+                         "r"(n0 + 32 * h), "r"(row0), "r"(su32(s.cst + h * TM * 32))
+                         : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
       if (g.rowdot_w) {  // the two column halves of a row meet in shared memory (fixed order)
         __shared__ float rsum[128];
         if (e >= 4 && gm < g.M) rsum[q * 32 + lane] = rpart;
@@ -340,6 +371,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   }
+  if (N == 64 && a.tma_store && warp == EPI0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
 }
@@ -391,7 +423,7 @@ cudaError_t launch(const Args& a, const CUtensorMap* maps, cudaStream_t st) {
   }
   const int64_t grid = a.total < sms ? a.total : sms;
   gemm_tc2_kernel<N, ACT><<<(unsigned)grid, THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
-                                                                  maps[6], maps[7], a);
+                                                                  maps[6], maps[7], maps[8], a);
   return cudaGetLastError();
 }
 
@@ -419,7 +451,7 @@ bool gemm_tc2(const GemmArgs& g, cudaStream_t st, int64_t mfold, cudaError_t* er
   if (!brows(g.sab, g.sam, &a.a1_brows) || !brows(g.sbb, g.sbn, &a.b1_brows)) return false;
   if (g.ksplit > 0 && (!brows(g.sab2, g.sam2, &a.a2_brows) || !brows(g.sbb2, g.sbn2, &a.b2_brows))) return false;
   const int NT = g.N <= 64 ? 64 : 128;
-  CUtensorMap maps[8];  // A1 A2 B1 B2, then their pre-split lo parts (copies of the hi maps when absent)
+  CUtensorMap maps[9];  // A1 A2 B1 B2, their pre-split lo parts (copies of the hi maps when absent), C
   std::memset(maps, 0, sizeof(maps));
   const int64_t rowsA1 = (g.batch - 1) * a.a1_brows + g.M, rowsB1 = (g.batch - 1) * a.b1_brows + g.N;
   if (!make_map(&maps[0], g.A, rowsA1, K1, g.sam, TM) || !make_map(&maps[2], g.B, rowsB1, K1, g.sbn, NT)) return false;
@@ -444,6 +476,23 @@ bool gemm_tc2(const GemmArgs& g, cudaStream_t st, int64_t mfold, cudaError_t* er
   if (!a.a2_pre) maps[5] = maps[1];
   if (!a.b2_pre) maps[7] = maps[3];
   if (std::getenv("SNOP_NO_PRESPLIT")) a.a1_pre = a.a2_pre = a.b1_pre = a.b2_pre = 0;
+  // TMA-store epilogue: N = 64 fp32 output, unit column stride, whole 128-row tiles per sample and
+  // samples contiguous (row b*M + m), no row-dot; C viewed as [batch*M][N] with row stride scm
+  a.tma_store = 0;
+  maps[8] = maps[0];
+  if (NT == 64 && g.N == 64 && g.C && !g.Cd && !g.rowdot_w && g.scn == 1 && g.M % TM == 0 &&
+      (g.batch == 1 || g.scb == (int64_t)g.M * g.scm) && !std::getenv("SNOP_NO_TMA_STORE")) {
+    EncodeFn enc = encoder();
+    const cuuint64_t dims[2] = {(cuuint64_t)g.N, (cuuint64_t)((int64_t)g.batch * g.M)};
+    const cuuint64_t strides[1] = {(cuuint64_t)(g.scm * 4)};
+    const cuuint32_t box[2] = {32, (cuuint32_t)TM};
+    const cuuint32_t es[2] = {1, 1};
+    if (enc && !(reinterpret_cast<uintptr_t>(g.C) & 15) && !((g.scm * 4) & 15) &&
+        enc(&maps[8], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, g.C, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+            CUDA_SUCCESS)
+      a.tma_store = 1;
+  }
   a.m_tiles = (g.M + TM - 1) / TM;
   a.n_tiles = (g.N + NT - 1) / NT;
   a.total = a.m_tiles * a.n_tiles * g.batch;
