@@ -173,12 +173,16 @@ __global__ void __launch_bounds__(THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s.tmem_base;
 
+  // tile -> (sample, row block, column block) in 32-bit arithmetic (the tile count is checked on
+  // the host; the 64-bit divisions showed up at ~5-9% of the warp samples of these short-K kernels)
+  const uint32_t n_t = (uint32_t)a.n_tiles, mn_t = (uint32_t)(a.n_tiles * a.m_tiles);
   auto tile_coords = [&](int64_t tile, int& b, int64_t& m0, int& n0) {
-    const int nt = (int)(tile % a.n_tiles);
-    const int64_t mt = (tile / a.n_tiles) % a.m_tiles;
-    b = (int)(tile / (a.n_tiles * a.m_tiles));
-    m0 = mt * TM;
-    n0 = nt * N;
+    const uint32_t t = (uint32_t)tile;
+    const uint32_t bq = t / mn_t, rem = t - bq * mn_t;
+    const uint32_t mt = rem / n_t, nt = rem - mt * n_t;
+    b = (int)bq;
+    m0 = (int64_t)mt * TM;
+    n0 = (int)nt * N;
   };
 
   if (warp == 0) {
@@ -317,9 +321,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           o[j] = act_c<ACT>(x);
         }
         if (g.rowdot_w) {
+          if (full) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (full || n0 + cc + j < g.N) rpart = fmaf(o[j], s.ep_rw[acc][cc + j], rpart);
+            for (int j = 0; j < 16; ++j) rpart = fmaf(o[j], s.ep_rw[acc][cc + j], rpart);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (n0 + cc + j < g.N) rpart = fmaf(o[j], s.ep_rw[acc][cc + j], rpart);
+          }
         } else if (N == 64 && a.tma_store) {
           // 128-B swizzled staging: half (cc >> 5), row r, 16-B chunk (c >> 2) ^ (r & 7)
           const int r = q * 32 + lane, hcol = cc & 31;
@@ -497,6 +506,7 @@ bool gemm_tc2(const GemmArgs& g, cudaStream_t st, int64_t mfold, cudaError_t* er
   a.n_tiles = (g.N + NT - 1) / NT;
   a.total = a.m_tiles * a.n_tiles * g.batch;
   if (a.total == 0) return true;
+  if (a.total >= ((int64_t)1 << 31)) return false;  // 32-bit tile arithmetic in the kernel
   switch (g.act) {
     case ACT_RELU: *err = NT == 64 ? launch<64, ACT_RELU>(a, maps, st) : launch<128, ACT_RELU>(a, maps, st); break;
     case ACT_TANH: *err = NT == 64 ? launch<64, ACT_TANH>(a, maps, st) : launch<128, ACT_TANH>(a, maps, st); break;
