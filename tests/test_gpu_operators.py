@@ -203,3 +203,17 @@ def test_precondition_fixed_source_deeponet_parity():
     assert r.converged.all()
     same = r.refine_iterations == o["refine_iterations"]
     assert _rel(r.phi[same], o["phi"][same]) < 1e-8
+
+
+@pytest.mark.parametrize("env", [{}, {"SNOP_DFT_GEMM": "1"}, {"SNOP_NO_TMA_STORE": "1", "SNOP_NO_PRESPLIT": "1"}])
+def test_fno_width64_kernel_paths(env, monkeypatch):
+    """The C5-width FNO runs on dedicated paths (exact-fp32 forward-DFT kernel, register-tiled mixing,
+    TMA-store epilogue, pre-split constant operands); each against the oracle and its fallback."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    prm = OPS.fno_init(64, 16, 2, 128, OPS.GELU, seed=11)
+    g = snop.Grid1D(10.0, 512)
+    op = snop.SolutionOperator.fno(g, prm, (1.0, 0.8))
+    oo = O.OracleOperator.fno(10.0, 512, (1.0, 0.8), OPS.GELU, 64, 16, 2, 128, prm.packed())
+    s = np.random.default_rng(7).uniform(0, 1, (13, 512))  # 13: ragged against the 8-sample DFT blocks
+    assert _rel(op.predict(s), oo.predict(s)) < OP_RTOL
