@@ -80,7 +80,13 @@ def c5_arm(snop, ctx, stream, args):
                                                                 recast_max_iterations=args.recast_max))
     it_cold = cold.iterations.to(torch.int64)
     it_warm = warm.refine_iterations.to(torch.int64)
+    upd = int(it_cold.sum().item()) * p.n_cells * p.order
+    alg = int(it_cold.sum().item()) * p.n_cells * BYTES_PER_CELL_ITER / t_cold / 1e9
     return {"workload": "C5 4096x1024 S16, p*=(1.0,0.8), tol 1e-8; FNO random-init (seeded), fp32 on tcgen05",
+            "zero_guess_updates_per_sec": upd / t_cold,
+            "zero_guess_roofline": {"bound": "hbm", "achieved": alg, "peak": peaks()[0], "unit": "GB/s",
+                                    "frac": alg / peaks()[0],
+                                    "note": "K1 at S16: 40 B per cell per iteration = 2.5 B per update"},
             "operator_ms": 1e3 * t_op, "zero_guess_ms": 1e3 * t_cold, "warm_start_ms": 1e3 * t_warm,
             "solves_per_sec_zero_guess": p.batch / t_cold, "solves_per_sec_warm_start": p.batch / t_warm,
             "iterations_mean_zero_guess": float(it_cold.float().mean().item()),
