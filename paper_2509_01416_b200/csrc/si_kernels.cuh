@@ -274,6 +274,8 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
 #pragma unroll
     for (int r = 0; r < K; ++r)
       if (cc(r) < Nc) phi_b[(size_t)g * Nc + cc(r)] /= F;
+  // coalesced-mapped writes above -> owner-mapped reads of the first group's staging below
+  __syncthreads();
 
   int64_t inner_total = 0;
   int outer = 0;

@@ -594,9 +594,9 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
   w.rl = cfg.bc_left == 1;
   w.rr = cfg.bc_right == 1;
 
-  if (t < kMaxPairs) {
-    sm.lag[0][t] = 0.0;
-    sm.lag[1][t] = 0.0;
+  for (int i = t; i < kMaxPairs; i += NT) {  // (NT may be 32 < kMaxPairs)
+    sm.lag[0][i] = 0.0;
+    sm.lag[1][i] = 0.0;
   }
 #pragma unroll
   for (int j = 0; j < K; ++j) {

@@ -217,3 +217,10 @@ def test_fno_width64_kernel_paths(env, monkeypatch):
     oo = O.OracleOperator.fno(10.0, 512, (1.0, 0.8), OPS.GELU, 64, 16, 2, 128, prm.packed())
     s = np.random.default_rng(7).uniform(0, 1, (13, 512))  # 13: ragged against the 8-sample DFT blocks
     assert _rel(op.predict(s), oo.predict(s)) < OP_RTOL
+
+
+def test_fno_predict_deterministic():
+    prm = OPS.fno_init(64, 16, 2, 128, OPS.GELU, seed=12)
+    op = snop.SolutionOperator.fno(snop.Grid1D(10.0, 256), prm, (1.0, 0.8))
+    s = np.random.default_rng(9).uniform(0, 1, (11, 256))
+    assert np.array_equal(op.predict(s), op.predict(s))

@@ -154,3 +154,19 @@ def test_tail_split_fixed_iterations(monkeypatch):
     assert (r.total_inner_iterations == o["inner"]).all()
     assert np.max(np.abs(r.phi - o["phi"])) / np.max(np.abs(o["phi"])) < K_RTOL
     assert np.max(np.abs(r.k - o["k"]) / o["k"]) < K_RTOL
+
+
+def test_tail_split_deterministic_and_batch_independent(monkeypatch):
+    """Repeated tail-split solves are bit-identical, and an instance's result does not depend on the
+    batch it is solved in (the schedule depends on (G, order) and its own outer count only)."""
+    monkeypatch.setenv("SNOP_PI_SPLIT", "4")
+    p = W.config3(batch=6, n_cells=700)
+    g = snop.Grid1D(p.length, p.n_cells)
+    cfg = _cfg(p)
+    a = snop.power_iteration(g, p.order, p.sigma_t, p.sigma_s0, p.nu_sigma_f, p.chi, cfg)
+    b = snop.power_iteration(g, p.order, p.sigma_t, p.sigma_s0, p.nu_sigma_f, p.chi, cfg)
+    assert np.array_equal(a.k, b.k) and np.array_equal(a.phi, b.phi)
+    q = p.subset([4, 1])
+    c = snop.power_iteration(g, q.order, q.sigma_t, q.sigma_s0, q.nu_sigma_f, q.chi, cfg)
+    assert np.array_equal(c.k, a.k[[4, 1]]) and np.array_equal(c.phi, a.phi[[4, 1]])
+    assert np.array_equal(c.outer_iterations, a.outer_iterations[[4, 1]])
