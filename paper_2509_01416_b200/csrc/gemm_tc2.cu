@@ -55,7 +55,7 @@ struct Smem {
   uint64_t full[stages<N>()], conv[stages<N>()], empty[stages<N>()];
   uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem_base;
-  float ep_bias[2][N];  // per accumulator: this tile's bias / row-dot weights / rank-2 columns
+  alignas(16) float ep_bias[2][N];  // per accumulator: this tile's bias / row-dot weights / rank-2 columns
   float ep_rw[2][N];
   float ep_ra[2][N];
   float ep_rb[2][N];
@@ -314,16 +314,44 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int cc = cbeg + c0;  // column within the tile
         const bool full = n0 + cc + 16 <= g.N;
         float o[16];
+        // bias / rank-2 terms read as float4 (16 consecutive columns); branches hoisted out of the
+        // element loop
+        const float4* bv = reinterpret_cast<const float4*>(&s.ep_bias[acc][cc]);
+        if (r2) {
+          const float4* av = reinterpret_cast<const float4*>(&s.ep_ra[acc][cc]);
+          const float4* cv = reinterpret_cast<const float4*>(&s.ep_rb[acc][cc]);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          float x = fmaf(g.alpha, __uint_as_float(v[j]), s.ep_bias[acc][cc + j]);
-          if (r2) x = fmaf(s.ep_ra[acc][cc + j], rs, fmaf(s.ep_rb[acc][cc + j], rx, x));
-          o[j] = act_c<ACT>(x);
+          for (int j4 = 0; j4 < 4; ++j4) {
+            const float4 b4 = bv[j4], a4 = av[j4], c4 = cv[j4];
+            const float bb[4] = {b4.x, b4.y, b4.z, b4.w}, aa[4] = {a4.x, a4.y, a4.z, a4.w},
+                        rr[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int j = 4 * j4 + u;
+              const float x = fmaf(g.alpha, __uint_as_float(v[j]), bb[u]);
+              o[j] = act_c<ACT>(fmaf(aa[u], rs, fmaf(rr[u], rx, x)));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j4 = 0; j4 < 4; ++j4) {
+            const float4 b4 = bv[j4];
+            const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) o[4 * j4 + u] = act_c<ACT>(fmaf(g.alpha, __uint_as_float(v[4 * j4 + u]), bb[u]));
+          }
         }
         if (g.rowdot_w) {
           if (full) {
+            const float4* wv = reinterpret_cast<const float4*>(&s.ep_rw[acc][cc]);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) rpart = fmaf(o[j], s.ep_rw[acc][cc + j], rpart);
+            for (int j4 = 0; j4 < 4; ++j4) {
+              const float4 w4 = wv[j4];
+              rpart = fmaf(o[4 * j4], w4.x, rpart);
+              rpart = fmaf(o[4 * j4 + 1], w4.y, rpart);
+              rpart = fmaf(o[4 * j4 + 2], w4.z, rpart);
+              rpart = fmaf(o[4 * j4 + 3], w4.w, rpart);
+            }
           } else {
 #pragma unroll
             for (int j = 0; j < 16; ++j)
