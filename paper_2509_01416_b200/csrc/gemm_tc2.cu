@@ -34,25 +34,31 @@ constexpr int NWARPS = 14;
 constexpr int THREADS = NWARPS * 32;
 constexpr int CONV0 = 2, EPI0 = 6, NEPI = 8;  // epilogue: 2 warps per TMEM lane quarter (column halves)
 
-template <int N>
-constexpr int stages() { return 3; }
+// BR ("B resident"): a batch-invariant, pre-split B operand with K <= 64 (the FNO projection
+// weights) is loaded into shared memory once per CTA; the stages then carry only A, so the TMA
+// streams 16 instead of 48 KB per K chunk and four stages fit.
+template <int N, bool BR = false>
+constexpr int stages() { return BR ? 4 : 3; }
+constexpr int BR_CHUNKS = 2;
 // N = 64 tiles are stored through shared memory by TMA (two 128 x 32 fp32 halves, 128-B swizzle)
 template <int N>
 constexpr int cst_floats() { return N == 64 ? TM * N : 4; }
 
-template <int N>
+template <int N, bool BR = false>
 struct alignas(1024) Stage {
   float a_hi[TM * KC];  // 16 KB, 1024-B aligned (swizzle atom = 8 rows x 128 B)
   float a_lo[TM * KC];
-  float b_hi[N * KC];
-  float b_lo[N * KC];
+  float b_hi[BR ? 4 : N * KC];
+  float b_lo[BR ? 4 : N * KC];
 };
 
-template <int N>
+template <int N, bool BR = false>
 struct Smem {
-  Stage<N> st[stages<N>()];
+  Stage<N, BR> st[stages<N, BR>()];
+  alignas(1024) float bres[BR ? 2 * BR_CHUNKS * N * KC : 4];  // resident B: [hi c0, hi c1, lo c0, lo c1]
+  uint64_t bres_full;
   alignas(1024) float cst[cst_floats<N>()];  // output tile staging for the TMA store (N = 64)
-  uint64_t full[stages<N>()], conv[stages<N>()], empty[stages<N>()];
+  uint64_t full[stages<N, BR>()], conv[stages<N, BR>()], empty[stages<N, BR>()];
   uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem_base;
   alignas(16) float ep_bias[2][N];  // per accumulator: this tile's bias / row-dot weights / rank-2 columns
@@ -134,19 +140,19 @@ __device__ __forceinline__ float act_c(float x) {
   else return x;
 }
 
-template <int N, int ACT>
+template <int N, int ACT, bool BR = false>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tA1, const __grid_constant__ CUtensorMap tA2,
                     const __grid_constant__ CUtensorMap tB1, const __grid_constant__ CUtensorMap tB2,
                     const __grid_constant__ CUtensorMap tA1l, const __grid_constant__ CUtensorMap tA2l,
                     const __grid_constant__ CUtensorMap tB1l, const __grid_constant__ CUtensorMap tB2l,
                     const __grid_constant__ CUtensorMap tC, const __grid_constant__ Args a) {
-  constexpr int S = stages<N>();
+  constexpr int S = stages<N, BR>();
   constexpr uint32_t TCOLS = 2 * N;
   extern __shared__ __align__(1024) unsigned char raw[];
   // the 128-B swizzle atoms need 1024-B aligned stages: align the dynamic window explicitly
   const uint32_t pad = (1024u - (su32(raw) & 1023u)) & 1023u;
-  auto& s = *reinterpret_cast<Smem<N>*>(raw + pad);
+  auto& s = *reinterpret_cast<Smem<N, BR>*>(raw + pad);
   const GemmArgs& g = a.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nchunks = (g.K + KC - 1) / KC;
@@ -166,6 +172,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       bar_init(&s.acc_full[i], 1);
       bar_init(&s.acc_empty[i], NEPI);
     }
+    bar_init(&s.bres_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -189,6 +196,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------- TMA producer (one lane; the rest of the warp waits at the final barrier) --
     if (lane == 0) {
       uint32_t it = 0;
+      if constexpr (BR) {  // resident B: hi and lo of every K chunk, once
+        bar_expect_tx(&s.bres_full, (uint32_t)(2 * nchunks * N * KC * sizeof(float)));
+        for (int c = 0; c < nchunks; ++c) {
+          tma_2d(s.bres + c * N * KC, &tB1, c * KC, 0, &s.bres_full);
+          tma_2d(s.bres + (BR_CHUNKS + c) * N * KC, &tB1l, c * KC, 0, &s.bres_full);
+        }
+      }
       for (int64_t tile = blockIdx.x; tile < a.total; tile += gridDim.x) {
         int b, n0;
         int64_t m0;
@@ -200,13 +214,16 @@ __global__ void __launch_bounds__(THREADS, 1)
           const bool seg2 = g.ksplit > 0 && k0 >= g.ksplit;
           const int kk = seg2 ? k0 - g.ksplit : k0;
           const bool apre = seg2 ? a.a2_pre : a.a1_pre, bpre = seg2 ? a.b2_pre : a.b1_pre;
-          bar_expect_tx(&s.full[st], (uint32_t)(((apre ? 2 : 1) * TM + (bpre ? 2 : 1) * N) * KC * sizeof(float)));
+          const int bmult = BR ? 0 : (bpre ? 2 : 1);
+          bar_expect_tx(&s.full[st], (uint32_t)(((apre ? 2 : 1) * TM + bmult * N) * KC * sizeof(float)));
           const int ar = (int)(b * (seg2 ? a.a2_brows : a.a1_brows) + m0);
           const int br = (int)(b * (seg2 ? a.b2_brows : a.b1_brows) + n0);
           tma_2d(s.st[st].a_hi, seg2 ? &tA2 : &tA1, kk, ar, &s.full[st]);
-          tma_2d(s.st[st].b_hi, seg2 ? &tB2 : &tB1, kk, br, &s.full[st]);
           if (apre) tma_2d(s.st[st].a_lo, seg2 ? &tA2l : &tA1l, kk, ar, &s.full[st]);
-          if (bpre) tma_2d(s.st[st].b_lo, seg2 ? &tB2l : &tB1l, kk, br, &s.full[st]);
+          if constexpr (!BR) {
+            tma_2d(s.st[st].b_hi, seg2 ? &tB2 : &tB1, kk, br, &s.full[st]);
+            if (bpre) tma_2d(s.st[st].b_lo, seg2 ? &tB2l : &tB1l, kk, br, &s.full[st]);
+          }
         }
       }
     }
@@ -221,12 +238,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         bar_wait(&s.acc_empty[acc], ((tcount >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * N;
+        if (BR && tcount == 0) bar_wait(&s.bres_full, 0);
         for (int c = 0; c < nchunks; ++c, ++it) {
           const int st = (int)(it % S);
           bar_wait(&s.conv[st], (it / S) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t ah = su32(s.st[st].a_hi), al = su32(s.st[st].a_lo);
-          const uint32_t bh = su32(s.st[st].b_hi), bl = su32(s.st[st].b_lo);
+          const uint32_t bh = BR ? su32(s.bres + c * N * KC) : su32(s.st[st].b_hi);
+          const uint32_t bl = BR ? su32(s.bres + (BR_CHUNKS + c) * N * KC) : su32(s.st[st].b_lo);
 #pragma unroll
           for (int ks = 0; ks < KC / 8; ++ks) {
             const uint32_t off = ks * 32;  // 8 tf32 = 32 B along K inside the swizzle row
@@ -257,7 +276,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int i = 0; i < TM * KC / 4 / 128; ++i) al[ct + i * 128] = split_lo(ah[ct + i * 128]);
         }
-        if (!bpre) {
+        if (!BR && !bpre) {
           float4* bh = reinterpret_cast<float4*>(s.st[st].b_hi);
           float4* bl = reinterpret_cast<float4*>(s.st[st].b_lo);
 #pragma unroll
@@ -444,14 +463,14 @@ bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int N, int ACT>
+template <int N, int ACT, bool BR = false>
 cudaError_t launch(const Args& a, const CUtensorMap* maps, cudaStream_t st) {
-  const size_t smem = sizeof(Smem<N>) + 1024;  // + alignment slack
+  const size_t smem = sizeof(Smem<N, BR>) + 1024;  // + alignment slack
   static bool attr = false;
   static int sms = 148;
   if (!attr) {
     const cudaError_t e =
-        cudaFuncSetAttribute(gemm_tc2_kernel<N, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(gemm_tc2_kernel<N, ACT, BR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -459,8 +478,8 @@ cudaError_t launch(const Args& a, const CUtensorMap* maps, cudaStream_t st) {
     attr = true;
   }
   const int64_t grid = a.total < sms ? a.total : sms;
-  gemm_tc2_kernel<N, ACT><<<(unsigned)grid, THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
-                                                                  maps[6], maps[7], maps[8], a);
+  gemm_tc2_kernel<N, ACT, BR><<<(unsigned)grid, THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4],
+                                                                      maps[5], maps[6], maps[7], maps[8], a);
   return cudaGetLastError();
 }
 
@@ -535,10 +554,16 @@ bool gemm_tc2(const GemmArgs& g, cudaStream_t st, int64_t mfold, cudaError_t* er
   a.total = a.m_tiles * a.n_tiles * g.batch;
   if (a.total == 0) return true;
   if (a.total >= ((int64_t)1 << 31)) return false;  // 32-bit tile arithmetic in the kernel
+  // resident B (see stages()): N = 128 tile, one column tile, batch-invariant pre-split B, K <= 64
+  const bool bres = NT == 128 && a.n_tiles == 1 && g.ksplit == 0 && g.sbb == 0 && a.b1_pre &&
+                    (g.K + KC - 1) / KC <= BR_CHUNKS && !std::getenv("SNOP_NO_BRES");
   switch (g.act) {
     case ACT_RELU: *err = NT == 64 ? launch<64, ACT_RELU>(a, maps, st) : launch<128, ACT_RELU>(a, maps, st); break;
     case ACT_TANH: *err = NT == 64 ? launch<64, ACT_TANH>(a, maps, st) : launch<128, ACT_TANH>(a, maps, st); break;
-    case ACT_GELU: *err = NT == 64 ? launch<64, ACT_GELU>(a, maps, st) : launch<128, ACT_GELU>(a, maps, st); break;
+    case ACT_GELU:
+      *err = NT == 64 ? launch<64, ACT_GELU>(a, maps, st)
+                      : (bres ? launch<128, ACT_GELU, true>(a, maps, st) : launch<128, ACT_GELU>(a, maps, st));
+      break;
     default: *err = NT == 64 ? launch<64, ACT_NONE>(a, maps, st) : launch<128, ACT_NONE>(a, maps, st); break;
   }
   return true;
