@@ -31,8 +31,13 @@ namespace tc2 {
 constexpr int TM = 128;
 constexpr int KC = 32;  // fp32 per 128-byte swizzle row
 constexpr int NWARPS = 14;
-constexpr int THREADS = NWARPS * 32;
-constexpr int CONV0 = 2, EPI0 = 6, NEPI = 8;  // epilogue: 2 warps per TMEM lane quarter (column halves)
+constexpr int CONV0 = 2, EPI0 = 6;
+// epilogue warps: 2 per TMEM lane quarter (column halves) for N = 64; 4 per quarter (column
+// quarters) for N = 128, whose 128-column GELU / row-dot epilogue is the pipeline's bottleneck
+template <int N>
+constexpr int nepi() { return N == 128 ? 16 : 8; }
+template <int N>
+constexpr int threads() { return (EPI0 + nepi<N>()) * 32; }
 
 // BR ("B resident"): a batch-invariant, pre-split B operand with K <= 64 (the FNO projection
 // weights) is loaded into shared memory once per CTA; the stages then carry only A, so the TMA
@@ -141,7 +146,7 @@ __device__ __forceinline__ float act_c(float x) {
 }
 
 template <int N, int ACT, bool BR = false>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(threads<N>(), 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tA1, const __grid_constant__ CUtensorMap tA2,
                     const __grid_constant__ CUtensorMap tB1, const __grid_constant__ CUtensorMap tB2,
                     const __grid_constant__ CUtensorMap tA1l, const __grid_constant__ CUtensorMap tA2l,
@@ -170,7 +175,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       bar_init(&s.acc_full[i], 1);
-      bar_init(&s.acc_empty[i], NEPI);
+      bar_init(&s.acc_empty[i], nepi<N>());
     }
     bar_init(&s.bres_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -289,10 +294,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp >= EPI0) {
     // ---------------- epilogue ----------------
-    const int e = warp - EPI0;             // 0..7
-    const int et = tid - EPI0 * 32;        // 0..255
+    constexpr int NEPI = nepi<N>();
+    const int e = warp - EPI0;             // 0..NEPI-1
+    const int et = tid - EPI0 * 32;        // 0..32 NEPI - 1
     const int q = warp & 3;                // TMEM lane quarter this warp may access
-    constexpr int NH = N / 2;              // columns per epilogue warp
+    constexpr int NH = N / (NEPI / 4);     // columns per epilogue warp (32)
     const int cbeg = (e >> 2) * NH;
     uint32_t tcount = 0;
     for (int64_t tile = blockIdx.x; tile < a.total; tile += gridDim.x, ++tcount) {
@@ -418,11 +424,17 @@ __global__ void __launch_bounds__(THREADS, 1)
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       }
-      if (g.rowdot_w) {  // the two column halves of a row meet in shared memory (fixed order)
-        __shared__ float rsum[128];
-        if (e >= 4 && gm < g.M) rsum[q * 32 + lane] = rpart;
+      if (g.rowdot_w) {  // the column groups of a row meet in shared memory (fixed order)
+        __shared__ float rsum[3][128];
+        const int gi = e >> 2;
+        if (gi > 0 && gm < g.M) rsum[gi - 1][q * 32 + lane] = rpart;
         asm volatile("bar.sync 2, %0;" ::"r"(NEPI * 32) : "memory");
-        if (e < 4 && gm < g.M) g.rowdot_out[row] = (double)rpart + (double)rsum[q * 32 + lane] + (double)g.rowdot_b;
+        if (gi == 0 && gm < g.M) {
+          double tot = (double)rpart;
+#pragma unroll
+          for (int k = 0; k < NEPI / 4 - 1; ++k) tot += (double)rsum[k][q * 32 + lane];
+          g.rowdot_out[row] = tot + (double)g.rowdot_b;
+        }
         asm volatile("bar.sync 2, %0;" ::"r"(NEPI * 32) : "memory");
       }
     }
@@ -478,7 +490,7 @@ cudaError_t launch(const Args& a, const CUtensorMap* maps, cudaStream_t st) {
     attr = true;
   }
   const int64_t grid = a.total < sms ? a.total : sms;
-  gemm_tc2_kernel<N, ACT, BR><<<(unsigned)grid, THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4],
+  gemm_tc2_kernel<N, ACT, BR><<<(unsigned)grid, threads<N>(), smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4],
                                                                       maps[5], maps[6], maps[7], maps[8], a);
   return cudaGetLastError();
 }
