@@ -31,7 +31,10 @@ namespace tc2 {
 constexpr int TM = 128;
 constexpr int KC = 32;  // fp32 per 128-byte swizzle row
 constexpr int NWARPS = 14;
-constexpr int CONV0 = 2, EPI0 = 6;
+#ifndef SNOP_TC2_NCONV
+#define SNOP_TC2_NCONV 4
+#endif
+constexpr int CONV0 = 2, NCONV = SNOP_TC2_NCONV, EPI0 = CONV0 + NCONV;
 // epilogue warps: 4 per TMEM lane quarter (column quarters: 16 columns at N = 64, 32 at N = 128).
 // The element-wise epilogue (bias, GELU, row-dot, staging) is the pipeline's bottleneck, so it gets
 // 16 of the 22 warps (80 registers each, no spills); 8 epilogue warps measured 3-6% slower.
@@ -171,7 +174,7 @@ __global__ void __launch_bounds__(threads<N>(), 1)
   if (tid == 0) {
     for (int i = 0; i < S; ++i) {
       bar_init(&s.full[i], 1);
-      bar_init(&s.conv[i], 4);
+      bar_init(&s.conv[i], NCONV);
       bar_init(&s.empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -266,9 +269,9 @@ __global__ void __launch_bounds__(threads<N>(), 1)
       }
     }
     __syncwarp();
-  } else if (warp >= CONV0 && warp < CONV0 + 4) {
+  } else if (warp >= CONV0 && warp < CONV0 + NCONV) {
     // ---------------- converters: hi = x as loaded, lo = rnd(x - trunc(x)) ----------------
-    const int ct = tid - CONV0 * 32;  // 0..127
+    const int ct = tid - CONV0 * 32;  // 0..32 NCONV - 1
     uint32_t it = 0;
     for (int64_t tile = blockIdx.x; tile < a.total; tile += gridDim.x) {
       for (int c = 0; c < nchunks; ++c, ++it) {
@@ -280,13 +283,13 @@ __global__ void __launch_bounds__(threads<N>(), 1)
           float4* ah = reinterpret_cast<float4*>(s.st[st].a_hi);
           float4* al = reinterpret_cast<float4*>(s.st[st].a_lo);
 #pragma unroll
-          for (int i = 0; i < TM * KC / 4 / 128; ++i) al[ct + i * 128] = split_lo(ah[ct + i * 128]);
+          for (int i = 0; i < TM * KC / 4 / (NCONV * 32); ++i) al[ct + i * NCONV * 32] = split_lo(ah[ct + i * NCONV * 32]);
         }
         if (!BR && !bpre) {
           float4* bh = reinterpret_cast<float4*>(s.st[st].b_hi);
           float4* bl = reinterpret_cast<float4*>(s.st[st].b_lo);
 #pragma unroll
-          for (int i = 0; i < N * KC / 4 / 128; ++i) bl[ct + i * 128] = split_lo(bh[ct + i * 128]);
+          for (int i = 0; i < N * KC / 4 / (NCONV * 32); ++i) bl[ct + i * NCONV * 32] = split_lo(bh[ct + i * NCONV * 32]);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
         __syncwarp();
