@@ -225,7 +225,11 @@ __global__ void fno_mix(int B, int C, int M, const float* __restrict__ Vh, const
 // 16-row chunk) with mbarrier transaction counts; operands are read as broadcast float4 (8 distinct
 // addresses per warp), so the loop is FFMA-bound: 64 FFMA per 4 LDS.128 (ncu: FMA pipe 64%, issue
 // 72%; 420 us per C5 layer against 487 us for the 3xTF32 tensor-core GEMM with per-thread staging).
-constexpr int DFT_ROWS = 16, DFT_ST = 3, DFT_S = 8;
+#ifndef SNOP_DFT_ROWS
+#define SNOP_DFT_ROWS 16
+#define SNOP_DFT_ST 3
+#endif
+constexpr int DFT_ROWS = SNOP_DFT_ROWS, DFT_ST = SNOP_DFT_ST, DFT_S = 8;
 struct DftStage {
   float v[DFT_S][DFT_ROWS * 64];
   float ft[DFT_ROWS * 32];
