@@ -170,3 +170,18 @@ def test_tail_split_deterministic_and_batch_independent(monkeypatch):
     c = snop.power_iteration(g, q.order, q.sigma_t, q.sigma_s0, q.nu_sigma_f, q.chi, cfg)
     assert np.array_equal(c.k, a.k[[4, 1]]) and np.array_equal(c.phi, a.phi[[4, 1]])
     assert np.array_equal(c.outer_iterations, a.outer_iterations[[4, 1]])
+
+
+@pytest.mark.parametrize("order", [10, 14])
+def test_pair_split_odd_pair_count(order, monkeypatch):
+    """S10 / S14: an odd number of +/-mu pairs (the tail pair goes to the last rank of the cluster)."""
+    monkeypatch.setenv("SNOP_PS", "2")
+    base = W.config3(batch=2, n_cells=300)
+    p = W.EigenProblem("odd", base.length, base.n_cells, order, 1, base.sigma_t, base.sigma_s0, base.nu_sigma_f,
+                       base.chi, None, base.bc_left, base.bc_right)
+    cfg = _cfg(p, tolerance_k=1e-300, tolerance_phi=1e-300, max_outer_iterations=3, max_inner_iterations=4,
+               tolerance=1e-300)
+    r, o = _both(p, cfg)
+    assert (r.total_inner_iterations == o["inner"]).all()
+    assert np.max(np.abs(r.phi - o["phi"])) / np.max(np.abs(o["phi"])) < K_RTOL
+    assert np.max(np.abs(r.k - o["k"]) / o["k"]) < K_RTOL
