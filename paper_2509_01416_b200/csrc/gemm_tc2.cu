@@ -499,6 +499,200 @@ cudaError_t launch(const Args& a, const CUtensorMap* maps, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+
+// ---- FNO forward truncated DFT on the tensor core -------------------------------------------
+// Vh[b][c][m'] = sum_i V[b][i][c] F[m'][i] for C = 64 channels, 2M = 32 modes. One work unit =
+// a sample pair: M = 128 rows (2 samples x 64 channels), N = 32 modes, K = all n cells in blocks
+// of 128 (4 chunks of 32). V is channel-contiguous (an MN-major A operand, which kind::tf32 does
+// not accept on this part), so the TMA lands four 32-channel x 32-cell boxes per chunk and the
+// converter warps transpose them into the K-major 128-byte-swizzled hi / lo buffers while
+// splitting (3xTF32). Each 128-cell block accumulates in TMEM (K = 128, as the other contractions);
+// the epilogue adds the blocks' results in registers in block order and writes Vh once.
+constexpr int DFT_STAGES = 3, DFT_NT = 32;
+struct alignas(1024) DftTcStage {
+  float a_raw[TM * KC];  // 4 boxes [32 cells][32 channels] (swizzled), as landed by TMA
+  float a_hi[TM * KC];   // K-major [128 rows][32 cells] (swizzled)
+  float a_lo[TM * KC];
+  float b_hi[DFT_NT * KC];  // F chunk, K-major [32 modes][32 cells]
+  float b_lo[DFT_NT * KC];
+};
+struct DftTcSmem {
+  DftTcStage st[DFT_STAGES];
+  uint64_t full[DFT_STAGES], conv[DFT_STAGES], empty[DFT_STAGES];
+  uint64_t acc_full[2], acc_empty[2];
+  uint32_t tmem_base;
+};
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
+      : "memory");
+}
+constexpr int DFT_NCONV = 8;
+constexpr int DFT_THREADS = (2 + DFT_NCONV + 4) * 32;  // producer, MMA, converters, 4 epilogue warps
+
+__global__ void __launch_bounds__(DFT_THREADS, 1)
+    dft_tc_kernel(const __grid_constant__ CUtensorMap tV, const __grid_constant__ CUtensorMap tF,
+                  float* __restrict__ Vh, int B, int n, int npairs) {
+  extern __shared__ __align__(1024) unsigned char raw[];
+  const uint32_t pad = (1024u - (su32(raw) & 1023u)) & 1023u;
+  auto& s = *reinterpret_cast<DftTcSmem*>(raw + pad);
+  constexpr int S = DFT_STAGES;
+  constexpr uint32_t TCOLS = 2 * DFT_NT;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nkb = n / 128, nch = nkb * 4;  // K chunks per sample pair
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&s.tmem_base)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      bar_init(&s.full[i], 1);
+      bar_init(&s.conv[i], DFT_NCONV);
+      bar_init(&s.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      bar_init(&s.acc_full[i], 1);
+      bar_init(&s.acc_empty[i], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s.tmem_base;
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int sp = blockIdx.x; sp < npairs; sp += gridDim.x) {
+        for (int c = 0; c < nch; ++c, ++it) {
+          const int st = (int)(it % S);
+          bar_wait(&s.empty[st], ((it / S) & 1) ^ 1);
+          bar_expect_tx(&s.full[st], (uint32_t)((TM + DFT_NT) * KC * sizeof(float)));
+          const int k0 = c * KC;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {  // box q = (sample 2 sp + q / 2, channel half q % 2)
+            const int b = min(2 * sp + (q >> 1), B - 1);
+            tma_3d(s.st[st].a_raw + q * 32 * KC, &tV, 32 * (q & 1), k0, b, &s.full[st]);
+          }
+          tma_2d(s.st[st].b_hi, &tF, k0, 0, &s.full[st]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      uint32_t it = 0, tcount = 0;
+      constexpr uint32_t id = idesc(DFT_NT);
+      for (int sp = blockIdx.x; sp < npairs; sp += gridDim.x) {
+        for (int kb = 0; kb < nkb; ++kb, ++tcount) {
+          const uint32_t acc = tcount & 1;
+          bar_wait(&s.acc_empty[acc], ((tcount >> 1) & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t d = tmem + acc * DFT_NT;
+          for (int c = 0; c < 4; ++c, ++it) {
+            const int st = (int)(it % S);
+            bar_wait(&s.conv[st], (it / S) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t ah = su32(s.st[st].a_hi), al = su32(s.st[st].a_lo);
+            const uint32_t bh = su32(s.st[st].b_hi), bl = su32(s.st[st].b_lo);
+#pragma unroll
+            for (int ks = 0; ks < KC / 8; ++ks) {
+              const uint32_t off = ks * 32;
+              const uint32_t first = (c == 0 && ks == 0) ? 0u : 1u;
+              mma(d, sw128_desc(al + off), sw128_desc(bh + off), id, first);
+              mma(d, sw128_desc(ah + off), sw128_desc(bl + off), id, 1u);
+              mma(d, sw128_desc(ah + off), sw128_desc(bh + off), id, 1u);
+            }
+            commit(&s.empty[st]);
+          }
+          commit(&s.acc_full[acc]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp < 2 + DFT_NCONV) {
+    // converters: transpose the landed boxes into K-major hi / lo (3xTF32 split), split B
+    const int ct = tid - 64;  // 0..32 DFT_NCONV - 1
+    uint32_t it = 0;
+    for (int sp = blockIdx.x; sp < npairs; sp += gridDim.x) {
+      for (int c = 0; c < nch; ++c, ++it) {
+        const int st = (int)(it % S);
+        bar_wait(&s.full[st], (it / S) & 1);
+        const float* ar = s.st[st].a_raw;
+        float* ah = s.st[st].a_hi;
+        float* al = s.st[st].a_lo;
+        // task = (box q, 4-cell group kg, 4-channel group jc): four 16-B loads of the landed box,
+        // a 4 x 4 register transpose, four 16-B stores each into K-major hi and lo
+        for (int task = ct; task < 4 * 8 * 8; task += DFT_NCONV * 32) {
+          const int jc = task & 7, kg = (task >> 3) & 7, q = task >> 6;
+          float4 v[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int kk = 4 * kg + r;
+            v[r] = *reinterpret_cast<const float4*>(ar + q * 1024 + kk * 32 + ((jc ^ (kk & 7)) << 2));
+          }
+          const float vv[4][4] = {{v[0].x, v[0].y, v[0].z, v[0].w}, {v[1].x, v[1].y, v[1].z, v[1].w},
+                                  {v[2].x, v[2].y, v[2].z, v[2].w}, {v[3].x, v[3].y, v[3].z, v[3].w}};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int m = q * 32 + 4 * jc + i;  // row = (sample q / 2) * 64 + (half q % 2) * 32 + channel
+            const int o = (m >> 3) * 256 + (m & 7) * 32 + ((kg ^ (m & 7)) << 2);
+            const float4 h = make_float4(vv[0][i], vv[1][i], vv[2][i], vv[3][i]);
+            *reinterpret_cast<float4*>(ah + o) = h;
+            *reinterpret_cast<float4*>(al + o) = split_lo(h);
+          }
+        }
+        float4* bh = reinterpret_cast<float4*>(s.st[st].b_hi);
+        float4* bl = reinterpret_cast<float4*>(s.st[st].b_lo);
+#pragma unroll
+        for (int i = ct; i < DFT_NT * KC / 4; i += DFT_NCONV * 32) bl[i] = split_lo(bh[i]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) bar_arrive(&s.conv[st]);
+      }
+    }
+  } else {
+    const int q = warp & 3;  // TMEM lane quarter = rows 32 q .. 32 q + 31
+    uint32_t tcount = 0;
+    for (int sp = blockIdx.x; sp < npairs; sp += gridDim.x) {
+      float sum[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) sum[j] = 0.f;
+      for (int kb = 0; kb < nkb; ++kb, ++tcount) {
+        const uint32_t acc = tcount & 1;
+        bar_wait(&s.acc_full[acc], (tcount >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * DFT_NT;
+        uint32_t v[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+            "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+              "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+              "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) bar_arrive(&s.acc_empty[acc]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sum[j] += __uint_as_float(v[j]);
+      }
+      const int r = q * 32 + lane, b = 2 * sp + (r >> 6);
+      if (b < B) {
+        float4* dst = reinterpret_cast<float4*>(Vh + ((size_t)b * 64 + (r & 63)) * DFT_NT);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dst[j] = make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+}
 }  // namespace tc2
 
 // Returns true (and launches) when the contraction fits this engine: K-contiguous operands,
@@ -585,4 +779,36 @@ bool gemm_tc2(const GemmArgs& g, cudaStream_t st, int64_t mfold, cudaError_t* er
   return true;
 }
 
+
+// FNO forward truncated DFT on the tensor core (dft_tc_kernel): Vh [B][64][32] from V [B][n][64].
+// Returns false (nothing launched) when the shape does not fit (C = 64, 2M = 32, n % 128 == 0).
+bool fno_dft_tc(const float* V, const float* F, float* Vh, int B, int n, cudaStream_t st, cudaError_t* err) {
+  using namespace tc2;
+  *err = cudaSuccess;
+  if (n % 128 != 0 || B < 1) return false;
+  EncodeFn enc = encoder();
+  if (!enc) return false;
+  CUtensorMap mv, mf;
+  const cuuint64_t dv[3] = {64, (cuuint64_t)n, (cuuint64_t)B};
+  const cuuint64_t sv[2] = {64 * 4, (cuuint64_t)n * 64 * 4};
+  const cuuint32_t bv[3] = {32, 32, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  if (enc(&mv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(V), dv, sv, bv, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  if (!make_map(&mf, F, 32, n, n, 32)) return false;
+  const int npairs = (B + 1) / 2;
+  const size_t smem = sizeof(DftTcSmem) + 1024;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(dft_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  const int grid = npairs < sms ? npairs : sms;
+  dft_tc_kernel<<<grid, DFT_THREADS, smem, st>>>(mv, mf, Vh, B, n, npairs);
+  *err = cudaGetLastError();
+  return true;
+}
 }  // namespace snop_ops

@@ -603,7 +603,17 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
     f.B = op.F; f.sbn = n; f.sbk = 1; f.sbb = 0;
     f.C = Vh; f.scm = 2 * M; f.scn = 1; f.scb = (int64_t)C * 2 * M;
     f.alpha = 1.f; f.act = ACT_NONE;
-    if (C == 64 && 2 * M == 32 && n % DFT_ROWS == 0 && op.FT && !std::getenv("SNOP_DFT_GEMM")) {
+    bool tc_done = false;
+    if (C == 64 && 2 * M == 32 && n % 128 == 0 && use_tc() && std::getenv("SNOP_DFT_TC")) {
+      cudaError_t e = cudaSuccess;
+      if (fno_dft_tc(V, op.F, Vh, B, n, ctx.stream, &e)) {
+        SNOP_TRY(cuda_status("fno_dft_tc", e));
+        ctx.launches++;
+        tc_done = true;
+      }
+    }
+    if (tc_done) {
+    } else if (C == 64 && 2 * M == 32 && n % DFT_ROWS == 0 && op.FT && !std::getenv("SNOP_DFT_GEMM")) {
       const size_t sm = DFT_ST * sizeof(DftStage) + 2 * DFT_ST * sizeof(uint64_t);
       cudaFuncSetAttribute(fno_dft64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       fno_dft64<<<(B + DFT_S - 1) / DFT_S, 32 * DFT_S, sm, ctx.stream>>>(B, n, V, op.FT, Vh);
