@@ -508,17 +508,26 @@ cudaError_t launch(const Args& a, const CUtensorMap* maps, cudaStream_t st) {
 // converter warps transpose them into the K-major 128-byte-swizzled hi / lo buffers while
 // splitting (3xTF32). Each 128-cell block accumulates in TMEM (K = 128, as the other contractions);
 // the epilogue adds the blocks' results in registers in block order and writes Vh once.
-constexpr int DFT_STAGES = 3, DFT_NT = 32;
-struct alignas(1024) DftTcStage {
-  float a_raw[TM * KC];  // 4 boxes [32 cells][32 channels] (swizzled), as landed by TMA
-  float a_hi[TM * KC];   // K-major [128 rows][32 cells] (swizzled)
+// Two rings: TMA landing stages (raw boxes + F chunk, freed by the converters right after the
+// transpose, so the loads run DFT_LAND chunks ahead) and converted K-major hi / lo slots for the MMA.
+#ifndef SNOP_DFT_LAND
+#define SNOP_DFT_LAND 6
+#endif
+constexpr int DFT_LAND = SNOP_DFT_LAND, DFT_CONV = 2, DFT_NT = 32;
+struct alignas(1024) DftTcLand {
+  float a_raw[TM * KC];      // 4 boxes [32 cells][32 channels] (swizzled), as landed by TMA
+  float b_raw[DFT_NT * KC];  // F chunk, K-major [32 modes][32 cells] (swizzled)
+};
+struct alignas(1024) DftTcConv {
+  float a_hi[TM * KC];  // K-major [128 rows][32 cells] (swizzled)
   float a_lo[TM * KC];
-  float b_hi[DFT_NT * KC];  // F chunk, K-major [32 modes][32 cells]
+  float b_hi[DFT_NT * KC];
   float b_lo[DFT_NT * KC];
 };
 struct DftTcSmem {
-  DftTcStage st[DFT_STAGES];
-  uint64_t full[DFT_STAGES], conv[DFT_STAGES], empty[DFT_STAGES];
+  DftTcLand land[DFT_LAND];
+  DftTcConv cv[DFT_CONV];
+  uint64_t full[DFT_LAND], lempty[DFT_LAND], cfull[DFT_CONV], cempty[DFT_CONV];
   uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem_base;
 };
@@ -538,7 +547,7 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
   extern __shared__ __align__(1024) unsigned char raw[];
   const uint32_t pad = (1024u - (su32(raw) & 1023u)) & 1023u;
   auto& s = *reinterpret_cast<DftTcSmem*>(raw + pad);
-  constexpr int S = DFT_STAGES;
+  constexpr int SL = DFT_LAND, SC = DFT_CONV;
   constexpr uint32_t TCOLS = 2 * DFT_NT;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nkb = n / 128, nch = nkb * 4;  // K chunks per sample pair
@@ -548,10 +557,13 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int i = 0; i < S; ++i) {
+    for (int i = 0; i < SL; ++i) {
       bar_init(&s.full[i], 1);
-      bar_init(&s.conv[i], DFT_NCONV);
-      bar_init(&s.empty[i], 1);
+      bar_init(&s.lempty[i], DFT_NCONV);
+    }
+    for (int i = 0; i < SC; ++i) {
+      bar_init(&s.cfull[i], DFT_NCONV);
+      bar_init(&s.cempty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       bar_init(&s.acc_full[i], 1);
@@ -568,16 +580,16 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
       uint32_t it = 0;
       for (int sp = blockIdx.x; sp < npairs; sp += gridDim.x) {
         for (int c = 0; c < nch; ++c, ++it) {
-          const int st = (int)(it % S);
-          bar_wait(&s.empty[st], ((it / S) & 1) ^ 1);
-          bar_expect_tx(&s.full[st], (uint32_t)((TM + DFT_NT) * KC * sizeof(float)));
+          const int sl = (int)(it % SL);
+          bar_wait(&s.lempty[sl], ((it / SL) & 1) ^ 1);
+          bar_expect_tx(&s.full[sl], (uint32_t)((TM + DFT_NT) * KC * sizeof(float)));
           const int k0 = c * KC;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {  // box q = (sample 2 sp + q / 2, channel half q % 2)
             const int b = min(2 * sp + (q >> 1), B - 1);
-            tma_3d(s.st[st].a_raw + q * 32 * KC, &tV, 32 * (q & 1), k0, b, &s.full[st]);
+            tma_3d(s.land[sl].a_raw + q * 32 * KC, &tV, 32 * (q & 1), k0, b, &s.full[sl]);
           }
-          tma_2d(s.st[st].b_hi, &tF, k0, 0, &s.full[st]);
+          tma_2d(s.land[sl].b_raw, &tF, k0, 0, &s.full[sl]);
         }
       }
     }
@@ -593,11 +605,11 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t d = tmem + acc * DFT_NT;
           for (int c = 0; c < 4; ++c, ++it) {
-            const int st = (int)(it % S);
-            bar_wait(&s.conv[st], (it / S) & 1);
+            const int sc = (int)(it % SC);
+            bar_wait(&s.cfull[sc], (it / SC) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t ah = su32(s.st[st].a_hi), al = su32(s.st[st].a_lo);
-            const uint32_t bh = su32(s.st[st].b_hi), bl = su32(s.st[st].b_lo);
+            const uint32_t ah = su32(s.cv[sc].a_hi), al = su32(s.cv[sc].a_lo);
+            const uint32_t bh = su32(s.cv[sc].b_hi), bl = su32(s.cv[sc].b_lo);
 #pragma unroll
             for (int ks = 0; ks < KC / 8; ++ks) {
               const uint32_t off = ks * 32;
@@ -606,7 +618,7 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
               mma(d, sw128_desc(ah + off), sw128_desc(bl + off), id, 1u);
               mma(d, sw128_desc(ah + off), sw128_desc(bh + off), id, 1u);
             }
-            commit(&s.empty[st]);
+            commit(&s.cempty[sc]);
           }
           commit(&s.acc_full[acc]);
         }
@@ -619,11 +631,12 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
     uint32_t it = 0;
     for (int sp = blockIdx.x; sp < npairs; sp += gridDim.x) {
       for (int c = 0; c < nch; ++c, ++it) {
-        const int st = (int)(it % S);
-        bar_wait(&s.full[st], (it / S) & 1);
-        const float* ar = s.st[st].a_raw;
-        float* ah = s.st[st].a_hi;
-        float* al = s.st[st].a_lo;
+        const int sl = (int)(it % SL), sc = (int)(it % SC);
+        bar_wait(&s.full[sl], (it / SL) & 1);
+        bar_wait(&s.cempty[sc], ((it / SC) & 1) ^ 1);  // the MMAs of chunk it - SC are done
+        const float* ar = s.land[sl].a_raw;
+        float* ah = s.cv[sc].a_hi;
+        float* al = s.cv[sc].a_lo;
         // task = (box q, 4-cell group kg, 4-channel group jc): four 16-B loads of the landed box,
         // a 4 x 4 register transpose, four 16-B stores each into K-major hi and lo
         for (int task = ct; task < 4 * 8 * 8; task += DFT_NCONV * 32) {
@@ -645,13 +658,20 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
             *reinterpret_cast<float4*>(al + o) = split_lo(h);
           }
         }
-        float4* bh = reinterpret_cast<float4*>(s.st[st].b_hi);
-        float4* bl = reinterpret_cast<float4*>(s.st[st].b_lo);
-#pragma unroll
-        for (int i = ct; i < DFT_NT * KC / 4; i += DFT_NCONV * 32) bl[i] = split_lo(bh[i]);
+        const float4* br = reinterpret_cast<const float4*>(s.land[sl].b_raw);
+        float4* bh = reinterpret_cast<float4*>(s.cv[sc].b_hi);
+        float4* bl = reinterpret_cast<float4*>(s.cv[sc].b_lo);
+        for (int i = ct; i < DFT_NT * KC / 4; i += DFT_NCONV * 32) {
+          const float4 x = br[i];
+          bh[i] = x;
+          bl[i] = split_lo(x);
+        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) bar_arrive(&s.conv[st]);
+        if (lane == 0) {
+          bar_arrive(&s.lempty[sl]);  // the landing stage may be refilled
+          bar_arrive(&s.cfull[sc]);
+        }
       }
     }
   } else {

@@ -604,7 +604,8 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
     f.C = Vh; f.scm = 2 * M; f.scn = 1; f.scb = (int64_t)C * 2 * M;
     f.alpha = 1.f; f.act = ACT_NONE;
     bool tc_done = false;
-    if (C == 64 && 2 * M == 32 && n % 128 == 0 && use_tc() && std::getenv("SNOP_DFT_TC")) {
+    const char* dft_tc_env = std::getenv("SNOP_DFT_TC");  // default on; "0" selects the FFMA kernel
+    if (C == 64 && 2 * M == 32 && n % 128 == 0 && use_tc() && !(dft_tc_env && dft_tc_env[0] == '0')) {
       cudaError_t e = cudaSuccess;
       if (fno_dft_tc(V, op.F, Vh, B, n, ctx.stream, &e)) {
         SNOP_TRY(cuda_status("fno_dft_tc", e));
