@@ -163,7 +163,8 @@ cudaError_t gemm_tc(const GemmArgs& g, cudaStream_t st, int64_t mfold = 0);
 // Warp-specialised TMA-fed engine (gemm_tc2.cu) for K-contiguous operands with K <= 128: returns
 // false when the contraction does not fit it (the caller then uses gemm_tc).
 bool gemm_tc2(const GemmArgs& g, cudaStream_t st, int64_t mfold, cudaError_t* err);
-bool fno_dft_tc(const float* V, const float* F, float* Vh, int B, int n, cudaStream_t st, cudaError_t* err);
+bool fno_dft_tc(const float* V, const float* F, const float* F_lo, float* Vh, int B, int n, cudaStream_t st,
+                cudaError_t* err);
 
 static inline cudaError_t gemm_f32(const GemmArgs& a, cudaStream_t s) {
   if (a.M <= 0 || a.N <= 0 || a.batch <= 0) return cudaSuccess;

@@ -508,21 +508,25 @@ cudaError_t launch(const Args& a, const CUtensorMap* maps, cudaStream_t st) {
 // converter warps transpose them into the K-major 128-byte-swizzled hi / lo buffers while
 // splitting (3xTF32). Each 128-cell block accumulates in TMEM (K = 128, as the other contractions);
 // the epilogue adds the blocks' results in registers in block order and writes Vh once.
-// Two rings: TMA landing stages (raw boxes + F chunk, freed by the converters right after the
-// transpose, so the loads run DFT_LAND chunks ahead) and converted K-major hi / lo slots for the MMA.
+// Two rings: TMA landing stages (raw boxes + the pre-split F chunk, which the MMA reads in place;
+// freed by the MMA commit) and converted K-major hi / lo A slots.
 #ifndef SNOP_DFT_LAND
 #define SNOP_DFT_LAND 6
 #endif
-constexpr int DFT_LAND = SNOP_DFT_LAND, DFT_CONV = 2, DFT_NT = 32;
+#ifndef SNOP_DFT_CONV
+#define SNOP_DFT_CONV 2
+#endif
+constexpr int DFT_LAND = SNOP_DFT_LAND, DFT_CONV = SNOP_DFT_CONV, DFT_NT = 32;
 struct alignas(1024) DftTcLand {
-  float a_raw[TM * KC];      // 4 boxes [32 cells][32 channels] (swizzled), as landed by TMA
-  float b_raw[DFT_NT * KC];  // F chunk, K-major [32 modes][32 cells] (swizzled)
+  float a_raw[TM * KC];     // 4 boxes [32 cells][32 channels] (swizzled), as landed by TMA
+  float b_hi[DFT_NT * KC];  // F chunk, K-major [32 modes][32 cells] (swizzled), pre-split hi / lo
+  float b_lo[DFT_NT * KC];
 };
+static_assert(offsetof(DftTcLand, b_lo) == offsetof(DftTcLand, b_hi) + DFT_NT * KC * sizeof(float),
+              "the N = 64 hi|lo MMA reads b_hi and b_lo as one 64-row K-major operand");
 struct alignas(1024) DftTcConv {
   float a_hi[TM * KC];  // K-major [128 rows][32 cells] (swizzled)
   float a_lo[TM * KC];
-  float b_hi[DFT_NT * KC];
-  float b_lo[DFT_NT * KC];
 };
 struct DftTcSmem {
   DftTcLand land[DFT_LAND];
@@ -543,12 +547,12 @@ constexpr int DFT_THREADS = (2 + DFT_NCONV + 4) * 32;  // producer, MMA, convert
 
 __global__ void __launch_bounds__(DFT_THREADS, 1)
     dft_tc_kernel(const __grid_constant__ CUtensorMap tV, const __grid_constant__ CUtensorMap tF,
-                  float* __restrict__ Vh, int B, int n, int npairs) {
+                  const __grid_constant__ CUtensorMap tFl, float* __restrict__ Vh, int B, int n, int npairs) {
   extern __shared__ __align__(1024) unsigned char raw[];
   const uint32_t pad = (1024u - (su32(raw) & 1023u)) & 1023u;
   auto& s = *reinterpret_cast<DftTcSmem*>(raw + pad);
   constexpr int SL = DFT_LAND, SC = DFT_CONV;
-  constexpr uint32_t TCOLS = 2 * DFT_NT;
+  constexpr uint32_t TCOLS = 4 * DFT_NT;  // two accumulators x [hi*hi (+ lo*hi) | hi*lo] columns
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nkb = n / 128, nch = nkb * 4;  // K chunks per sample pair
   if (warp == 1) {
@@ -559,7 +563,7 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
   if (tid == 0) {
     for (int i = 0; i < SL; ++i) {
       bar_init(&s.full[i], 1);
-      bar_init(&s.lempty[i], DFT_NCONV);
+      bar_init(&s.lempty[i], 1);  // released by the MMA commit (B is read in place)
     }
     for (int i = 0; i < SC; ++i) {
       bar_init(&s.cfull[i], DFT_NCONV);
@@ -582,14 +586,15 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
         for (int c = 0; c < nch; ++c, ++it) {
           const int sl = (int)(it % SL);
           bar_wait(&s.lempty[sl], ((it / SL) & 1) ^ 1);
-          bar_expect_tx(&s.full[sl], (uint32_t)((TM + DFT_NT) * KC * sizeof(float)));
+          bar_expect_tx(&s.full[sl], (uint32_t)((TM + 2 * DFT_NT) * KC * sizeof(float)));
           const int k0 = c * KC;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {  // box q = (sample 2 sp + q / 2, channel half q % 2)
             const int b = min(2 * sp + (q >> 1), B - 1);
             tma_3d(s.land[sl].a_raw + q * 32 * KC, &tV, 32 * (q & 1), k0, b, &s.full[sl]);
           }
-          tma_2d(s.land[sl].b_raw, &tF, k0, 0, &s.full[sl]);
+          tma_2d(s.land[sl].b_hi, &tF, k0, 0, &s.full[sl]);
+          tma_2d(s.land[sl].b_lo, &tFl, k0, 0, &s.full[sl]);
         }
       }
     }
@@ -597,28 +602,29 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       uint32_t it = 0, tcount = 0;
-      constexpr uint32_t id = idesc(DFT_NT);
+      constexpr uint32_t id = idesc(DFT_NT), id2 = idesc(2 * DFT_NT);
       for (int sp = blockIdx.x; sp < npairs; sp += gridDim.x) {
         for (int kb = 0; kb < nkb; ++kb, ++tcount) {
           const uint32_t acc = tcount & 1;
           bar_wait(&s.acc_empty[acc], ((tcount >> 1) & 1) ^ 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t d = tmem + acc * DFT_NT;
+          const uint32_t d = tmem + acc * 2 * DFT_NT;
           for (int c = 0; c < 4; ++c, ++it) {
-            const int sc = (int)(it % SC);
+            const int sc = (int)(it % SC), sl = (int)(it % SL);
             bar_wait(&s.cfull[sc], (it / SC) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t ah = su32(s.cv[sc].a_hi), al = su32(s.cv[sc].a_lo);
-            const uint32_t bh = su32(s.cv[sc].b_hi), bl = su32(s.cv[sc].b_lo);
+            const uint32_t bh = su32(s.land[sl].b_hi), bl = su32(s.land[sl].b_lo);
 #pragma unroll
             for (int ks = 0; ks < KC / 8; ++ks) {
               const uint32_t off = ks * 32;
               const uint32_t first = (c == 0 && ks == 0) ? 0u : 1u;
-              mma(d, sw128_desc(al + off), sw128_desc(bh + off), id, first);
-              mma(d, sw128_desc(ah + off), sw128_desc(bl + off), id, 1u);
-              mma(d, sw128_desc(ah + off), sw128_desc(bh + off), id, 1u);
+              // b_hi / b_lo are adjacent: one N = 64 MMA reads A_hi once for hi*hi and hi*lo
+              mma(d, sw128_desc(ah + off), sw128_desc(bh + off), id2, first);
+              mma(d, sw128_desc(al + off), sw128_desc(bh + off), id, 1u);
             }
             commit(&s.cempty[sc]);
+            commit(&s.lempty[sl]);
           }
           commit(&s.acc_full[acc]);
         }
@@ -638,9 +644,14 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
         float* ah = s.cv[sc].a_hi;
         float* al = s.cv[sc].a_lo;
         // task = (box q, 4-cell group kg, 4-channel group jc): four 16-B loads of the landed box,
-        // a 4 x 4 register transpose, four 16-B stores each into K-major hi and lo
+        // a 4 x 4 register transpose, four 16-B stores each into K-major hi and lo. A 16-B access
+        // is served eight lanes at a time and both swizzled layouts put a 16-B chunk's bank group
+        // at (chunk index) only, so each 8-lane group takes kg = l and jc = (l ^ 4 (l & 1)) ^ g:
+        // the load chunks jc ^ (4 kg + r) and the store chunks kg ^ (4 jc + i) are then both
+        // permutations of 0..7 (no bank conflicts on either side of the transpose).
         for (int task = ct; task < 4 * 8 * 8; task += DFT_NCONV * 32) {
-          const int jc = task & 7, kg = (task >> 3) & 7, q = task >> 6;
+          const int l = task & 7, g = (task >> 3) & 7, q = task >> 6;
+          const int kg = l, jc = (l ^ ((l & 1) << 2)) ^ g;
           float4 v[4];
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
@@ -658,20 +669,9 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
             *reinterpret_cast<float4*>(al + o) = split_lo(h);
           }
         }
-        const float4* br = reinterpret_cast<const float4*>(s.land[sl].b_raw);
-        float4* bh = reinterpret_cast<float4*>(s.cv[sc].b_hi);
-        float4* bl = reinterpret_cast<float4*>(s.cv[sc].b_lo);
-        for (int i = ct; i < DFT_NT * KC / 4; i += DFT_NCONV * 32) {
-          const float4 x = br[i];
-          bh[i] = x;
-          bl[i] = split_lo(x);
-        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) {
-          bar_arrive(&s.lempty[sl]);  // the landing stage may be refilled
-          bar_arrive(&s.cfull[sc]);
-        }
+        if (lane == 0) bar_arrive(&s.cfull[sc]);
       }
     }
   } else {
@@ -685,8 +685,8 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
         const uint32_t acc = tcount & 1;
         bar_wait(&s.acc_full[acc], (tcount >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * DFT_NT;
-        uint32_t v[32];
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * 2 * DFT_NT;
+        uint32_t v[32], w[32];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
             "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -695,12 +695,20 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
               "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
               "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+            "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]), "=r"(w[8]),
+              "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15]), "=r"(w[16]),
+              "=r"(w[17]), "=r"(w[18]), "=r"(w[19]), "=r"(w[20]), "=r"(w[21]), "=r"(w[22]), "=r"(w[23]), "=r"(w[24]),
+              "=r"(w[25]), "=r"(w[26]), "=r"(w[27]), "=r"(w[28]), "=r"(w[29]), "=r"(w[30]), "=r"(w[31])
+            : "r"(taddr + DFT_NT));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) bar_arrive(&s.acc_empty[acc]);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) sum[j] += __uint_as_float(v[j]);
+        for (int j = 0; j < 32; ++j) sum[j] += __uint_as_float(v[j]) + __uint_as_float(w[j]);
       }
       const int r = q * 32 + lane, b = 2 * sp + (r >> 6);
       if (b < B) {
@@ -802,13 +810,15 @@ bool gemm_tc2(const GemmArgs& g, cudaStream_t st, int64_t mfold, cudaError_t* er
 
 // FNO forward truncated DFT on the tensor core (dft_tc_kernel): Vh [B][64][32] from V [B][n][64].
 // Returns false (nothing launched) when the shape does not fit (C = 64, 2M = 32, n % 128 == 0).
-bool fno_dft_tc(const float* V, const float* F, float* Vh, int B, int n, cudaStream_t st, cudaError_t* err) {
+bool fno_dft_tc(const float* V, const float* F, const float* F_lo, float* Vh, int B, int n, cudaStream_t st,
+                cudaError_t* err) {
   using namespace tc2;
   *err = cudaSuccess;
   if (n % 128 != 0 || B < 1) return false;
   EncodeFn enc = encoder();
   if (!enc) return false;
-  CUtensorMap mv, mf;
+  CUtensorMap mv, mf, mfl;
+  if (!F_lo) return false;
   const cuuint64_t dv[3] = {64, (cuuint64_t)n, (cuuint64_t)B};
   const cuuint64_t sv[2] = {64 * 4, (cuuint64_t)n * 64 * 4};
   const cuuint32_t bv[3] = {32, 32, 1};
@@ -816,7 +826,7 @@ bool fno_dft_tc(const float* V, const float* F, float* Vh, int B, int n, cudaStr
   if (enc(&mv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(V), dv, sv, bv, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
-  if (!make_map(&mf, F, 32, n, n, 32)) return false;
+  if (!make_map(&mf, F, 32, n, n, 32) || !make_map(&mfl, F_lo, 32, n, n, 32)) return false;
   const int npairs = (B + 1) / 2;
   const size_t smem = sizeof(DftTcSmem) + 1024;
   static int sms = 0;
@@ -827,7 +837,7 @@ bool fno_dft_tc(const float* V, const float* F, float* Vh, int B, int n, cudaStr
     cudaFuncSetAttribute(dft_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
   const int grid = npairs < sms ? npairs : sms;
-  dft_tc_kernel<<<grid, DFT_THREADS, smem, st>>>(mv, mf, Vh, B, n, npairs);
+  dft_tc_kernel<<<grid, DFT_THREADS, smem, st>>>(mv, mf, mfl, Vh, B, n, npairs);
   *err = cudaGetLastError();
   return true;
 }

@@ -44,7 +44,7 @@ struct snop_op {
   float *F = nullptr, *Ginv = nullptr;  // forward [2M][n] and inverse [n][2M] truncated DFT
   float* FT = nullptr;                  // forward DFT transposed, [n][2M] (fno_dft64)
   // pre-split 3xTF32 lo parts of the constant GEMM operands (TMA engine loads them, no conversion)
-  float *Ginv_lo = nullptr, *P1W_lo = nullptr;
+  float *Ginv_lo = nullptr, *P1W_lo = nullptr, *F_lo = nullptr;
   // exact operator
   int order = 16;
   snop_solver_config cfg{};
@@ -607,7 +607,7 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
     const char* dft_tc_env = std::getenv("SNOP_DFT_TC");  // default on; "0" selects the FFMA kernel
     if (C == 64 && 2 * M == 32 && n % 128 == 0 && use_tc() && !(dft_tc_env && dft_tc_env[0] == '0')) {
       cudaError_t e = cudaSuccess;
-      if (fno_dft_tc(V, op.F, Vh, B, n, ctx.stream, &e)) {
+      if (fno_dft_tc(V, op.F, op.F_lo, Vh, B, n, ctx.stream, &e)) {
         SNOP_TRY(cuda_status("fno_dft_tc", e));
         ctx.launches++;
         tc_done = true;
@@ -1180,6 +1180,7 @@ snop_status snop_fno_create(snop_ctx* ctx, const snop_grid* grid, double tstar, 
   op->F = op->upload(F.data(), F.size());
   op->Ginv = op->upload(G.data(), G.size());
   op->Ginv_lo = op->upload_lo(G.data(), G.size());
+  op->F_lo = op->upload_lo(F.data(), F.size());
   {
     std::vector<float> FTh((size_t)n * 2 * M);
     for (size_t m = 0; m < 2 * M; ++m)
