@@ -15,17 +15,30 @@ enum Act : int { ACT_RELU = 0, ACT_TANH = 1, ACT_GELU = 2, ACT_NONE = 3 };
 
 // GELU(x) = x Phi(x) = 0.5 x (1 + erf(x / sqrt 2)) (exact-erf form), erf from
 // Abramowitz & Stegun 7.1.26: erf(z) = 1 - t (a1 + a2 t + ... + a5 t^4) exp(-z^2), t = 1/(1 + p z),
-// |error| <= 1.5e-7 (<= 5e-7 absolute on GELU in fp32 arithmetic): one MUFU.RCP + one MUFU.EX2 and
-// ~9 FMA-pipe instructions instead of erff's ~25 (select-heavy) path. The epilogues of the FNO
-// GEMMs evaluate it ~1.3e9 times per C5 forward.
+// |error| <= 1.5e-7 (<= 5e-7 absolute on GELU in fp32 arithmetic). The reciprocal and the
+// exponential are the raw flush-to-zero MUFU ops (rcp.approx.ftz, ex2.approx.ftz: __fdividef /
+// __expf add denormal-range fix-ups, 6 + 9 instructions at the source line in ncu; a flushed
+// exp(-z^2) < 2^-126 changes nothing at fp32), and the sign is folded algebraically,
+// GELU = x/2 + |x|/2 erf(|x| / sqrt 2), so no copysign: ~14 instructions, 2 MUFU. The epilogues
+// of the FNO GEMMs evaluate it ~1.3e9 times per C5 forward (issue-bound there).
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ float gelu_f(float x) {
   const float z = fabsf(x) * 0.70710678118654752440f;
-  const float t = __fdividef(1.0f, fmaf(0.3275911f, z, 1.0f));
+  const float t = rcp_ftz(fmaf(0.3275911f, z, 1.0f));
   const float p =
       fmaf(fmaf(fmaf(fmaf(1.061405429f, t, -1.453152027f), t, 1.421413741f), t, -0.284496736f), t, 0.254829592f) * t;
-  const float er = copysignf(fmaf(-p, __expf(-z * z), 1.0f), x);
+  const float e = ex2_ftz((x * x) * -0.72134752044448170368f);  // exp(-z^2) = 2^(-x^2 log2(e) / 2)
   const float h = 0.5f * x;
-  return fmaf(h, er, h);
+  return fmaf(fabsf(h), fmaf(-p, e, 1.0f), h);
 }
 
 __device__ __forceinline__ float act_f(float x, int act) {
