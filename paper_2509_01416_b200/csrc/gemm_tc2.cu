@@ -76,8 +76,24 @@ struct Smem {
   float ep_rb[2][N];
 };
 
+// n / d for n < 2^31 by multiply-high (host-computed magic; q = (umulhi(n, m) + n) >> s): the tile
+// decomposition runs in every warp for every tile, and the K = 64..96 contractions have ~3 K chunks
+// per tile, so the two integer divisions were ~8% of the warp samples.
+struct FastDiv {
+  uint32_t m, s;
+  void init(uint32_t d) {
+    s = 0;
+    while ((1ull << s) < d) ++s;
+    m = (uint32_t)(((1ull << 32) * ((1ull << s) - d)) / d + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return (uint32_t)(((uint64_t)__umulhi(n, m) + n) >> s);
+  }
+};
+
 struct Args {
   GemmArgs g;
+  FastDiv div_n, div_mn;  // by n_tiles, by n_tiles * m_tiles
   int64_t a1_brows, a2_brows, b1_brows, b2_brows;  // batch stride in rows of each 2-D view
   int64_t m_tiles, n_tiles, total;
   int a1_pre, a2_pre, b1_pre, b2_pre;  // operand has a pre-split lo array (loaded, not converted)
@@ -194,8 +210,8 @@ __global__ void __launch_bounds__(threads<N>(), 1)
   const uint32_t n_t = (uint32_t)a.n_tiles, mn_t = (uint32_t)(a.n_tiles * a.m_tiles);
   auto tile_coords = [&](int64_t tile, int& b, int64_t& m0, int& n0) {
     const uint32_t t = (uint32_t)tile;
-    const uint32_t bq = t / mn_t, rem = t - bq * mn_t;
-    const uint32_t mt = rem / n_t, nt = rem - mt * n_t;
+    const uint32_t bq = a.div_mn.div(t), rem = t - bq * mn_t;
+    const uint32_t mt = a.div_n.div(rem), nt = rem - mt * n_t;
     b = (int)bq;
     m0 = (int64_t)mt * TM;
     n0 = (int)nt * N;
@@ -310,7 +326,9 @@ __global__ void __launch_bounds__(threads<N>(), 1)
       int b, n0;
       int64_t m0;
       tile_coords(tile, b, m0, n0);
-      // this tile's bias / row-dot weights (epilogue warps only; named barrier 1)
+      // this tile's bias / row-dot weights (epilogue warps only; named barrier 1); with one column
+      // tile they are the same for every tile, so each accumulator slot's copy is loaded once
+      if (a.n_tiles != 1 || tcount < 2)
       for (int j = et; j < N; j += NEPI * 32) {
         const int gn = n0 + j;
         s.ep_bias[acc][j] = (g.bias && gn < g.N) ? g.bias[gn] : 0.f;
@@ -792,6 +810,8 @@ bool gemm_tc2(const GemmArgs& g, cudaStream_t st, int64_t mfold, cudaError_t* er
   a.total = a.m_tiles * a.n_tiles * g.batch;
   if (a.total == 0) return true;
   if (a.total >= ((int64_t)1 << 31)) return false;  // 32-bit tile arithmetic in the kernel
+  a.div_n.init((uint32_t)a.n_tiles);
+  a.div_mn.init((uint32_t)(a.n_tiles * a.m_tiles));
   // resident B (see stages()): N = 128 tile, one column tile, batch-invariant pre-split B, K <= 64
   const bool bres = NT == 128 && a.n_tiles == 1 && g.ksplit == 0 && g.sbb == 0 && a.b1_pre &&
                     (g.K + KC - 1) / KC <= BR_CHUNKS && !std::getenv("SNOP_NO_BRES");
