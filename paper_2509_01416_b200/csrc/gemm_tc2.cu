@@ -46,12 +46,18 @@ constexpr int threads() { return (EPI0 + nepi<N>()) * 32; }
 // BR ("B resident"): a batch-invariant, pre-split B operand with K <= 64 (the FNO projection
 // weights) is loaded into shared memory once per CTA; the stages then carry only A, so the TMA
 // streams 16 instead of 48 KB per K chunk and four stages fit.
+#ifndef SNOP_TC2_S64
+#define SNOP_TC2_S64 3
+#endif
 template <int N, bool BR = false>
-constexpr int stages() { return BR ? 4 : 3; }
+constexpr int stages() { return BR ? 4 : (N == 64 ? SNOP_TC2_S64 : 3); }
 constexpr int BR_CHUNKS = 2;
 // N = 64 tiles are stored through shared memory by TMA (two 128 x 32 fp32 halves, 128-B swizzle)
 template <int N>
-constexpr int cst_floats() { return N == 64 ? TM * N : 4; }
+#ifndef SNOP_TC2_CST
+#define SNOP_TC2_CST 1
+#endif
+constexpr int cst_floats() { return (N == 64 && SNOP_TC2_CST) ? 2 * TM * N : 4; }  // double-buffered
 
 template <int N, bool BR = false>
 struct alignas(1024) Stage {
@@ -336,8 +342,8 @@ __global__ void __launch_bounds__(threads<N>(), 1)
         s.ep_ra[acc][j] = (g.r2_a && gn < g.N) ? g.r2_a[gn] : 0.f;
         s.ep_rb[acc][j] = (g.r2_b && gn < g.N) ? g.r2_b[gn] : 0.f;
       }
-      if (N == 64 && a.tma_store && et == 0)  // the previous tile's TMA store has read the staging
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      if (N == 64 && a.tma_store && et == 0)  // the TMA store two tiles back has read this staging buffer
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       asm volatile("bar.sync 1, %0;" ::"r"(NEPI * 32) : "memory");
       bar_wait(&s.acc_full[acc], (tcount >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -407,7 +413,7 @@ __global__ void __launch_bounds__(threads<N>(), 1)
         } else if (N == 64 && a.tma_store) {
           // 128-B swizzled staging: half (cc >> 5), row r, 16-B chunk (c >> 2) ^ (r & 7)
           const int r = q * 32 + lane, hcol = cc & 31;
-          float* hbase = s.cst + (cc >> 5) * (TM * 32) + r * 32;
+          float* hbase = s.cst + (tcount & 1) * (TM * N) + (cc >> 5) * (TM * 32) + r * 32;
 #pragma unroll
           for (int v4 = 0; v4 < 4; ++v4) {
             const int chunk = ((hcol >> 2) + v4) ^ (r & 7);
@@ -441,7 +447,7 @@ __global__ void __launch_bounds__(threads<N>(), 1)
           for (int h = 0; h < 2; ++h)
             asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                              reinterpret_cast<uint64_t>(&tC)),
-                         "r"(n0 + 32 * h), "r"(row0), "r"(su32(s.cst + h * TM * 32))
+                         "r"(n0 + 32 * h), "r"(row0), "r"(su32(s.cst + (tcount & 1) * (TM * N) + h * TM * 32))
                          : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
@@ -793,7 +799,7 @@ bool gemm_tc2(const GemmArgs& g, cudaStream_t st, int64_t mfold, cudaError_t* er
   a.tma_store = 0;
   maps[8] = maps[0];
   if (NT == 64 && g.N == 64 && g.C && !g.Cd && !g.rowdot_w && g.scn == 1 && g.M % TM == 0 &&
-      (g.batch == 1 || g.scb == (int64_t)g.M * g.scm) && !std::getenv("SNOP_NO_TMA_STORE")) {
+      (g.batch == 1 || g.scb == (int64_t)g.M * g.scm) && SNOP_TC2_CST && !std::getenv("SNOP_NO_TMA_STORE")) {
     EncodeFn enc = encoder();
     const cuuint64_t dims[2] = {(cuuint64_t)g.N, (cuuint64_t)((int64_t)g.batch * g.M)};
     const cuuint64_t strides[1] = {(cuuint64_t)(g.scm * 4)};
