@@ -226,3 +226,18 @@ def test_fno_predict_deterministic():
     op = snop.SolutionOperator.fno(snop.Grid1D(10.0, 256), prm, (1.0, 0.8))
     s = np.random.default_rng(9).uniform(0, 1, (11, 256))
     assert np.array_equal(op.predict(s), op.predict(s))
+
+
+def test_fno_width64_persistent_wrap():
+    """More sample pairs / tiles than CTAs (151 pairs, 604 inverse+W tiles on 148 SMs): the
+    persistent kernels' ring phases, the double-buffered TMA-store staging and the multiply-high
+    tile decomposition cross tile boundaries; an odd batch leaves a one-sample last pair."""
+    prm = OPS.fno_init(64, 16, 2, 128, OPS.GELU, seed=13)
+    g = snop.Grid1D(10.0, 512)
+    op = snop.SolutionOperator.fno(g, prm, (1.0, 0.8))
+    oo = O.OracleOperator.fno(10.0, 512, (1.0, 0.8), OPS.GELU, 64, 16, 2, 128, prm.packed())
+    s = np.random.default_rng(17).uniform(0, 1, (301, 512))
+    got = op.predict(s)
+    idx = np.r_[0:8, 140:160, 290:301]  # oracle on a subset (CPU time); first, wrapped and last pairs
+    assert _rel(got[idx], oo.predict(s[idx])) < OP_RTOL
+    assert _rel(got[idx], op.predict(s[idx])) < 1e-6  # a sample's result does not depend on its batch
