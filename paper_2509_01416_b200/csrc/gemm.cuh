@@ -18,9 +18,10 @@ enum Act : int { ACT_RELU = 0, ACT_TANH = 1, ACT_GELU = 2, ACT_NONE = 3 };
 // |error| <= 1.5e-7 (<= 5e-7 absolute on GELU in fp32 arithmetic). The reciprocal and the
 // exponential are the raw flush-to-zero MUFU ops (rcp.approx.ftz, ex2.approx.ftz: __fdividef /
 // __expf add denormal-range fix-ups, 6 + 9 instructions at the source line in ncu; a flushed
-// exp(-z^2) < 2^-126 changes nothing at fp32), and the sign is folded algebraically,
-// GELU = x/2 + |x|/2 erf(|x| / sqrt 2), so no copysign: ~14 instructions, 2 MUFU. The epilogues
-// of the FNO GEMMs evaluate it ~1.3e9 times per C5 forward (issue-bound there).
+// exp(-z^2) < 2^-126 changes nothing at fp32), and the sign is folded algebraically (below), so
+// no copysign or |.|: ~13 instructions, 2 MUFU, |error| <= 3.4e-7 absolute on GELU (fp32, swept
+// over [-12, 12]). The epilogues of the FNO GEMMs evaluate it ~1.6e9 times per C5 forward
+// (the projection is issue-bound on it).
 __device__ __forceinline__ float rcp_ftz(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -32,13 +33,14 @@ __device__ __forceinline__ float ex2_ftz(float x) {
   return r;
 }
 __device__ __forceinline__ float gelu_f(float x) {
+  // GELU = x/2 + |x|/2 erf(z) = max(x, 0) - (|x|/2) t P(t) e^{-z^2}, z = |x|/sqrt 2, and
+  // |x|/2 = z / sqrt 2: the factor 1/sqrt 2 is folded into the A&S coefficients (a_i / sqrt 2).
   const float z = fabsf(x) * 0.70710678118654752440f;
   const float t = rcp_ftz(fmaf(0.3275911f, z, 1.0f));
   const float p =
-      fmaf(fmaf(fmaf(fmaf(1.061405429f, t, -1.453152027f), t, 1.421413741f), t, -0.284496736f), t, 0.254829592f) * t;
-  const float e = ex2_ftz((x * x) * -0.72134752044448170368f);  // exp(-z^2) = 2^(-x^2 log2(e) / 2)
-  const float h = 0.5f * x;
-  return fmaf(fabsf(h), fmaf(-p, e, 1.0f), h);
+      fmaf(fmaf(fmaf(fmaf(7.505269764e-01f, t, -1.027533652e+00f), t, 1.005091295e+00f), t, -2.011695713e-01f), t, 1.801917326e-01f) * t;
+  const float e = ex2_ftz((z * z) * -1.44269504088896340736f);  // exp(-z^2)
+  return fmaf(-z, p * e, fmaxf(x, 0.0f));
 }
 
 __device__ __forceinline__ float act_f(float x, int act) {
