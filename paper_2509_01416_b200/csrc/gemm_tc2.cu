@@ -75,6 +75,7 @@ struct Smem {
   alignas(1024) float cst[cst_floats<N>()];  // output tile staging for the TMA store (N = 64)
   uint64_t full[stages<N, BR>()], conv[stages<N, BR>()], empty[stages<N, BR>()];
   uint64_t acc_full[2], acc_empty[2];
+  uint64_t stg_full[2], stg_free[2];  // TMA-store staging hand-off (decoupled epilogue)
   uint32_t tmem_base;
   alignas(16) float ep_bias[2][N];  // per accumulator: this tile's bias / row-dot weights / rank-2 columns
   float ep_rw[2][N];
@@ -104,6 +105,7 @@ struct Args {
   int64_t m_tiles, n_tiles, total;
   int a1_pre, a2_pre, b1_pre, b2_pre;  // operand has a pre-split lo array (loaded, not converted)
   int tma_store;                       // N = 64, contiguous fp32 rows: epilogue stores by TMA
+  int decouple;                        // mbarrier staging hand-off instead of per-tile named barriers
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -204,6 +206,10 @@ __global__ void __launch_bounds__(threads<N>(), 1)
       bar_init(&s.acc_empty[i], nepi<N>());
     }
     bar_init(&s.bres_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      bar_init(&s.stg_full[i], nepi<N>());
+      bar_init(&s.stg_free[i], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -342,11 +348,17 @@ __global__ void __launch_bounds__(threads<N>(), 1)
         s.ep_ra[acc][j] = (g.r2_a && gn < g.N) ? g.r2_a[gn] : 0.f;
         s.ep_rb[acc][j] = (g.r2_b && gn < g.N) ? g.r2_b[gn] : 0.f;
       }
-      if (N == 64 && a.tma_store && et == 0)  // the TMA store two tiles back has read this staging buffer
-        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-      asm volatile("bar.sync 1, %0;" ::"r"(NEPI * 32) : "memory");
+      // decoupled staging (a.decouple): the warps hand the staged tile to one storing thread by
+      // mbarrier instead of two named barriers per tile, so they do not wait for each other
+      const bool dec = N == 64 && a.tma_store && a.decouple;
+      if (!dec || a.n_tiles != 1 || tcount < 2) {
+        if (N == 64 && a.tma_store && et == 0 && !dec)  // the store two tiles back has read this buffer
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"r"(NEPI * 32) : "memory");
+      }
       bar_wait(&s.acc_full[acc], (tcount >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (dec && tcount >= 2) bar_wait(&s.stg_free[tcount & 1], ((tcount >> 1) & 1) ^ 1);
       const int64_t gm = m0 + q * 32 + lane;
       const int64_t row = (int64_t)b * g.scb + gm * g.scm;
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * N + cbeg;
@@ -438,7 +450,25 @@ __global__ void __launch_bounds__(threads<N>(), 1)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) bar_arrive(&s.acc_empty[acc]);
-      if (N == 64 && a.tma_store) {  // whole tile staged -> two TMA stores by one thread
+      if (dec) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) bar_arrive(&s.stg_full[tcount & 1]);
+        if (et == 0) {
+          bar_wait(&s.stg_full[tcount & 1], (tcount >> 1) & 1);
+          const int row0 = (int)(b * g.M + m0);
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                             reinterpret_cast<uint64_t>(&tC)),
+                         "r"(n0 + 32 * h), "r"(row0), "r"(su32(s.cst + (tcount & 1) * (TM * N) + h * TM * 32))
+                         : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          bar_arrive(&s.stg_free[tcount & 1]);
+        }
+        __syncwarp();
+      } else if (N == 64 && a.tma_store) {  // whole tile staged -> two TMA stores by one thread
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("bar.sync 3, %0;" ::"r"(NEPI * 32) : "memory");
         if (et == 0) {
@@ -816,6 +846,10 @@ bool gemm_tc2(const GemmArgs& g, cudaStream_t st, int64_t mfold, cudaError_t* er
   a.total = a.m_tiles * a.n_tiles * g.batch;
   if (a.total == 0) return true;
   if (a.total >= ((int64_t)1 << 31)) return false;  // 32-bit tile arithmetic in the kernel
+  // single-K-chunk tiles (the FNO layer-0 inverse with its rank-2 epilogue) are epilogue-bound and
+  // gain from the decoupled hand-off (496 -> 456 us); the 3-chunk inverse+W tiles measured 611 vs
+  // 620 us with it, so they keep the named barriers
+  a.decouple = a.tma_store && g.K <= KC && !std::getenv("SNOP_TC2_NO_DECOUPLE");
   a.div_n.init((uint32_t)a.n_tiles);
   a.div_mn.init((uint32_t)(a.n_tiles * a.m_tiles));
   // resident B (see stages()): N = 128 tile, one column tile, batch-invariant pre-split B, K <= 64

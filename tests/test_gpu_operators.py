@@ -206,7 +206,8 @@ def test_precondition_fixed_source_deeponet_parity():
 
 
 @pytest.mark.parametrize("env", [{}, {"SNOP_DFT_TC": "0"}, {"SNOP_DFT_TC": "0", "SNOP_DFT_GEMM": "1"},
-                                 {"SNOP_NO_TMA_STORE": "1", "SNOP_NO_PRESPLIT": "1", "SNOP_NO_BRES": "1"}])
+                                 {"SNOP_NO_TMA_STORE": "1", "SNOP_NO_PRESPLIT": "1", "SNOP_NO_BRES": "1"},
+                                 {"SNOP_TC2_NO_DECOUPLE": "1"}])
 def test_fno_width64_kernel_paths(env, monkeypatch):
     """The C5-width FNO runs on dedicated paths (exact-fp32 forward-DFT kernel, register-tiled mixing,
     TMA-store epilogue, resident pre-split weights, tensor-core forward DFT); each against the oracle,
