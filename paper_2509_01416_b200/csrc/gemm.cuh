@@ -178,6 +178,8 @@ cudaError_t gemm_tc(const GemmArgs& g, cudaStream_t st, int64_t mfold = 0);
 // Warp-specialised TMA-fed engine (gemm_tc2.cu) for K-contiguous operands with K <= 128: returns
 // false when the contraction does not fit it (the caller then uses gemm_tc).
 bool gemm_tc2(const GemmArgs& g, cudaStream_t st, int64_t mfold, cudaError_t* err);
+// FNO forward truncated DFT on the tensor core (C = 64, 2M = 32, n % 128 == 0): V [B][n][64] ->
+// Vh MODE-MAJOR [32][B][64] (the layout fno_mix64<true> stages with coalesced rows).
 bool fno_dft_tc(const float* V, const float* F, const float* F_lo, float* Vh, int B, int n, cudaStream_t st,
                 cudaError_t* err);
 

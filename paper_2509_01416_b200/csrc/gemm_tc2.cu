@@ -765,10 +765,9 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
         for (int j = 0; j < 32; ++j) sum[j] += __uint_as_float(v[j]) + __uint_as_float(w[j]);
       }
       const int r = q * 32 + lane, b = 2 * sp + (r >> 6);
-      if (b < B) {
-        float4* dst = reinterpret_cast<float4*>(Vh + ((size_t)b * 64 + (r & 63)) * DFT_NT);
+      if (b < B) {  // mode-major Vh[m'][b][c]: a warp's 32 channels are one contiguous 128-B row
 #pragma unroll
-        for (int j = 0; j < 8; ++j) dst[j] = make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]);
+        for (int j = 0; j < DFT_NT; ++j) Vh[((size_t)j * B + b) * 64 + (r & 63)] = sum[j];
       }
     }
   }

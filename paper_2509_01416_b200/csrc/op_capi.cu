@@ -121,13 +121,17 @@ __global__ void fno_lift(int B, int n, int C, const double* __restrict__ S, cons
 // (three 16-byte shared loads per 32 FFMA). C = 64 (the FNO width) is the tuned shape; other widths
 // use the generic loop below.
 constexpr int MIX_S = 64;
+// MM: Vh is mode-major [2M][B][C] (written so by the tensor-core forward DFT): the staging loads
+// are then contiguous channel rows (consecutive threads -> consecutive channels) instead of one
+// float per 128-B [b][c][2M] row, and Vt gets a padded pitch for the transposed stores.
+template <bool MM>
 __global__ void __launch_bounds__(256) fno_mix64(int B, int M, const float* __restrict__ Vh,
                                                  const float* __restrict__ Rr, const float* __restrict__ Ri,
                                                  float* __restrict__ U) {
-  constexpr int C = 64, C2 = 128;
+  constexpr int C = 64, C2 = 128, VP = MM ? MIX_S + 4 : MIX_S;
   extern __shared__ __align__(16) float smx[];
   float* Mx = smx;             // [2C][2C]
-  float* Vt = smx + C2 * C2;   // [2C][MIX_S]: Vt[k][s]
+  float* Vt = smx + C2 * C2;   // [2C][VP]: Vt[k][s]
   const int m = blockIdx.y, b0 = blockIdx.x * MIX_S, t = threadIdx.x;
   const float* rr = Rr + (size_t)m * C * C;
   const float* ri = Ri + (size_t)m * C * C;
@@ -141,11 +145,18 @@ __global__ void __launch_bounds__(256) fno_mix64(int B, int M, const float* __re
     rb[r] = ri[t + 256 * r];
   }
 #pragma unroll
-  for (int r = 0; r < NV; ++r) {  // consecutive threads -> consecutive samples (conflict-free stores)
-    const int e = t + 256 * r, c = e / MIX_S, b = b0 + (e - c * MIX_S);
-    const float* v = Vh + ((size_t)(b < B ? b : B - 1) * C + c) * 2 * M;
-    va[r] = v[m];
-    vb[r] = v[M + m];
+  for (int r = 0; r < NV; ++r) {
+    if constexpr (MM) {  // consecutive threads -> consecutive channels (coalesced rows)
+      const int e = t + 256 * r, c = e & (C - 1), b = b0 + (e >> 6);
+      const size_t bb = (size_t)(b < B ? b : B - 1);
+      va[r] = Vh[((size_t)m * B + bb) * C + c];
+      vb[r] = Vh[((size_t)(M + m) * B + bb) * C + c];
+    } else {  // consecutive threads -> consecutive samples (conflict-free stores)
+      const int e = t + 256 * r, c = e / MIX_S, b = b0 + (e - c * MIX_S);
+      const float* v = Vh + ((size_t)(b < B ? b : B - 1) * C + c) * 2 * M;
+      va[r] = v[m];
+      vb[r] = v[M + m];
+    }
   }
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
@@ -157,9 +168,10 @@ __global__ void __launch_bounds__(256) fno_mix64(int B, int M, const float* __re
   }
 #pragma unroll
   for (int r = 0; r < NV; ++r) {
-    const int e = t + 256 * r, c = e / MIX_S, sidx = e - c * MIX_S;
-    Vt[c * MIX_S + sidx] = va[r];
-    Vt[(C + c) * MIX_S + sidx] = vb[r];
+    const int e = t + 256 * r;
+    const int c = MM ? (e & (C - 1)) : e / MIX_S, sidx = MM ? (e >> 6) : e - c * MIX_S;
+    Vt[c * VP + sidx] = va[r];
+    Vt[(C + c) * VP + sidx] = vb[r];
   }
   __syncthreads();
   const int sg = t & 15, og = t >> 4;  // samples 4 sg .. 4 sg + 3, outputs 8 og .. 8 og + 7
@@ -170,7 +182,7 @@ __global__ void __launch_bounds__(256) fno_mix64(int B, int M, const float* __re
     for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
 #pragma unroll 4
   for (int k = 0; k < C2; ++k) {
-    const float4 v = *reinterpret_cast<const float4*>(Vt + k * MIX_S + 4 * sg);
+    const float4 v = *reinterpret_cast<const float4*>(Vt + k * VP + 4 * sg);
     const float4 w0 = *reinterpret_cast<const float4*>(Mx + k * C2 + 8 * og);
     const float4 w1 = *reinterpret_cast<const float4*>(Mx + k * C2 + 8 * og + 4);
     const float vv[4] = {v.x, v.y, v.z, v.w};
@@ -628,10 +640,14 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
       SNOP_TRY(gemm(ctx, f));
     }
     // complex channel mixing per retained mode
-    if (C == 64) {
+    if (C == 64 && tc_done) {  // the tensor-core DFT wrote Vh mode-major
+      const size_t sm = (size_t)(128 * 128 + 128 * (MIX_S + 4)) * sizeof(float);
+      cudaFuncSetAttribute(fno_mix64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      fno_mix64<true><<<dim3((B + MIX_S - 1) / MIX_S, M), 256, sm, ctx.stream>>>(B, M, Vh, op.Rr[l], op.Ri[l], U);
+    } else if (C == 64) {
       const size_t sm = (size_t)(128 * 128 + 128 * MIX_S) * sizeof(float);
-      cudaFuncSetAttribute(fno_mix64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      fno_mix64<<<dim3((B + MIX_S - 1) / MIX_S, M), 256, sm, ctx.stream>>>(B, M, Vh, op.Rr[l], op.Ri[l], U);
+      cudaFuncSetAttribute(fno_mix64<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      fno_mix64<false><<<dim3((B + MIX_S - 1) / MIX_S, M), 256, sm, ctx.stream>>>(B, M, Vh, op.Rr[l], op.Ri[l], U);
     } else {
       fno_mix<<<dim3((B + 3) / 4 < 1024 ? (B + 3) / 4 : 1024, M), 4 * C, 2 * C * C * sizeof(float), ctx.stream>>>(
           B, C, M, Vh, op.Rr[l], op.Ri[l], U);
