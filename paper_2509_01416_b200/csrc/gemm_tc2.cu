@@ -37,9 +37,13 @@ constexpr int NWARPS = 14;
 constexpr int CONV0 = 2, NCONV = SNOP_TC2_NCONV, EPI0 = CONV0 + NCONV;
 // epilogue warps: 4 per TMEM lane quarter (column quarters: 16 columns at N = 64, 32 at N = 128).
 // The element-wise epilogue (bias, GELU, row-dot, staging) is the pipeline's bottleneck, so it gets
-// 16 of the 22 warps (80 registers each, no spills); 8 epilogue warps measured 3-6% slower.
+// 16 of the 22 warps (80 registers each, no spills); 8 epilogue warps measured 3-6% slower
+// (N = 64: layer-0 inverse 455 -> 504 us, the 3-chunk inverse+W tiles unchanged at ~620 us).
+#ifndef SNOP_TC2_NEPI64
+#define SNOP_TC2_NEPI64 16
+#endif
 template <int N>
-constexpr int nepi() { return 16; }
+constexpr int nepi() { return N == 64 ? SNOP_TC2_NEPI64 : 16; }
 template <int N>
 constexpr int threads() { return (EPI0 + nepi<N>()) * 32; }
 
