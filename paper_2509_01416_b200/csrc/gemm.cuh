@@ -32,15 +32,57 @@ __device__ __forceinline__ float ex2_ftz(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+// A&S coefficients a_i / sqrt 2, negated (so the last step is a plain fma; -(a b) = (-a) b exactly)
+#define SNOP_GELU_C0 (-7.505269764e-01f)
+#define SNOP_GELU_C1 (1.027533652e+00f)
+#define SNOP_GELU_C2 (-1.005091295e+00f)
+#define SNOP_GELU_C3 (2.011695713e-01f)
+#define SNOP_GELU_C4 (-1.801917326e-01f)
 __device__ __forceinline__ float gelu_f(float x) {
   // GELU = x/2 + |x|/2 erf(z) = max(x, 0) - (|x|/2) t P(t) e^{-z^2}, z = |x|/sqrt 2, and
   // |x|/2 = z / sqrt 2: the factor 1/sqrt 2 is folded into the A&S coefficients (a_i / sqrt 2).
   const float z = fabsf(x) * 0.70710678118654752440f;
   const float t = rcp_ftz(fmaf(0.3275911f, z, 1.0f));
-  const float p =
-      fmaf(fmaf(fmaf(fmaf(7.505269764e-01f, t, -1.027533652e+00f), t, 1.005091295e+00f), t, -2.011695713e-01f), t, 1.801917326e-01f) * t;
+  const float p = fmaf(fmaf(fmaf(fmaf(SNOP_GELU_C0, t, SNOP_GELU_C1), t, SNOP_GELU_C2), t, SNOP_GELU_C3), t, SNOP_GELU_C4) * t;
   const float e = ex2_ftz((z * z) * -1.44269504088896340736f);  // exp(-z^2)
-  return fmaf(-z, p * e, fmaxf(x, 0.0f));
+  return fmaf(z, p * e, fmaxf(x, 0.0f));
+}
+
+// Two GELUs with packed FP32 (fma.rn.f32x2 / mul.rn.f32x2 -> FFMA2 / FMUL2): the same operations
+// in the same order per element as gelu_f (bit-identical results) in ~9 instead of ~13 issue slots
+// per element; the FNO projection epilogue is issue-bound on GELU.
+__device__ __forceinline__ unsigned long long f2_pk(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_upk(unsigned long long r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ void gelu2(float& xa, float& xb) {
+  const unsigned long long z = f2_mul(f2_pk(fabsf(xa), fabsf(xb)), f2_pk(0.70710678118654752440f, 0.70710678118654752440f));
+  float da, db;
+  f2_upk(f2_fma(f2_pk(0.3275911f, 0.3275911f), z, f2_pk(1.0f, 1.0f)), da, db);
+  const unsigned long long t = f2_pk(rcp_ftz(da), rcp_ftz(db));
+  unsigned long long p = f2_fma(f2_pk(SNOP_GELU_C0, SNOP_GELU_C0), t, f2_pk(SNOP_GELU_C1, SNOP_GELU_C1));
+  p = f2_fma(p, t, f2_pk(SNOP_GELU_C2, SNOP_GELU_C2));
+  p = f2_fma(p, t, f2_pk(SNOP_GELU_C3, SNOP_GELU_C3));
+  p = f2_fma(p, t, f2_pk(SNOP_GELU_C4, SNOP_GELU_C4));
+  p = f2_mul(p, t);
+  float ga, gb;
+  f2_upk(f2_mul(f2_mul(z, z), f2_pk(-1.44269504088896340736f, -1.44269504088896340736f)), ga, gb);
+  const unsigned long long e = f2_pk(ex2_ftz(ga), ex2_ftz(gb));
+  f2_upk(f2_fma(z, f2_mul(p, e), f2_pk(fmaxf(xa, 0.0f), fmaxf(xb, 0.0f))), xa, xb);
 }
 
 __device__ __forceinline__ float act_f(float x, int act) {

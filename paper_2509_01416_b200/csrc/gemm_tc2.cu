@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(threads<N>(), 1)
             for (int u = 0; u < 4; ++u) {
               const int j = 4 * j4 + u;
               const float x = fmaf(g.alpha, __uint_as_float(v[j]), bb[u]);
-              o[j] = act_c<ACT>(fmaf(aa[u], rs, fmaf(rr[u], rx, x)));
+              o[j] = fmaf(aa[u], rs, fmaf(rr[u], rx, x));
             }
           }
         } else {
@@ -407,8 +407,15 @@ __global__ void __launch_bounds__(threads<N>(), 1)
             const float4 b4 = bv[j4];
             const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-            for (int u = 0; u < 4; ++u) o[4 * j4 + u] = act_c<ACT>(fmaf(g.alpha, __uint_as_float(v[4 * j4 + u]), bb[u]));
+            for (int u = 0; u < 4; ++u) o[4 * j4 + u] = fmaf(g.alpha, __uint_as_float(v[4 * j4 + u]), bb[u]);
           }
+        }
+        if constexpr (ACT == ACT_GELU) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 2) gelu2(o[j], o[j + 1]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) o[j] = act_c<ACT>(o[j]);
         }
         if (g.rowdot_w) {
           if (full) {
