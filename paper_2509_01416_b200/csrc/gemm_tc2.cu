@@ -407,7 +407,10 @@ __global__ void __launch_bounds__(threads<N>(), 1)
             const float4 b4 = bv[j4];
             const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-            for (int u = 0; u < 4; ++u) o[4 * j4 + u] = fmaf(g.alpha, __uint_as_float(v[4 * j4 + u]), bb[u]);
+            for (int u = 0; u < 4; u += 2)  // packed pairs (same rounding as fmaf per element)
+              f2_upk(f2_fma(f2_pk(g.alpha, g.alpha), f2_pk(__uint_as_float(v[4 * j4 + u]), __uint_as_float(v[4 * j4 + u + 1])),
+                            f2_pk(bb[u], bb[u + 1])),
+                     o[4 * j4 + u], o[4 * j4 + u + 1]);
           }
         }
         if constexpr (ACT == ACT_GELU) {
