@@ -103,6 +103,13 @@ class Context {
   Context(const Context&) = delete;
   Context& operator=(const Context&) = delete;
   snop_ctx* get() const { return ctx_; }
+  // execution options (include/snop_cuda.h snop_ctx_options; zero fields = automatic)
+  snop_ctx_options options() const {
+    snop_ctx_options o{};
+    check(snop_ctx_get_options(ctx_, &o));
+    return o;
+  }
+  void set_options(const snop_ctx_options& o) { check(snop_ctx_set_options(ctx_, &o)); }
 
  private:
   snop_ctx* ctx_ = nullptr;

@@ -109,6 +109,35 @@ const char* snop_last_error(void);
 
 snop_status snop_ctx_create(int32_t device, snop_ctx** out);
 snop_status snop_ctx_destroy(snop_ctx* ctx);
+
+/* Per-context execution options (no process-global state, no environment variables). Every
+ * field's zero value means "automatic" (the measured default); results of a solve never depend on
+ * the execution options except where noted (the kernels are deterministic for a given shape).
+ *   cell_cluster   K1/K2 cell split over a thread-block cluster: 0 auto (one CTA per instance up to
+ *                  4096 cells, the smallest cluster that holds the slab above), 1 never, 2/4/8/16
+ *                  force that cluster size. Instances above 16 * 4096 cells use the streaming
+ *                  multi-CTA path regardless.
+ *   pair_split     single-group eigen pair-split cluster size: 0 auto (8 with the tail split), -1
+ *                  off, 2..8 force.
+ *   pi_tail_cap    outer iterations of the tail split's first phase: 0 auto (48), -1 off (one launch).
+ *   host_chunks    pageable-host pipeline chunk count: 0 auto (4), 1..8.
+ *   gemm_engine    operator contractions: 0 auto (tcgen05 engines), 1 tcgen05 engine v1 only,
+ *                  2 FFMA engine (fp32 cross-check; slow).
+ *   fno_dft        FNO forward truncated DFT of layers >= 1: 0 auto (tcgen05), 1 FFMA kernel.
+ *   fno_mix        FNO spectral channel mixing: 0 auto (tcgen05), 1 FFMA kernel. */
+typedef struct {
+  int32_t cell_cluster;
+  int32_t pair_split;
+  int32_t pi_tail_cap;
+  int32_t host_chunks;
+  int32_t gemm_engine;
+  int32_t fno_dft;
+  int32_t fno_mix;
+  int32_t reserved[9];
+} snop_ctx_options;
+
+snop_status snop_ctx_set_options(snop_ctx* ctx, const snop_ctx_options* options);
+snop_status snop_ctx_get_options(const snop_ctx* ctx, snop_ctx_options* options);
 snop_status snop_ctx_synchronize(snop_ctx* ctx);
 /* Number of snop kernels this context has launched (for the bench's gpu_launches claim). */
 int64_t snop_ctx_launch_count(const snop_ctx* ctx);

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-from ._types import STATUS_NAMES, SnopDatasetInfo, SnopGrfSpec, SnopGrid, SnopModelInfo, SnopSolverConfig
+from ._types import STATUS_NAMES, SnopCtxOptions, SnopDatasetInfo, SnopGrfSpec, SnopGrid, SnopModelInfo, SnopSolverConfig
 from .errors import raise_for_status
 
 PKG = Path(__file__).resolve().parent
@@ -25,7 +25,7 @@ EXPORTS = [
     "snop_precondition_fixed_source", "snop_sp_eigen_batched", "snop_cp_eigen_batched",
     "snop_op_save", "snop_op_load", "snop_model_write_deeponet", "snop_model_write_fno", "snop_model_inspect",
     "snop_grf_sample", "snop_normalize_source", "snop_generate_dataset", "snop_dataset_write", "snop_dataset_read",
-    "snop_source_iteration_leakage_batched", "snop_balance_report",
+    "snop_source_iteration_leakage_batched", "snop_balance_report", "snop_ctx_set_options", "snop_ctx_get_options",
 ]
 
 _lib = None
@@ -54,6 +54,8 @@ def load():
     lib.snop_ctx_launch_count.restype = C.c_int64
     lib.snop_ctx_stream.argtypes = [vp]
     lib.snop_ctx_stream.restype = vp
+    lib.snop_ctx_set_options.argtypes = [vp, C.POINTER(SnopCtxOptions)]
+    lib.snop_ctx_get_options.argtypes = [vp, C.POINTER(SnopCtxOptions)]
     lib.snop_gauss_legendre.argtypes = [i32, vp, vp]
     lib.snop_source_iteration_batched.argtypes = [
         vp, i32, C.POINTER(SnopGrid), i32, i32, vp, vp, vp, vp, C.POINTER(SnopSolverConfig), vp, vp, vp, vp, vp]

@@ -54,6 +54,12 @@ class SnopDatasetInfo(C.Structure):
                 ("tolerance", C.c_double)]
 
 
+class SnopCtxOptions(C.Structure):
+    _fields_ = [("cell_cluster", C.c_int32), ("pair_split", C.c_int32), ("pi_tail_cap", C.c_int32),
+                ("host_chunks", C.c_int32), ("gemm_engine", C.c_int32), ("fno_dft", C.c_int32),
+                ("fno_mix", C.c_int32), ("reserved", C.c_int32 * 9)]
+
+
 def make_grid(length: float, n_cells: int) -> SnopGrid:
     return SnopGrid(float(length), int(n_cells), 0)
 

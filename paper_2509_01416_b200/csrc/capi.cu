@@ -41,6 +41,7 @@ Ctx* Ctx::sub(size_t i) {
     if (!c) return nullptr;
     c->device = device;
     c->sm_count = sm_count;
+    c->opt = opt;
     // later sub-contexts get higher stream priority: in the chunked host pipeline the last chunk's
     // data arrives last, so its CTAs must be dispatched ahead of earlier chunks' remaining ones
     int least = 0, greatest = 0;
@@ -140,7 +141,7 @@ snop_status invalid(const std::string& m) {
 snop_status check_grid(const snop_grid* g, int order) {
   if (!g) return invalid("grid is NULL");
   if (!(g->length_cm > 0.0) || g->n_cells < 1) return invalid("grid: length and n_cells must be positive");
-  if (g->n_cells > kMaxCells) return invalid("grid: n_cells > 4096 exceeds the per-CTA sweep limit");
+  if (g->n_cells > kMaxCells) return invalid("grid: n_cells exceeds the cluster sweep limit (16384)");
   if (order < 2 || order > 128 || order % 2) return invalid("quadrature order must be even in [2,128]");
   return SNOP_OK;
 }
@@ -287,6 +288,29 @@ snop_status snop_ctx_synchronize(snop_ctx* ctx) {
   return drain_flags(*ctx);
 }
 
+snop_status snop_ctx_set_options(snop_ctx* ctx, const snop_ctx_options* o) {
+  if (!ctx || !o) return invalid("ctx/options is NULL");
+  const int cc = o->cell_cluster;
+  if (!(cc == 0 || cc == 1 || cc == 2 || cc == 4 || cc == 8 || cc == 16))
+    return invalid("options: cell_cluster must be 0, 1, 2, 4, 8 or 16");
+  if (o->pair_split < -1 || o->pair_split > 8 || o->pair_split == 1)
+    return invalid("options: pair_split must be -1, 0 or 2..8");
+  if (o->pi_tail_cap < -1) return invalid("options: pi_tail_cap must be >= -1");
+  if (o->host_chunks < 0 || o->host_chunks > 8) return invalid("options: host_chunks must be in [0, 8]");
+  if (o->gemm_engine < 0 || o->gemm_engine > 2) return invalid("options: gemm_engine must be 0, 1 or 2");
+  if (o->fno_dft < 0 || o->fno_dft > 1 || o->fno_mix < 0 || o->fno_mix > 1)
+    return invalid("options: fno_dft / fno_mix must be 0 or 1");
+  ctx->opt = *o;
+  for (Ctx* s : ctx->subs) s->opt = *o;
+  return SNOP_OK;
+}
+
+snop_status snop_ctx_get_options(const snop_ctx* ctx, snop_ctx_options* o) {
+  if (!ctx || !o) return invalid("ctx/options is NULL");
+  *o = ctx->opt;
+  return SNOP_OK;
+}
+
 int64_t snop_ctx_launch_count(const snop_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
 
 void* snop_ctx_stream(snop_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
@@ -306,11 +330,7 @@ static snop_status si_host_pipelined(Ctx& ctx, const snop_grid& grid, int order,
                                      const snop_solver_config& cfg, const double* initial_phi, double* phi_out,
                                      double* current_out, int32_t* iterations, uint8_t* converged,
                                      double* leakage_out) {
-  static const int NCH = [] {  // experiment override: SNOP_HOST_CHUNKS (1..8)
-    const char* e = std::getenv("SNOP_HOST_CHUNKS");
-    const int v = e ? std::atoi(e) : 4;
-    return v < 1 ? 1 : (v > 8 ? 8 : v);
-  }();
+  const int NCH = ctx.opt.host_chunks > 0 ? std::min(ctx.opt.host_chunks, 8) : 4;
   const size_t Nc = grid.n_cells, n = (size_t)batch * Nc;
   auto dbuf = [&](size_t i, size_t count) { return static_cast<double*>(ctx.slot(i, count * sizeof(double))); };
   double* st = dbuf(0, n);
@@ -405,7 +425,8 @@ static snop_status si_entry(snop_ctx* ctx, int32_t memspace, const snop_grid* gr
                                    initial_phi, phi_out, current_out, iterations, converged, leakage_out);
   }
   if (memspace != SNOP_MEM_HOST) return invalid("memspace must be HOST(0) or DEVICE(1)");
-  if (!current_out && pinned(sigma_t) && pinned(sigma_s0) && pinned(source) && (!sigma_s1 || pinned(sigma_s1)) &&
+  const bool one_cta = grid->n_cells <= kMaxCtaCells && ctx->opt.cell_cluster <= 1;
+  if (one_cta && !current_out && pinned(sigma_t) && pinned(sigma_s0) && pinned(source) && (!sigma_s1 || pinned(sigma_s1)) &&
       (!initial_phi || pinned(initial_phi)) && pinned(phi_out) && pinned(iterations) && pinned(converged) &&
       (!leakage_out || pinned(leakage_out))) {
     // zero-copy: the kernel reads its instance's inputs over the bus and writes its results back

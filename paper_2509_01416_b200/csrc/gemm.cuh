@@ -8,8 +8,31 @@
 
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <mutex>
 
 namespace snop_ops {
+
+// One-time per-device launch setup (kernel attributes) and the device's SM count, thread-safe: a
+// second context on another device in the same process gets its own entry.
+constexpr int kMaxDevices = 64;
+struct DeviceOnce {
+  std::once_flag flag[kMaxDevices];
+  cudaError_t err[kMaxDevices] = {};
+  int sms[kMaxDevices] = {};
+};
+template <class F>
+inline cudaError_t device_once(DeviceOnce& d, int* sms, F&& setup) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  std::call_once(d.flag[dev], [&] {
+    d.err[dev] = setup();
+    if (cudaDeviceGetAttribute(&d.sms[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) d.sms[dev] = 1;
+  });
+  *sms = d.sms[dev] > 0 ? d.sms[dev] : 1;
+  return d.err[dev];
+}
 
 enum Act : int { ACT_RELU = 0, ACT_TANH = 1, ACT_GELU = 2, ACT_NONE = 3 };
 

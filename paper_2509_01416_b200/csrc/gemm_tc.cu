@@ -453,17 +453,12 @@ __global__ void __launch_bounds__(THREADS, (N <= 64 ? (SPLIT ? 2 : 4) : 1))
 template <int N, bool SPLIT>
 cudaError_t launch(const GemmArgs& g, int64_t mfold, cudaStream_t st) {
   const size_t smem = sizeof(Smem<N, stages<SPLIT>()>);
-  static bool attr = false;
-  static int sms = 148;
-  if (!attr) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(gemm_tc_kernel<N, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    attr = true;
-  }
+  static DeviceOnce once;
+  int sms = 1;
+  const cudaError_t e = device_once(once, &sms, [&] {
+    return cudaFuncSetAttribute(gemm_tc_kernel<N, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (e != cudaSuccess) return e;
   const int64_t m_tiles = (g.M + TM - 1) / TM;
   const int64_t n_tiles = (g.N + N - 1) / N;
   const int64_t total = m_tiles * n_tiles * (mfold > 0 ? 1 : g.batch);

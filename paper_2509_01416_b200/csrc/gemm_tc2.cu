@@ -550,17 +550,12 @@ bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int
 template <int N, int ACT, bool BR = false>
 cudaError_t launch(const Args& a, const CUtensorMap* maps, cudaStream_t st) {
   const size_t smem = sizeof(Smem<N, BR>) + 1024;  // + alignment slack
-  static bool attr = false;
-  static int sms = 148;
-  if (!attr) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(gemm_tc2_kernel<N, ACT, BR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    attr = true;
-  }
+  static DeviceOnce once;
+  int sms = 1;
+  const cudaError_t e = device_once(once, &sms, [&] {
+    return cudaFuncSetAttribute(gemm_tc2_kernel<N, ACT, BR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (e != cudaSuccess) return e;
   const int64_t grid = a.total < sms ? a.total : sms;
   gemm_tc2_kernel<N, ACT, BR><<<(unsigned)grid, threads<N>(), smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4],
                                                                       maps[5], maps[6], maps[7], maps[8], a);
@@ -796,7 +791,6 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
 bool gemm_tc2(const GemmArgs& g, cudaStream_t st, int64_t mfold, cudaError_t* err) {
   using namespace tc2;
   *err = cudaSuccess;
-  if (std::getenv("SNOP_GEMM_V1")) return false;
   if (mfold > 0 || g.beta != 0.f || g.K > 128 || g.N > 128 || g.sak != 1 || g.sbk != 1) return false;
   if (g.ksplit > 0 && (g.ksplit % KC != 0 || g.sak2 != 1 || g.sbk2 != 1)) return false;
   if (g.rowdot_w && g.N > 128) return false;
@@ -836,13 +830,12 @@ bool gemm_tc2(const GemmArgs& g, cudaStream_t st, int64_t mfold, cudaError_t* er
   if (!a.b1_pre) maps[6] = maps[2];
   if (!a.a2_pre) maps[5] = maps[1];
   if (!a.b2_pre) maps[7] = maps[3];
-  if (std::getenv("SNOP_NO_PRESPLIT")) a.a1_pre = a.a2_pre = a.b1_pre = a.b2_pre = 0;
   // TMA-store epilogue: N = 64 fp32 output, unit column stride, whole 128-row tiles per sample and
   // samples contiguous (row b*M + m), no row-dot; C viewed as [batch*M][N] with row stride scm
   a.tma_store = 0;
   maps[8] = maps[0];
   if (NT == 64 && g.N == 64 && g.C && !g.Cd && !g.rowdot_w && g.scn == 1 && g.M % TM == 0 &&
-      (g.batch == 1 || g.scb == (int64_t)g.M * g.scm) && SNOP_TC2_CST && !std::getenv("SNOP_NO_TMA_STORE")) {
+      (g.batch == 1 || g.scb == (int64_t)g.M * g.scm) && SNOP_TC2_CST) {
     EncodeFn enc = encoder();
     const cuuint64_t dims[2] = {(cuuint64_t)g.N, (cuuint64_t)((int64_t)g.batch * g.M)};
     const cuuint64_t strides[1] = {(cuuint64_t)(g.scm * 4)};
@@ -862,12 +855,12 @@ bool gemm_tc2(const GemmArgs& g, cudaStream_t st, int64_t mfold, cudaError_t* er
   // single-K-chunk tiles (the FNO layer-0 inverse with its rank-2 epilogue) are epilogue-bound and
   // gain from the decoupled hand-off (496 -> 456 us); the 3-chunk inverse+W tiles measured 611 vs
   // 620 us with it, so they keep the named barriers
-  a.decouple = a.tma_store && g.K <= KC && !std::getenv("SNOP_TC2_NO_DECOUPLE");
+  a.decouple = a.tma_store && g.K <= KC;
   a.div_n.init((uint32_t)a.n_tiles);
   a.div_mn.init((uint32_t)(a.n_tiles * a.m_tiles));
   // resident B (see stages()): N = 128 tile, one column tile, batch-invariant pre-split B, K <= 64
   const bool bres = NT == 128 && a.n_tiles == 1 && g.ksplit == 0 && g.sbb == 0 && a.b1_pre &&
-                    (g.K + KC - 1) / KC <= BR_CHUNKS && !std::getenv("SNOP_NO_BRES");
+                    (g.K + KC - 1) / KC <= BR_CHUNKS;
   switch (g.act) {
     case ACT_RELU: *err = NT == 64 ? launch<64, ACT_RELU>(a, maps, st) : launch<128, ACT_RELU>(a, maps, st); break;
     case ACT_TANH: *err = NT == 64 ? launch<64, ACT_TANH>(a, maps, st) : launch<128, ACT_TANH>(a, maps, st); break;
@@ -902,13 +895,12 @@ bool fno_dft_tc(const float* V, const float* F, const float* F_lo, float* Vh, in
   if (!make_map(&mf, F, 32, n, n, 32) || !make_map(&mfl, F_lo, 32, n, n, 32)) return false;
   const int npairs = (B + 1) / 2;
   const size_t smem = sizeof(DftTcSmem) + 1024;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(dft_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  }
+  static DeviceOnce once;
+  int sms = 1;
+  *err = device_once(once, &sms, [&] {
+    return cudaFuncSetAttribute(dft_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (*err != cudaSuccess) return true;
   const int grid = npairs < sms ? npairs : sms;
   dft_tc_kernel<<<grid, DFT_THREADS, smem, st>>>(mv, mf, mfl, Vh, B, n, npairs);
   *err = cudaGetLastError();

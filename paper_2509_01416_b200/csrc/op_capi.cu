@@ -475,21 +475,15 @@ unsigned grid_for(const Ctx& c, size_t n, int threads = 256) {
   return (unsigned)(blocks ? blocks : 1);
 }
 
-// Dense contractions run on the tcgen05 3xTF32 engine (gemm_tc.cu); SNOP_GEMM=ffma selects the
-// FFMA engine (cross-check / fallback for debugging only).
-bool use_tc() {
-  static const bool tc = [] {
-    const char* e = std::getenv("SNOP_GEMM");
-    return !(e && std::string(e) == "ffma");
-  }();
-  return tc;
-}
+// Dense contractions run on the tcgen05 3xTF32 engines (gemm_tc2.cu, gemm_tc.cu);
+// ctx.opt.gemm_engine = 2 selects the FFMA engine (cross-check only), 1 the tcgen05 engine v1 only.
+bool use_tc(const Ctx& ctx) { return ctx.opt.gemm_engine != 2; }
 
 snop_status gemm(Ctx& ctx, const GemmArgs& a, int64_t mfold = 0) {
   ctx.launches++;
-  if (use_tc()) {
+  if (use_tc(ctx)) {
     cudaError_t e = cudaSuccess;
-    if (gemm_tc2(a, ctx.stream, mfold, &e)) return cuda_status("gemm_tc2", e);
+    if (ctx.opt.gemm_engine == 0 && gemm_tc2(a, ctx.stream, mfold, &e)) return cuda_status("gemm_tc2", e);
     return cuda_status("gemm_tc", gemm_tc(a, ctx.stream, mfold));
   }
   if (mfold > 0) return invalid("batch-folded GEMM requires the tensor-core engine");
@@ -582,9 +576,9 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
   float* Vh = static_cast<float*>(ctx.slot(47, (size_t)B * C * 2 * M * sizeof(float)));
   float* U = static_cast<float*>(ctx.slot(48, (size_t)B * C * 2 * M * sizeof(float)));
   if (!V || !Vn || !Vh || !U) return cuda_status("FNO workspace", cudaErrorMemoryAllocation);
-  const bool tc_fused = use_tc() && (2 * M) % 32 == 0;
+  const bool tc_fused = use_tc(ctx) && (2 * M) % 32 == 0;
   // layer 0 without materialising the lifted field (TMA engine with the rank-2 epilogue)
-  const bool l0 = tc_fused && op.layers >= 1 && op.l0_P && 2 * M <= 128 && C <= 128 && !std::getenv("SNOP_GEMM_V1");
+  const bool l0 = tc_fused && op.layers >= 1 && op.l0_P && 2 * M <= 128 && C <= 128 && ctx.opt.gemm_engine == 0;
   if (l0) {
     cast_f64_to_f32<<<grid_for(ctx, rowsN), 256, 0, ctx.stream>>>(rowsN, in, X);
     ctx.launches++;
@@ -616,8 +610,7 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
     f.C = Vh; f.scm = 2 * M; f.scn = 1; f.scb = (int64_t)C * 2 * M;
     f.alpha = 1.f; f.act = ACT_NONE;
     bool tc_done = false;
-    const char* dft_tc_env = std::getenv("SNOP_DFT_TC");  // default on; "0" selects the FFMA kernel
-    if (C == 64 && 2 * M == 32 && n % 128 == 0 && use_tc() && !(dft_tc_env && dft_tc_env[0] == '0')) {
+    if (C == 64 && 2 * M == 32 && n % 128 == 0 && use_tc(ctx) && ctx.opt.fno_dft == 0) {
       cudaError_t e = cudaSuccess;
       if (fno_dft_tc(V, op.F, op.F_lo, Vh, B, n, ctx.stream, &e)) {
         SNOP_TRY(cuda_status("fno_dft_tc", e));
@@ -626,13 +619,13 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
       }
     }
     if (tc_done) {
-    } else if (C == 64 && 2 * M == 32 && n % DFT_ROWS == 0 && op.FT && !std::getenv("SNOP_DFT_GEMM")) {
+    } else if (C == 64 && 2 * M == 32 && n % DFT_ROWS == 0 && op.FT) {
       const size_t sm = DFT_ST * sizeof(DftStage) + 2 * DFT_ST * sizeof(uint64_t);
       cudaFuncSetAttribute(fno_dft64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       fno_dft64<<<(B + DFT_S - 1) / DFT_S, 32 * DFT_S, sm, ctx.stream>>>(B, n, V, op.FT, Vh);
       ctx.launches++;
       SNOP_TRY(cuda_status("fno_dft64", cudaGetLastError()));
-    } else if (use_tc()) {
+    } else if (use_tc(ctx)) {
       f.M = B * C;
       f.batch = 1;
       SNOP_TRY(gemm(ctx, f, C));
@@ -687,7 +680,7 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
   }
   // projection 64 -> hidden (act) -> 1. Tensor-core engine: one GEMM whose epilogue does the
   // second layer as a row-dot (no hidden tensor in HBM); FFMA engine: chunked GEMM + rowdot.
-  if (use_tc() && H <= 128) {
+  if (use_tc(ctx) && H <= 128) {
     GemmArgs pj = rowmajor((int)rowsN, H, C, V, C, op.P1W, C, nullptr, 1, op.P1b, op.act);
     pj.B_lo = op.P1W_lo;
     pj.scm = 1;

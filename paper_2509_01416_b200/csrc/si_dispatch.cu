@@ -32,21 +32,20 @@ struct Shape {
   int cs, nt;
 };
 
-// Cluster size: one CTA per instance by default. Spreading an instance over a thread-block
-// cluster (cells split across SMs, joined through DSMEM) is correct but measured slower on every
-// BASELINE config (C2-C5, DESIGN.md §K1 "clusters"): the per-pair-group cluster barrier costs more
-// than the split saves. SNOP_CLUSTER=2|4|8 selects it explicitly.
-Shape pick_shape(int n_cells, int batch, int sm_count) {
-  (void)batch;
-  (void)sm_count;
+// Cluster size: one CTA per instance whenever the slab fits one CTA (<= 4096 cells). Spreading an
+// instance over a thread-block cluster (cells split across SMs, joined through DSMEM) is correct
+// but measured slower on every BASELINE config (C2-C5, DESIGN.md §K1 "clusters"): the
+// per-pair-group cluster barrier costs more than the split saves. Above 4096 cells the smallest
+// cluster that holds the slab is used (up to 8 CTAs x 256 threads x K cells = 16384 cells).
+// ctx.opt.cell_cluster = 1 / 2 / 4 / 8 forces a size (1 = never split).
+Shape pick_shape(const snop_impl::Ctx& ctx, int n_cells) {
   int cs = 1;
-  if (const char* e = std::getenv("SNOP_CLUSTER")) {
-    const int v = std::atoi(e);
-    cs = (v == 2 || v == 4 || v == 8) ? v : 1;
-  }
-  const int per_cta = (n_cells + cs - 1) / cs;
-  int nt = pow2_at_least((per_cta + K - 1) / K, 32);
-  if (cs > 1 && nt > 256) {  // clusters are instantiated up to NT = 256
+  const int force = ctx.opt.cell_cluster;
+  if (force == 2 || force == 4 || force == 8) cs = force;
+  int nt = pow2_at_least(((n_cells + cs - 1) / cs + K - 1) / K, 32);
+  if (force != 1 && (nt > 512 || (cs > 1 && nt > 256))) {  // clusters are instantiated up to NT = 256
+    if (cs == 1) cs = 2;
+    nt = pow2_at_least(((n_cells + cs - 1) / cs + K - 1) / K, 32);
     while (cs < 8 && nt > 256) {
       cs <<= 1;
       nt = pow2_at_least(((n_cells + cs - 1) / cs + K - 1) / K, 32);
@@ -76,9 +75,9 @@ snop_status launch_source_iteration(Ctx& ctx, const snop_grid& g, int order, int
   if (batch == 0) return SNOP_OK;
   const SweepConsts sc = make_consts(g, order);
   const SolveConfig c = inner_cfg(cfg);
-  const Shape s = pick_shape(g.n_cells, batch, ctx.sm_count);
+  const Shape s = pick_shape(ctx, g.n_cells);
   if (stage && s.cs > 1) {
-    set_error("host-resident inputs need the one-CTA-per-instance kernel (unset SNOP_CLUSTER)");
+    set_error("host-resident inputs need the one-CTA-per-instance kernel");
     return SNOP_INVALID_ARGUMENT;
   }
 #define SNOP_SI(NN, CC)                       \
@@ -88,7 +87,7 @@ snop_status launch_source_iteration(Ctx& ctx, const snop_grid& g, int order, int
   SNOP_SI(32, false) SNOP_SI(64, false) SNOP_SI(128, false) SNOP_SI(256, false) SNOP_SI(512, false)
   SNOP_SI(32, true) SNOP_SI(64, true) SNOP_SI(128, true) SNOP_SI(256, true)
 #undef SNOP_SI
-  set_error("n_cells exceeds the register-resident sweep limit (4096 per instance)");
+  set_error("n_cells exceeds the cluster sweep limit (16384 per instance)");
   return SNOP_INVALID_ARGUMENT;
 }
 
@@ -105,7 +104,7 @@ snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int 
   ep.tol_phi = cfg.tolerance_phi;
   ep.max_outer = cfg.max_outer;
   ep.norm = cfg.norm;
-  const Shape s = pick_shape(g.n_cells, batch, ctx.sm_count);
+  const Shape s = pick_shape(ctx, g.n_cells);
   // Pair-split clusters (si_solve PS): a single-group eigen solve is one long chain of dependent
   // sweeps and a batch finishes with its slowest instance, so the sweep of one instance is spread
   // over cs CTAs (measured on C3, slowest instance alone: 320 ms on one CTA, 153 ms at cs = 4,
@@ -113,13 +112,12 @@ snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int 
   // (361 -> 275 ms; at cs = 8 the batch becomes throughput-bound). Multigroup solves spend their time in the outer
   // loop, which every CTA of a cluster repeats, so they stay on one CTA (C4: 37 vs 49 ms). The
   // rule depends on (G, order) only, never on the batch, so an instance's result does not depend
-  // on what it is batched with. SNOP_PS=0 disables it, SNOP_PS=n sets the cluster size (<= 8).
-  int cap = 48;  // tail split, see below
-  if (const char* e = std::getenv("SNOP_PI_SPLIT")) cap = std::atoi(e);
+  // on what it is batched with. ctx.opt.pair_split = -1 disables it, n sets the cluster size (<= 8).
+  const int cap = ctx.opt.pi_tail_cap == 0 ? 48 : (ctx.opt.pi_tail_cap < 0 ? 0 : ctx.opt.pi_tail_cap);  // tail split
   int ps = 0;
   if (!ss1 && s.cs == 1) {
     int want = G == 1 ? (cap > 0 ? 8 : 4) : 0;
-    if (const char* e = std::getenv("SNOP_PS")) want = std::atoi(e);
+    if (ctx.opt.pair_split != 0) want = ctx.opt.pair_split < 0 ? 0 : ctx.opt.pair_split;
     ps = std::min(std::min(want, 8), (order / 2) / 2);
     if (ps < 2 || (s.nt % ps) != 0) ps = 0;
   }
@@ -127,7 +125,7 @@ snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int 
   // longest instances (C3: outer counts 17 ... 1303). Phase 1 runs every instance on one CTA for at
   // most `cap` outer iterations; phase 2 continues the unconverged ones from their (k, phi, counts)
   // on pair-split clusters, so the long tails get cs SMs each once the bulk has drained. The cap is a
-  // constant (SNOP_PI_SPLIT, default 48; 0 disables), so an instance's result depends on its own data
+  // constant (ctx.opt.pi_tail_cap, default 48; -1 disables), so an instance's result depends on its own data
   // only.
   if (ps && cap > 0 && cfg.max_outer > cap) {
     EigenParams e1 = ep, e2 = ep;
@@ -167,7 +165,7 @@ snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int 
   SNOP_PI(32, false) SNOP_PI(64, false) SNOP_PI(128, false) SNOP_PI(256, false) SNOP_PI(512, false)
   SNOP_PI(32, true) SNOP_PI(64, true) SNOP_PI(128, true) SNOP_PI(256, true)
 #undef SNOP_PI
-  set_error("n_cells exceeds the register-resident sweep limit (4096 per instance)");
+  set_error("n_cells exceeds the cluster sweep limit (16384 per instance)");
   return SNOP_INVALID_ARGUMENT;
 }
 

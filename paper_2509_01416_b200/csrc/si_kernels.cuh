@@ -251,12 +251,14 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
     reduce2<NT, CL>(s, dummy, false, sm.red2, sm.cred2, rphase++, sm);
     return s * sc.dx;
   };
+  int64_t inner_total = 0;
+  int outer = 0;
   auto fail = [&](int flag) {
     if (t == 0 && rank == 0) {
       atomicOr(flags, flag);
       k_g[b] = __longlong_as_double(0x7ff8000000000000ll);
-      outer_g[b] = 0;
-      inner_g[b] = 0;
+      outer_g[b] = outer0 + outer;  // counts so far (a resumed phase keeps the earlier phase's)
+      inner_g[b] = inner0 + inner_total;
       conv_g[b] = 0;
     }
     if constexpr (CL) cl_sync();  // no CTA of the cluster leaves while others may read its smem
@@ -265,20 +267,20 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
     fail(snop_impl::FLAG_BAD_SIGMA_T);
     return;
   }
-  double F = fission_integral();
-  if (!(F != 0.0) || !isfinite(F)) {
-    fail(snop_impl::FLAG_DEGENERATE);
-    return;
-  }
-  for (int g = 0; g < G; ++g)
+  if (!resume) {  // a resumed phase continues from the already normalised flux of the earlier phase
+    const double F = fission_integral();
+    if (!(F != 0.0) || !isfinite(F)) {
+      fail(snop_impl::FLAG_DEGENERATE);
+      return;
+    }
+    for (int g = 0; g < G; ++g)
 #pragma unroll
-    for (int r = 0; r < K; ++r)
-      if (cc(r) < Nc) phi_b[(size_t)g * Nc + cc(r)] /= F;
+      for (int r = 0; r < K; ++r)
+        if (cc(r) < Nc) phi_b[(size_t)g * Nc + cc(r)] /= F;
+  }
   // coalesced-mapped writes above -> owner-mapped reads of the first group's staging below
   __syncthreads();
 
-  int64_t inner_total = 0;
-  int outer = 0;
   bool converged = false;
   SNOP_TSTAMP(tpi0);
   while (outer < ep.max_outer) {

@@ -24,6 +24,7 @@ struct DevBuf {
 };
 
 struct Ctx {
+  snop_ctx_options opt{};  // execution options (snop_ctx_set_options); zero = automatic
   int device = 0;
   cudaStream_t stream = nullptr;
   int* d_flags = nullptr;
@@ -66,8 +67,9 @@ snop_status launch_balance(Ctx& ctx, const snop_grid& g, int batch, const double
 snop_status launch_recast(Ctx& ctx, size_t n, const double* S, const double* phi, const double* st,
                           const double* ss, double tstar, double sstar, double* out);
 
-// Largest n_cells the register-resident CTA sweep supports.
-constexpr int kMaxCells = 4096;
+// Largest n_cells one CTA's register-resident sweep holds, and the largest a cluster holds.
+constexpr int kMaxCtaCells = 4096;
+constexpr int kMaxCells = 16384;
 
 }  // namespace snop_impl
 

@@ -26,7 +26,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _capi
-from ._types import SnopDatasetInfo, SnopGrfSpec, SnopGrid, SnopModelInfo, SnopSolverConfig, make_grid
+from ._types import SnopCtxOptions, SnopDatasetInfo, SnopGrfSpec, SnopGrid, SnopModelInfo, SnopSolverConfig, make_grid
 
 VACUUM, REFLECTIVE = 0, 1
 REL_LINF, REL_L2 = 0, 1
@@ -111,6 +111,24 @@ class Context:
     def synchronize(self):
         _capi.check(self._lib.snop_ctx_synchronize(self.h))
 
+    OPTION_NAMES = ("cell_cluster", "pair_split", "pi_tail_cap", "host_chunks", "gemm_engine", "fno_dft", "fno_mix")
+
+    def options(self) -> dict:
+        """Execution options of this context (snop_ctx_options, include/snop_cuda.h); 0 = automatic."""
+        o = SnopCtxOptions()
+        _capi.check(self._lib.snop_ctx_get_options(self.h, C.byref(o)))
+        return {k: int(getattr(o, k)) for k in self.OPTION_NAMES}
+
+    def set_options(self, **kw) -> dict:
+        """Update execution options (unknown names raise); returns the previous options."""
+        prev = self.options()
+        bad = set(kw) - set(self.OPTION_NAMES)
+        if bad:
+            raise ValueError(f"unknown context options {sorted(bad)}")
+        o = SnopCtxOptions(**{**prev, **{k: int(v) for k, v in kw.items()}})
+        _capi.check(self._lib.snop_ctx_set_options(self.h, C.byref(o)))
+        return prev
+
     @property
     def launch_count(self) -> int:
         return int(self._lib.snop_ctx_launch_count(self.h))
@@ -145,6 +163,20 @@ class _Args:
             raise ValueError("mix of host (numpy) and device (torch CUDA) arrays in one call")
         self.device = bool(dev) and all(dev)
         self.keep = []
+        self.outs = []
+
+    def ready(self, ctx: "Context") -> None:
+        """Device calls: order the context's stream after torch's current stream (the producers of
+        the inputs, including the dtype/contiguity conversions made here), and tell torch's caching
+        allocator that every tensor of the call is in use on the context's stream, so temporaries
+        freed when this function returns are not reused before the kernels that read them finish."""
+        if not self.device:
+            return
+        import torch
+        ext = torch.cuda.ExternalStream(ctx.stream_ptr)
+        ext.wait_stream(torch.cuda.current_stream())
+        for t in self.keep + self.outs:
+            t.record_stream(ext)
 
     @property
     def memspace(self) -> int:
@@ -179,6 +211,7 @@ class _Args:
                 tdt = {np.float64: torch.float64, np.int32: torch.int32, np.uint8: torch.uint8}[dtype]
                 ok = into.dtype == tdt and into.is_contiguous() and tuple(into.shape) == tuple(shape)
                 ptr = into.data_ptr()
+                self.outs.append(into)
             else:
                 ok = into.dtype == dtype and into.flags.c_contiguous and into.shape == tuple(shape)
                 ptr = into.ctypes.data
@@ -190,6 +223,7 @@ class _Args:
             tdt = {np.float64: torch.float64, np.float32: torch.float32, np.int32: torch.int32,
                    np.int64: torch.int64, np.uint8: torch.uint8}[dtype]
             t = torch.empty(shape, dtype=tdt, device="cuda")
+            self.outs.append(t)
             return t, t.data_ptr()
         a = np.empty(shape, dtype=dtype)
         return a, a.ctypes.data
@@ -225,6 +259,7 @@ def source_iteration(grid: Grid1D, order: int, sigma_t, sigma_s0, source, config
     it, it_p = a.out((B,), np.int32, into=o_it)
     cv, cv_p = a.out((B,), np.uint8, into=o_cv)
     g, cfg = grid.c(), config.c()
+    a.ready(ctx)
     if want_leakage:
         lk, lk_p = a.out((B, 2))
         _capi.check(ctx._lib.snop_source_iteration_leakage_batched(
@@ -249,6 +284,7 @@ def balance_report(grid: Grid1D, sigma_t, sigma_s0_out, source, phi, leakage, ct
     lk = a.inp(leakage, shape=(B, 2))
     res, res_p = a.out((B,))
     g = grid.c()
+    a.ready(ctx)
     _capi.check(ctx._lib.snop_balance_report(ctx.h, a.memspace, C.byref(g), B, st, ss, S, p, lk, res_p))
     if a.device:
         ctx.synchronize()
@@ -290,6 +326,7 @@ def power_iteration(grid: Grid1D, order: int, sigma_t, sigma_s0, nu_sigma_f, chi
     inner, i_p = a.out((B,), np.int64)
     cv, cv_p = a.out((B,), np.uint8)
     g, cfg = grid.c(), config.c()
+    a.ready(ctx)
     _capi.check(ctx._lib.snop_power_iteration_batched(ctx.h, a.memspace, C.byref(g), int(order), B, G, st, ss, s1,
                                                       nsf, ch, C.byref(cfg), k0, p0, k_p, phi_p, o_p, i_p, cv_p))
     if a.device and sync:
@@ -304,6 +341,7 @@ def recast_source(source, phi, sigma_t, sigma_s0, reference_params=(1.0, 0.5), c
     B, n = (int(x) for x in source.shape)
     s, p, st, ss = (a.inp(x, shape=(B, n)) for x in (source, phi, sigma_t, sigma_s0))
     out, out_p = a.out((B, n))
+    a.ready(ctx)
     _capi.check(ctx._lib.snop_recast_source(ctx.h, a.memspace, B, n, s, p, st, ss, float(reference_params[0]),
                                             float(reference_params[1]), out_p))
     if a.device:
@@ -392,6 +430,7 @@ class SolutionOperator:
         n = self.grid.n_cells
         s = a.inp(source, shape=(B, n))
         out, out_p = a.out((B, n))
+        a.ready(self.ctx)
         _capi.check(self.ctx._lib.snop_op_predict(self.ctx.h, self.h, a.memspace, B, s, out_p))
         if a.device and sync:
             self.ctx.synchronize()
@@ -416,6 +455,7 @@ def recast_fixed_point(op: SolutionOperator, source, sigma_t, sigma_s0, toleranc
     phi, phi_p = a.out((B, n))
     it, it_p = a.out((B,), np.int32)
     stt, st_p = a.out((B,), np.int32)
+    a.ready(op.ctx)
     _capi.check(op.ctx._lib.snop_recast_fixed_point(op.ctx.h, op.h, a.memspace, B, S, st, ss, float(tolerance),
                                                     int(max_iterations), int(norm), p0, phi_p, it_p, st_p))
     if a.device:
@@ -448,6 +488,7 @@ def precondition_fixed_source(op: SolutionOperator, order: int, sigma_t, sigma_s
     rit, rit_p = a.out((B,), np.int32)
     cv, cv_p = a.out((B,), np.uint8)
     cfg = config.c()
+    a.ready(op.ctx)
     _capi.check(op.ctx._lib.snop_precondition_fixed_source(
         op.ctx.h, op.h, a.memspace, int(order), B, st, ss, s1, S, float(recast_tolerance), int(recast_max_iterations),
         C.byref(cfg), phi_p, pit_p, rst_p, rit_p, cv_p))
@@ -493,6 +534,7 @@ def _hybrid_eigen(fn: str, op: SolutionOperator, order: int, sigma_t, sigma_s0, 
     cv, cv_p = a.out((B,), np.uint8)
     fb, fb_p = a.out((B,), np.uint8)
     cfg = config.c()
+    a.ready(op.ctx)
     _capi.check(getattr(op.ctx._lib, fn)(
         op.ctx.h, op.h, a.memspace, int(order), B, G, st, ss, s1, nsf, ch, C.byref(cfg), float(recast_tolerance),
         int(recast_max_iterations), k_p, phi_p, k1_p, o1_p, i1_p, o2_p, i2_p, cv_p, fb_p))
@@ -572,6 +614,7 @@ def sample_grf(grid: Grid1D, spec: GrfSpec, n_samples: int, first_sample: int = 
         import torch
         out = torch.empty((n, grid.n_cells), dtype=torch.float64, device=f"cuda:{ctx.device}")
         neg = torch.empty(n, dtype=torch.int64, device=out.device) if with_negatives else None
+        torch.cuda.ExternalStream(ctx.stream_ptr).wait_stream(torch.cuda.current_stream())
         _capi.check(ctx._lib.snop_grf_sample(ctx.h, 1, C.byref(g), C.byref(sp), int(first_sample), n, out.data_ptr(),
                                              neg.data_ptr() if neg is not None else None))
         ctx.synchronize()
@@ -591,6 +634,7 @@ def normalize_source(grid: Grid1D, raw, ctx: Context | None = None):
     r = a.inp(raw, shape=(n, grid.n_cells))
     out, out_p = a.out((n, grid.n_cells))
     g = grid.c()
+    a.ready(ctx)
     _capi.check(ctx._lib.snop_normalize_source(ctx.h, a.memspace, C.byref(g), n, r, out_p))
     if a.device:
         ctx.synchronize()

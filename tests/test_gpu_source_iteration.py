@@ -220,35 +220,38 @@ def test_deterministic_repeat():
     assert np.array_equal(a.phi, b.phi)
 
 
-@pytest.mark.parametrize("cs", ["2", "4", "8"])
+@pytest.mark.parametrize("cs", [2, 4, 8])
 def test_cluster_mode_parity(cs):
-    """The thread-block-cluster variant (instance split across CTAs, DSMEM scan) is selected with
-    SNOP_CLUSTER; it must match the oracle like the one-CTA path. Runs in a subprocess because the
-    dispatcher reads the variable once."""
-    import os
-    import subprocess
-    import sys
-    import textwrap
-    from pathlib import Path
-    code = textwrap.dedent('''
-        import numpy as np
-        from paper_2509_01416_b200 import snop, workloads as W
-        from tests import oracle_lib as O
+    """The thread-block-cluster variant (instance split across CTAs, DSMEM scan), forced through the
+    context's execution options, must match the oracle like the one-CTA path."""
+    ctx = snop.Context(0)
+    try:
+        ctx.set_options(cell_cluster=cs)
+        assert ctx.options()["cell_cluster"] == cs
         p = W.config2(batch=6, n_cells=2000)
         for bc in ((0, 0), (1, 0), (1, 1)):
             cfg = snop.SolverConfig(tolerance=1e-300, max_inner_iterations=6, boundary_left=bc[0], boundary_right=bc[1])
-            r = snop.source_iteration(snop.Grid1D(10.0, 2000), 32, p.sigma_t, p.sigma_s0, p.source, cfg)
+            r = snop.source_iteration(snop.Grid1D(10.0, 2000), 32, p.sigma_t, p.sigma_s0, p.source, cfg, ctx=ctx)
             o = O.source_iteration(10.0, 2000, 32, p.sigma_t, p.sigma_s0, p.source, cfg.c())
             e = np.max(np.abs(r.phi - o["phi"])) / np.max(np.abs(o["phi"]))
             assert e < 1e-10, (bc, e)
         q = W.config4(batch=2, n_cells=500)
         cfg = snop.SolverConfig(tolerance=1e-7, tolerance_k=1e-8, tolerance_phi=1e-7)
-        k = snop.power_iteration(snop.Grid1D(10.0, 500), 16, q.sigma_t, q.sigma_s0, q.nu_sigma_f, q.chi, cfg).k
+        k = snop.power_iteration(snop.Grid1D(10.0, 500), 16, q.sigma_t, q.sigma_s0, q.nu_sigma_f, q.chi, cfg,
+                                 ctx=ctx).k
         ko = O.power_iteration(10.0, 500, 16, 7, q.sigma_t, q.sigma_s0, q.nu_sigma_f, q.chi, cfg.c())["k"]
-        assert np.max(np.abs(k - ko) / ko) < 1e-9
-        print("ok")
-    ''')
-    env = dict(os.environ, SNOP_CLUSTER=cs)
-    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
-                         cwd=str(Path(__file__).resolve().parents[1]))
-    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+        assert np.max(np.abs(k - ko) / ko) < 1e-10
+    finally:
+        ctx.close()
+
+
+def test_context_options_validation():
+    ctx = snop.Context(0)
+    try:
+        with pytest.raises(InvalidArgument):
+            ctx.set_options(cell_cluster=3)
+        with pytest.raises(ValueError):
+            ctx.set_options(no_such_option=1)
+        assert ctx.options()["cell_cluster"] == 0
+    finally:
+        ctx.close()

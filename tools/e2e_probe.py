@@ -32,4 +32,4 @@ for rep in range(3):
     torch.cuda.synchronize()
     t = time.perf_counter()
     snop.source_iteration(g, p.order, *host, cfg, out=out)
-    print(f"host path (SNOP_HOST_CHUNKS={os.environ.get('SNOP_HOST_CHUNKS', '4')}): {(time.perf_counter() - t) * 1e3:.2f} ms")
+    print(f"host path (host_chunks={snop.default_context().options()['host_chunks']}): {(time.perf_counter() - t) * 1e3:.2f} ms")
