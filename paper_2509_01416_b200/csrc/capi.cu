@@ -110,6 +110,7 @@ snop_dev::SweepConsts make_consts(const snop_grid& g, int order) {
   for (int p = 0; p < order / 2; ++p) {
     const double m = mu[order / 2 + p];
     sc.c[p] = 2.0 * m / sc.dx;
+    sc.w[p] = w[order / 2 + p];
     sc.wmu[p] = w[order / 2 + p] * m;
     sc.mu3[p] = 3.0 * m;
   }

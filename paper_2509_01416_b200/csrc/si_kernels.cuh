@@ -62,7 +62,7 @@ si_fixed_source_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   io.ss0 = ss0_g + base;
   io.src = src_g + base;
   io.ss1 = ANISO ? ss1_g + base : nullptr;
-  io.jc = (ANISO || CUR) ? jc_g + base : nullptr;
+  io.jc = ((ANISO || CUR) && jc_g) ? jc_g + base : nullptr;  // CUR without jc: leakages only
   io.leak = leak_g ? leak_g + 2 * (size_t)b : nullptr;
   bool bad = false;
   if (!CL && stage_g) {
@@ -499,9 +499,10 @@ inline snop_status launch_si_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
                                double* leak, double* stage) {
   const bool aniso = ss1 != nullptr;
   const size_t smem = smem_bytes<K, NT>();
+  // the edge currents are accumulated only when wanted: P1 emission, current output, leakages
   auto kern = aniso ? si_fixed_source_kernel<K, NT, true, true, CL>
-                    : (cur ? si_fixed_source_kernel<K, NT, false, true, CL>
-                           : si_fixed_source_kernel<K, NT, false, false, CL>);
+                    : ((cur || leak) ? si_fixed_source_kernel<K, NT, false, true, CL>
+                                     : si_fixed_source_kernel<K, NT, false, false, CL>);
   double* jc = cur;
   if (aniso && !jc) {  // P1 needs the cell current even when the caller does not want it
     jc = static_cast<double*>(ctx.slot(21, (size_t)batch * sc.n_cells * sizeof(double)));

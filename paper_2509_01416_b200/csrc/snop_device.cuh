@@ -12,11 +12,16 @@
 //     share alpha_i and r_i (and beta_i for isotropic emission), so one reciprocal serves two
 //     updates. Maps are composed per thread (K cells), scanned across the warp with shuffles
 //     (prefix for mu>0, suffix for mu<0), then across warps through shared memory, and replayed.
-//   * The scalar flux is not summed from psi_avg: the DD balance  mu (psi_R - psi_L)/dx +
-//     St psi_avg = q  summed with the quadrature weights gives
-//        phi_i = (Ss0_i phi_i^old + S_i - (J_{i+1/2} - J_{i-1/2}) / dx) / St_i,
-//     J_e = sum_n w_n mu_n psi_n(e), so each update accumulates one edge current (1 FMA) instead
-//     of two cell-average terms. Exact in exact arithmetic; ~1e-14 relative in fp64.
+//   * The scalar flux is accumulated on cell EDGES: diamond difference makes every cell average
+//     the mean of its two edge fluxes, psi_avg = (psi_L + psi_R)/2, so with the edge scalar flux
+//     Phi_e = sum_n w_n psi_n(e)
+//        phi_i = sum_n w_n psi_avg,n = (Phi_{i-1/2} + Phi_{i+1/2}) / 2
+//     and each update accumulates one edge term (1 FMA) instead of a cell-average one. The sum is
+//     of like-signed terms for nonnegative emission, so it is as well conditioned as SPEC's
+//     sum of psi_avg at any optical thickness. (Round 1 took phi from the DD balance
+//     (q - dJ/dx)/St, whose cancellation grows like 1/(St dx): 4e-10 relative at St = 1e-4.)
+//     The edge current J_e = sum_n w_n mu_n psi_n(e) is accumulated as well only when the cell
+//     current (P1 emission, current output) or the face leakages are requested.
 //   * The convergence norm (relative L-inf or L2 of successive scalar fluxes) is
 //     a block reduction fused in the same kernel; max is order-independent (bit-deterministic),
 //     the L2 sums use a fixed lane/warp order.
@@ -37,6 +42,7 @@ struct SweepConsts {
   double dx;
   double inv_dx;
   double c[kMaxPairs];     // 2 mu_p / dx  (mu_p > 0, ascending p)
+  double w[kMaxPairs];     // w_p (weight of +mu_p and of -mu_p)
   double wmu[kMaxPairs];   // w_p mu_p
   double mu3[kMaxPairs];   // 3 mu_p (P1 emission term)
 };
@@ -170,7 +176,6 @@ struct SweepSmem {
   static constexpr int NW = NT / 32;
   double st[K * NT];           // Sigma_t (0 on padding cells)
   double q2[K * NT];           // 2 x isotropic emission: Ss0 phi + S (rebuilt every iteration)
-  double ist[K * NT];          // 1 / Sigma_t (0 on padding), set at solver entry
   double phi[K * NT];          // scalar flux
   // chunk-indexed arrays use spos(): one pad slot per E = NT/32 entries, so the scan warp's
   // lane-strided reads (lane l owns chunks l*E .. l*E+E-1) are bank-conflict free
@@ -465,17 +470,35 @@ __device__ __forceinline__ void scan_phase(SweepSmem<K, NT>& sm, int lane, int w
   }
 }
 
+// Edge accumulators of one thread: the scalar flux Phi at the left edge of each own cell (Fl)
+// and at the right edge of the last one (Fr); with WJ also the current J at the same edges.
+template <int K, bool WJ>
+struct EdgeAcc {
+  double Fl[K], Fr;
+  double Jl[WJ ? K : 1], Jr;
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int j = 0; j < K; ++j) Fl[j] = 0.0;
+    Fr = 0.0;
+#pragma unroll
+    for (int j = 0; j < (WJ ? K : 1); ++j) Jl[j] = 0.0;
+    Jr = 0.0;
+  }
+};
+
 // Phase C: boundary inflows (SURVEY §9 #2 ordering), the inflow of this CTA (cluster mode:
 // composed from the other CTAs' totals read through DSMEM) and of this thread's chunk, then the
-// replay that accumulates the edge currents J_e += w mu (psi+ - psi-).
-template <int K, int NT, int NP, bool CL>
+// replay that accumulates the edge scalar fluxes Phi_e += w (psi+ + psi-) (and, with WJ, the edge
+// currents J_e += w mu (psi+ - psi-)).
+template <int K, int NT, int NP, bool CL, bool WJ>
 __device__ __forceinline__ void replay_phase(const SweepConsts& sc, SweepSmem<K, NT>& sm, int p0, const SweepCtl& w,
                                              const double (&al)[NP][K], const double (&bp)[NP][K],
-                                             const double (&bm)[NP][K], double (&Jl)[K], double& Jr) {
+                                             const double (&bm)[NP][K], EdgeAcc<K, WJ>& acc) {
   const int t = w.t;
 #pragma unroll
   for (int q = 0; q < NP; ++q) {
     const int p = p0 + q;
+    const double wq = sc.w[p];
     const double wm = sc.wmu[p];
     // whole-domain totals (needed for reflective faces) and this CTA's entry maps
     double TAf, TBf, TAb, TBb;           // whole domain
@@ -526,18 +549,22 @@ __device__ __forceinline__ void replay_phase(const SweepConsts& sc, SweepSmem<K,
     const double psib_in = psib;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-      Jl[j] = fma(wm, psi, Jl[j]);
+      acc.Fl[j] = fma(wq, psi, acc.Fl[j]);
+      if constexpr (WJ) acc.Jl[j] = fma(wm, psi, acc.Jl[j]);
       psi = fma(al[q][j], psi, bp[q][j]);
       psib = fma(al[q][K - 1 - j], psib, bm[q][K - 1 - j]);
-      Jl[K - 1 - j] = fma(-wm, psib, Jl[K - 1 - j]);
+      acc.Fl[K - 1 - j] = fma(wq, psib, acc.Fl[K - 1 - j]);
+      if constexpr (WJ) acc.Jl[K - 1 - j] = fma(-wm, psib, acc.Jl[K - 1 - j]);
     }
-    Jr = fma(wm, psi - psib_in, Jr);  // J at this thread's right chunk edge (no neighbour exchange)
+    // Phi (and J) at this thread's right chunk edge (no neighbour exchange)
+    acc.Fr = fma(wq, psi + psib_in, acc.Fr);
+    if constexpr (WJ) acc.Jr = fma(wm, psi - psib_in, acc.Jr);
   }
 }
 
-template <int K, int NT, bool ANISO, int NP, bool CL>
+template <int K, int NT, bool ANISO, int NP, bool CL, bool WJ>
 __device__ __forceinline__ void sweep_pair_group(const SweepConsts& sc, SweepSmem<K, NT>& sm, const CellIO& io,
-                                                 int p0, SweepCtl& w, double (&Jl)[K], double& Jr) {
+                                                 int p0, SweepCtl& w, EdgeAcc<K, WJ>& acc) {
   double al[NP][K], bp[NP][K], bm[NP][K];
   SNOP_TSTAMP(t0);
   maps_phase<K, NT, ANISO, NP>(sc, sm, io, p0, w, al, bp, bm);
@@ -549,7 +576,7 @@ __device__ __forceinline__ void sweep_pair_group(const SweepConsts& sc, SweepSme
   if constexpr (CL) cl_sync();
   else __syncthreads();
   SNOP_TSTAMP(t4);
-  replay_phase<K, NT, NP, CL>(sc, sm, p0, w, al, bp, bm, Jl, Jr);
+  replay_phase<K, NT, NP, CL, WJ>(sc, sm, p0, w, al, bp, bm, acc);
   SNOP_TSTAMP(t5);
   SNOP_TACC(0, t0, t1);
   SNOP_TACC(1, t1, t2);
@@ -579,6 +606,7 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
                         bool* converged) {
   static_assert(!(PS && CL), "pair split and cell split are exclusive");
   static_assert((K + 1) * NT <= 14 * SweepSmem<K, NT>::NP_PAD, "exchange buffer must fit in agg + xmap");
+  constexpr bool WJ = ANISO || CUR;  // edge currents wanted (P1 emission, current, leakages)
   const int t = threadIdx.x;
   const int Nc = sc.n_cells, P = sc.n_pairs;
   SweepCtl w;
@@ -598,11 +626,6 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
     sm.lag[0][i] = 0.0;
     sm.lag[1][i] = 0.0;
   }
-#pragma unroll
-  for (int j = 0; j < K; ++j) {
-    const double stj = sm.st[j * NT + t];
-    sm.ist[j * NT + t] = stj > 0.0 ? 1.0 / stj : 0.0;  // iteration-invariant
-  }
   if constexpr (CL) cl_sync();
   else __syncthreads();
 
@@ -618,10 +641,8 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
   while (it < cfg.max_it) {
     ++it;
     w.it = it;
-    double Jl[K];
-#pragma unroll
-    for (int j = 0; j < K; ++j) Jl[j] = 0.0;
-    double Jr = 0.0;
+    EdgeAcc<K, WJ> acc;
+    acc.zero();
     SNOP_TSTAMP(ti0);
     int p = 0, pend = P;
     if constexpr (PS) {  // this CTA's contiguous range of pair groups (the odd tail pair: last rank)
@@ -631,15 +652,15 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
       pend = prank == psz - 1 ? P : 2 * g1;
     }
     if constexpr (NP == 2) {
-      for (; p + 1 < pend; p += 2) sweep_pair_group<K, NT, ANISO, 2, CL>(sc, sm, io, p, w, Jl, Jr);
+      for (; p + 1 < pend; p += 2) sweep_pair_group<K, NT, ANISO, 2, CL, WJ>(sc, sm, io, p, w, acc);
     }
-    for (; p < pend; ++p) sweep_pair_group<K, NT, ANISO, 1, CL>(sc, sm, io, p, w, Jl, Jr);
+    for (; p < pend; ++p) sweep_pair_group<K, NT, ANISO, 1, CL, WJ>(sc, sm, io, p, w, acc);
     SNOP_TSTAMP(ti1);
     SNOP_TACC(5, ti0, ti1);
     double num = 0.0, den = 0.0;
     if constexpr (PS) {
       // Rank r owns the flux update of the cells of owner threads [r per, (r+1) per), per = NT/CS.
-      // Every CTA pushes its partial edge currents (K + 1 per thread) into the owner rank's
+      // Every CTA pushes its partial edge scalar fluxes (K + 1 per thread) into the owner rank's
       // incoming buffer (agg + xmap, by source rank: [CS][K+1][per]); the owner sums the CS
       // partials in rank order, updates phi locally and pushes the new emission into every CTA.
       // All remote traffic is stores; the convergence norm is a cluster reduction (reduce2<CL =
@@ -651,22 +672,22 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
         const int ro = t / per, uu = t - ro * per;
         double* dst = cl_map(xb, ro) + (size_t)prank * (K + 1) * per + uu;
 #pragma unroll
-        for (int j = 0; j < K; ++j) dst[j * per] = Jl[j];
-        dst[K * per] = Jr;
+        for (int j = 0; j < K; ++j) dst[j * per] = acc.Fl[j];
+        dst[K * per] = acc.Fr;
       }
       cl_sync();
       for (int idx = t; idx < per * K; idx += NT) {
         const int j = idx / per, uu = idx - j * per, u = prank * per + uu;
         const int i = u * K + j;
         if (i < Nc) {
-          double JL = 0.0, JR = 0.0;
+          double FL = 0.0, FR = 0.0;
           for (int r = 0; r < psz; ++r) {
             const double* src = xb + (size_t)r * (K + 1) * per + uu;
-            JL += src[j * per];
-            JR += src[(j + 1) * per];
+            FL += src[j * per];
+            FR += src[(j + 1) * per];
           }
           const int o = j * NT + u;
-          const double pn = (sm.q2[o] - (JR - JL) * sc.inv_dx) * sm.ist[o];
+          const double pn = 0.5 * (FL + FR);
           const double d = pn - sm.phi[o];
           if (cfg.norm == 0) {
             num = fmax(num, fabs(d));
@@ -682,8 +703,8 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
       }
       reduce2<NT, true>(num, den, cfg.norm == 0, sm.red, sm.cred, rphase++, sm);
     } else {
-    // J at the right edge of the own last cell was accumulated locally (Jr); padding cells after
-    // the global last cell are identity maps, so Jl[j+1] of a padding cell is J at x = L.
+    // Phi (J) at the right edge of the own last cell was accumulated locally (Fr, Jr); padding
+    // cells after the global last cell are identity maps, so Jl[j+1] of a padding cell is J at L.
     double ssv[K], srcv[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
@@ -693,12 +714,14 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       if (c0 + j < Nc) {
-        const double JR = (j + 1 < K) ? Jl[j + 1] : Jr;
-        // balance form of phi = sum_n w_n psi_avg,n
-        const double pn = (sm.q2[j * NT + t] - (JR - Jl[j]) * sc.inv_dx) * sm.ist[j * NT + t];
-        if constexpr (ANISO || CUR) io.jc[c0 + j] = 0.5 * (Jl[j] + JR);
-        if (j == 0 && c0 == 0) sm.leak[0] = -Jl[0];  // J(0) = in - out at the left face
-        if (c0 + j == Nc - 1) sm.leak[1] = JR;       // J(L) = out - in at the right face
+        // phi = sum_n w_n psi_avg,n = mean of the two edge scalar fluxes (diamond difference)
+        const double pn = 0.5 * (acc.Fl[j] + ((j + 1 < K) ? acc.Fl[j + 1] : acc.Fr));
+        if constexpr (WJ) {
+          const double JR = (j + 1 < K) ? acc.Jl[j + 1] : acc.Jr;
+          if (io.jc) io.jc[c0 + j] = 0.5 * (acc.Jl[j] + JR);
+          if (j == 0 && c0 == 0) sm.leak[0] = -acc.Jl[0];  // J(0) = in - out at the left face
+          if (c0 + j == Nc - 1) sm.leak[1] = JR;           // J(L) = out - in at the right face
+        }
         const double d = pn - sm.phi[j * NT + t];
         if (cfg.norm == 0) {
           num = fmax(num, fabs(d));
@@ -722,7 +745,7 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
       break;
     }
   }
-  if (io.leak) {  // balance diagnostic: net leakages of the last sweep
+  if (WJ && io.leak) {  // balance diagnostic: net leakages of the last sweep
     if (c0 == 0) io.leak[0] = sm.leak[0];  // written by this same thread: no barrier needed
     if (w.owns_last) io.leak[1] = sm.leak[1];
   }

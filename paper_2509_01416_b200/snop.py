@@ -96,9 +96,14 @@ class Context:
         _capi.check(self._lib.snop_ctx_create(int(device), C.byref(h)))
         self.h = h
         self.device = device
+        # torch tensors read or written by device calls still in flight on this context's stream
+        # (inputs converted by the call, outputs it allocated); released by synchronize()
+        self._pending: list = []
 
     def close(self):
         if getattr(self, "h", None) is not None and self.h.value:
+            self._lib.snop_ctx_synchronize(self.h)
+            self._pending = []
             self._lib.snop_ctx_destroy(self.h)
             self.h = C.c_void_p()
 
@@ -109,7 +114,10 @@ class Context:
             pass
 
     def synchronize(self):
-        _capi.check(self._lib.snop_ctx_synchronize(self.h))
+        try:
+            _capi.check(self._lib.snop_ctx_synchronize(self.h))
+        finally:
+            self._pending = []
 
     OPTION_NAMES = ("cell_cluster", "pair_split", "pi_tail_cap", "host_chunks", "gemm_engine", "fno_dft", "fno_mix")
 
@@ -167,16 +175,18 @@ class _Args:
 
     def ready(self, ctx: "Context") -> None:
         """Device calls: order the context's stream after torch's current stream (the producers of
-        the inputs, including the dtype/contiguity conversions made here), and tell torch's caching
-        allocator that every tensor of the call is in use on the context's stream, so temporaries
-        freed when this function returns are not reused before the kernels that read them finish."""
+        the inputs, including the dtype/contiguity conversions made here), and keep every tensor of
+        the call referenced by the context until its next synchronize(), so torch's caching
+        allocator cannot hand their memory to other work while the kernels still read or write it.
+        (No record_stream on the context's stream: the allocator would record events on that stream
+        when the tensors die, possibly after the context destroyed it.)"""
         if not self.device:
             return
         import torch
         ext = torch.cuda.ExternalStream(ctx.stream_ptr)
         ext.wait_stream(torch.cuda.current_stream())
-        for t in self.keep + self.outs:
-            t.record_stream(ext)
+        ctx._pending.extend(self.keep)
+        ctx._pending.extend(self.outs)
 
     @property
     def memspace(self) -> int:
