@@ -19,3 +19,17 @@ def ctx():
     c = snop.Context(0)
     yield c
     c.close()
+
+
+@pytest.fixture
+def ctx_options():
+    """Set execution options (snop_ctx_options) on the default context for one test; restored after."""
+    from paper_2509_01416_b200 import snop
+    c = snop.default_context()
+    saved = c.options()
+
+    def set_(**kw):
+        c.set_options(**{**saved, **kw})
+
+    yield set_
+    c.set_options(**saved)

@@ -205,15 +205,12 @@ def test_precondition_fixed_source_deeponet_parity():
     assert _rel(r.phi[same], o["phi"][same]) < 1e-8
 
 
-@pytest.mark.parametrize("env", [{}, {"SNOP_DFT_TC": "0"}, {"SNOP_DFT_TC": "0", "SNOP_DFT_GEMM": "1"},
-                                 {"SNOP_NO_TMA_STORE": "1", "SNOP_NO_PRESPLIT": "1", "SNOP_NO_BRES": "1"},
-                                 {"SNOP_TC2_NO_DECOUPLE": "1"}])
-def test_fno_width64_kernel_paths(env, monkeypatch):
-    """The C5-width FNO runs on dedicated paths (exact-fp32 forward-DFT kernel, register-tiled mixing,
-    TMA-store epilogue, resident pre-split weights, tensor-core forward DFT); each against the oracle,
-    with the fallbacks (FFMA forward DFT, generic GEMM engine, direct stores)."""
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+@pytest.mark.parametrize("opts", [{}, {"fno_dft": 1}, {"gemm_engine": 1}, {"gemm_engine": 2}])
+def test_fno_width64_kernel_paths(opts, ctx_options):
+    """The C5-width FNO runs on dedicated paths (tensor-core forward DFT, register-tiled mixing,
+    TMA-store epilogue, resident pre-split weights); each against the oracle, with the other paths
+    selectable through the context options (FFMA forward DFT, tcgen05 engine v1 only, FFMA engine)."""
+    ctx_options(**opts)
     prm = OPS.fno_init(64, 16, 2, 128, OPS.GELU, seed=11)
     g = snop.Grid1D(10.0, 512)
     op = snop.SolutionOperator.fno(g, prm, (1.0, 0.8))

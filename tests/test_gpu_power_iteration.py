@@ -99,11 +99,11 @@ def test_zero_fission_is_degenerate():
 
 
 @pytest.mark.parametrize("cs", ["0", "2", "4", "8"])
-def test_pair_split_cluster_parity(cs, monkeypatch):
+def test_pair_split_cluster_parity(cs, ctx_options):
     """Pair-split clusters (si_solve PS, single-group eigen): each CTA sweeps a range of pair groups
     and the partial edge currents are exchanged through DSMEM. Fixed iteration counts: flux and k
-    against the oracle at 1e-10; SNOP_PS=0 is the one-CTA kernel. C3 shapes (reflective left)."""
-    monkeypatch.setenv("SNOP_PS", cs)
+    against the oracle at 1e-10; cs = 0 is the one-CTA kernel. C3 shapes (reflective left)."""
+    ctx_options(pair_split=int(cs) if cs != "0" else -1)
     p = W.config3(batch=3, n_cells=1000)
     cfg = _cfg(p, tolerance_k=1e-300, tolerance_phi=1e-300, max_outer_iterations=4, max_inner_iterations=5,
                tolerance=1e-300)
@@ -113,39 +113,38 @@ def test_pair_split_cluster_parity(cs, monkeypatch):
     assert np.max(np.abs(r.k - o["k"]) / o["k"]) < K_RTOL
 
 
-def test_pair_split_converged_matches_single_cta(monkeypatch):
+def test_pair_split_converged_matches_single_cta(ctx_options):
     p = W.config3(batch=4, n_cells=777)  # ragged cell count (padding cells in the last chunk)
     g = snop.Grid1D(p.length, p.n_cells)
     out = {}
     for cs in ("0", "4"):
-        monkeypatch.setenv("SNOP_PS", cs)
+        ctx_options(pair_split=int(cs) if cs != "0" else -1, pi_tail_cap=-1)
         out[cs] = snop.power_iteration(g, p.order, p.sigma_t, p.sigma_s0, p.nu_sigma_f, p.chi, _cfg(p))
     a, b = out["0"], out["4"]
     assert np.all(np.abs(a.outer_iterations.astype(int) - b.outer_iterations.astype(int)) <= 1)
     assert np.max(np.abs(a.k - b.k) / a.k) < 1e-10
 
 
-def test_tail_split_resume_parity(monkeypatch):
+def test_tail_split_resume_parity(ctx_options):
     """Tail split: phase 1 (one CTA, outer <= cap) then phase 2 (pair-split clusters) resuming from
     (k, phi, counts) for the unconverged instances. cap = 3 forces every instance through both
     phases; converged k against the oracle and against the unsplit single-CTA solve."""
     p = W.config3(batch=5, n_cells=640)
     g = snop.Grid1D(p.length, p.n_cells)
-    monkeypatch.setenv("SNOP_PI_SPLIT", "3")
+    ctx_options(pi_tail_cap=3)
     r, o = _both(p, _cfg(p))
     assert np.all(np.abs(r.outer_iterations.astype(int) - o["outer"].astype(int)) <= 1)
     assert np.max(np.abs(r.k - o["k"]) / o["k"]) < 1e-9
-    monkeypatch.setenv("SNOP_PI_SPLIT", "0")
-    monkeypatch.setenv("SNOP_PS", "0")
+    ctx_options(pi_tail_cap=-1, pair_split=-1)
     a = snop.power_iteration(g, p.order, p.sigma_t, p.sigma_s0, p.nu_sigma_f, p.chi, _cfg(p))
     assert np.all(np.abs(a.outer_iterations.astype(int) - r.outer_iterations.astype(int)) <= 1)
     assert np.all(np.abs(a.total_inner_iterations - r.total_inner_iterations) <= 2 * a.total_inner_iterations // 100 + 5)
     assert np.max(np.abs(a.k - r.k) / a.k) < 1e-10
 
 
-def test_tail_split_fixed_iterations(monkeypatch):
+def test_tail_split_fixed_iterations(ctx_options):
     """Fixed iteration counts across the phase boundary (cap 2 of 5 outers): flux and k at 1e-10."""
-    monkeypatch.setenv("SNOP_PI_SPLIT", "2")
+    ctx_options(pi_tail_cap=2)
     p = W.config3(batch=3, n_cells=512)
     cfg = _cfg(p, tolerance_k=1e-300, tolerance_phi=1e-300, max_outer_iterations=5, max_inner_iterations=4,
                tolerance=1e-300)
@@ -156,10 +155,10 @@ def test_tail_split_fixed_iterations(monkeypatch):
     assert np.max(np.abs(r.k - o["k"]) / o["k"]) < K_RTOL
 
 
-def test_tail_split_deterministic_and_batch_independent(monkeypatch):
+def test_tail_split_deterministic_and_batch_independent(ctx_options):
     """Repeated tail-split solves are bit-identical, and an instance's result does not depend on the
     batch it is solved in (the schedule depends on (G, order) and its own outer count only)."""
-    monkeypatch.setenv("SNOP_PI_SPLIT", "4")
+    ctx_options(pi_tail_cap=4)
     p = W.config3(batch=6, n_cells=700)
     g = snop.Grid1D(p.length, p.n_cells)
     cfg = _cfg(p)
@@ -173,9 +172,9 @@ def test_tail_split_deterministic_and_batch_independent(monkeypatch):
 
 
 @pytest.mark.parametrize("order", [10, 14])
-def test_pair_split_odd_pair_count(order, monkeypatch):
+def test_pair_split_odd_pair_count(order, ctx_options):
     """S10 / S14: an odd number of +/-mu pairs (the tail pair goes to the last rank of the cluster)."""
-    monkeypatch.setenv("SNOP_PS", "2")
+    ctx_options(pair_split=2)
     base = W.config3(batch=2, n_cells=300)
     p = W.EigenProblem("odd", base.length, base.n_cells, order, 1, base.sigma_t, base.sigma_s0, base.nu_sigma_f,
                        base.chi, None, base.bc_left, base.bc_right)
