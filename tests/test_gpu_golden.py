@@ -41,7 +41,8 @@ def test_table9_golden():
     e = snop.power_iteration(snop.Grid1D(10.0, 100), 32, t9.sigma_t, t9.sigma_s0, t9.nu_sigma_f, t9.chi,
                              snop.SolverConfig(tolerance=1e-7, tolerance_k=1e-8, tolerance_phi=1e-7))
     assert abs(e.outer_iterations[0] - G["t9_outer"][0]) <= 1
-    assert abs(e.k[0] - G["t9_k"][0]) / G["t9_k"][0] < 1e-9
+    tol = 1e-10 if e.outer_iterations[0] == G["t9_outer"][0] else 1e-8
+    assert abs(e.k[0] - G["t9_k"][0]) / G["t9_k"][0] < tol
 
 
 def test_operator_goldens():
