@@ -23,6 +23,7 @@ void* Ctx::slot(size_t i, size_t bytes) {
   if (slots.size() <= i) slots.resize(i + 1);
   DevBuf& b = slots[i];
   if (b.bytes < bytes) {
+    ++slot_gen;
     if (b.ptr) cudaFree(b.ptr);
     b.ptr = nullptr;
     b.bytes = 0;
@@ -57,7 +58,16 @@ Ctx* Ctx::sub(size_t i) {
   return subs[i];
 }
 
+void Ctx::settle_loops() {
+  for (const auto& p : pending_loops) launches += (int64_t)h_loop[p.first] * p.second;
+  pending_loops.clear();
+}
+
 Ctx::~Ctx() {
+  if (stream) cudaStreamSynchronize(stream);
+  for (auto& g : graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (h_loop) cudaFreeHost(h_loop);
   for (Ctx* c : subs) delete c;
   for (auto& b : slots)
     if (b.ptr) cudaFree(b.ptr);
@@ -164,6 +174,7 @@ snop_status drain_flags(Ctx& ctx) {
   cudaError_t e = cudaMemcpyAsync(&flags, ctx.d_flags, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx.stream);
   if (e != cudaSuccess) return cuda_fail("synchronize", e);
+  ctx.settle_loops();
   if (flags) cudaMemsetAsync(ctx.d_flags, 0, sizeof(int), ctx.stream);
   if (flags & FLAG_BAD_SIGMA_T) return invalid("nonpositive sigma_t (or initial k) in at least one instance");
   if (flags & FLAG_DEGENERATE) {

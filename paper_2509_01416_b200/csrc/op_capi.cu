@@ -4,6 +4,7 @@
 // inverse DFT + W path, projection) goes through one GEMM entry point (gemm.cuh / the tcgen05
 // engine); the elementwise parts (lift, spectral mixing, recast, row projection, fixed-point
 // bookkeeping) are small fused kernels here. Neural operators compute in fp32; the API is fp64.
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -50,6 +51,14 @@ struct snop_op {
   snop_solver_config cfg{};
   double *cst = nullptr, *css = nullptr;
   size_t cst_n = 0;
+  // identity of this operator for cached device-loop graphs: a process-unique serial, and a
+  // generation bumped when its own device buffers are reallocated
+  uint64_t serial = next_serial();
+  uint64_t gen = 0;
+  static uint64_t next_serial() {
+    static std::atomic<uint64_t> n{1};
+    return n++;
+  }
   std::vector<void*> owned;
   ~snop_op() {
     for (void* p : owned) cudaFree(p);
@@ -371,12 +380,13 @@ __global__ void rowdot(size_t rows, int H, const float* __restrict__ h, const fl
 
 // recast fixed-point bookkeeping, one CTA per instance: relative change,
 // divergence guard (non-finite or > 1e6 x initial max-norm -> restore phi0), freeze when done.
-__global__ void recast_update(int n, int norm, double tol, int it, const double* __restrict__ nx,
+__global__ void recast_update(int n, int norm, double tol, const int* __restrict__ it_done, const double* __restrict__ nx,
                               double* __restrict__ phi, const double* __restrict__ phi0,
                               const double* __restrict__ norm0, uint8_t* __restrict__ active,
                               int32_t* __restrict__ iters, int32_t* __restrict__ status, int* __restrict__ n_active) {
   const int b = blockIdx.x;
   if (!active[b]) return;
+  const int it = *it_done + 1;
   const double* x = nx + (size_t)b * n;
   double* p = phi + (size_t)b * n;
   double num = 0.0, den = 0.0, mx = 0.0;
@@ -451,6 +461,19 @@ __global__ void recast_update(int n, int norm, double tol, int it, const double*
       atomicAdd(n_active, 1);
     }
   }
+}
+
+// Loop control of a device-looped iteration (WHILE conditional graph node): counts the iteration
+// and continues while any instance is active and the cap is not reached.
+__global__ void loop_ctl(cudaGraphConditionalHandle h, int* __restrict__ it_done, const int* __restrict__ n_active,
+                         int max_it) {
+  const int it = *it_done + 1;
+  *it_done = it;
+  cudaGraphSetConditional(h, (*n_active > 0 && it < max_it) ? 1u : 0u);
+}
+
+__global__ void fill_i32(int n, int32_t v, int32_t* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = v;
 }
 
 __global__ void maxabs_rows(int n, const double* __restrict__ x, double* __restrict__ out) {
@@ -539,6 +562,7 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
       if (op.cst) cudaFree(op.cst);
       if (op.css) cudaFree(op.css);
       op.cst = op.css = nullptr;
+      ++op.gen;
       if (cudaMalloc(&op.cst, rowsN * sizeof(double)) != cudaSuccess ||
           cudaMalloc(&op.css, rowsN * sizeof(double)) != cudaSuccess)
         return cuda_status("cudaMalloc exact-op materials", cudaErrorMemoryAllocation);
@@ -708,6 +732,7 @@ snop_status drain(Ctx& ctx) {
   cudaError_t e = cudaMemcpyAsync(&flags, ctx.d_flags, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx.stream);
   if (e != cudaSuccess) return cuda_status("synchronize", e);
+  ctx.settle_loops();
   if (flags) cudaMemsetAsync(ctx.d_flags, 0, sizeof(int), ctx.stream);
   if (flags & FLAG_BAD_SIGMA_T) return invalid("nonpositive sigma_t in at least one instance");
   if (flags & FLAG_DEGENERATE) {
@@ -721,6 +746,76 @@ snop_status drain(Ctx& ctx) {
   return SNOP_OK;
 }
 
+// Runs `body` (which enqueues one iteration on ctx.stream and ends with loop_ctl on handle h) as
+// the body of a WHILE conditional node of a CUDA graph: the iteration loop runs on the device with
+// no host round trip per iteration. The executable is cached on the context under `key` (every
+// pointer and scalar the body captures, plus the workspace generation), so repeated calls with the
+// same buffers relaunch it directly. `d_it` counts iterations (copied to pinned memory for the
+// launch accounting).
+template <class Body>
+snop_status device_loop(Ctx& ctx, std::vector<uint64_t> key, const int* d_it, Body&& body) {
+  key.push_back(ctx.slot_gen);
+  Ctx::LoopGraph* lg = nullptr;
+  for (auto& g : ctx.graphs)
+    if (g.key == key) lg = &g;
+  if (!lg) {
+    if (ctx.graphs.size() >= 8) {  // evict the oldest (it may still be running: wait first)
+      cudaStreamSynchronize(ctx.stream);
+      ctx.settle_loops();
+      cudaGraphExecDestroy(ctx.graphs.front().exec);
+      ctx.graphs.erase(ctx.graphs.begin());
+    }
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaGraphCreate(&g, 0);
+    cudaGraphConditionalHandle h{};
+    if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams np{};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    if (e == cudaSuccess) e = cudaGraphAddNode(&node, g, nullptr, 0, &np);
+    if (e != cudaSuccess) {
+      if (g) cudaGraphDestroy(g);
+      return cuda_status("device loop graph", e);
+    }
+    cudaGraph_t bodyg = np.conditional.phGraph_out[0];
+    e = cudaStreamBeginCaptureToGraph(ctx.stream, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) {
+      cudaGraphDestroy(g);
+      return cuda_status("device loop capture", e);
+    }
+    const int64_t l0 = ctx.launches;
+    const snop_status bs = body(h);
+    const int64_t nb = ctx.launches - l0;
+    ctx.launches = l0;  // captured, not launched
+    cudaGraph_t out = nullptr;
+    e = cudaStreamEndCapture(ctx.stream, &out);
+    if (bs != SNOP_OK || e != cudaSuccess) {
+      cudaGraphDestroy(g);
+      return bs != SNOP_OK ? bs : cuda_status("device loop capture", e);
+    }
+    cudaGraphExec_t ex = nullptr;
+    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_status("device loop instantiate", e);
+    ctx.graphs.push_back({key, ex, nb});
+    lg = &ctx.graphs.back();
+  }
+  SNOP_TRY(cuda_status("device loop launch", cudaGraphLaunch(lg->exec, ctx.stream)));
+  if (!ctx.h_loop && cudaMallocHost(&ctx.h_loop, Ctx::kLoopSlots * sizeof(int)) != cudaSuccess)
+    return cuda_status("cudaMallocHost", cudaErrorMemoryAllocation);
+  if ((int)ctx.pending_loops.size() >= Ctx::kLoopSlots) {
+    SNOP_TRY(cuda_status("synchronize", cudaStreamSynchronize(ctx.stream)));
+    ctx.settle_loops();
+  }
+  const int slotn = (int)ctx.pending_loops.size();
+  cudaMemcpyAsync(ctx.h_loop + slotn, d_it, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream);
+  ctx.pending_loops.push_back({slotn, lg->body_launches});
+  return SNOP_OK;
+}
+
 snop_status recast_fp_dev(Ctx& ctx, snop_op& op, int B, const double* S, const double* st, const double* ss,
                           double tol, int max_it, int norm, const double* init, double* phi, int32_t* iters,
                           int32_t* status) {
@@ -731,8 +826,9 @@ snop_status recast_fp_dev(Ctx& ctx, snop_op& op, int B, const double* S, const d
   double* nx = static_cast<double*>(ctx.slot(52, N * sizeof(double)));
   double* norm0 = static_cast<double*>(ctx.slot(53, (size_t)B * sizeof(double)));
   uint8_t* active = static_cast<uint8_t*>(ctx.slot(54, (size_t)B));
-  int* n_active = static_cast<int*>(ctx.slot(55, sizeof(int)));
+  int* n_active = static_cast<int*>(ctx.slot(55, 2 * sizeof(int)));
   if (!phi0 || !s || !nx || !norm0 || !active || !n_active) return cuda_status("workspace", cudaErrorMemoryAllocation);
+  int* it_done = n_active + 1;
   if (init) SNOP_TRY(cuda_status("copy", cudaMemcpyAsync(phi0, init, N * sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream)));
   else SNOP_TRY(op_predict_dev(ctx, op, B, S, phi0));  // Eq. 9 with zero initial guess
   maxabs_rows<<<B, 256, 0, ctx.stream>>>(n, phi0, norm0);
@@ -740,20 +836,29 @@ snop_status recast_fp_dev(Ctx& ctx, snop_op& op, int B, const double* S, const d
   SNOP_TRY(cuda_status("copy", cudaMemcpyAsync(phi, phi0, N * sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream)));
   cudaMemsetAsync(active, 1, (size_t)B, ctx.stream);
   cudaMemsetAsync(iters, 0, (size_t)B * sizeof(int32_t), ctx.stream);
-  std::vector<int32_t> maxed(B, SNOP_RECAST_MAXED);
-  cudaMemcpyAsync(status, maxed.data(), (size_t)B * sizeof(int32_t), cudaMemcpyHostToDevice, ctx.stream);
-  for (int it = 1; it <= max_it; ++it) {
+  cudaMemsetAsync(it_done, 0, sizeof(int), ctx.stream);
+  fill_i32<<<grid_for(ctx, (size_t)B), 256, 0, ctx.stream>>>(B, SNOP_RECAST_MAXED, status);
+  ctx.launches++;
+  if (max_it < 1) return cuda_status("recast fixed point", cudaGetLastError());
+  // One iteration per pass of the device loop: recast source, operator
+  // forward, per-instance update/freeze, loop control.
+  auto body = [&](cudaGraphConditionalHandle h) -> snop_status {
     SNOP_TRY(launch_recast(ctx, N, S, phi, st, ss, op.tstar, op.sstar, s));
     SNOP_TRY(op_predict_dev(ctx, op, B, s, nx));
     cudaMemsetAsync(n_active, 0, sizeof(int), ctx.stream);
-    recast_update<<<B, 256, 0, ctx.stream>>>(n, norm, tol, it, nx, phi, phi0, norm0, active, iters, status, n_active);
-    ctx.launches++;
-    int h_active = 0;
-    cudaMemcpyAsync(&h_active, n_active, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream);
-    SNOP_TRY(cuda_status("recast iteration", cudaStreamSynchronize(ctx.stream)));
-    if (h_active == 0) break;
-  }
-  return SNOP_OK;
+    recast_update<<<B, 256, 0, ctx.stream>>>(n, norm, tol, it_done, nx, phi, phi0, norm0, active, iters, status,
+                                             n_active);
+    loop_ctl<<<1, 1, 0, ctx.stream>>>(h, it_done, n_active, max_it);
+    ctx.launches += 2;
+    return cuda_status("recast iteration", cudaGetLastError());
+  };
+  uint64_t tolbits;
+  std::memcpy(&tolbits, &tol, sizeof tolbits);
+  const std::vector<uint64_t> key = {1, (uint64_t)(uintptr_t)&op, op.serial, (uint64_t)B, (uint64_t)(uintptr_t)S,
+                                     (uint64_t)(uintptr_t)st, (uint64_t)(uintptr_t)ss, (uint64_t)(uintptr_t)phi,
+                                     (uint64_t)(uintptr_t)iters, (uint64_t)(uintptr_t)status, tolbits,
+                                     (uint64_t)max_it, (uint64_t)norm, op.gen};
+  return device_loop(ctx, key, it_done, body);
 }
 
 snop_status check_op(snop_ctx* ctx, snop_op* op) {

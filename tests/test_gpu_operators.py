@@ -177,6 +177,31 @@ def test_recast_divergence_guard():
     assert np.isfinite(r.phi).all()
 
 
+def test_recast_device_loop_cache_and_launch_accounting():
+    """The recast fixed point iterates on the device (a CUDA graph with a WHILE conditional node,
+    cached on the context by its buffers and scalars): repeated calls on the same device buffers
+    relaunch the cached graph and give bit-identical results; a different iteration cap or
+    tolerance is a different graph; the context's launch counter counts every iteration's kernels."""
+    import torch
+    op, oo = _deeponet(64, width=16)
+    rng = np.random.default_rng(4)
+    S, st = rng.uniform(0, 1, (5, 64)), rng.uniform(0.8, 1.4, (5, 64))
+    ss = st * 0.6
+    dS, dst, dss = (torch.from_numpy(a).cuda() for a in (S, st, ss))
+    ctx = op.ctx
+    runs = []
+    for max_it in (50, 50, 3, 50):
+        n0 = ctx.launch_count
+        r = snop.recast_fixed_point(op, dS, dst, dss, tolerance=1e-6, max_iterations=max_it)
+        runs.append((r.phi.cpu().numpy(), r.iterations.cpu().numpy(), r.status.cpu().numpy(), ctx.launch_count - n0))
+    assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][0], runs[3][0])
+    assert runs[0][3] == runs[1][3] == runs[3][3]
+    assert runs[2][1].max() <= 3 and runs[2][3] < runs[0][3]
+    o = oo.recast_fixed_point(S, st, ss, tol=1e-6, max_it=50)
+    assert np.array_equal(runs[0][2], o["status"])
+    assert np.all(np.abs(runs[0][1] - o["iterations"]) <= 1)
+
+
 def test_precondition_fixed_source_exact_operator():
     # SPEC.md:421: exact operator, dp = 0 -> refinement converges in <= 2 iterations
     n, order = 200, 16
