@@ -94,11 +94,13 @@ def test_c3_full_fixed_iterations_across_phase_boundary():
     cfg = _eig_cfg(p, tolerance=1e-300, tolerance_k=1e-300, tolerance_phi=1e-300, max_outer_iterations=52,
                    max_inner_iterations=2)
     r = _gpu_eig(p, cfg)
-    # a fast-converging instance can reach a bit-exact fixed point (dk = dphi = 0 < 1e-300) and
-    # stop early; its flux is then compared against the oracle's 52-outer flux like the others
-    early = np.nonzero(r.outer_iterations != 52)[0]
-    assert r.converged[early].all() and (r.outer_iterations[early] > 30).all()
-    assert (r.total_inner_iterations == 2 * r.outer_iterations).all()
+    # a fast-converging instance can reach a bit-exact fixed point (an inner sweep or an outer
+    # iteration that changes nothing: 0 < 1e-300) and stop early; its flux is then compared against
+    # the oracle's 52-outer flux like the others
+    early = np.nonzero(r.converged)[0]
+    assert (r.outer_iterations[early] > 30).all()
+    run = ~r.converged
+    assert (r.outer_iterations[run] == 52).all() and (r.total_inner_iterations[run] == 104).all()
     idx = np.union1d(np.random.default_rng(5).choice(p.batch, 16, replace=False), early)
     o = _oracle_eig(p.subset(idx), cfg)
     assert _rel_rows(r.phi[idx], o["phi"]).max() < RTOL
