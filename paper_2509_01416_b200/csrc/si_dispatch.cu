@@ -7,20 +7,20 @@
 #include "si_kernels.cuh"
 
 namespace snop_si {
-SNOP_DECL_SI(8, 32, false) SNOP_DECL_SI(8, 64, false) SNOP_DECL_SI(8, 128, false) SNOP_DECL_SI(8, 256, false)
-SNOP_DECL_SI(8, 512, false)
-SNOP_DECL_SI(8, 32, true) SNOP_DECL_SI(8, 64, true) SNOP_DECL_SI(8, 128, true) SNOP_DECL_SI(8, 256, true)
-SNOP_DECL_PI(8, 32, false) SNOP_DECL_PI(8, 64, false) SNOP_DECL_PI(8, 128, false) SNOP_DECL_PI(8, 256, false)
-SNOP_DECL_PI(8, 512, false)
-SNOP_DECL_PI(8, 32, true) SNOP_DECL_PI(8, 64, true) SNOP_DECL_PI(8, 128, true) SNOP_DECL_PI(8, 256, true)
-SNOP_DECL_PS(8, 32) SNOP_DECL_PS(8, 64) SNOP_DECL_PS(8, 128) SNOP_DECL_PS(8, 256) SNOP_DECL_PS(8, 512)
+SNOP_DECL_SI(SNOP_K, 32, false) SNOP_DECL_SI(SNOP_K, 64, false) SNOP_DECL_SI(SNOP_K, 128, false) SNOP_DECL_SI(SNOP_K, 256, false)
+SNOP_DECL_SI(SNOP_K, 512, false)
+SNOP_DECL_SI(SNOP_K, 32, true) SNOP_DECL_SI(SNOP_K, 64, true) SNOP_DECL_SI(SNOP_K, 128, true) SNOP_DECL_SI(SNOP_K, 256, true)
+SNOP_DECL_PI(SNOP_K, 32, false) SNOP_DECL_PI(SNOP_K, 64, false) SNOP_DECL_PI(SNOP_K, 128, false) SNOP_DECL_PI(SNOP_K, 256, false)
+SNOP_DECL_PI(SNOP_K, 512, false)
+SNOP_DECL_PI(SNOP_K, 32, true) SNOP_DECL_PI(SNOP_K, 64, true) SNOP_DECL_PI(SNOP_K, 128, true) SNOP_DECL_PI(SNOP_K, 256, true)
+SNOP_DECL_PS(SNOP_K, 32) SNOP_DECL_PS(SNOP_K, 64) SNOP_DECL_PS(SNOP_K, 128) SNOP_DECL_PS(SNOP_K, 256) SNOP_DECL_PS(SNOP_K, 512)
 }  // namespace snop_si
 
 using namespace snop_si;
 
 namespace {
 
-constexpr int K = 8;
+constexpr int K = SNOP_K;  // cells per thread (experiments: -DSNOP_K=4)
 
 int pow2_at_least(int v, int lo) {
   int p = lo;

@@ -3,11 +3,11 @@
 #include "si_kernels.cuh"
 
 namespace snop_si {
-SNOP_INST_PI(8, 32, false)
-SNOP_INST_PI(8, 64, false)
-SNOP_INST_PI(8, 128, false)
-SNOP_INST_PI(8, 256, false)
-SNOP_INST_PI(8, 512, false)
+SNOP_INST_PI(SNOP_K, 32, false)
+SNOP_INST_PI(SNOP_K, 64, false)
+SNOP_INST_PI(SNOP_K, 128, false)
+SNOP_INST_PI(SNOP_K, 256, false)
+SNOP_INST_PI(SNOP_K, 512, false)
 }  // namespace snop_si
 
 #ifdef SNOP_PHASE_TIMING

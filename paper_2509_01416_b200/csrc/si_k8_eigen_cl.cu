@@ -3,10 +3,10 @@
 #include "si_kernels.cuh"
 
 namespace snop_si {
-SNOP_INST_PI(8, 32, true)
-SNOP_INST_PI(8, 64, true)
-SNOP_INST_PI(8, 128, true)
-SNOP_INST_PI(8, 256, true)
+SNOP_INST_PI(SNOP_K, 32, true)
+SNOP_INST_PI(SNOP_K, 64, true)
+SNOP_INST_PI(SNOP_K, 128, true)
+SNOP_INST_PI(SNOP_K, 256, true)
 }  // namespace snop_si
 
 #ifdef SNOP_PHASE_TIMING

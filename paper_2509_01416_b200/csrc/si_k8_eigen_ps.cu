@@ -3,11 +3,11 @@
 #include "si_kernels.cuh"
 
 namespace snop_si {
-SNOP_INST_PS(8, 32)
-SNOP_INST_PS(8, 64)
-SNOP_INST_PS(8, 128)
-SNOP_INST_PS(8, 256)
-SNOP_INST_PS(8, 512)
+SNOP_INST_PS(SNOP_K, 32)
+SNOP_INST_PS(SNOP_K, 64)
+SNOP_INST_PS(SNOP_K, 128)
+SNOP_INST_PS(SNOP_K, 256)
+SNOP_INST_PS(SNOP_K, 512)
 }  // namespace snop_si
 
 #ifdef SNOP_PHASE_TIMING

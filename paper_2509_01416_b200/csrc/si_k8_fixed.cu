@@ -2,11 +2,11 @@
 #include "si_kernels.cuh"
 
 namespace snop_si {
-SNOP_INST_SI(8, 32, false)
-SNOP_INST_SI(8, 64, false)
-SNOP_INST_SI(8, 128, false)
-SNOP_INST_SI(8, 256, false)
-SNOP_INST_SI(8, 512, false)
+SNOP_INST_SI(SNOP_K, 32, false)
+SNOP_INST_SI(SNOP_K, 64, false)
+SNOP_INST_SI(SNOP_K, 128, false)
+SNOP_INST_SI(SNOP_K, 256, false)
+SNOP_INST_SI(SNOP_K, 512, false)
 }  // namespace snop_si
 
 #ifdef SNOP_PHASE_TIMING

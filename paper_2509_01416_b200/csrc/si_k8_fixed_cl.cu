@@ -3,8 +3,8 @@
 #include "si_kernels.cuh"
 
 namespace snop_si {
-SNOP_INST_SI(8, 32, true)
-SNOP_INST_SI(8, 64, true)
-SNOP_INST_SI(8, 128, true)
-SNOP_INST_SI(8, 256, true)
+SNOP_INST_SI(SNOP_K, 32, true)
+SNOP_INST_SI(SNOP_K, 64, true)
+SNOP_INST_SI(SNOP_K, 128, true)
+SNOP_INST_SI(SNOP_K, 256, true)
 }  // namespace snop_si

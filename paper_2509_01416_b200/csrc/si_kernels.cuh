@@ -12,6 +12,11 @@
 namespace snop_si {
 using namespace snop_dev;
 
+// Cells per thread of the one-CTA-per-instance layout (8; experiment builds may override).
+#ifndef SNOP_K
+#define SNOP_K 8
+#endif
+
 // Register budget: 128 regs/thread (16 resident warps per SM at NT * minBlocks = 512).
 #ifndef SNOP_WARPS_PER_SM
 #define SNOP_WARPS_PER_SM 16

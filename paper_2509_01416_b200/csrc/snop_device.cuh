@@ -55,12 +55,18 @@ struct SolveConfig {
   int norm;      // 0 rel-Linf, 1 rel-L2
 };
 
+#ifndef SNOP_RCP_CUBIC
+#define SNOP_RCP_CUBIC 1
+#endif
 __device__ __forceinline__ double rcp_fast(double t) {
   // MUFU.RCP64H seed + one cubic Newton step: rel. error ~ e0^3 (< 1e-18 for a ~2^-22 seed).
+  // (SNOP_RCP_CUBIC=0: quadratic step, ~e0^2.)
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(t));
   double e = fma(-t, r, 1.0);
+#if SNOP_RCP_CUBIC
   e = fma(e, e, e);
+#endif
   return fma(r, e, r);
 }
 
@@ -168,6 +174,18 @@ __device__ __forceinline__ void pmul(double& d, double a, double b, bool p) {
       : "+d"(d) : "d"(a), "d"(b), "r"((unsigned)p));
 }
 
+// Stage Sigma_s0 and the external source in shared memory for the solve (the per-iteration flux
+// update then reads no global memory).
+#ifndef SNOP_STAGE_SS
+#define SNOP_STAGE_SS 1
+#endif
+
+// Pairs per pair group (maps/scan/replay are done for NP +/-mu pairs per CTA barrier phase).
+#ifndef SNOP_NP
+#define SNOP_NP 2
+#endif
+constexpr int kNP = SNOP_NP;
+
 // Shared-memory workspace of one CTA solver (the P1 moment array, when present, is a separate
 // dynamic-smem region passed as a pointer so isotropic launches do not pay for it). Per-cell
 // arrays use the [j][t] layout: thread t's cell j sits at j*NT + t (conflict-free, private).
@@ -177,21 +195,27 @@ struct SweepSmem {
   double st[K * NT];           // Sigma_t (0 on padding cells)
   double q2[K * NT];           // 2 x isotropic emission: Ss0 phi + S (rebuilt every iteration)
   double phi[K * NT];          // scalar flux
+#if SNOP_STAGE_SS
+  double ss[K * NT];           // within-group Sigma_s0 and external source, staged at solver entry
+  double src[K * NT];
+#endif
   // chunk-indexed arrays use spos(): one pad slot per E = NT/32 entries, so the scan warp's
   // lane-strided reads (lane l owns chunks l*E .. l*E+E-1) are bank-conflict free
   static constexpr int E = NT / 32;
   static constexpr int NP_PAD = NT + (E > 1 ? 32 : 0);
   __device__ static constexpr int spos(int idx) { return E > 1 ? idx + idx / E : idx; }
-  double agg[2][3][NP_PAD];    // chunk maps of the current pair group: [q][{A, Bfwd, Bbwd}][chunk]
-  double xmap[2][4][NP_PAD];   // exclusive maps entering each chunk: [q][{Af, Bf, Ab, Bb}][chunk]
-  double total[2][4];          // whole-domain maps [q][{Af, Bf, Ab, Bb}]
+  // chunk maps of the current pair group: [q][{A, Bf, Bb}][chunk]; the scan replaces Bf / Bb in
+  // place by the exclusive maps' offsets and writes their slopes to xmap [q][{Af, Ab}][chunk]
+  double agg[kNP][3][NP_PAD];
+  double xmap[kNP][2][NP_PAD];
+  double total[kNP][4];         // whole-domain maps [q][{Af, Bf, Ab, Bb}]
   double leak[2];              // net face currents of the latest sweep (written by the face owners)
   double red[4 * NW];          // reductions inside si_solve
   double red2[4 * NW];         // reductions of the enclosing (eigen) kernel
   double lag[2][kMaxPairs];    // both-reflective: lagged mu>0 outflow at x=L, by iteration parity
   // cluster mode (one instance spread over the CTAs of a thread-block cluster): per-CTA values
   // published for the other CTAs, read through distributed shared memory
-  double ctot[2][2][4];        // CTA-level scan totals [group slot][q][{Af,Bf,Ab,Bb}]
+  double ctot[2][kNP][4];      // CTA-level scan totals [group slot][q][{Af,Bf,Ab,Bb}]
   double cred[2][2];           // CTA-level reduction results (si_solve), by phase
   double cred2[2][2];          // CTA-level reduction results (enclosing kernel), by phase
   int cflag[2];                // CTA-level flags (validation)
@@ -363,8 +387,8 @@ __device__ __forceinline__ void scan_one(SweepSmem<K, NT>& sm, int q, int lane, 
   const int base = FWD ? lane * S : (31 - lane) * S + (E - 1);
   const double* a = sm.agg[q][0] + base;
   const double* b = sm.agg[q][FWD ? 1 : 2] + base;
-  double* XA = sm.xmap[q][FWD ? 0 : 2] + base;
-  double* XB = sm.xmap[q][FWD ? 1 : 3] + base;
+  double* XA = sm.xmap[q][FWD ? 0 : 1] + base;
+  double* XB = sm.agg[q][FWD ? 1 : 2] + base;  // in place: chunk e's offset is read before it is replaced
   // Loads are batched ahead of the dependent chain in runs of H chunks: stores to the xmap
   // scratch may alias later agg loads as far as the compiler knows, so without batching every
   // step would pay a full shared-memory round trip.
@@ -544,8 +568,8 @@ __device__ __forceinline__ void replay_phase(const SweepConsts& sc, SweepSmem<K,
     const double cta_left = fma(EfA, psi_left_in, EfB);
     const double cta_right = fma(EbA, psi_right_in, EbB);
     const int pt = SweepSmem<K, NT>::spos(t);
-    double psi = fma(sm.xmap[q][0][pt], cta_left, sm.xmap[q][1][pt]);
-    double psib = fma(sm.xmap[q][2][pt], cta_right, sm.xmap[q][3][pt]);
+    double psi = fma(sm.xmap[q][0][pt], cta_left, sm.agg[q][1][pt]);
+    double psib = fma(sm.xmap[q][1][pt], cta_right, sm.agg[q][2][pt]);
     const double psib_in = psib;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
@@ -593,9 +617,6 @@ __device__ __forceinline__ void sweep_pair_group(const SweepConsts& sc, SweepSme
 // are the natural-layout global arrays of the instance. On exit sm.phi holds the final flux and
 // io.jc the cell-average current of the last sweep (written when ANISO || CUR). Returns sweeps
 // performed; *converged is uniform across the CTA / cluster.
-#ifndef SNOP_NP
-#define SNOP_NP 2
-#endif
 // PS (pair split, eigen kernel only): the CTAs of a thread-block cluster each sweep a contiguous
 // range of pair groups over ALL cells of the instance; after the pairs of a source iteration the
 // partial edge currents are exchanged through distributed shared memory and summed in rank order,
@@ -605,7 +626,7 @@ template <int K, int NT, bool ANISO, bool CUR, bool CL = false, int NP = SNOP_NP
 __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem<K, NT>& sm, const CellIO& io,
                         bool* converged) {
   static_assert(!(PS && CL), "pair split and cell split are exclusive");
-  static_assert((K + 1) * NT <= 14 * SweepSmem<K, NT>::NP_PAD, "exchange buffer must fit in agg + xmap");
+  static_assert((K + 1) * NT <= 5 * kNP * SweepSmem<K, NT>::NP_PAD, "exchange buffer must fit in agg + xmap");
   constexpr bool WJ = ANISO || CUR;  // edge currents wanted (P1 emission, current, leakages)
   const int t = threadIdx.x;
   const int Nc = sc.n_cells, P = sc.n_pairs;
@@ -635,6 +656,15 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
   // emission (x2): q2 = Ss0 phi + S ; angular q_n = q2/2 + 3/2 Ss1 mu_n J. Built
   // here for the first sweep and then in each flux update for the next one, so the L2 loads of
   // Ss0 and S overlap the flux update and the convergence reduction.
+#if SNOP_STAGE_SS
+  if constexpr (!PS) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      sm.ss[j * NT + t] = (c0 + j < Nc) ? io.ss0[c0 + j] : 0.0;
+      sm.src[j * NT + t] = (c0 + j < Nc) ? io.src[c0 + j] : 0.0;
+    }
+  }
+#endif
 #pragma unroll
   for (int j = 0; j < K; ++j)
     sm.q2[j * NT + t] = (c0 + j < Nc) ? fma(io.ss0[c0 + j], sm.phi[j * NT + t], io.src[c0 + j]) : 0.0;
@@ -651,7 +681,10 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
       p = 2 * g0;
       pend = prank == psz - 1 ? P : 2 * g1;
     }
-    if constexpr (NP == 2) {
+    if constexpr (NP > 2) {
+      for (; p + NP - 1 < pend; p += NP) sweep_pair_group<K, NT, ANISO, NP, CL, WJ>(sc, sm, io, p, w, acc);
+    }
+    if constexpr (NP >= 2) {
       for (; p + 1 < pend; p += 2) sweep_pair_group<K, NT, ANISO, 2, CL, WJ>(sc, sm, io, p, w, acc);
     }
     for (; p < pend; ++p) sweep_pair_group<K, NT, ANISO, 1, CL, WJ>(sc, sm, io, p, w, acc);
@@ -708,8 +741,13 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
     double ssv[K], srcv[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
+#if SNOP_STAGE_SS
+      ssv[j] = sm.ss[j * NT + t];  // (own cells: written by this thread at entry)
+      srcv[j] = sm.src[j * NT + t];
+#else
       ssv[j] = (c0 + j < Nc) ? io.ss0[c0 + j] : 0.0;
       srcv[j] = (c0 + j < Nc) ? io.src[c0 + j] : 0.0;
+#endif
     }
 #pragma unroll
     for (int j = 0; j < K; ++j) {
