@@ -554,7 +554,8 @@ snop_status dense_forward(Ctx& ctx, int rows, const std::vector<int>& sizes, con
 }
 
 // predict: in/out fp64 device arrays [B][Nc].
-snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, double* out) {
+snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, double* out,
+                           const uint8_t* active = nullptr) {
   const int n = op.grid.n_cells;
   const size_t rowsN = (size_t)B * n;
   if (op.kind == 2) {  // exact operator: model-based solve at p*
@@ -573,8 +574,9 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
     }
     int32_t* it = static_cast<int32_t*>(ctx.slot(40, (size_t)B * sizeof(int32_t)));
     uint8_t* cv = static_cast<uint8_t*>(ctx.slot(41, (size_t)B));
+    // (active: a device loop's frozen instances are skipped; the neural operators run whole batches)
     return launch_source_iteration(ctx, op.grid, op.order, B, op.cst, op.css, nullptr, in, op.cfg, nullptr, out,
-                                   nullptr, it, cv);
+                                   nullptr, it, cv, nullptr, nullptr, active);
   }
   float* X = static_cast<float*>(ctx.slot(42, rowsN * sizeof(float)));
   if (!X) return cuda_status("workspace", cudaErrorMemoryAllocation);
@@ -844,7 +846,7 @@ snop_status recast_fp_dev(Ctx& ctx, snop_op& op, int B, const double* S, const d
   // forward, per-instance update/freeze, loop control.
   auto body = [&](cudaGraphConditionalHandle h) -> snop_status {
     SNOP_TRY(launch_recast(ctx, N, S, phi, st, ss, op.tstar, op.sstar, s));
-    SNOP_TRY(op_predict_dev(ctx, op, B, s, nx));
+    SNOP_TRY(op_predict_dev(ctx, op, B, s, nx, active));
     cudaMemsetAsync(n_active, 0, sizeof(int), ctx.stream);
     recast_update<<<B, 256, 0, ctx.stream>>>(n, norm, tol, it_done, nx, phi, phi0, norm0, active, iters, status,
                                              n_active);

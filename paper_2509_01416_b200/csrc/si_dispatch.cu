@@ -71,7 +71,8 @@ namespace snop_impl {
 snop_status launch_source_iteration(Ctx& ctx, const snop_grid& g, int order, int batch, const double* st,
                                     const double* ss0, const double* ss1, const double* src,
                                     const snop_solver_config& cfg, const double* phi0, double* phi, double* cur,
-                                    int32_t* iters, uint8_t* conv, double* leak, double* stage) {
+                                    int32_t* iters, uint8_t* conv, double* leak, double* stage,
+                                    const uint8_t* active) {
   if (batch == 0) return SNOP_OK;
   const SweepConsts sc = make_consts(g, order);
   const SolveConfig c = inner_cfg(cfg);
@@ -83,7 +84,7 @@ snop_status launch_source_iteration(Ctx& ctx, const snop_grid& g, int order, int
 #define SNOP_SI(NN, CC)                       \
   if (s.nt == NN && (s.cs > 1) == CC)         \
     return launch_si_t<K, NN, CC>(ctx, sc, c, batch, s.cs, st, ss0, ss1, src, phi0, phi, cur, iters, conv, leak, \
-                                  stage);
+                                  stage, active);
   SNOP_SI(32, false) SNOP_SI(64, false) SNOP_SI(128, false) SNOP_SI(256, false) SNOP_SI(512, false)
   SNOP_SI(32, true) SNOP_SI(64, true) SNOP_SI(128, true) SNOP_SI(256, true)
 #undef SNOP_SI

@@ -54,13 +54,14 @@ si_fixed_source_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
                        const double* __restrict__ phi0_g, double* __restrict__ phi_g,
                        double* __restrict__ jc_g, int32_t* __restrict__ iters, uint8_t* __restrict__ conv,
                        int* __restrict__ flags, const int* __restrict__ order, double* __restrict__ leak_g,
-                       double* __restrict__ stage_g) {
+                       double* __restrict__ stage_g, const uint8_t* __restrict__ active) {
   extern __shared__ __align__(32) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<SweepSmem<K, NT>*>(smem_raw);
   const int t = threadIdx.x, Nc = sc.n_cells;
   int b, rank;
   instance_of_block<CL>(b, rank);
   if (order) b = order[b];  // longest-expected-first dispatch (see launch_si_t)
+  if (active && !active[b]) return;  // frozen instance of a device loop: outputs left as they are
   const size_t base = (size_t)b * Nc;
   const int c0 = rank * NT * K + t * K;
   CellIO io;
@@ -501,7 +502,7 @@ template <int K, int NT, bool CL>
 inline snop_status launch_si_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveConfig& cfg, int batch, int cs,
                                const double* st, const double* ss0, const double* ss1, const double* src,
                                const double* phi0, double* phi, double* cur, int32_t* iters, uint8_t* conv,
-                               double* leak, double* stage) {
+                               double* leak, double* stage, const uint8_t* active) {
   const bool aniso = ss1 != nullptr;
   const size_t smem = smem_bytes<K, NT>();
   // the edge currents are accumulated only when wanted: P1 emission, current output, leakages
@@ -520,7 +521,7 @@ inline snop_status launch_si_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
   const int* order =
       (!CL && batch > 4 * ctx.sm_count) ? make_order(ctx, batch, sc.n_cells, st, ss0, stage != nullptr) : nullptr;
   const cudaError_t e = launch_k(kern, batch, CL ? cs : 1, NT, smem, ctx.stream, sc, cfg, st, ss0, ss1, src, phi0,
-                                 phi, jc, iters, conv, ctx.d_flags, order, leak, CL ? nullptr : stage);
+                                 phi, jc, iters, conv, ctx.d_flags, order, leak, CL ? nullptr : stage, active);
   ctx.launches++;
   if (e != cudaSuccess) {
     snop_impl::set_error(std::string("si_fixed_source_kernel launch: ") + cudaGetErrorString(e));
@@ -584,7 +585,7 @@ static __global__ void pi_tail_list_kernel(int B, int cap, const int32_t* __rest
 // Explicitly instantiated in si_k8_{fixed,eigen}{,_cl}.cu (one TU per variant, parallel build).
 #define SNOP_SI_ARGS                                                                                          \
   snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, int, int, const double*, const double*, const double*, \
-      const double*, const double*, double*, double*, int32_t*, uint8_t*, double*, double*
+      const double*, const double*, double*, double*, int32_t*, uint8_t*, double*, double*, const uint8_t*
 #define SNOP_PI_ARGS                                                                                          \
   snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, const EigenParams&, int, int, const double*,          \
       const double*, const double*, const double*, const double*, const double*, const double*, double*, double*, \

@@ -105,15 +105,24 @@ __device__ __forceinline__ double block_sum(double v, double* scratch, int phase
   return r;
 }
 
-// Two independent block maxima with a single barrier.
+// Warp maximum of a NON-NEGATIVE double (sign bit clear; +inf and NaN patterns included): for such
+// values the order of the bit patterns as unsigned integers is the order of the values, so two
+// 32-bit warp reductions (REDUX) give the exact maximum - the high words first, then the low words
+// of the lanes that hold the maximal high word.
+__device__ __forceinline__ double warp_max_nonneg(double v) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  const unsigned hi = (unsigned)(u >> 32), lo = (unsigned)u;
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  return __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+}
+
+// Two independent block maxima of non-negative values (|d|, |phi|) with a single barrier.
 template <int NT>
 __device__ __forceinline__ void block_max2(double& a, double& b, double* scratch, int phase) {
   constexpr int NW = NT / 32;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    a = fmax(a, shfl_xor_d(a, o));
-    b = fmax(b, shfl_xor_d(b, o));
-  }
+  a = warp_max_nonneg(a);
+  b = warp_max_nonneg(b);
   double* s = scratch + (phase & 1) * 2 * NW;
   if ((threadIdx.x & 31) == 0) {
     s[threadIdx.x >> 5] = a;
@@ -437,10 +446,8 @@ __device__ __forceinline__ void scan_one(SweepSmem<K, NT>& sm, int q, int lane, 
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const double ap = __shfl_up_sync(0xffffffffu, A, o), bq = __shfl_up_sync(0xffffffffu, B, o);
-    if (lane >= o) {
-      B = fma(A, bq, B);
-      A *= ap;
-    }
+    pfma(B, A, bq, B, lane >= o);  // predicated: no selects on the dependent chain
+    pmul(A, A, ap, lane >= o);
   }
 #endif
   double Ax = __shfl_up_sync(0xffffffffu, A, 1), Bx = __shfl_up_sync(0xffffffffu, B, 1);
@@ -749,28 +756,48 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
       srcv[j] = (c0 + j < Nc) ? io.src[c0 + j] : 0.0;
 #endif
     }
+    // phi = sum_n w_n psi_avg,n = mean of the two edge scalar fluxes (diamond difference); the
+    // next sweep's emission; the convergence norm's two reductions. Specialised per norm and for
+    // threads whose K cells are all real cells (no per-cell predicates on the common path).
+    auto phi_cell = [&](int j) -> double {
+      const double pn = 0.5 * (acc.Fl[j] + ((j + 1 < K) ? acc.Fl[j + 1] : acc.Fr));
+      if constexpr (WJ) {
+        const double JR = (j + 1 < K) ? acc.Jl[j + 1] : acc.Jr;
+        if (io.jc) io.jc[c0 + j] = 0.5 * (acc.Jl[j] + JR);
+        if (j == 0 && c0 == 0) sm.leak[0] = -acc.Jl[0];  // J(0) = in - out at the left face
+        if (c0 + j == Nc - 1) sm.leak[1] = JR;           // J(L) = out - in at the right face
+      }
+      const double d = pn - sm.phi[j * NT + t];
+      sm.phi[j * NT + t] = pn;
+      sm.q2[j * NT + t] = fma(ssv[j], pn, srcv[j]);  // emission of the next sweep
+      return d;
+    };
+    const bool full = c0 + K <= Nc;
+    if (cfg.norm == 0) {
+      if (full) {
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      if (c0 + j < Nc) {
-        // phi = sum_n w_n psi_avg,n = mean of the two edge scalar fluxes (diamond difference)
-        const double pn = 0.5 * (acc.Fl[j] + ((j + 1 < K) ? acc.Fl[j + 1] : acc.Fr));
-        if constexpr (WJ) {
-          const double JR = (j + 1 < K) ? acc.Jl[j + 1] : acc.Jr;
-          if (io.jc) io.jc[c0 + j] = 0.5 * (acc.Jl[j] + JR);
-          if (j == 0 && c0 == 0) sm.leak[0] = -acc.Jl[0];  // J(0) = in - out at the left face
-          if (c0 + j == Nc - 1) sm.leak[1] = JR;           // J(L) = out - in at the right face
-        }
-        const double d = pn - sm.phi[j * NT + t];
-        if (cfg.norm == 0) {
+        for (int j = 0; j < K; ++j) {
+          const double d = phi_cell(j);
           num = fmax(num, fabs(d));
-          den = fmax(den, fabs(pn));
-        } else {
+          den = fmax(den, fabs(sm.phi[j * NT + t]));
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+          if (c0 + j < Nc) {
+            const double d = phi_cell(j);
+            num = fmax(num, fabs(d));
+            den = fmax(den, fabs(sm.phi[j * NT + t]));
+          }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (c0 + j < Nc) {
+          const double d = phi_cell(j), pn = sm.phi[j * NT + t];
           num = fma(d, d, num);
           den = fma(pn, pn, den);
         }
-        sm.phi[j * NT + t] = pn;
-        sm.q2[j * NT + t] = fma(ssv[j], pn, srcv[j]);  // emission of the next sweep
-      }
     }
     reduce2<NT, CL>(num, den, cfg.norm == 0, sm.red, sm.cred, rphase++, sm);
     }

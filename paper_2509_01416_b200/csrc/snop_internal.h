@@ -63,7 +63,8 @@ snop_status launch_source_iteration(Ctx& ctx, const snop_grid& g, int order, int
                                     const double* ss0, const double* ss1, const double* src,
                                     const snop_solver_config& cfg, const double* phi0, double* phi,
                                     double* cur, int32_t* iters, uint8_t* conv, double* leak = nullptr,
-                                    double* stage = nullptr);
+                                    double* stage = nullptr, const uint8_t* active = nullptr);
+// active != nullptr: instances b with active[b] == 0 are skipped (their outputs are not written).
 // stage != nullptr: st/ss0/ss1/src/phi0 and phi/iters/conv/leak may be pinned host memory (read
 // and written by the kernel over the bus); stage is a device workspace of batch * (ss1 ? 3 : 2) *
 // n_cells doubles. cur must then be device memory or null.

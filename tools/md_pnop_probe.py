@@ -66,9 +66,9 @@ def c3(ctx):
             t0 = time.perf_counter()
             r, t = timed(ctx, lambda: fn(op, p.order, *dev, cfg), reps=1)
             print(f"C3 {alg.upper()} {opname}: {t:.1f} ms (wall {1e3 * (time.perf_counter() - t0):.0f}), "
-                  f"stage1 outer mean {np.mean(np.asarray(r.stage1_outer)):.1f}, stage2 outer mean "
-                  f"{np.mean(np.asarray(r.stage2_outer)):.1f}, stage2 inner total {np.sum(np.asarray(r.stage2_inner))}, "
-                  f"k err vs cold {np.max(np.abs(np.asarray(r.k) - cold.k.cpu().numpy()) / cold.k.cpu().numpy()):.1e}")
+                  f"stage1 outer mean {r.stage1_outer.float().mean().item():.1f}, stage2 outer mean "
+                  f"{r.stage2_outer.float().mean().item():.1f}, stage2 inner total {int(r.stage2_inner.sum().item())}, "
+                  f"k err vs cold {(r.k - cold.k).abs().div(cold.k).max().item():.1e}")
 
 
 if __name__ == "__main__":
