@@ -49,10 +49,55 @@ def peaks():
     return 6650.0, "fallback"
 
 
+def fno_flops_per_sample(n, width=64, modes=16, layers=4, hidden=128):
+    """Algorithmic FLOPs of one FNO forward per sample: lift 2 -> C, per layer the
+    truncated forward DFT (2 n 2M C), the complex mixing (M C C x 8), the inverse DFT and the W
+    path (2 n C C), projection C -> hidden -> 1."""
+    lift = 2 * n * 2 * width
+    layer = 2 * n * 2 * modes * width * 2 + modes * width * width * 8 + 2 * n * width * width
+    proj = 2 * n * (width * hidden + hidden)
+    return lift + layers * layer + proj
+
+
+def timed_device(ctx, stream, fn, reps=2):
+    """min device time (s) of fn() over reps runs, CUDA events on the solver stream, after one
+    untimed run; returns the last result too."""
+    import torch
+    out = fn()
+    ts = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out = fn()
+        e1.record(stream)
+        ctx.synchronize()
+        ts.append(e0.elapsed_time(e1) / 1e3)
+    return out, float(np.min(ts))
+
+
+def warm_stats(r, t, batch, it_cold_mean):
+    """One MD-PNOP arm (precondition_fixed_source) as a bench record."""
+    pit, ref = r.precond_iterations.to(torch_int64()), r.refine_iterations.to(torch_int64())
+    return {"ms": 1e3 * t, "solves_per_sec": batch / t,
+            "recast_iterations_mean": float(pit.float().mean().item()), "recast_iterations_max": int(pit.max().item()),
+            "recast_status_counts": [int((r.recast_status == k).sum().item()) for k in range(3)],
+            "refine_iterations_mean": float(ref.float().mean().item()), "refine_iterations_max": int(ref.max().item()),
+            "refine_iteration_ratio_vs_zero_guess": float(ref.float().mean().item()) / it_cold_mean}
+
+
+def torch_int64():
+    import torch
+    return torch.int64
+
+
 def c5_arm(snop, ctx, stream, args):
-    """BASELINE configs[4] (C5): FNO (4 layers, width 64, 16 modes, lift 2->64, proj 64->128->1, GELU,
-    random-init) on the recast source of 4096 x 1024-cell instances -> warm-started S16 solve, against
-    the zero-guess solve. Device-resident inputs, CUDA-event timing on the solver stream."""
+    """BASELINE configs[4] (C5): the MD-PNOP warm start on 4096 x 1024-cell S16 instances
+    (SURVEY §9 #11): zero guess; the random-init FNO (4 layers, width 64, 16 modes, lift 2->64,
+    proj 64->128->1, GELU) single shot (Eq. 9) and as the full recast fixed point (tol 1e-4, max
+    50); the exact operator (the model-based solve at p*) single shot and full fixed
+    point - the arm that shows the mechanism, since no trained weights ship; and Delta p = 0 with
+    the exact operator (refine <= 2 iterations). Device-resident inputs, CUDA events."""
     import torch
     from paper_2509_01416_b200 import operators as OPS, workloads as W
     p = W.config5()
@@ -60,38 +105,55 @@ def c5_arm(snop, ctx, stream, args):
     cfg = snop.SolverConfig(tolerance=p.tolerance)
     st, ss, src = (torch.from_numpy(a).cuda() for a in (p.sigma_t, p.sigma_s0, p.source))
     fno = snop.SolutionOperator.fno(g, OPS.fno_init(64, 16, 4, 128, OPS.GELU), p.ref_params, ctx=ctx)
+    exact = snop.SolutionOperator.exact(g, p.order, p.ref_params, snop.SolverConfig(tolerance=p.tolerance), ctx=ctx)
 
-    def timed(fn, reps=2):
-        fn()
-        ts = []
-        for _ in range(reps):
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            out = fn()
-            e1.record(stream)
-            ctx.synchronize()
-            ts.append(e0.elapsed_time(e1) / 1e3)
-        return out, float(np.min(ts))
-
-    cold, t_cold = timed(lambda: snop.source_iteration(g, p.order, st, ss, src, cfg, ctx=ctx, sync=False))
-    _, t_op = timed(lambda: fno.predict(src, sync=False))
-    warm, t_warm = timed(lambda: snop.precondition_fixed_source(fno, p.order, st, ss, src, cfg,
-                                                                recast_max_iterations=args.recast_max))
+    cold, t_cold = timed_device(ctx, stream, lambda: snop.source_iteration(g, p.order, st, ss, src, cfg, ctx=ctx,
+                                                                           sync=False))
+    _, t_op = timed_device(ctx, stream, lambda: fno.predict(src, sync=False), reps=3)
     it_cold = cold.iterations.to(torch.int64)
-    it_warm = warm.refine_iterations.to(torch.int64)
+    it_mean = float(it_cold.float().mean().item())
     upd = int(it_cold.sum().item()) * p.n_cells * p.order
     alg = int(it_cold.sum().item()) * p.n_cells * BYTES_PER_CELL_ITER / t_cold / 1e9
-    return {"workload": "C5 4096x1024 S16, p*=(1.0,0.8), tol 1e-8; FNO random-init (seeded), fp32 on tcgen05",
-            "zero_guess_updates_per_sec": upd / t_cold,
-            "zero_guess_roofline": {"bound": "hbm", "achieved": alg, "peak": peaks()[0], "unit": "GB/s",
-                                    "frac": alg / peaks()[0],
-                                    "note": "K1 at S16: 40 B per cell per iteration = 2.5 B per update"},
-            "operator_ms": 1e3 * t_op, "zero_guess_ms": 1e3 * t_cold, "warm_start_ms": 1e3 * t_warm,
-            "solves_per_sec_zero_guess": p.batch / t_cold, "solves_per_sec_warm_start": p.batch / t_warm,
-            "iterations_mean_zero_guess": float(it_cold.float().mean().item()),
-            "iterations_mean_warm_start": float(it_warm.float().mean().item()),
-            "recast_max_iterations": args.recast_max}
+    flops = fno_flops_per_sample(p.n_cells) * p.batch
+    tf32 = tf32_peak()
+    arms = {}
+    for name, op, rmax in (("fno_single_shot", fno, 1), ("fno_recast_fixed_point", fno, 50),
+                           ("exact_single_shot", exact, 1), ("exact_recast_fixed_point", exact, 50)):
+        r, t = timed_device(ctx, stream, lambda: snop.precondition_fixed_source(
+            op, p.order, st, ss, src, cfg, recast_tolerance=1e-4, recast_max_iterations=rmax))
+        arms[name] = warm_stats(r, t, p.batch, it_mean)
+    one = torch.ones_like(st)
+    r, t = timed_device(ctx, stream, lambda: snop.precondition_fixed_source(exact, p.order, one, 0.8 * one, src, cfg))
+    arms["exact_delta_p0"] = warm_stats(r, t, p.batch, it_mean)
+    arms["exact_delta_p0"]["note"] = "instances at p* (Sigma_t = 1, Sigma_s = 0.8): SPEC.md:421 refine <= 2"
+    out = {"workload": "C5 4096x1024 S16, p*=(1.0,0.8), tol 1e-8; FNO random-init (seeded), fp32 on tcgen05 (3xTF32)",
+           "zero_guess_ms": 1e3 * t_cold, "solves_per_sec_zero_guess": p.batch / t_cold,
+           "zero_guess_updates_per_sec": upd / t_cold, "iterations_mean_zero_guess": it_mean,
+           "zero_guess_roofline": {"bound": "hbm", "achieved": alg, "peak": peaks()[0], "unit": "GB/s",
+                                   "frac": alg / peaks()[0],
+                                   "note": "K1 at S16: 40 B per cell per iteration = 2.5 B per update"},
+           "operator_ms": 1e3 * t_op,
+           "operator_roofline": None,
+           "warm_start": arms,
+           # the fixed-point arm is the warm start SURVEY §9 #11 names; single shot beside it
+           "warm_start_ms": arms["fno_recast_fixed_point"]["ms"],
+           "solves_per_sec_warm_start": arms["fno_recast_fixed_point"]["solves_per_sec"],
+           "iterations_mean_warm_start": arms["fno_recast_fixed_point"]["refine_iterations_mean"]}
+    if tf32:
+        out["operator_roofline"] = {
+            "bound": "tensor", "achieved": flops / t_op / 1e12, "peak": tf32, "unit": "TFLOP/s",
+            "frac": flops / t_op / 1e12 / tf32, "flops_per_forward": flops,
+            "frac_3xtf32_issued": 3 * flops / t_op / 1e12 / tf32,
+            "note": "algorithmic FNO FLOPs (SURVEY §8d) / forward time vs the measured tcgen05 TF32 burst peak "
+                    "(profiles/tf32_peak.json); the GEMMs issue 3 TF32 products per fp32 product (3xTF32)"}
+    return out
+
+
+def tf32_peak():
+    p = ROOT / "profiles" / "tf32_peak.json"
+    if not p.exists():
+        return None
+    return float(json.loads(p.read_text())["tf32_tflops"])
 
 
 def eigen_arms(snop, ctx, stream, args):
@@ -240,6 +302,14 @@ def cpu_baseline(problem, n_inst: int, threads: int):
     return upd / dt, dt, upd, r
 
 
+def bench_config(batch, world):
+    """The workload both arms report (identical dicts; the reference arm's per-step CPU sample is
+    described in its cpu_baseline.sample)."""
+    return {"workload": "C2 fixed-source 2048x2000 S32, zero guess, tol 1e-8", "instances_per_gpu": batch,
+            "n_cells": 2000, "order": 32, "l2": "GPU arm: flushed between timed steps (256 MB write)",
+            "parallelism": f"instance-sharded x{world}" if world > 1 else "single GPU"}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -261,8 +331,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE C2)",
-        "config": {"workload": "C2 fixed-source 2048x2000 S32, zero guess, tol 1e-8 (sample of "
-                               f"{n_inst} instances per step)", "instances": n_inst, "n_cells": 2000, "order": 32},
+        "config": bench_config(args.batch, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{n_inst} of the 2048 C2 instances per step (same seeds), full solve"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -344,43 +413,25 @@ def run_gpu(args):
     d2h = p.batch * p.n_cells * 8 + p.batch * 4 + p.batch
 
     # MD-PNOP warm-start arm (BASELINE C2): random-init DeepONet (branch 2000->128x4, trunk 1->128x4,
-    # tanh) on the recast source, then the model-based solve from phi_NO.
+    # tanh) on the recast source, then the model-based solve from phi_NO: single
+    # shot (Eq. 9) and the full recast fixed point (tol 1e-4, max 50).
     warm = None
     if not args.no_warm_start:
         from paper_2509_01416_b200 import operators as OPS
         don = snop.SolutionOperator.deeponet(g, OPS.deeponet_init(p.n_cells), p.ref_params, ctx=ctx)
-        snop.precondition_fixed_source(don, p.order, st, ss, src, cfg, recast_max_iterations=args.recast_max)
-        wt = []
-        for _ in range(max(3, args.steps // 4)):
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            rw = snop.precondition_fixed_source(don, p.order, st, ss, src, cfg, recast_max_iterations=args.recast_max)
-            e1.record(stream)
-            ctx.synchronize()
-            wt.append(e0.elapsed_time(e1) / 1e3)
-        if os.environ.get("SNOP_BENCH_DEBUG"):
-            print("warm step times (ms):", [round(1e3 * x, 3) for x in wt], file=sys.stderr)
-        tp = []
-        for _ in range(3):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            don.predict(src, sync=False)
-            e1.record(stream)
-            ctx.synchronize()
-            tp.append(e0.elapsed_time(e1) / 1e3)
-        ri = rw.refine_iterations.to(torch.int64)
+        it_mean = float(iters.float().mean().item())
+        arms = {}
+        for name, rmax in (("single_shot", 1), ("recast_fixed_point", 50)):
+            rw, tw = timed_device(ctx, stream, lambda: snop.precondition_fixed_source(
+                don, p.order, st, ss, src, cfg, recast_tolerance=1e-4, recast_max_iterations=rmax), reps=3)
+            arms[name] = warm_stats(rw, tw, p.batch, it_mean)
+        _, t_op = timed_device(ctx, stream, lambda: don.predict(src, sync=False), reps=3)
         warm = {"operator": "DeepONet 2000->128x4 / 1->128x4, p=128, tanh, random-init (seeded Xavier), fp32 "
                             "on tcgen05 (3xTF32)",
-                "recast_max_iterations": args.recast_max,
-                "solves_per_sec": p.batch / float(np.median(wt)), "ms_per_step": 1e3 * float(np.median(wt)),
-                "timing": f"median of {len(wt)} device-timed steps",
-                "operator_ms": 1e3 * float(np.min(tp)),
-                "refine_iterations_mean": float(ri.float().mean().item()),
-                "recast_iterations_mean": float(rw.precond_iterations.float().mean().item()),
-                "recast_status_counts": [int((rw.recast_status == k).sum().item()) for k in range(3)],
-                "zero_guess_iterations_mean": float(iters.float().mean().item()),
-                "note": "random-init operator: the warm start does not reduce iterations (DESIGN.md §5)"}
+                "operator_ms": 1e3 * t_op, "zero_guess_iterations_mean": it_mean, "arms": arms,
+                "timing": "min of 3 device-timed solves (CUDA events on the solver stream)",
+                "note": "random-init operator: the warm start does not reduce iterations (DESIGN.md §5); "
+                        "the exact-operator arms of c5_fno_warm_start show the mechanism"}
 
     c5 = None if (args.no_c5 or world > 1) else c5_arm(snop, ctx, stream, args)
     eig = None if (args.no_eigen or world > 1) else eigen_arms(snop, ctx, stream, args)
@@ -398,14 +449,14 @@ def run_gpu(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE C2)",
-        "config": {"workload": "C2 fixed-source 2048x2000 S32, zero guess, tol 1e-8", "instances_per_gpu": p.batch,
-                   "n_cells": p.n_cells, "order": p.order, "l2": "flushed between timed steps (256 MB write)",
-                   "parallelism": f"instance-sharded x{world}" if world > 1 else "single GPU"},
+        "config": bench_config(p.batch, world),
         "solves_per_sec": solves_per_s,
         "iterations": {"mean": float(iters.float().mean().item()), "max": int(iters.max().item()),
                        "min": int(iters.min().item())},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_kind,
+                     "traffic_source": "profile-derived: ncu dram__bytes_read.sum + dram__bytes_write.sum of one "
+                                       "launch of this workload (profiles/k1_dram_bytes.json), not measured here",
                      "note": "algorithmic bytes = 40 B per cell per source iteration; the kernel keeps instance "
                              "state on-chip, so DRAM traffic is far below this; fp64-issue bound (DESIGN.md)"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -454,7 +505,6 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-warm-start", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 FNO warm-start arm")
-    ap.add_argument("--recast-max", type=int, default=1)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -59,15 +59,19 @@ Ctx* Ctx::sub(size_t i) {
 }
 
 void Ctx::settle_loops() {
-  for (const auto& p : pending_loops) launches += (int64_t)h_loop[p.first] * p.second;
-  pending_loops.clear();
+  if (!d_loop_launches) return;
+  unsigned long long n = 0;
+  if (cudaMemcpy(&n, d_loop_launches, sizeof(n), cudaMemcpyDeviceToHost) != cudaSuccess) return;
+  launches += (int64_t)(n - loop_launches_seen);
+  loop_launches_seen = n;
 }
 
 Ctx::~Ctx() {
   if (stream) cudaStreamSynchronize(stream);
   for (auto& g : graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
-  if (h_loop) cudaFreeHost(h_loop);
+  if (d_loop_launches) cudaFree(d_loop_launches);
+  if (side) cudaStreamDestroy(side);
   for (Ctx* c : subs) delete c;
   for (auto& b : slots)
     if (b.ptr) cudaFree(b.ptr);

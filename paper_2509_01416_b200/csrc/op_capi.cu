@@ -466,11 +466,14 @@ __global__ void recast_update(int n, int norm, double tol, const int* __restrict
 // Loop control of a device-looped iteration (WHILE conditional graph node): counts the iteration
 // and continues while any instance is active and the cap is not reached.
 __global__ void loop_ctl(cudaGraphConditionalHandle h, int* __restrict__ it_done, const int* __restrict__ n_active,
-                         int max_it) {
+                         int max_it, int n_body, unsigned long long* __restrict__ launches) {
   const int it = *it_done + 1;
   *it_done = it;
+  *launches += (unsigned long long)n_body;  // this pass's kernels (loop bodies run one at a time)
   cudaGraphSetConditional(h, (*n_active > 0 && it < max_it) ? 1u : 0u);
 }
+
+__global__ void loop_arm(cudaGraphConditionalHandle h) { cudaGraphSetConditional(h, 1u); }
 
 __global__ void fill_i32(int n, int32_t v, int32_t* __restrict__ out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = v;
@@ -568,10 +571,12 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
           cudaMalloc(&op.css, rowsN * sizeof(double)) != cudaSuccess)
         return cuda_status("cudaMalloc exact-op materials", cudaErrorMemoryAllocation);
       op.cst_n = rowsN;
-      fill_f64<<<grid_for(ctx, rowsN), 256, 0, ctx.stream>>>(rowsN, op.tstar, op.cst);
-      fill_f64<<<grid_for(ctx, rowsN), 256, 0, ctx.stream>>>(rowsN, op.sstar, op.css);
-      ctx.launches += 2;
     }
+    // filled on every call: a device loop may capture this call into a graph that is discarded
+    // and captured again, so a fill done only on allocation could be lost
+    fill_f64<<<grid_for(ctx, rowsN), 256, 0, ctx.stream>>>(rowsN, op.tstar, op.cst);
+    fill_f64<<<grid_for(ctx, rowsN), 256, 0, ctx.stream>>>(rowsN, op.sstar, op.css);
+    ctx.launches += 2;
     int32_t* it = static_cast<int32_t*>(ctx.slot(40, (size_t)B * sizeof(int32_t)));
     uint8_t* cv = static_cast<uint8_t*>(ctx.slot(41, (size_t)B));
     // (active: a device loop's frozen instances are skipped; the neural operators run whole batches)
@@ -748,14 +753,71 @@ snop_status drain(Ctx& ctx) {
   return SNOP_OK;
 }
 
-// Runs `body` (which enqueues one iteration on ctx.stream and ends with loop_ctl on handle h) as
-// the body of a WHILE conditional node of a CUDA graph: the iteration loop runs on the device with
-// no host round trip per iteration. The executable is cached on the context under `key` (every
-// pointer and scalar the body captures, plus the workspace generation), so repeated calls with the
-// same buffers relaunch it directly. `d_it` counts iterations (copied to pinned memory for the
-// launch accounting).
+// Runs `body` (which enqueues one iteration on ctx.stream and ends with loop_ctl on the handle it
+// is given) as the body of a WHILE conditional node of a CUDA graph: the iteration loop runs on
+// the device with no host round trip per iteration. Top level: the executable is cached on the
+// context under `key` (every pointer and scalar the body captures, plus the workspace
+// generation), so repeated calls with the same buffers relaunch it directly. Nested (ctx.stream is
+// being captured by an enclosing device loop): the conditional node is added to the enclosing
+// body graph and this body is captured into it through the context's side stream.
+// The body returns its kernel count through `n_body` for loop_ctl's launch accounting.
 template <class Body>
-snop_status device_loop(Ctx& ctx, std::vector<uint64_t> key, const int* d_it, Body&& body) {
+snop_status device_loop(Ctx& ctx, std::vector<uint64_t> key, Body&& body) {
+  if (!ctx.d_loop_launches) {
+    if (cudaMalloc(&ctx.d_loop_launches, sizeof(unsigned long long)) != cudaSuccess)
+      return cuda_status("cudaMalloc", cudaErrorMemoryAllocation);
+    cudaMemsetAsync(ctx.d_loop_launches, 0, sizeof(unsigned long long), ctx.stream);
+  }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  SNOP_TRY(cuda_status("capture status", cudaStreamIsCapturing(ctx.stream, &cs)));
+  const bool nested = cs == cudaStreamCaptureStatusActive;
+  // capture `body` into the body graph of a new WHILE node of graph g (after deps)
+  auto build = [&](cudaGraph_t g, const cudaGraphNode_t* deps, size_t ndeps, cudaStream_t cap,
+                   cudaGraphNode_t* node_out, cudaGraphConditionalHandle h) -> snop_status {
+    cudaError_t e = cudaSuccess;
+    cudaGraphNodeParams np{};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    if (e == cudaSuccess) e = cudaGraphAddNode(node_out, g, deps, ndeps, &np);
+    if (e != cudaSuccess) return cuda_status("device loop node", e);
+    const cudaStream_t outer = ctx.stream;
+    ctx.stream = cap;
+    e = cudaStreamBeginCaptureToGraph(cap, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeRelaxed);
+    snop_status bs = SNOP_OK;
+    if (e == cudaSuccess) {
+      const int64_t l0 = ctx.launches;
+      bs = body(h);
+      ctx.launches = l0;  // captured, not launched: counted on the device per pass
+      cudaGraph_t out = nullptr;
+      e = cudaStreamEndCapture(cap, &out);
+    }
+    ctx.stream = outer;
+    if (bs != SNOP_OK) return bs;
+    return cuda_status("device loop capture", e);
+  };
+  if (nested) {
+    if (!ctx.side && cudaStreamCreateWithFlags(&ctx.side, cudaStreamNonBlocking) != cudaSuccess)
+      return cuda_status("side stream", cudaErrorUnknown);
+    cudaGraph_t g = nullptr;
+    SNOP_TRY(cuda_status("capture info", cudaStreamGetCaptureInfo(ctx.stream, &cs, nullptr, &g, nullptr, nullptr)));
+    // A nested handle's default value is applied only when the top-level graph is launched, so
+    // every pass of the enclosing body re-arms it explicitly before the loop node.
+    cudaGraphConditionalHandle h{};
+    SNOP_TRY(cuda_status("conditional handle", cudaGraphConditionalHandleCreate(&h, g, 1, 0)));
+    loop_arm<<<1, 1, 0, ctx.stream>>>(h);
+    ctx.launches++;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    SNOP_TRY(cuda_status("capture info", cudaStreamGetCaptureInfo(ctx.stream, &cs, nullptr, &g, &deps, &ndeps)));
+    std::vector<cudaGraphNode_t> dv(deps, deps + ndeps);  // (the returned array is invalidated below)
+    cudaGraphNode_t node;
+    SNOP_TRY(build(g, dv.data(), dv.size(), ctx.side, &node, h));
+    return cuda_status("capture dependencies",
+                       cudaStreamUpdateCaptureDependencies(ctx.stream, &node, 1, cudaStreamSetCaptureDependencies));
+  }
   key.push_back(ctx.slot_gen);
   Ctx::LoopGraph* lg = nullptr;
   for (auto& g : ctx.graphs)
@@ -763,64 +825,40 @@ snop_status device_loop(Ctx& ctx, std::vector<uint64_t> key, const int* d_it, Bo
   if (!lg) {
     if (ctx.graphs.size() >= 8) {  // evict the oldest (it may still be running: wait first)
       cudaStreamSynchronize(ctx.stream);
-      ctx.settle_loops();
       cudaGraphExecDestroy(ctx.graphs.front().exec);
       ctx.graphs.erase(ctx.graphs.begin());
     }
+    // A body may size workspaces on first use while it is captured; nodes captured before a
+    // reallocation would hold stale pointers, so such a graph is discarded and captured again.
     cudaGraph_t g = nullptr;
-    cudaError_t e = cudaGraphCreate(&g, 0);
-    cudaGraphConditionalHandle h{};
-    if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
-    cudaGraphNodeParams np{};
-    np.type = cudaGraphNodeTypeConditional;
-    np.conditional.handle = h;
-    np.conditional.type = cudaGraphCondTypeWhile;
-    np.conditional.size = 1;
-    cudaGraphNode_t node;
-    if (e == cudaSuccess) e = cudaGraphAddNode(&node, g, nullptr, 0, &np);
-    if (e != cudaSuccess) {
-      if (g) cudaGraphDestroy(g);
-      return cuda_status("device loop graph", e);
-    }
-    cudaGraph_t bodyg = np.conditional.phGraph_out[0];
-    e = cudaStreamBeginCaptureToGraph(ctx.stream, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
-    if (e != cudaSuccess) {
+    snop_status bs = SNOP_OK;
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      const uint64_t gen0 = ctx.slot_gen;
+      SNOP_TRY(cuda_status("device loop graph", cudaGraphCreate(&g, 0)));
+      cudaGraphNode_t node;
+      cudaGraphConditionalHandle h{};
+      SNOP_TRY(cuda_status("conditional handle", cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault)));
+      bs = build(g, nullptr, 0, ctx.stream, &node, h);
+      if (bs == SNOP_OK && ctx.slot_gen == gen0) break;
       cudaGraphDestroy(g);
-      return cuda_status("device loop capture", e);
+      g = nullptr;
+      cudaGetLastError();  // a capture broken by an allocation leaves a sticky-free error state
     }
-    const int64_t l0 = ctx.launches;
-    const snop_status bs = body(h);
-    const int64_t nb = ctx.launches - l0;
-    ctx.launches = l0;  // captured, not launched
-    cudaGraph_t out = nullptr;
-    e = cudaStreamEndCapture(ctx.stream, &out);
-    if (bs != SNOP_OK || e != cudaSuccess) {
-      cudaGraphDestroy(g);
-      return bs != SNOP_OK ? bs : cuda_status("device loop capture", e);
-    }
+    if (!g) return bs != SNOP_OK ? bs : cuda_status("device loop capture", cudaErrorStreamCaptureInvalidated);
+    key.back() = ctx.slot_gen;
     cudaGraphExec_t ex = nullptr;
-    e = cudaGraphInstantiate(&ex, g, 0);
+    const cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return cuda_status("device loop instantiate", e);
-    ctx.graphs.push_back({key, ex, nb});
+    ctx.graphs.push_back({key, ex});
     lg = &ctx.graphs.back();
   }
-  SNOP_TRY(cuda_status("device loop launch", cudaGraphLaunch(lg->exec, ctx.stream)));
-  if (!ctx.h_loop && cudaMallocHost(&ctx.h_loop, Ctx::kLoopSlots * sizeof(int)) != cudaSuccess)
-    return cuda_status("cudaMallocHost", cudaErrorMemoryAllocation);
-  if ((int)ctx.pending_loops.size() >= Ctx::kLoopSlots) {
-    SNOP_TRY(cuda_status("synchronize", cudaStreamSynchronize(ctx.stream)));
-    ctx.settle_loops();
-  }
-  const int slotn = (int)ctx.pending_loops.size();
-  cudaMemcpyAsync(ctx.h_loop + slotn, d_it, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream);
-  ctx.pending_loops.push_back({slotn, lg->body_launches});
-  return SNOP_OK;
+  return cuda_status("device loop launch", cudaGraphLaunch(lg->exec, ctx.stream));
 }
 
 snop_status recast_fp_dev(Ctx& ctx, snop_op& op, int B, const double* S, const double* st, const double* ss,
                           double tol, int max_it, int norm, const double* init, double* phi, int32_t* iters,
-                          int32_t* status) {
+                          int32_t* status, const uint8_t* outer_active = nullptr) {
   const int n = op.grid.n_cells;
   const size_t N = (size_t)B * n;
   double* phi0 = static_cast<double*>(ctx.slot(50, N * sizeof(double)));
@@ -836,7 +874,10 @@ snop_status recast_fp_dev(Ctx& ctx, snop_op& op, int B, const double* S, const d
   maxabs_rows<<<B, 256, 0, ctx.stream>>>(n, phi0, norm0);
   ctx.launches++;
   SNOP_TRY(cuda_status("copy", cudaMemcpyAsync(phi, phi0, N * sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream)));
-  cudaMemsetAsync(active, 1, (size_t)B, ctx.stream);
+  if (outer_active)  // instances an enclosing loop has frozen do not iterate
+    cudaMemcpyAsync(active, outer_active, (size_t)B, cudaMemcpyDeviceToDevice, ctx.stream);
+  else
+    cudaMemsetAsync(active, 1, (size_t)B, ctx.stream);
   cudaMemsetAsync(iters, 0, (size_t)B * sizeof(int32_t), ctx.stream);
   cudaMemsetAsync(it_done, 0, sizeof(int), ctx.stream);
   fill_i32<<<grid_for(ctx, (size_t)B), 256, 0, ctx.stream>>>(B, SNOP_RECAST_MAXED, status);
@@ -845,13 +886,14 @@ snop_status recast_fp_dev(Ctx& ctx, snop_op& op, int B, const double* S, const d
   // One iteration per pass of the device loop: recast source, operator
   // forward, per-instance update/freeze, loop control.
   auto body = [&](cudaGraphConditionalHandle h) -> snop_status {
+    const int64_t l0 = ctx.launches;
     SNOP_TRY(launch_recast(ctx, N, S, phi, st, ss, op.tstar, op.sstar, s));
     SNOP_TRY(op_predict_dev(ctx, op, B, s, nx, active));
     cudaMemsetAsync(n_active, 0, sizeof(int), ctx.stream);
     recast_update<<<B, 256, 0, ctx.stream>>>(n, norm, tol, it_done, nx, phi, phi0, norm0, active, iters, status,
                                              n_active);
-    loop_ctl<<<1, 1, 0, ctx.stream>>>(h, it_done, n_active, max_it);
-    ctx.launches += 2;
+    const int nb = (int)(ctx.launches - l0) + 2;
+    loop_ctl<<<1, 1, 0, ctx.stream>>>(h, it_done, n_active, max_it, nb, ctx.d_loop_launches);
     return cuda_status("recast iteration", cudaGetLastError());
   };
   uint64_t tolbits;
@@ -859,8 +901,8 @@ snop_status recast_fp_dev(Ctx& ctx, snop_op& op, int B, const double* S, const d
   const std::vector<uint64_t> key = {1, (uint64_t)(uintptr_t)&op, op.serial, (uint64_t)B, (uint64_t)(uintptr_t)S,
                                      (uint64_t)(uintptr_t)st, (uint64_t)(uintptr_t)ss, (uint64_t)(uintptr_t)phi,
                                      (uint64_t)(uintptr_t)iters, (uint64_t)(uintptr_t)status, tolbits,
-                                     (uint64_t)max_it, (uint64_t)norm, op.gen};
-  return device_loop(ctx, key, it_done, body);
+                                     (uint64_t)max_it, (uint64_t)norm, op.gen, (uint64_t)(uintptr_t)outer_active};
+  return device_loop(ctx, key, body);
 }
 
 snop_status check_op(snop_ctx* ctx, snop_op* op) {
@@ -1016,7 +1058,8 @@ __global__ void hy_group_out(int g, int G, int Nc, const double* __restrict__ ph
 }
 
 // k_new = k F1 (old flux had unit fission integral), phi /= F1, convergence on dk and dphi.
-__global__ void __launch_bounds__(HY_THREADS) hy_outer_end(int G, int Nc, double dx, int outer_it, double tol_k,
+__global__ void __launch_bounds__(HY_THREADS) hy_outer_end(int G, int Nc, double dx, const int* __restrict__ outer_done,
+                                                           double tol_k,
                                                            double tol_phi, int norm, const double* __restrict__ nsf,
                                                            double* __restrict__ phi, const double* __restrict__ old,
                                                            double* __restrict__ k, uint8_t* __restrict__ active,
@@ -1025,6 +1068,7 @@ __global__ void __launch_bounds__(HY_THREADS) hy_outer_end(int G, int Nc, double
   __shared__ double sh[HY_THREADS / 32];
   const int b = blockIdx.x;
   if (!active[b]) return;
+  const int outer_it = *outer_done + 1;  // this outer iteration (the device loop counts them)
   const size_t GN = (size_t)G * Nc;
   double* p = phi + b * GN;
   const double F1 = hy_fission_integral(G, Nc, dx, nsf + b * GN, p, sh);
@@ -1115,32 +1159,51 @@ snop_status hybrid_eigen_dev(Ctx& ctx, snop_op& op, int algorithm, int order, in
   hy_init<<<B, HY_THREADS, 0, s>>>(G, Nc, dx, st, nsf, phi1, o.k1, active, o.fb, div, o.outer1, o.inner1,
                                    ctx.d_flags);
   ctx.launches++;
-  for (int outer = 1; outer <= cfg.max_outer; ++outer) {
-    hy_outer_begin<<<B, HY_THREADS, 0, s>>>(G, Nc, nsf, phi1, old, fiss, active);
+  // Stage 1: the outer loop runs on the device (WHILE conditional node); each group's recast fixed
+  // point is a nested device loop. Instances whose stage 1 has finished are frozen (skipped).
+  int* outer_done = static_cast<int*>(ctx.slot(99, sizeof(int)));
+  if (!outer_done) return cuda_status("workspace", cudaErrorMemoryAllocation);
+  cudaMemsetAsync(outer_done, 0, sizeof(int), s);
+  auto body = [&](cudaGraphConditionalHandle h) -> snop_status {
+    const cudaStream_t cs = ctx.stream;  // (the capture stream of this body)
+    const int64_t l0 = ctx.launches;
+    hy_outer_begin<<<B, HY_THREADS, 0, cs>>>(G, Nc, nsf, phi1, old, fiss, active);
     ctx.launches++;
     for (int g = 0; g < G; ++g) {
-      hy_group_in<<<B, HY_THREADS, 0, s>>>(g, G, Nc, chi, o.k1, st, ss0, ss1, phi1, fiss, qext, stg, ssg, s1g, phig);
+      hy_group_in<<<B, HY_THREADS, 0, cs>>>(g, G, Nc, chi, o.k1, st, ss0, ss1, phi1, fiss, qext, stg, ssg, s1g, phig);
       ctx.launches++;
-      SNOP_TRY(recast_fp_dev(ctx, op, B, qext, stg, ssg, rtol, rmax, cfg.norm, phig, pred, rit, rst));
+      SNOP_TRY(recast_fp_dev(ctx, op, B, qext, stg, ssg, rtol, rmax, cfg.norm, phig, pred, rit, rst, active));
       const double* result = pred;
-      if (algorithm == 1) {
+      if (algorithm == 1) {  // (instances whose stage 1 has finished are skipped)
         SNOP_TRY(launch_source_iteration(ctx, op.grid, order, B, stg, ssg, s1g, qext, cfg, pred, refined, nullptr,
-                                         sit, scv));
+                                         sit, scv, nullptr, nullptr, active));
         result = refined;
       }
-      hy_group_out<<<B, HY_THREADS, 0, s>>>(g, G, Nc, result, phi1, active, rit, algorithm == 1 ? sit : nullptr,
-                                            rst, o.inner1, div);
+      hy_group_out<<<B, HY_THREADS, 0, cs>>>(g, G, Nc, result, phi1, active, rit, algorithm == 1 ? sit : nullptr,
+                                             rst, o.inner1, div);
       ctx.launches++;
     }
-    cudaMemsetAsync(n_active, 0, sizeof(int), s);
-    hy_outer_end<<<B, HY_THREADS, 0, s>>>(G, Nc, dx, outer, cfg.tolerance_k, cfg.tolerance_phi, cfg.norm, nsf, phi1,
-                                          old, o.k1, active, o.fb, o.outer1, n_active);
-    ctx.launches++;
-    int h_active = 0;
-    cudaMemcpyAsync(&h_active, n_active, sizeof(int), cudaMemcpyDeviceToHost, s);
-    SNOP_TRY(cuda_status("hybrid stage 1", cudaStreamSynchronize(s)));
-    if (h_active == 0) break;
-  }
+    cudaMemsetAsync(n_active, 0, sizeof(int), cs);
+    hy_outer_end<<<B, HY_THREADS, 0, cs>>>(G, Nc, dx, outer_done, cfg.tolerance_k, cfg.tolerance_phi, cfg.norm,
+                                           nsf, phi1, old, o.k1, active, o.fb, o.outer1, n_active);
+    const int nb = (int)(ctx.launches - l0) + 2;
+    loop_ctl<<<1, 1, 0, cs>>>(h, outer_done, n_active, cfg.max_outer, nb, ctx.d_loop_launches);
+    return cuda_status("hybrid stage 1", cudaGetLastError());
+  };
+  uint64_t bits[4];
+  std::memcpy(&bits[0], &rtol, 8);
+  std::memcpy(&bits[1], &cfg.tolerance, 8);
+  std::memcpy(&bits[2], &cfg.tolerance_k, 8);
+  std::memcpy(&bits[3], &cfg.tolerance_phi, 8);
+  const std::vector<uint64_t> key = {2, (uint64_t)(uintptr_t)&op, op.serial, op.gen, (uint64_t)algorithm,
+                                     (uint64_t)order, (uint64_t)B, (uint64_t)G, (uint64_t)(uintptr_t)st,
+                                     (uint64_t)(uintptr_t)ss0, (uint64_t)(uintptr_t)ss1, (uint64_t)(uintptr_t)nsf,
+                                     (uint64_t)(uintptr_t)chi, (uint64_t)(uintptr_t)o.k1,
+                                     (uint64_t)(uintptr_t)o.fb, (uint64_t)(uintptr_t)o.outer1,
+                                     (uint64_t)(uintptr_t)o.inner1, bits[0], bits[1], bits[2], bits[3],
+                                     (uint64_t)rmax, (uint64_t)cfg.max_outer, (uint64_t)cfg.max_inner,
+                                     (uint64_t)cfg.norm, (uint64_t)cfg.bc_left, (uint64_t)cfg.bc_right};
+  SNOP_TRY(device_loop(ctx, key, body));
   hy_stage2_init<<<B, HY_THREADS, 0, s>>>(G, Nc, phi1, o.k1, k0, o.fb, div);
   ctx.launches++;
   return launch_power_iteration(ctx, op.grid, order, B, G, st, ss0, ss1, nsf, chi, cfg, k0, phi1, o.k, o.phi,

@@ -35,18 +35,17 @@ struct Ctx {
   std::vector<double> grf_key;  // (length, n_cells, variance, length scale, jitter) of the cached GRF factor
   void* slot(size_t i, size_t bytes);  // grow-only
   // Device-looped iterations (a CUDA graph whose WHILE conditional node re-runs a captured body
-  // until a kernel of the body clears the condition): executables cached by their parameters, so a
-  // repeated call relaunches without re-capture. Launch accounting: each launched loop copies its
-  // iteration count into h_loop; synchronisation adds count x body kernels to `launches`.
+  // until a kernel of the body clears the condition; loops nest): executables cached by their
+  // parameters, so a repeated call relaunches without re-capture. Launch accounting: each pass of
+  // a loop body adds its kernel count to a device counter; synchronisation folds it into launches.
   struct LoopGraph {
     std::vector<uint64_t> key;
     cudaGraphExec_t exec = nullptr;
-    int64_t body_launches = 0;
   };
   std::vector<LoopGraph> graphs;
-  int* h_loop = nullptr;  // pinned, kLoopSlots counters
-  static constexpr int kLoopSlots = 64;
-  std::vector<std::pair<int, int64_t>> pending_loops;  // (h_loop index, body kernels)
+  unsigned long long* d_loop_launches = nullptr;  // device counter (kernels launched by loop bodies)
+  unsigned long long loop_launches_seen = 0;
+  cudaStream_t side = nullptr;                    // capture stream for nested loop bodies
   void settle_loops();  // call after the stream has been synchronised
   // Sub-contexts (own stream, flag word and workspace) for host-memspace calls that pipeline
   // H2D / compute / D2H over chunks of the batch; created on first use, owned by this context.
