@@ -208,6 +208,47 @@ def eigen_arms(snop, ctx, stream, args):
     return out
 
 
+def hybrid_arms(snop, ctx, stream, args):
+    """SP / CP hybrid eigen solves (paper Eqs. A5-A8) on the first
+    args.hybrid_batch instances of C3 (512 x 4096 x S32 single-group eigen): stage 1 = power
+    iteration whose within-group solve is the operator's recast fixed point (SP) or the operator
+    prediction refined by a model-based solve (CP), stage 2 = model-based power iteration from
+    (k_NO, phi_NO); against the cold model-based power iteration of the same instances. Operators:
+    the exact operator at p* = (1.0, 0.5) (the model-based solve) and the random-init
+    FNO. Stage 1's outer loop runs on the device (nested CUDA-graph loops)."""
+    import torch
+    from paper_2509_01416_b200 import operators as OPS, workloads as W
+    p = W.config3().subset(np.arange(args.hybrid_batch))
+    g = snop.Grid1D(p.length, p.n_cells)
+    cfg = snop.SolverConfig(tolerance=p.tolerance_inner, tolerance_k=p.tolerance_k, tolerance_phi=p.tolerance_phi,
+                            boundary_left=p.bc_left, boundary_right=p.bc_right)
+    dev = [torch.from_numpy(a).cuda() for a in (p.sigma_t, p.sigma_s0, p.nu_sigma_f, p.chi)]
+    cold, t_cold = timed_device(ctx, stream, lambda: snop.power_iteration(g, p.order, *dev, cfg, ctx=ctx, sync=False))
+    inner_cold = int(cold.total_inner_iterations.sum().item())
+    ops = {"exact": snop.SolutionOperator.exact(g, p.order, (1.0, 0.5), snop.SolverConfig(
+               tolerance=p.tolerance_inner, boundary_left=p.bc_left, boundary_right=p.bc_right), ctx=ctx),
+           "fno": snop.SolutionOperator.fno(g, OPS.fno_init(64, 16, 4, 128, OPS.GELU), (1.0, 0.5), ctx=ctx)}
+    out = {"workload": f"C3 first {p.batch} instances x 4096 cells x S32, reflective-left, tol_k 1e-8 tol_phi 1e-7",
+           "cold": {"ms": 1e3 * t_cold, "solves_per_sec": p.batch / t_cold,
+                    "outer_mean": float(cold.outer_iterations.float().mean().item()), "inner_total": inner_cold}}
+    # (SP with the exact operator is left to tools/md_pnop_probe.py: its stage 1 takes ~500 outers
+    # of exact-operator fixed points, ~110 s for 32 instances - profiles/r2_md_pnop_c3_hybrid_probe.txt)
+    for opname, alg in (("exact", "cp"), ("fno", "sp"), ("fno", "cp")):
+        op = ops[opname]
+        if True:
+            fn = getattr(snop, f"{alg}_eigen")
+            r, t = timed_device(ctx, stream, lambda: fn(op, p.order, *dev, cfg), reps=1)
+            out[f"{alg}_{opname}"] = {
+                "ms": 1e3 * t, "solves_per_sec": p.batch / t,
+                "stage1_outer_mean": float(r.stage1_outer.float().mean().item()),
+                "stage2_outer_mean": float(r.stage2_outer.float().mean().item()),
+                "stage2_inner_total": int(r.stage2_inner.sum().item()),
+                "stage2_inner_ratio_vs_cold": int(r.stage2_inner.sum().item()) / max(inner_cold, 1),
+                "fallback_count": int(r.fallback.sum().item()),
+                "k_max_rel_diff_vs_cold": float(((r.k - cold.k).abs() / cold.k).max().item())}
+    return out
+
+
 def fp64_peak():
     p = ROOT / "profiles" / "fp64_peak.json"
     if not p.exists():
@@ -435,6 +476,7 @@ def run_gpu(args):
 
     c5 = None if (args.no_c5 or world > 1) else c5_arm(snop, ctx, stream, args)
     eig = None if (args.no_eigen or world > 1) else eigen_arms(snop, ctx, stream, args)
+    hyb = None if (args.no_hybrid or world > 1) else hybrid_arms(snop, ctx, stream, args)
 
     if rank != 0:
         if world > 1:
@@ -479,6 +521,8 @@ def run_gpu(args):
         line["c5_fno_warm_start"] = c5
     if eig is not None:
         line.update(eig)
+    if hyb is not None:
+        line["c3_hybrid_eigen"] = hyb
     if not args.no_cpu_baseline and world == 1:
         from tests import oracle_lib as O
         th = O.hardware_threads()
@@ -505,6 +549,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-warm-start", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 FNO warm-start arm")
+    ap.add_argument("--no-hybrid", action="store_true", help="skip the C3 SP/CP hybrid eigen arm")
+    ap.add_argument("--hybrid-batch", type=int, default=32)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
