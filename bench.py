@@ -235,17 +235,16 @@ def hybrid_arms(snop, ctx, stream, args):
     # of exact-operator fixed points, ~110 s for 32 instances - profiles/r2_md_pnop_c3_hybrid_probe.txt)
     for opname, alg in (("exact", "cp"), ("fno", "sp"), ("fno", "cp")):
         op = ops[opname]
-        if True:
-            fn = getattr(snop, f"{alg}_eigen")
-            r, t = timed_device(ctx, stream, lambda: fn(op, p.order, *dev, cfg), reps=1)
-            out[f"{alg}_{opname}"] = {
-                "ms": 1e3 * t, "solves_per_sec": p.batch / t,
-                "stage1_outer_mean": float(r.stage1_outer.float().mean().item()),
-                "stage2_outer_mean": float(r.stage2_outer.float().mean().item()),
-                "stage2_inner_total": int(r.stage2_inner.sum().item()),
-                "stage2_inner_ratio_vs_cold": int(r.stage2_inner.sum().item()) / max(inner_cold, 1),
-                "fallback_count": int(r.fallback.sum().item()),
-                "k_max_rel_diff_vs_cold": float(((r.k - cold.k).abs() / cold.k).max().item())}
+        fn = getattr(snop, f"{alg}_eigen")
+        r, t = timed_device(ctx, stream, lambda: fn(op, p.order, *dev, cfg), reps=1)
+        out[f"{alg}_{opname}"] = {
+            "ms": 1e3 * t, "solves_per_sec": p.batch / t,
+            "stage1_outer_mean": float(r.stage1_outer.float().mean().item()),
+            "stage2_outer_mean": float(r.stage2_outer.float().mean().item()),
+            "stage2_inner_total": int(r.stage2_inner.sum().item()),
+            "stage2_inner_ratio_vs_cold": int(r.stage2_inner.sum().item()) / max(inner_cold, 1),
+            "fallback_count": int(r.fallback.sum().item()),
+            "k_max_rel_diff_vs_cold": float(((r.k - cold.k).abs() / cold.k).max().item())}
     return out
 
 
