@@ -114,9 +114,9 @@ snop_status snop_ctx_destroy(snop_ctx* ctx);
  * field's zero value means "automatic" (the measured default); results of a solve never depend on
  * the execution options except where noted (the kernels are deterministic for a given shape).
  *   cell_cluster   K1/K2 cell split over a thread-block cluster: 0 auto (one CTA per instance up to
- *                  4096 cells, the smallest cluster that holds the slab above), 1 never, 2/4/8/16
- *                  force that cluster size. Instances above 16 * 4096 cells use the streaming
- *                  multi-CTA path regardless.
+ *                  4096 cells, the smallest cluster that holds the slab up to 16384 cells, the
+ *                  streaming kernel beyond), 1 never, 2/4/8 force that cluster size, -1 force the
+ *                  streaming kernel (tile-by-tile sweep, per-cell state in a device workspace).
  *   pair_split     single-group eigen pair-split cluster size: 0 auto (8 with the tail split), -1
  *                  off, 2..8 force.
  *   pi_tail_cap    outer iterations of the tail split's first phase: 0 auto (48), -1 off (one launch).

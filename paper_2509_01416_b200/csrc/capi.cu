@@ -156,7 +156,7 @@ snop_status invalid(const std::string& m) {
 snop_status check_grid(const snop_grid* g, int order) {
   if (!g) return invalid("grid is NULL");
   if (!(g->length_cm > 0.0) || g->n_cells < 1) return invalid("grid: length and n_cells must be positive");
-  if (g->n_cells > kMaxCells) return invalid("grid: n_cells exceeds the cluster sweep limit (16384)");
+  if (g->n_cells > kMaxCellsAny) return invalid("grid: n_cells exceeds 2^26");
   if (order < 2 || order > 128 || order % 2) return invalid("quadrature order must be even in [2,128]");
   return SNOP_OK;
 }
@@ -307,8 +307,8 @@ snop_status snop_ctx_synchronize(snop_ctx* ctx) {
 snop_status snop_ctx_set_options(snop_ctx* ctx, const snop_ctx_options* o) {
   if (!ctx || !o) return invalid("ctx/options is NULL");
   const int cc = o->cell_cluster;
-  if (!(cc == 0 || cc == 1 || cc == 2 || cc == 4 || cc == 8 || cc == 16))
-    return invalid("options: cell_cluster must be 0, 1, 2, 4, 8 or 16");
+  if (!(cc == -1 || cc == 0 || cc == 1 || cc == 2 || cc == 4 || cc == 8))
+    return invalid("options: cell_cluster must be -1, 0, 1, 2, 4 or 8");
   if (o->pair_split < -1 || o->pair_split > 8 || o->pair_split == 1)
     return invalid("options: pair_split must be -1, 0 or 2..8");
   if (o->pi_tail_cap < -1) return invalid("options: pi_tail_cap must be >= -1");

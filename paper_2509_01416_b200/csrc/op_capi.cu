@@ -1210,9 +1210,178 @@ snop_status hybrid_eigen_dev(Ctx& ctx, snop_op& op, int algorithm, int order, in
                                 pi_old, o.outer2, o.inner2, o.conv);
 }
 
+
+// ---- power iteration for slabs beyond the resident kernels ------------------
+// The fused K2 kernel keeps an instance in one CTA's (or cluster's) shared memory; above 16384
+// cells the outer loop runs instead as a device loop (WHILE graph) over the same bookkeeping the
+// hybrid stage 1 uses - fission density, group sources (Gauss-Seidel, newest flux, upscatter),
+// warm-started inner solves on the streaming K1, k update, renormalisation, dual test - with
+// K2's validation and error semantics.
+__global__ void __launch_bounds__(HY_THREADS) pi_big_init(int G, int Nc, double dx, const double* __restrict__ st,
+                                                          const double* __restrict__ nsf, const double* __restrict__ k0,
+                                                          const double* __restrict__ phi0, double* __restrict__ phi,
+                                                          double* __restrict__ k, uint8_t* __restrict__ active,
+                                                          uint8_t* __restrict__ conv, int32_t* __restrict__ outer,
+                                                          int64_t* __restrict__ inner, int* __restrict__ flags) {
+  __shared__ double sh[HY_THREADS / 32];
+  const int b = blockIdx.x;
+  const size_t GN = (size_t)G * Nc;
+  double* p = phi + b * GN;
+  int bad = 0;
+  for (size_t i = threadIdx.x; i < GN; i += HY_THREADS) {
+    p[i] = phi0 ? phi0[b * GN + i] : 1.0;
+    bad |= !(st[b * GN + i] > 0.0);
+  }
+  const double kb = k0 ? k0[b] : 1.0;
+  bad = __syncthreads_or(bad) || !(kb > 0.0);
+  const double F = bad ? 1.0 : hy_fission_integral(G, Nc, dx, nsf + b * GN, p, sh);
+  const bool degen = !bad && (!(F != 0.0) || !isfinite(F));
+  if (!bad && !degen)
+    for (size_t i = threadIdx.x; i < GN; i += HY_THREADS) p[i] /= F;
+  if (threadIdx.x == 0) {
+    if (bad) atomicOr(flags, FLAG_BAD_SIGMA_T);
+    if (degen) atomicOr(flags, FLAG_DEGENERATE);
+    k[b] = (bad || degen) ? __longlong_as_double(0x7ff8000000000000ll) : kb;
+    active[b] = (bad || degen) ? 0 : 1;
+    conv[b] = 0;
+    outer[b] = 0;
+    inner[b] = 0;
+  }
+}
+
+__global__ void pi_big_group_out(int g, int G, int Nc, const double* __restrict__ phig, double* __restrict__ phi,
+                                 const uint8_t* __restrict__ active, const int32_t* __restrict__ it,
+                                 int64_t* __restrict__ inner) {
+  const int b = blockIdx.x;
+  if (!active[b]) return;
+  const size_t GN = (size_t)G * Nc;
+  for (int i = threadIdx.x; i < Nc; i += blockDim.x) phi[b * GN + (size_t)g * Nc + i] = phig[(size_t)b * Nc + i];
+  if (threadIdx.x == 0) inner[b] += it[b];
+}
+
+__global__ void __launch_bounds__(HY_THREADS) pi_big_outer_end(int G, int Nc, double dx, const int* __restrict__ outer_done,
+                                                               double tol_k, double tol_phi, int norm,
+                                                               const double* __restrict__ nsf, double* __restrict__ phi,
+                                                               const double* __restrict__ old, double* __restrict__ k,
+                                                               uint8_t* __restrict__ active, uint8_t* __restrict__ conv,
+                                                               int32_t* __restrict__ outer, int* __restrict__ n_active,
+                                                               int* __restrict__ flags) {
+  __shared__ double sh[HY_THREADS / 32];
+  const int b = blockIdx.x;
+  if (!active[b]) return;
+  const int outer_it = *outer_done + 1;
+  const size_t GN = (size_t)G * Nc;
+  double* p = phi + b * GN;
+  const double F1 = hy_fission_integral(G, Nc, dx, nsf + b * GN, p, sh);
+  if (!(F1 != 0.0) || !isfinite(F1)) {  // zero fission integral -> degenerate
+    if (threadIdx.x == 0) {
+      atomicOr(flags, FLAG_DEGENERATE);
+      k[b] = __longlong_as_double(0x7ff8000000000000ll);
+      active[b] = 0;
+      outer[b] = outer_it;
+    }
+    return;
+  }
+  const double kb = k[b], k_new = kb * F1;
+  double num = 0.0, den = 0.0;
+  for (size_t i = threadIdx.x; i < GN; i += HY_THREADS) {
+    const double pn = p[i] / F1;
+    p[i] = pn;
+    const double d = pn - old[b * GN + i];
+    if (norm == 0) {
+      num = fmax(num, fabs(d));
+      den = fmax(den, fabs(pn));
+    } else {
+      num = fma(d, d, num);
+      den = fma(pn, pn, den);
+    }
+  }
+  if (norm == 0) {
+    num = hy_block_max(num, sh);
+    den = hy_block_max(den, sh);
+  } else {
+    num = hy_block_sum(num, sh);
+    den = hy_block_sum(den, sh);
+  }
+  if (threadIdx.x == 0) {
+    const double dphi = snop_dev::rel_change(num, den, norm);
+    const double dk = fabs(k_new - kb) / fabs(k_new);
+    k[b] = k_new;
+    outer[b] = outer_it;
+    if (dk < tol_k && dphi < tol_phi) {
+      active[b] = 0;
+      conv[b] = 1;
+    } else {
+      atomicAdd(n_active, 1);
+    }
+  }
+}
+
 }  // namespace
 
+namespace snop_impl {
+snop_status launch_power_iteration_big(Ctx& ctx, const snop_grid& grid, int order, int B, int G, const double* st,
+                                       const double* ss0, const double* ss1, const double* nsf, const double* chi,
+                                       const snop_solver_config& cfg, const double* k0, const double* phi0, double* k,
+                                       double* phi, int32_t* outer, int64_t* inner, uint8_t* conv) {
+  if (B == 0) return SNOP_OK;
+  const int Nc = grid.n_cells;
+  const size_t N = (size_t)B * Nc, GNB = N * G;
+  const double dx = grid.length_cm / Nc;
+  auto dslot = [&](int i, size_t n) { return static_cast<double*>(ctx.slot(i, n * sizeof(double))); };
+  double *old = dslot(100, GNB), *fiss = dslot(101, N), *qext = dslot(102, N), *stg = dslot(103, N);
+  double *ssg = dslot(104, N), *s1g = ss1 ? dslot(105, N) : nullptr, *phig = dslot(106, N), *solved = dslot(107, N);
+  uint8_t* active = static_cast<uint8_t*>(ctx.slot(108, (size_t)B));
+  int32_t* sit = static_cast<int32_t*>(ctx.slot(109, (size_t)B * sizeof(int32_t)));
+  uint8_t* scv = static_cast<uint8_t*>(ctx.slot(110, (size_t)B));
+  int* cnt = static_cast<int*>(ctx.slot(111, 2 * sizeof(int)));
+  if (!old || !fiss || !qext || !stg || !ssg || (ss1 && !s1g) || !phig || !solved || !active || !sit || !scv || !cnt)
+    return cuda_status("workspace", cudaErrorMemoryAllocation);
+  int *n_active = cnt, *outer_done = cnt + 1;
+  // chi is per instance [B][G]; the gather kernels read it as such
+  pi_big_init<<<B, HY_THREADS, 0, ctx.stream>>>(G, Nc, dx, st, nsf, k0, phi0, phi, k, active, conv, outer, inner,
+                                               ctx.d_flags);
+  ctx.launches++;
+  cudaMemsetAsync(outer_done, 0, sizeof(int), ctx.stream);
+  snop_solver_config icfg = cfg;  // inner solves: the flux tolerance, warm-started
+  auto body = [&](cudaGraphConditionalHandle h) -> snop_status {
+    const cudaStream_t cs = ctx.stream;
+    const int64_t l0 = ctx.launches;
+    hy_outer_begin<<<B, HY_THREADS, 0, cs>>>(G, Nc, nsf, phi, old, fiss, active);
+    ctx.launches++;
+    for (int g = 0; g < G; ++g) {
+      hy_group_in<<<B, HY_THREADS, 0, cs>>>(g, G, Nc, chi, k, st, ss0, ss1, phi, fiss, qext, stg, ssg, s1g, phig);
+      ctx.launches++;
+      SNOP_TRY(launch_source_iteration(ctx, grid, order, B, stg, ssg, s1g, qext, icfg, phig, solved, nullptr, sit,
+                                       scv, nullptr, nullptr, active));
+      pi_big_group_out<<<B, HY_THREADS, 0, cs>>>(g, G, Nc, solved, phi, active, sit, inner);
+      ctx.launches++;
+    }
+    cudaMemsetAsync(n_active, 0, sizeof(int), cs);
+    pi_big_outer_end<<<B, HY_THREADS, 0, cs>>>(G, Nc, dx, outer_done, cfg.tolerance_k, cfg.tolerance_phi, cfg.norm,
+                                               nsf, phi, old, k, active, conv, outer, n_active, ctx.d_flags);
+    const int nb = (int)(ctx.launches - l0) + 2;
+    loop_ctl<<<1, 1, 0, cs>>>(h, outer_done, n_active, cfg.max_outer, nb, ctx.d_loop_launches);
+    return cuda_status("power iteration (streaming)", cudaGetLastError());
+  };
+  uint64_t bits[3];
+  std::memcpy(&bits[0], &cfg.tolerance, 8);
+  std::memcpy(&bits[1], &cfg.tolerance_k, 8);
+  std::memcpy(&bits[2], &cfg.tolerance_phi, 8);
+  const std::vector<uint64_t> key = {3, (uint64_t)order, (uint64_t)B, (uint64_t)G, (uint64_t)Nc,
+                                     (uint64_t)(uintptr_t)st, (uint64_t)(uintptr_t)ss0, (uint64_t)(uintptr_t)ss1,
+                                     (uint64_t)(uintptr_t)nsf, (uint64_t)(uintptr_t)chi, (uint64_t)(uintptr_t)k,
+                                     (uint64_t)(uintptr_t)phi, (uint64_t)(uintptr_t)outer,
+                                     (uint64_t)(uintptr_t)inner, (uint64_t)(uintptr_t)conv, bits[0], bits[1],
+                                     bits[2], (uint64_t)cfg.max_outer, (uint64_t)cfg.max_inner, (uint64_t)cfg.norm,
+                                     (uint64_t)cfg.bc_left, (uint64_t)cfg.bc_right,
+                                     (uint64_t)std::llround(grid.length_cm * 1e12)};
+  return device_loop(ctx, key, body);
+}
+}  // namespace snop_impl
+
 extern "C" {
+
 
 snop_status snop_deeponet_create(snop_ctx* ctx, const snop_grid* grid, double tstar, double sstar, int32_t act,
                                  int32_t nb, const int32_t* bs, const float* bp, int32_t nt, const int32_t* ts,

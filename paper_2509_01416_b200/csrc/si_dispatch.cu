@@ -14,6 +14,10 @@ SNOP_DECL_PI(SNOP_K, 32, false) SNOP_DECL_PI(SNOP_K, 64, false) SNOP_DECL_PI(SNO
 SNOP_DECL_PI(SNOP_K, 512, false)
 SNOP_DECL_PI(SNOP_K, 32, true) SNOP_DECL_PI(SNOP_K, 64, true) SNOP_DECL_PI(SNOP_K, 128, true) SNOP_DECL_PI(SNOP_K, 256, true)
 SNOP_DECL_PS(SNOP_K, 32) SNOP_DECL_PS(SNOP_K, 64) SNOP_DECL_PS(SNOP_K, 128) SNOP_DECL_PS(SNOP_K, 256) SNOP_DECL_PS(SNOP_K, 512)
+extern template snop_status launch_tiled_t<SNOP_K, 256>(snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, int,
+                                                        const double*, const double*, const double*, const double*,
+                                                        const double*, double*, double*, int32_t*, uint8_t*, double*,
+                                                        const uint8_t*);
 }  // namespace snop_si
 
 using namespace snop_si;
@@ -37,7 +41,8 @@ struct Shape {
 // but measured slower on every BASELINE config (C2-C5, DESIGN.md §K1 "clusters"): the
 // per-pair-group cluster barrier costs more than the split saves. Above 4096 cells the smallest
 // cluster that holds the slab is used (up to 8 CTAs x 256 threads x K cells = 16384 cells).
-// ctx.opt.cell_cluster = 1 / 2 / 4 / 8 forces a size (1 = never split).
+// ctx.opt.cell_cluster = 1 / 2 / 4 / 8 forces a size (1 = never split). Beyond the cluster limit,
+// or with ctx.opt.cell_cluster = -1, the streaming kernel (si_tiled.cu) sweeps the slab in tiles.
 Shape pick_shape(const snop_impl::Ctx& ctx, int n_cells) {
   int cs = 1;
   const int force = ctx.opt.cell_cluster;
@@ -76,6 +81,13 @@ snop_status launch_source_iteration(Ctx& ctx, const snop_grid& g, int order, int
   if (batch == 0) return SNOP_OK;
   const SweepConsts sc = make_consts(g, order);
   const SolveConfig c = inner_cfg(cfg);
+  if (ctx.opt.cell_cluster == -1 || g.n_cells > kMaxCells) {
+    if (stage) {
+      set_error("host-resident inputs need the one-CTA-per-instance kernel");
+      return SNOP_INVALID_ARGUMENT;
+    }
+    return launch_tiled_t<K, 256>(ctx, sc, c, batch, st, ss0, ss1, src, phi0, phi, cur, iters, conv, leak, active);
+  }
   const Shape s = pick_shape(ctx, g.n_cells);
   if (stage && s.cs > 1) {
     set_error("host-resident inputs need the one-CTA-per-instance kernel");
@@ -97,6 +109,9 @@ snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int 
                                    const snop_solver_config& cfg, const double* k0, const double* phi0, double* k,
                                    double* phi, double* old, int32_t* outer, int64_t* inner, uint8_t* conv) {
   if (batch == 0) return SNOP_OK;
+  if (ctx.opt.cell_cluster == -1 || g.n_cells > kMaxCells)  // streaming inner solves, device outer loop
+    return launch_power_iteration_big(ctx, g, order, batch, G, st, ss0, ss1, nsf, chi, cfg, k0, phi0, k, phi, outer,
+                                      inner, conv);
   const SweepConsts sc = make_consts(g, order);
   const SolveConfig ic = inner_cfg(cfg);
   EigenParams ep;

@@ -582,6 +582,13 @@ static __global__ void pi_tail_list_kernel(int B, int cap, const int32_t* __rest
     if (!conv[b] && outer[b] == cap) order[atomicAdd(count, 1)] = b;
 }
 
+// K1 for slabs of any length (streaming, per-cell state in a global workspace): si_tiled.cu.
+template <int K, int NT>
+snop_status launch_tiled_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const SolveConfig& cfg, int batch,
+                           const double* st, const double* ss0, const double* ss1, const double* src,
+                           const double* phi0, double* phi, double* cur, int32_t* iters, uint8_t* conv,
+                           double* leak, const uint8_t* active);
+
 // Explicitly instantiated in si_k8_{fixed,eigen}{,_cl}.cu (one TU per variant, parallel build).
 #define SNOP_SI_ARGS                                                                                          \
   snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, int, int, const double*, const double*, const double*, \

@@ -74,6 +74,13 @@ snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int 
                                    double* k, double* phi, double* phi_old_ws, int32_t* outer, int64_t* inner,
                                    uint8_t* conv);
 
+// Power iteration for slabs beyond the resident kernels (op_capi.cu): device-looped outer
+// iterations around the streaming K1.
+snop_status launch_power_iteration_big(Ctx& ctx, const snop_grid& g, int order, int batch, int G, const double* st,
+                                       const double* ss0, const double* ss1, const double* nsf, const double* chi,
+                                       const snop_solver_config& cfg, const double* k0, const double* phi0, double* k,
+                                       double* phi, int32_t* outer, int64_t* inner, uint8_t* conv);
+
 // balance_report, batched: residual[b] = |leak_l + leak_r + absorption - production|
 // / production with absorption = dx sum (Sigma_t - Sigma_s0,out) phi, production = dx sum S.
 snop_status launch_balance(Ctx& ctx, const snop_grid& g, int batch, const double* st, const double* ss_out,
@@ -82,9 +89,11 @@ snop_status launch_balance(Ctx& ctx, const snop_grid& g, int batch, const double
 snop_status launch_recast(Ctx& ctx, size_t n, const double* S, const double* phi, const double* st,
                           const double* ss, double tstar, double sstar, double* out);
 
-// Largest n_cells one CTA's register-resident sweep holds, and the largest a cluster holds.
+// Largest n_cells one CTA's register-resident sweep holds, and the largest a cluster holds; above
+// it the streaming path (si_tiled.cu) runs, up to kMaxCellsAny.
 constexpr int kMaxCtaCells = 4096;
 constexpr int kMaxCells = 16384;
+constexpr int kMaxCellsAny = 1 << 26;
 
 }  // namespace snop_impl
 

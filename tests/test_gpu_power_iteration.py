@@ -195,3 +195,23 @@ def test_pair_split_odd_pair_count(order, ctx_options):
     assert (r.total_inner_iterations == o["inner"]).all()
     assert np.max(np.abs(r.phi - o["phi"])) / np.max(np.abs(o["phi"])) < K_RTOL
     assert np.max(np.abs(r.k - o["k"]) / o["k"]) < K_RTOL
+
+
+@pytest.mark.parametrize("forced", [True, False])
+def test_streaming_power_iteration(forced, ctx_options):
+    """Power iteration beyond the resident kernels: the device-looped outer iteration around the
+    streaming K1 (forced on a C4-like multigroup problem, and automatic at 20000 cells single-group),
+    fixed counts at 1e-10 and converged k against the oracle."""
+    if forced:
+        ctx_options(cell_cluster=-1)
+        p = W.config4(batch=2, n_cells=300)
+    else:
+        p = W.config3(batch=2, n_cells=20000)
+    cfg = _cfg(p, tolerance_k=1e-300, tolerance_phi=1e-300, max_outer_iterations=3, max_inner_iterations=4,
+               tolerance=1e-300)
+    r, o = _both(p, cfg)
+    assert (r.outer_iterations == 3).all() and (r.total_inner_iterations == o["inner"]).all()
+    assert np.max(np.abs(r.phi - o["phi"])) / np.max(np.abs(o["phi"])) < K_RTOL
+    assert np.max(np.abs(r.k - o["k"]) / o["k"]) < K_RTOL
+    r, o = _both(p, _cfg(p))
+    _converged_parity(r, o)

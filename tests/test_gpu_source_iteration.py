@@ -275,3 +275,50 @@ def test_context_options_validation():
         assert ctx.options()["cell_cluster"] == 0
     finally:
         ctx.close()
+
+
+# ---- slabs of any length: cluster path (4097..16384 cells) and streaming path (beyond) -------
+def _slab(B, n, order, seed, ratio=(0.3, 0.9)):
+    rng = np.random.default_rng(seed)
+    x = (np.arange(n) + 0.5) * (10.0 / n)
+    st = rng.uniform(0.5, 1.5, (B, 1)) * (1.0 + 0.5 * np.sin(2 * np.pi * rng.integers(1, 5, (B, 1)) * x / 10.0))
+    ss = st * rng.uniform(*ratio, (B, 1))
+    return W.FixedSourceProblem("slab", 10.0, n, order, st, ss, rng.uniform(0.5, 1.5, (B, n)))
+
+
+@pytest.mark.parametrize("n_cells", [5000, 12000, 20000])
+def test_long_slab_parity(n_cells):
+    """SPEC.md:23 (n_cells: any positive integer): 5000 and 12000 cells run on thread-block
+    clusters, 20000 on the streaming kernel; fixed iterations at 1e-10 for every BC combination and
+    converged counts +-1 against the oracle."""
+    p = _slab(3, n_cells, 16, n_cells)
+    for bc in ((0, 0), (1, 0), (1, 1)):
+        r, o = _run_both(p, dict(tolerance=1e-300, max_inner_iterations=5, boundary_left=bc[0], boundary_right=bc[1]))
+        assert (r.iterations == 5).all()
+        assert _rel(r.phi, o["phi"]) < FLUX_RTOL, bc
+        assert np.max(np.abs(r.current - o["current"])) < 1e-10 * np.max(np.abs(o["phi"]))
+    r, o = _run_both(p, dict(tolerance=1e-8))
+    d = np.abs(r.iterations.astype(int) - o["iterations"].astype(int))
+    assert d.max() <= 1
+    assert _rel(r.phi[d == 0], o["phi"][d == 0]) < FLUX_RTOL
+
+
+@pytest.mark.parametrize("n_cells", [1, 7, 100, 2047, 2048, 2049, 4500])
+@pytest.mark.parametrize("order", [8, 16, 32])
+def test_streaming_path_forced(n_cells, order, ctx_options):
+    """The streaming kernel (ctx option cell_cluster = -1) on small slabs against the oracle: tile
+    edges (2048-cell tiles), ragged last tiles, all BC combinations, P1 and the face leakages."""
+    ctx_options(cell_cluster=-1)
+    p = _slab(2, n_cells, order, 100 + n_cells + order)
+    for bc in ((0, 0), (1, 0), (0, 1), (1, 1)):
+        r, o = _run_both(p, dict(tolerance=1e-300, max_inner_iterations=4, boundary_left=bc[0], boundary_right=bc[1]))
+        assert _rel(r.phi, o["phi"]) < FLUX_RTOL, bc
+        assert np.max(np.abs(r.current - o["current"])) < 1e-10 * np.max(np.abs(o["phi"])), bc
+    r, o = _run_both(p, dict(tolerance=1e-300, max_inner_iterations=4), sigma_s1=0.2 * p.sigma_s0)
+    assert _rel(r.phi, o["phi"]) < FLUX_RTOL
+    cfg = snop.SolverConfig(tolerance=1e-10)
+    g = snop.Grid1D(p.length, p.n_cells)
+    lk = snop.source_iteration(g, p.order, p.sigma_t, p.sigma_s0, p.source, cfg, want_leakage=True)
+    ol = O.source_iteration(p.length, p.n_cells, p.order, p.sigma_t, p.sigma_s0, p.source, cfg.c(), want_leak=True)
+    same = lk.iterations == ol["iterations"]
+    assert np.max(np.abs(lk.leakage[same] - ol["leak"][same])) < 1e-10 * np.max(np.abs(ol["phi"]))
