@@ -46,6 +46,9 @@ struct snop_op {
   float* FT = nullptr;                  // forward DFT transposed, [n][2M] (fno_dft64)
   // pre-split 3xTF32 lo parts of the constant GEMM operands (TMA engine loads them, no conversion)
   float *Ginv_lo = nullptr, *P1W_lo = nullptr, *F_lo = nullptr;
+  // spectral mixing as tensor-core GEMMs (per layer): the per-mode real forms of R, K-major,
+  // [4][M][C][C] = {Rr^T, -Ri^T (U_re), Ri^T, Rr^T (U_im)} with [o][c] rows, and their lo parts
+  std::vector<float*> mixB, mixB_lo;
   // exact operator
   int order = 16;
   snop_solver_config cfg{};
@@ -664,7 +667,27 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
       SNOP_TRY(gemm(ctx, f));
     }
     // complex channel mixing per retained mode
-    if (C == 64 && tc_done) {  // the tensor-core DFT wrote Vh mode-major
+    if (tc_done && use_tc(ctx) && ctx.opt.fno_mix == 0) {
+      // on the tensor core: per mode m, U_re = [V_re | V_im] . [Rr ; -Ri] and U_im = [V_re | V_im] .
+      // [Ri ; Rr] - two batched (over the modes) 3xTF32 GEMMs, samples x C outputs x 2C, reading the
+      // mode-major spectra Vh [2M][B][C] (re rows, then im rows) as two K segments and writing U in
+      // the [b][o][m'] rows the inverse GEMM consumes
+      for (int part = 0; part < 2; ++part) {
+        const size_t MCC = (size_t)M * C * C;
+        GemmArgs mx{};
+        mx.M = B; mx.N = C; mx.K = 2 * C; mx.batch = M;
+        mx.A = Vh; mx.sam = C; mx.sak = 1; mx.sab = (int64_t)B * C;
+        mx.ksplit = C;
+        mx.A2 = Vh + (size_t)M * B * C; mx.sam2 = C; mx.sak2 = 1; mx.sab2 = (int64_t)B * C;
+        mx.B = op.mixB[l] + (2 * part) * MCC; mx.sbn = C; mx.sbk = 1; mx.sbb = (int64_t)C * C;
+        mx.B2 = op.mixB[l] + (2 * part + 1) * MCC; mx.sbn2 = C; mx.sbk2 = 1; mx.sbb2 = (int64_t)C * C;
+        mx.B_lo = op.mixB_lo[l] + (2 * part) * MCC;
+        mx.B2_lo = op.mixB_lo[l] + (2 * part + 1) * MCC;
+        mx.C = U + part * M; mx.scb = 1; mx.scm = (int64_t)C * 2 * M; mx.scn = 2 * M;
+        mx.alpha = 1.f; mx.act = ACT_NONE;
+        SNOP_TRY(gemm(ctx, mx));
+      }
+    } else if (C == 64 && tc_done) {  // the tensor-core DFT wrote Vh mode-major
       const size_t sm = (size_t)(128 * 128 + 128 * (MIX_S + 4)) * sizeof(float);
       cudaFuncSetAttribute(fno_mix64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       fno_mix64<true><<<dim3((B + MIX_S - 1) / MIX_S, M), 256, sm, ctx.stream>>>(B, M, Vh, op.Rr[l], op.Ri[l], U);
@@ -676,7 +699,7 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
       fno_mix<<<dim3((B + 3) / 4 < 1024 ? (B + 3) / 4 : 1024, M), 4 * C, 2 * C * C * sizeof(float), ctx.stream>>>(
           B, C, M, Vh, op.Rr[l], op.Ri[l], U);
     }
-    ctx.launches++;
+    if (!(tc_done && use_tc(ctx) && ctx.opt.fno_mix == 0)) ctx.launches++;
     if (tc_fused) {
       // inverse truncated DFT + W path + bias + activation as ONE contraction per sample:
       // Vn[b][i][o] = act( [Ginv | V_b](i, :) . [U_b | W](o, :) + b[o] ),  K = 2M + C
@@ -1493,9 +1516,23 @@ snop_status snop_fno_create(snop_ctx* ctx, const snop_grid* grid, double tstar, 
   p += C;
   for (int l = 0; l < layers; ++l) {
     op->Rr.push_back(op->upload(p, M * C * C));
-    p += M * C * C;
-    op->Ri.push_back(op->upload(p, M * C * C));
-    p += M * C * C;
+    op->Ri.push_back(op->upload(p + M * C * C, M * C * C));
+    {  // U_re = V_re Rr - V_im Ri, U_im = V_re Ri + V_im Rr per mode, as B operands [o][c]
+      const float *rr = p, *ri = p + M * C * C;
+      std::vector<float> mb(4 * M * C * C);
+      for (size_t m = 0; m < M; ++m)
+        for (size_t c = 0; c < C; ++c)
+          for (size_t o = 0; o < C; ++o) {
+            const size_t src = (m * C + c) * C + o, dst = (m * C + o) * C + c;
+            mb[0 * M * C * C + dst] = rr[src];
+            mb[1 * M * C * C + dst] = -ri[src];
+            mb[2 * M * C * C + dst] = ri[src];
+            mb[3 * M * C * C + dst] = rr[src];
+          }
+      op->mixB.push_back(op->upload(mb.data(), mb.size()));
+      op->mixB_lo.push_back(op->upload_lo(mb.data(), mb.size()));
+    }
+    p += 2 * M * C * C;
     op->W.push_back(op->upload(p, C * C));
     p += C * C;
     op->b.push_back(op->upload(p, C));

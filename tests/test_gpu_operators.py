@@ -230,7 +230,7 @@ def test_precondition_fixed_source_deeponet_parity():
     assert _rel(r.phi[same], o["phi"][same]) < 1e-8
 
 
-@pytest.mark.parametrize("opts", [{}, {"fno_dft": 1}, {"gemm_engine": 1}, {"gemm_engine": 2}])
+@pytest.mark.parametrize("opts", [{}, {"fno_mix": 1}, {"fno_dft": 1}, {"gemm_engine": 1}, {"gemm_engine": 2}])
 def test_fno_width64_kernel_paths(opts, ctx_options):
     """The C5-width FNO runs on dedicated paths (tensor-core forward DFT, register-tiled mixing,
     TMA-store epilogue, resident pre-split weights); each against the oracle, with the other paths
