@@ -150,10 +150,12 @@ def test_thin_cell_flux_parity(sigma_scale, bc, order, n_cells):
     assert _rel(r.phi, o["phi"]) < FLUX_RTOL
 
 
-def test_too_many_cells_is_invalid_argument():
-    n = 16385
-    with pytest.raises(InvalidArgument):
-        snop.source_iteration(snop.Grid1D(10.0, n), 8, np.ones((1, n)), np.zeros((1, n)), np.ones((1, n)))
+def test_grid_limits_are_invalid_argument():
+    # n_cells must be positive; the C ABI's upper bound is 2^26 cells per instance (the
+    # streaming path has no smaller limit: 16385+ cells are solved, test_long_slab_parity)
+    for n in (0, 2**26 + 1):
+        with pytest.raises(InvalidArgument):
+            snop.source_iteration(snop.Grid1D(10.0, n), 8, np.ones((0, n)), np.zeros((0, n)), np.ones((0, n)))
 
 
 def test_empty_batch():

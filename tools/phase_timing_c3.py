@@ -24,6 +24,9 @@ cfg = snop.SolverConfig(tolerance=p.tolerance_inner, tolerance_k=p.tolerance_k, 
                         boundary_left=p.bc_left, boundary_right=p.bc_right)
 g = snop.Grid1D(p.length, p.n_cells)
 q = p.subset([int(sys.argv[1]) if len(sys.argv) > 1 else 491])
+cs = int(sys.argv[2]) if len(sys.argv) > 2 else 8  # pair-split cluster size for the whole solve (-1: one CTA)
+snop.default_context().set_options(pair_split=cs, pi_tail_cap=-1)
+nctas = cs if cs > 1 else 1
 args = [torch.from_numpy(a).cuda() for a in (q.sigma_t, q.sigma_s0, q.nu_sigma_f, q.chi)]
 import time
 snop.power_iteration(g, p.order, *args, cfg); torch.cuda.synchronize()
@@ -35,7 +38,8 @@ f(buf.ctypes.data, 1)
 print(f"single instance: {dt*1e3:.1f} ms, {dt*1e6/int(r.total_inner_iterations[0]):.2f} us per sweep")
 sweeps = int(r.total_inner_iterations[0]); outer = int(r.outer_iterations[0])
 row = buf[:10].astype(np.float64)
-groups = sweeps * (p.order // 4)
-print(f"C3 inst: sweeps {sweeps} outer {outer}: per pair group maps {row[0]/groups:.0f} bar1 {row[1]/groups:.0f} "
+groups = sweeps * max(1, (p.order // 4) // nctas) * nctas  # pair groups summed over the CTAs
+sweeps *= nctas  # per-sweep sums below: per CTA
+print(f"pair_split {cs}; C3 inst: sweeps {sweeps // nctas} outer {outer}: cycles per pair group (per CTA) maps {row[0]/groups:.0f} bar1 {row[1]/groups:.0f} "
       f"scan {row[2]/groups:.0f} bar2 {row[3]/groups:.0f} replay {row[4]/groups:.0f} | per sweep pairs {row[5]/sweeps:.0f} "
       f"phi {row[6]/sweeps:.0f} | in solve per sweep {row[7]/sweeps:.0f} | loop per sweep {row[8]/sweeps:.0f}")
