@@ -226,6 +226,7 @@ struct SweepSmem {
   // published for the other CTAs, read through distributed shared memory
   double ctot[2][kNP][4];      // CTA-level scan totals [group slot][q][{Af,Bf,Ab,Bb}]
   double cred[2][2];           // CTA-level reduction results (si_solve), by phase
+  double credx[2][8][2];       // every rank's reduction results pushed here (si_solve), [phase][rank]
   double cred2[2][2];          // CTA-level reduction results (enclosing kernel), by phase
   int cflag[2];                // CTA-level flags (validation)
 };
@@ -257,13 +258,31 @@ __device__ __forceinline__ void reduce2(double& a, double& b, bool is_max, doubl
   if (is_max) block_max2<NT>(a, b, scratch, phase);
   else block_sum2<NT>(a, b, scratch, phase);
   if constexpr (CL) {
-    const int s = phase & 1;
+    const int s = phase & 1, n = cl_size();
+    if (cred == sm.cred) {
+      // si_solve's reductions: every CTA pushes its pair into every rank's credx slot (remote
+      // stores, published by the cluster barrier), so the combine reads local shared memory only
+      if ((int)threadIdx.x < n) {
+        double* dst = cl_map(&sm.credx[s][cl_rank()][0], (int)threadIdx.x);
+        dst[0] = a;
+        dst[1] = b;
+      }
+      cl_sync();
+      double ra = sm.credx[s][0][0], rb = sm.credx[s][0][1];
+      for (int r = 1; r < n; ++r) {
+        const double x = sm.credx[s][r][0], y = sm.credx[s][r][1];
+        if (is_max) { ra = fmax(ra, x); rb = fmax(rb, y); }
+        else { ra += x; rb += y; }
+      }
+      a = ra;
+      b = rb;
+      return;
+    }
     if (threadIdx.x == 0) {
       cred[s][0] = a;
       cred[s][1] = b;
     }
     cl_sync();
-    const int n = cl_size();
     double ra = 0.0, rb = 0.0;
     for (int r = 0; r < n; ++r) {
       const double* rc = cl_map(&cred[s][0], r);
@@ -609,11 +628,13 @@ __device__ __forceinline__ void sweep_pair_group(const SweepConsts& sc, SweepSme
   SNOP_TSTAMP(t4);
   replay_phase<K, NT, NP, CL, WJ>(sc, sm, p0, w, al, bp, bm, acc);
   SNOP_TSTAMP(t5);
+#ifndef SNOP_PS_TIMING
   SNOP_TACC(0, t0, t1);
   SNOP_TACC(1, t1, t2);
   SNOP_TACC(2, t2, t3);
   SNOP_TACC(3, t3, t4);
   SNOP_TACC(4, t4, t5);
+#endif
   w.gslot ^= 1;
 }
 
@@ -664,12 +685,12 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
   // here for the first sweep and then in each flux update for the next one, so the L2 loads of
   // Ss0 and S overlap the flux update and the convergence reduction.
 #if SNOP_STAGE_SS
-  if constexpr (!PS) {
+  // (pair split: every CTA stages all cells, so an owner reads any cell's values locally; the
+  // barriers of the first exchange order these stores before those reads)
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      sm.ss[j * NT + t] = (c0 + j < Nc) ? io.ss0[c0 + j] : 0.0;
-      sm.src[j * NT + t] = (c0 + j < Nc) ? io.src[c0 + j] : 0.0;
-    }
+  for (int j = 0; j < K; ++j) {
+    sm.ss[j * NT + t] = (c0 + j < Nc) ? io.ss0[c0 + j] : 0.0;
+    sm.src[j * NT + t] = (c0 + j < Nc) ? io.src[c0 + j] : 0.0;
   }
 #endif
 #pragma unroll
@@ -707,7 +728,9 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
       // true>) whose barrier also publishes the pushed emission. phi is pushed once, at the end.
       double* xb = &sm.agg[0][0][0];
       const int prank = cl_rank(), psz = cl_size(), per = NT / psz;
+      SNOP_TSTAMP(tx0);
       cl_sync();  // every CTA has finished its replays (agg / xmap are free cluster-wide)
+      SNOP_TSTAMP(tx1);
       {
         const int ro = t / per, uu = t - ro * per;
         double* dst = cl_map(xb, ro) + (size_t)prank * (K + 1) * per + uu;
@@ -715,7 +738,9 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
         for (int j = 0; j < K; ++j) dst[j * per] = acc.Fl[j];
         dst[K * per] = acc.Fr;
       }
+      SNOP_TSTAMP(tx2);
       cl_sync();
+      SNOP_TSTAMP(tx3);
       for (int idx = t; idx < per * K; idx += NT) {
         const int j = idx / per, uu = idx - j * per, u = prank * per + uu;
         const int i = u * K + j;
@@ -737,11 +762,24 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
             den = fma(pn, pn, den);
           }
           sm.phi[o] = pn;
+#if SNOP_STAGE_SS
+          const double q2n = fma(sm.ss[o], pn, sm.src[o]);
+#else
           const double q2n = fma(io.ss0[i], pn, io.src[i]);
+#endif
           for (int r = 0; r < psz; ++r) cl_map(sm.q2, r)[o] = q2n;
         }
       }
+      SNOP_TSTAMP(tx4);
       reduce2<NT, true>(num, den, cfg.norm == 0, sm.red, sm.cred, rphase++, sm);
+      SNOP_TSTAMP(tx5);
+#ifdef SNOP_PS_TIMING
+      SNOP_TACC(0, tx0, tx1);  // wait for the slowest CTA's replays
+      SNOP_TACC(1, tx1, tx2);  // push partials
+      SNOP_TACC(2, tx2, tx3);  // cluster barrier
+      SNOP_TACC(3, tx3, tx4);  // owner sums, flux update, emission push
+      SNOP_TACC(4, tx4, tx5);  // norm reduction (block + cluster)
+#endif
     } else {
     // Phi (J) at the right edge of the own last cell was accumulated locally (Fr, Jr); padding
     // cells after the global last cell are identity maps, so Jl[j+1] of a padding cell is J at L.
