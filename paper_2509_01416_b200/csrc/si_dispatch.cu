@@ -129,7 +129,7 @@ snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int 
   // loop, which every CTA of a cluster repeats, so they stay on one CTA (C4: 37 vs 49 ms). The
   // rule depends on (G, order) only, never on the batch, so an instance's result does not depend
   // on what it is batched with. ctx.opt.pair_split = -1 disables it, n sets the cluster size (<= 8).
-  const int cap = ctx.opt.pi_tail_cap == 0 ? 48 : (ctx.opt.pi_tail_cap < 0 ? 0 : ctx.opt.pi_tail_cap);  // tail split
+  const int cap = ctx.opt.pi_tail_cap == 0 ? 32 : (ctx.opt.pi_tail_cap < 0 ? 0 : ctx.opt.pi_tail_cap);  // tail split
   int ps = 0;
   if (!ss1 && s.cs == 1) {
     int want = G == 1 ? (cap > 0 ? 8 : 4) : 0;
@@ -141,27 +141,28 @@ snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int 
   // longest instances (C3: outer counts 17 ... 1303). Phase 1 runs every instance on one CTA for at
   // most `cap` outer iterations; phase 2 continues the unconverged ones from their (k, phi, counts)
   // on pair-split clusters, so the long tails get cs SMs each once the bulk has drained. The cap is a
-  // constant (ctx.opt.pi_tail_cap, default 48; -1 disables), so an instance's result depends on its own data
+  // constant (ctx.opt.pi_tail_cap, default 32; -1 disables), so an instance's result depends on its own data
   // only.
   if (ps && cap > 0 && cfg.max_outer > cap) {
     EigenParams e1 = ep, e2 = ep;
     e1.max_outer = cap;
     e2.max_outer = cfg.max_outer - cap;
     int* lst = static_cast<int*>(ctx.slot(25, ((size_t)batch + 1) * sizeof(int)));
-    if (!lst) {
+    float* key = static_cast<float*>(ctx.slot(26, (size_t)batch * sizeof(float)));
+    if (!lst || !key) {
       set_error("cudaMalloc (tail list) failed");
       return SNOP_CUDA_ERROR;
     }
     int* cnt = lst + batch;
 #define SNOP_P1(NN) \
-  if (s.nt == NN) st1 = launch_pi_t<K, NN, false>(ctx, sc, ic, e1, batch, 1, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv);
+  if (s.nt == NN) st1 = launch_pi_t<K, NN, false>(ctx, sc, ic, e1, batch, 1, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv, nullptr, nullptr, 0, key);
 #define SNOP_P2(NN) \
   if (s.nt == NN) st2 = launch_pi_t<K, NN, false, true>(ctx, sc, ic, e2, batch, ps, st, ss0, ss1, nsf, chi, k, phi, k, phi, old, outer, inner, conv, lst, cnt, 1);
     snop_status st1 = SNOP_INVALID_ARGUMENT, st2 = SNOP_INVALID_ARGUMENT;
     SNOP_P1(32) SNOP_P1(64) SNOP_P1(128) SNOP_P1(256) SNOP_P1(512)
     if (st1 != SNOP_OK) return st1;
     cudaMemsetAsync(cnt, 0, sizeof(int), ctx.stream);
-    pi_tail_list_kernel<<<(batch + 255) / 256, 256, 0, ctx.stream>>>(batch, cap, outer, conv, lst, cnt);
+    pi_tail_list_kernel<<<(batch + 255) / 256, 256, 0, ctx.stream>>>(batch, cap, outer, conv, key, lst, cnt);
     ctx.launches++;
     SNOP_P2(32) SNOP_P2(64) SNOP_P2(128) SNOP_P2(256) SNOP_P2(512)
 #undef SNOP_P1

@@ -179,7 +179,8 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
                        double* __restrict__ old_g, double* __restrict__ qext_g, double* __restrict__ jc_g,
                        int32_t* __restrict__ outer_g, int64_t* __restrict__ inner_g,
                        uint8_t* __restrict__ conv_g, int* __restrict__ flags, double* __restrict__ psw_g,
-                       const int* __restrict__ order, const int* __restrict__ order_count, int resume) {
+                       const int* __restrict__ order, const int* __restrict__ order_count, int resume,
+                       float* __restrict__ tail_key) {
   static_assert(!(PS && (CL || ANISO)), "pair split: isotropic, no cell split");
   extern __shared__ __align__(32) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<SweepSmem<K, NT>*>(smem_raw);
@@ -288,6 +289,7 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
   __syncthreads();
 
   bool converged = false;
+  double gap = 0.0;  // distance from the dual test at the last outer: max(dk / tol_k, dphi / tol_phi)
   SNOP_TSTAMP(tpi0);
   while (outer < ep.max_outer) {
     ++outer;
@@ -386,6 +388,7 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
     const double dphi = rel_change(num, den, ep.norm);
     const double dk = fabs(k_new - k) / fabs(k_new);
     k = k_new;
+    gap = fmax(dk / ep.tol_k, dphi / ep.tol_phi);
     if (dk < ep.tol_k && dphi < ep.tol_phi) {
       converged = true;
       break;
@@ -398,6 +401,7 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
     outer_g[b] = outer0 + outer;
     inner_g[b] = inner0 + inner_total;
     conv_g[b] = converged ? 1 : 0;
+    if (tail_key) tail_key[b] = converged ? 0.f : (float)fmin(gap, 3.0e38);  // tail-phase order (below)
   }
   if constexpr (CL) cl_sync();
 }
@@ -536,7 +540,7 @@ inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
                                const double* ss1, const double* nsf, const double* chi, const double* k0,
                                const double* phi0, double* k, double* phi, double* old, int32_t* outer,
                                int64_t* inner, uint8_t* conv, const int* order = nullptr,
-                               const int* order_count = nullptr, int resume = 0) {
+                               const int* order_count = nullptr, int resume = 0, float* tail_key = nullptr) {
   const bool aniso = ss1 != nullptr;
   const size_t smem = smem_bytes<K, NT>();
   auto kern = PS ? power_iteration_kernel<K, NT, false, false, PS>
@@ -563,7 +567,7 @@ inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
   }
   const cudaError_t e = launch_k(kern, batch, (CL || PS) ? cs : 1, NT, smem, ctx.stream, sc, icfg, ep, st, ss0, ss1,
                                  nsf, chi, k0, phi0, k, phi, old, qext, jc, outer, inner, conv, ctx.d_flags, psw,
-                                 order, order_count, resume);
+                                 order, order_count, resume, tail_key);
   ctx.launches++;
   if (e != cudaSuccess) {
     snop_impl::set_error(std::string("power_iteration_kernel launch: ") + cudaGetErrorString(e));
@@ -573,13 +577,22 @@ inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
 }
 
 // Tail phase of a split power iteration: the instances still iterating after the first launch
-// (not converged, outer count == the phase-1 cap) -> order[0 .. *count). Their position in the list
-// does not affect their results.
+// (not converged, outer count == the phase-1 cap) -> order[0 .. *count), furthest from convergence
+// first (key = max(dk / tol_k, dphi / tol_phi) at the cap, ties by index), so the slowest instance
+// gets a cluster at once instead of waiting behind others. Rank by counting (deterministic);
+// positions never affect an instance's results.
 static __global__ void pi_tail_list_kernel(int B, int cap, const int32_t* __restrict__ outer,
-                                           const uint8_t* __restrict__ conv, int* __restrict__ order,
-                                           int* __restrict__ count) {
-  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x)
-    if (!conv[b] && outer[b] == cap) order[atomicAdd(count, 1)] = b;
+                                           const uint8_t* __restrict__ conv, const float* __restrict__ key,
+                                           int* __restrict__ order, int* __restrict__ count) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
+    if (conv[b] || outer[b] != cap) continue;
+    atomicAdd(count, 1);
+    const float kb = key[b];
+    int rank = 0;
+    for (int c = 0; c < B; ++c)
+      if (!conv[c] && outer[c] == cap && (key[c] > kb || (key[c] == kb && c < b))) ++rank;
+    order[rank] = b;
+  }
 }
 
 // K1 for slabs of any length (streaming, per-cell state in a global workspace): si_tiled.cu.
@@ -596,7 +609,7 @@ snop_status launch_tiled_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const Sol
 #define SNOP_PI_ARGS                                                                                          \
   snop_impl::Ctx&, const SweepConsts&, const SolveConfig&, const EigenParams&, int, int, const double*,          \
       const double*, const double*, const double*, const double*, const double*, const double*, double*, double*, \
-      double*, int32_t*, int64_t*, uint8_t*, const int*, const int*, int
+      double*, int32_t*, int64_t*, uint8_t*, const int*, const int*, int, float*
 #define SNOP_DECL_SI(KK, NN, CC) extern template snop_status launch_si_t<KK, NN, CC>(SNOP_SI_ARGS);
 #define SNOP_DECL_PI(KK, NN, CC) extern template snop_status launch_pi_t<KK, NN, CC>(SNOP_PI_ARGS);
 #define SNOP_DECL_PS(KK, NN) extern template snop_status launch_pi_t<KK, NN, false, true>(SNOP_PI_ARGS);
