@@ -119,7 +119,7 @@ snop_status snop_ctx_destroy(snop_ctx* ctx);
  *                  streaming kernel (tile-by-tile sweep, per-cell state in a device workspace).
  *   pair_split     single-group eigen pair-split cluster size: 0 auto (8 with the tail split), -1
  *                  off, 2..8 force.
- *   pi_tail_cap    outer iterations of the tail split's first phase: 0 auto (32), -1 off (one launch).
+ *   pi_tail_cap    outer iterations of the tail split's first phase: 0 auto (12), -1 off (one launch).
  *   host_chunks    pageable-host pipeline chunk count: 0 auto (4), 1..8.
  *   gemm_engine    operator contractions: 0 auto (tcgen05 engines), 1 tcgen05 engine v1 only,
  *                  2 FFMA engine (fp32 cross-check; slow).

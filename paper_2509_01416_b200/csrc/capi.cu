@@ -72,6 +72,9 @@ Ctx::~Ctx() {
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (d_loop_launches) cudaFree(d_loop_launches);
   if (side) cudaStreamDestroy(side);
+  if (aux) cudaStreamDestroy(aux);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
   for (Ctx* c : subs) delete c;
   for (auto& b : slots)
     if (b.ptr) cudaFree(b.ptr);

@@ -129,7 +129,7 @@ snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int 
   // loop, which every CTA of a cluster repeats, so they stay on one CTA (C4: 37 vs 49 ms). The
   // rule depends on (G, order) only, never on the batch, so an instance's result does not depend
   // on what it is batched with. ctx.opt.pair_split = -1 disables it, n sets the cluster size (<= 8).
-  const int cap = ctx.opt.pi_tail_cap == 0 ? 32 : (ctx.opt.pi_tail_cap < 0 ? 0 : ctx.opt.pi_tail_cap);  // tail split
+  const int cap = ctx.opt.pi_tail_cap == 0 ? 12 : (ctx.opt.pi_tail_cap < 0 ? 0 : ctx.opt.pi_tail_cap);  // tail split
   int ps = 0;
   if (!ss1 && s.cs == 1) {
     int want = G == 1 ? (cap > 0 ? 8 : 4) : 0;
@@ -138,36 +138,77 @@ snop_status launch_power_iteration(Ctx& ctx, const snop_grid& g, int order, int 
     if (ps < 2 || (s.nt % ps) != 0) ps = 0;
   }
   // Tail split (single-group, pair-split eligible): a batch of eigen solves ends with its few
-  // longest instances (C3: outer counts 17 ... 1303). Phase 1 runs every instance on one CTA for at
-  // most `cap` outer iterations; phase 2 continues the unconverged ones from their (k, phi, counts)
-  // on pair-split clusters, so the long tails get cs SMs each once the bulk has drained. The cap is a
-  // constant (ctx.opt.pi_tail_cap, default 32; -1 disables), so an instance's result depends on its own data
-  // only.
+  // longest instances (C3: outer counts 17 ... 1303), and the batch time is the slowest instance's
+  // chain of sweeps. Phase 1 runs every instance on one CTA for `cap` outers and predicts each
+  // one's remaining outers from its own convergence rate (gap ratio over its last 4 outers). Then,
+  // concurrently: the predicted-long instances (> kLongOuters) continue on pair-split clusters to
+  // the end (main stream, longest first); the others continue on single CTAs for up to kMidOuters
+  // outers (aux stream) and whatever is still iterating after that finishes on clusters. Routing
+  // depends on an instance's own data only (constant cap and threshold), so results never depend on
+  // the batch. ctx.opt.pi_tail_cap sets the phase-1 cap (default 12; -1 disables the split).
+  constexpr float kLongOuters = 256.f;
+  constexpr int kMidOuters = 32;
   if (ps && cap > 0 && cfg.max_outer > cap) {
-    EigenParams e1 = ep, e2 = ep;
+    EigenParams e1 = ep, e2 = ep, em = ep, e3 = ep;
     e1.max_outer = cap;
     e2.max_outer = cfg.max_outer - cap;
-    int* lst = static_cast<int*>(ctx.slot(25, ((size_t)batch + 1) * sizeof(int)));
+    em.max_outer = std::min(kMidOuters, cfg.max_outer - cap);
+    e3.max_outer = cfg.max_outer - cap - em.max_outer;
+    int* lst = static_cast<int*>(ctx.slot(25, (3 * (size_t)batch + 4) * sizeof(int)));
     float* key = static_cast<float*>(ctx.slot(26, (size_t)batch * sizeof(float)));
     if (!lst || !key) {
       set_error("cudaMalloc (tail list) failed");
       return SNOP_CUDA_ERROR;
     }
-    int* cnt = lst + batch;
+    if (!ctx.aux) {
+      if (cudaStreamCreateWithFlags(&ctx.aux, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ctx.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ctx.ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        set_error("tail split: stream / event creation failed");
+        return SNOP_CUDA_ERROR;
+      }
+    }
+    int *lA = lst, *lB = lst + batch, *lC = lst + 2 * (size_t)batch, *cnt = lst + 3 * (size_t)batch;
+    snop_status st1 = SNOP_INVALID_ARGUMENT, st2 = SNOP_OK, stm = SNOP_OK, st3 = SNOP_OK;
 #define SNOP_P1(NN) \
   if (s.nt == NN) st1 = launch_pi_t<K, NN, false>(ctx, sc, ic, e1, batch, 1, st, ss0, ss1, nsf, chi, k0, phi0, k, phi, old, outer, inner, conv, nullptr, nullptr, 0, key);
-#define SNOP_P2(NN) \
-  if (s.nt == NN) st2 = launch_pi_t<K, NN, false, true>(ctx, sc, ic, e2, batch, ps, st, ss0, ss1, nsf, chi, k, phi, k, phi, old, outer, inner, conv, lst, cnt, 1);
-    snop_status st1 = SNOP_INVALID_ARGUMENT, st2 = SNOP_INVALID_ARGUMENT;
+#define SNOP_PSR(NN, EP, L, C, ST) \
+  if (s.nt == NN) ST = launch_pi_t<K, NN, false, true>(ctx, sc, ic, EP, batch, ps, st, ss0, ss1, nsf, chi, k, phi, k, phi, old, outer, inner, conv, L, C, 1);
+#define SNOP_MID(NN) \
+  if (s.nt == NN) stm = launch_pi_t<K, NN, false>(ctx, sc, ic, em, batch, 1, st, ss0, ss1, nsf, chi, k, phi, k, phi, old, outer, inner, conv, lB, cnt + 1, 1, key);
     SNOP_P1(32) SNOP_P1(64) SNOP_P1(128) SNOP_P1(256) SNOP_P1(512)
     if (st1 != SNOP_OK) return st1;
-    cudaMemsetAsync(cnt, 0, sizeof(int), ctx.stream);
-    pi_tail_list_kernel<<<(batch + 255) / 256, 256, 0, ctx.stream>>>(batch, cap, outer, conv, key, lst, cnt);
+    cudaMemsetAsync(cnt, 0, 4 * sizeof(int), ctx.stream);
+    pi_tail_list_kernel<<<(batch + 255) / 256, 256, 0, ctx.stream>>>(batch, cap, outer, conv, key, kLongOuters, lA,
+                                                                     cnt, lB, cnt + 1);
     ctx.launches++;
-    SNOP_P2(32) SNOP_P2(64) SNOP_P2(128) SNOP_P2(256) SNOP_P2(512)
+    cudaEventRecord(ctx.ev_fork, ctx.stream);
+    // main stream: the predicted-long instances on clusters, launched first so their clusters are
+    // placed before the single-CTA work of the aux stream fills the SMs
+    SNOP_PSR(32, e2, lA, cnt, st2) SNOP_PSR(64, e2, lA, cnt, st2) SNOP_PSR(128, e2, lA, cnt, st2)
+    SNOP_PSR(256, e2, lA, cnt, st2) SNOP_PSR(512, e2, lA, cnt, st2)
+    // aux stream: the rest on single CTAs, then the still-iterating ones on clusters
+    const cudaStream_t main_stream = ctx.stream;
+    cudaStreamWaitEvent(ctx.aux, ctx.ev_fork, 0);
+    ctx.stream = ctx.aux;
+    SNOP_MID(32) SNOP_MID(64) SNOP_MID(128) SNOP_MID(256) SNOP_MID(512)
+    if (stm == SNOP_OK && e3.max_outer > 0) {
+      pi_tail_list_kernel<<<(batch + 255) / 256, 256, 0, ctx.stream>>>(batch, cap + em.max_outer, outer, conv, key,
+                                                                       0.f, lC, cnt + 2, nullptr, nullptr, lB,
+                                                                       cnt + 1);
+      ctx.launches++;
+      SNOP_PSR(32, e3, lC, cnt + 2, st3) SNOP_PSR(64, e3, lC, cnt + 2, st3) SNOP_PSR(128, e3, lC, cnt + 2, st3)
+      SNOP_PSR(256, e3, lC, cnt + 2, st3) SNOP_PSR(512, e3, lC, cnt + 2, st3)
+    }
+    cudaEventRecord(ctx.ev_join, ctx.stream);
+    ctx.stream = main_stream;
+    cudaStreamWaitEvent(ctx.stream, ctx.ev_join, 0);
 #undef SNOP_P1
-#undef SNOP_P2
-    return st2;
+#undef SNOP_PSR
+#undef SNOP_MID
+    if (st2 != SNOP_OK) return st2;
+    if (stm != SNOP_OK) return stm;
+    return st3;
   }
   if (ps) {
 #define SNOP_PS(NN) \

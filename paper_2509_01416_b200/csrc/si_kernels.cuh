@@ -290,6 +290,7 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
 
   bool converged = false;
   double gap = 0.0;  // distance from the dual test at the last outer: max(dk / tol_k, dphi / tol_phi)
+  double gap4 = -1.0;  // the same 4 outers before the end of this launch (convergence-rate estimate)
   SNOP_TSTAMP(tpi0);
   while (outer < ep.max_outer) {
     ++outer;
@@ -389,6 +390,7 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
     const double dk = fabs(k_new - k) / fabs(k_new);
     k = k_new;
     gap = fmax(dk / ep.tol_k, dphi / ep.tol_phi);
+    if (outer == ep.max_outer - 4) gap4 = gap;
     if (dk < ep.tol_k && dphi < ep.tol_phi) {
       converged = true;
       break;
@@ -401,7 +403,14 @@ power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig
     outer_g[b] = outer0 + outer;
     inner_g[b] = inner0 + inner_total;
     conv_g[b] = converged ? 1 : 0;
-    if (tail_key) tail_key[b] = converged ? 0.f : (float)fmin(gap, 3.0e38);  // tail-phase order (below)
+    if (tail_key) {  // predicted remaining outers (tail-phase routing and order, launch_power_iteration)
+      double rem = gap;
+      if (gap4 > 0.0 && gap > 0.0) {  // geometric convergence: gap ~ rho^n -> n_rem = log(gap) / -log(rho)
+        const double rho = fmin(fmax(pow(gap / gap4, 0.25), 1e-6), 1.0 - 1e-9);
+        rem = log(fmax(gap, 1.0)) / -log(rho);
+      }
+      tail_key[b] = converged ? 0.f : (float)fmin(rem, 3.0e38);
+    }
   }
   if constexpr (CL) cl_sync();
 }
@@ -576,22 +585,33 @@ inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
   return SNOP_OK;
 }
 
-// Tail phase of a split power iteration: the instances still iterating after the first launch
-// (not converged, outer count == the phase-1 cap) -> order[0 .. *count), furthest from convergence
-// first (key = max(dk / tol_k, dphi / tol_phi) at the cap, ties by index), so the slowest instance
-// gets a cluster at once instead of waiting behind others. Rank by counting (deterministic);
-// positions never affect an instance's results.
+// Tail phase of a split power iteration: the instances still iterating after a launch (not
+// converged, outer count == cap) -> list A (key > thresh) or list B (the rest; no list B: all in A),
+// each ordered by key descending (ties by index): key = the predicted remaining outers, so the
+// slowest instance gets its cluster first. Rank by counting (deterministic); an instance's list
+// depends on its own key only, and positions never affect its results. cand (nullable): consider
+// only the instances of that list (cand[0 .. *cand_count)), e.g. while other instances are still
+// being solved by a concurrent launch.
 static __global__ void pi_tail_list_kernel(int B, int cap, const int32_t* __restrict__ outer,
                                            const uint8_t* __restrict__ conv, const float* __restrict__ key,
-                                           int* __restrict__ order, int* __restrict__ count) {
-  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
-    if (conv[b] || outer[b] != cap) continue;
-    atomicAdd(count, 1);
+                                           float thresh, int* __restrict__ orderA, int* __restrict__ countA,
+                                           int* __restrict__ orderB, int* __restrict__ countB,
+                                           const int* __restrict__ cand = nullptr,
+                                           const int* __restrict__ cand_count = nullptr) {
+  const int n = cand ? *cand_count : B;
+  auto in = [&](int c) { return !conv[c] && outer[c] == cap; };
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int b = cand ? cand[i] : i;
+    if (!in(b)) continue;
     const float kb = key[b];
+    const bool a = !orderB || kb > thresh;
+    atomicAdd(a ? countA : countB, 1);
     int rank = 0;
-    for (int c = 0; c < B; ++c)
-      if (!conv[c] && outer[c] == cap && (key[c] > kb || (key[c] == kb && c < b))) ++rank;
-    order[rank] = b;
+    for (int j = 0; j < n; ++j) {
+      const int c = cand ? cand[j] : j;
+      if (in(c) && ((!orderB || key[c] > thresh) == a) && (key[c] > kb || (key[c] == kb && c < b))) ++rank;
+    }
+    (a ? orderA : orderB)[rank] = b;
   }
 }
 

@@ -46,6 +46,8 @@ struct Ctx {
   unsigned long long* d_loop_launches = nullptr;  // device counter (kernels launched by loop bodies)
   unsigned long long loop_launches_seen = 0;
   cudaStream_t side = nullptr;                    // capture stream for nested loop bodies
+  cudaStream_t aux = nullptr;                     // second stream of the eigen tail split
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void settle_loops();  // call after the stream has been synchronised
   // Sub-contexts (own stream, flag word and workspace) for host-memspace calls that pipeline
   // H2D / compute / D2H over chunks of the batch; created on first use, owned by this context.

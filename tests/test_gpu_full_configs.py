@@ -2,7 +2,7 @@
 SURVEY §8a). The reduced-size suites elsewhere pin the kernels' arithmetic; these pin the
 production schedules that only appear at full size: the tail split of the single-group eigen
 solve (phase 1 on one CTA per instance, phase 2 on 8-CTA pair-split clusters for the instances
-still iterating after 32 outers), the longest-first dispatch of the 2048-instance fixed-source
+still iterating after 12 outers: predicted-long ones on clusters at once, the rest after up to 32 more single-CTA outers), the longest-first dispatch of the 2048-instance fixed-source
 batch, and the C5 MD-PNOP pipeline (FNO -> recast fixed point -> warm-started K1).
 
 Tolerances (north_star): outer/inner iteration counts within +-1; k and scalar flux within
@@ -89,7 +89,7 @@ def test_c3_full_tail_and_random_instances(c3):
 
 def test_c3_full_fixed_iterations_across_phase_boundary():
     """Fixed counts (52 outers x 2 inner sweeps, tolerances 0): every instance crosses the tail-split
-    boundary at 32 outers; flux and k at 1e-10 on 16 instances of the full 512-instance batch."""
+    boundaries (12 and 44 outers); flux and k at 1e-10 on 16 instances of the full 512-instance batch."""
     p = W.config3()
     cfg = _eig_cfg(p, tolerance=1e-300, tolerance_k=1e-300, tolerance_phi=1e-300, max_outer_iterations=52,
                    max_inner_iterations=2)
