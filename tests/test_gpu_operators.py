@@ -76,6 +76,26 @@ def test_zero_weights_zero_output():
     assert np.all(op.predict(np.ones((2, 50))) == 0)
 
 
+@pytest.mark.parametrize("c", [2.0, 0.37])
+def test_deeponet_branch_linearity(c):
+    """scaling the branch's final layer by c scales predictions by c. c = 2 is exact in
+    floating point (the 3xTF32 split of 2x is 2 x the split of x), so the device result is
+    bit-identical; other c within the fp32 operator tolerance."""
+    n = 300
+    prm = OPS.deeponet_init(n, width=64, activation=OPS.TANH, seed=6)
+    prm.branch.biases[-1][:] = np.random.default_rng(3).uniform(-0.1, 0.1, prm.branch.biases[-1].shape)
+    g = snop.Grid1D(10.0, n)
+    s = np.random.default_rng(4).uniform(0, 1, (9, n))
+    base = snop.SolutionOperator.deeponet(g, prm).predict(s)
+    prm.branch.weights[-1] *= np.float32(c)
+    prm.branch.biases[-1] *= np.float32(c)
+    scaled = snop.SolutionOperator.deeponet(g, prm).predict(s)
+    if c == 2.0:
+        assert np.array_equal(scaled, 2.0 * base)
+    else:
+        assert _rel(scaled, c * base) < OP_RTOL
+
+
 def test_fno_identity_spectral_layer_is_lowpass():
     # SPEC.md:326: W = 0, b = 0, R = identity on retained modes -> DFT truncation low-pass
     n, C, M = 64, 4, 6

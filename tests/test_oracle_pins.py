@@ -162,3 +162,65 @@ def test_determinism_across_thread_counts():
     a = O.source_iteration(p.length, p.n_cells, 16, p.sigma_t, p.sigma_s0, p.source, cfg, n_threads=1)
     b = O.source_iteration(p.length, p.n_cells, 16, p.sigma_t, p.sigma_s0, p.source, cfg, n_threads=4)
     assert np.array_equal(a["phi"], b["phi"])
+
+
+# ---- SPEC operator properties on the fp64 oracle -------------------------
+def _identity_layer_fno(n, C=4, M=6):
+    from paper_2509_01416_b200 import operators as OPS
+    prm = OPS.fno_init(C, M, 1, 4, OPS.RELU, seed=1)
+    prm.W[0][:] = 0
+    prm.R_re[0][:] = 0
+    prm.R_im[0][:] = 0
+    for m in range(M):
+        prm.R_re[0][m] = np.eye(C, dtype=np.float32)
+    prm.lift_W[:] = 0
+    prm.lift_W[:, 0] = 1.0  # every lifted channel = S
+    prm.P1_W[:] = 0
+    prm.P1_W[0, 0] = 1.0
+    prm.P2_W[:] = 0
+    prm.P2_W[0] = 1.0
+    return prm
+
+
+@pytest.mark.parametrize("n", [64, 100, 37])
+def test_oracle_fno_identity_spectral_layer_is_lowpass(n):
+    """W = 0, b = 0, R = identity on the retained modes -> the layer is the DFT-truncation
+    low-pass of its input; the oracle (fp64 arithmetic) matches a brute-force DFT truncation within
+    1e-10 (arbitrary lengths: 100 and a prime)."""
+    from paper_2509_01416_b200 import operators as OPS
+    M = 6
+    prm = _identity_layer_fno(n, M=M)
+    x = np.arange(n)
+    s = (1.0 + 0.5 * np.sin(2 * np.pi * 3 * x / n) + 0.2 * np.cos(2 * np.pi * 11 * x / n))[None, :]
+    s = s.astype(np.float32).astype(np.float64)  # the operator's input is fp32 (SPEC.md:319); all else fp64
+    oo = O.OracleOperator.fno(10.0, n, (1.0, 0.8), OPS.RELU, 4, M, 1, 4, prm.packed())
+    got = oo.predict(s)[0]
+    # brute-force truncated DFT (no FFT): modes 0..M-1, imaginary part of DC dropped, inverse 1/n
+    k = np.arange(M)[:, None]
+    E = np.exp(-2j * np.pi * k * x[None, :] / n)
+    X = E @ s[0]
+    X[0] = X[0].real
+    w = np.where(np.arange(M) == 0, 1.0, 2.0)
+    if n % 2 == 0 and M > n // 2:
+        w[n // 2] = 1.0
+    low = (w[:, None] * (X[:, None] * np.conj(E))).real.sum(axis=0) / n
+    want = np.maximum(low, 0.0)
+    assert np.max(np.abs(got - want)) < 1e-10 * np.max(np.abs(want))
+
+
+@pytest.mark.parametrize("c", [2.0, 0.37])
+def test_oracle_deeponet_branch_linearity(c):
+    """scaling the branch's final-layer weights (and bias) by c scales every prediction
+    by c (inner-product structure, paper Eq. 11)."""
+    from paper_2509_01416_b200 import operators as OPS
+    n = 50
+    prm = OPS.deeponet_init(n, width=16, activation=OPS.TANH, seed=4)
+    prm.branch.biases[-1][:] = np.random.default_rng(1).uniform(-0.1, 0.1, prm.branch.biases[-1].shape)
+    s = np.random.default_rng(2).uniform(0, 1, (3, n))
+    mk = lambda p: O.OracleOperator.deeponet(10.0, n, (1.0, 0.5), OPS.TANH, p.branch.sizes, p.branch.packed(),
+                                             p.trunk.sizes, p.trunk.packed(), None)
+    base = mk(prm).predict(s)
+    prm.branch.weights[-1] *= np.float32(c)
+    prm.branch.biases[-1] *= np.float32(c)
+    scaled = mk(prm).predict(s)
+    assert np.max(np.abs(scaled - c * base)) < 1e-6 * np.max(np.abs(c * base))
