@@ -842,6 +842,10 @@ snop_status device_loop(Ctx& ctx, std::vector<uint64_t> key, Body&& body) {
                        cudaStreamUpdateCaptureDependencies(ctx.stream, &node, 1, cudaStreamSetCaptureDependencies));
   }
   key.push_back(ctx.slot_gen);
+  {  // execution options select kernels inside the body: a graph captured under others is stale
+    const int32_t* o = reinterpret_cast<const int32_t*>(&ctx.opt);
+    for (size_t i = 0; i < sizeof(ctx.opt) / sizeof(int32_t); ++i) key.push_back((uint64_t)(uint32_t)o[i]);
+  }
   Ctx::LoopGraph* lg = nullptr;
   for (auto& g : ctx.graphs)
     if (g.key == key) lg = &g;
@@ -868,7 +872,7 @@ snop_status device_loop(Ctx& ctx, std::vector<uint64_t> key, Body&& body) {
       cudaGetLastError();  // a capture broken by an allocation leaves a sticky-free error state
     }
     if (!g) return bs != SNOP_OK ? bs : cuda_status("device loop capture", cudaErrorStreamCaptureInvalidated);
-    key.back() = ctx.slot_gen;
+    key[key.size() - 1 - sizeof(ctx.opt) / sizeof(int32_t)] = ctx.slot_gen;
     cudaGraphExec_t ex = nullptr;
     const cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
