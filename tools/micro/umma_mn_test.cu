@@ -1,6 +1,9 @@
-// Bring-up test: one tcgen05.mma.kind::tf32 (M = 128, N = 32, K = 8) with an MN-major A operand in
-// the 128-byte-swizzled layout, B K-major 128-byte-swizzled. A's four 32-row M blocks are placed
-// MBS bytes apart; the descriptor's LBO / SBO fields are varied to find the convention.
+// Bring-up test: one tcgen05.mma.kind::tf32 (M = 128, N = 32, K = 8) with an MN-major A operand,
+// B K-major 128-byte-swizzled. Round 1 used the plain 128-B swizzle for MN-major A and got zeros:
+// for MN-major tf32 the only valid layout is SWIZZLE_128B_BASE32B (layout type 1; CUTLASS
+// Layout_MN_SW128_32B_Atom): 128-B rows (32 MN elements) per K index, atoms of 4 K rows with the
+// 32-byte chunk index XOR (k % 4), K groups of 4 rows SBO apart, 32-element MN blocks LBO apart.
+// amaj = 2 tests that layout (M-block stride MBS, K-group stride KGS).
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -o umma_mn_test umma_mn_test.cu
 #include <cstdio>
 #include <cstdint>
@@ -9,7 +12,8 @@
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__global__ void k(const float* A, const float* Bm, float* D, uint32_t mbs, uint32_t lbo, uint32_t sbo, int amaj) {
+__global__ void k(const float* A, const float* Bm, float* D, uint32_t mbs, uint32_t lbo, uint32_t sbo, int amaj,
+                  uint32_t kgs) {
   extern __shared__ __align__(1024) unsigned char raw[];
   const uint32_t pad = (1024u - (su32(raw) & 1023u)) & 1023u;
   unsigned char* sm = raw + pad;
@@ -24,7 +28,9 @@ __global__ void k(const float* A, const float* Bm, float* D, uint32_t mbs, uint3
   // A[m][k], k < 8: MN-major SW128: block m/32 at mbs, row k (128 B), 16-B chunk ((m%32)/4) ^ (k%8)
   for (int i = t; i < 128 * 8; i += blockDim.x) {
     const int m = i / 8, kk = i % 8;
-    const uint32_t off = amaj ? (m / 32) * mbs + kk * 128 + ((((m % 32) / 4) ^ (kk % 8)) * 16) + (m % 4) * 4
+    const uint32_t off = amaj == 2 ? (m / 32) * mbs + (kk / 4) * kgs + (kk % 4) * 128 +
+                                         ((((m % 32) / 8) ^ (kk % 4)) * 32) + (m % 8) * 4
+                       : amaj ? (m / 32) * mbs + kk * 128 + ((((m % 32) / 4) ^ (kk % 8)) * 16) + (m % 4) * 4
                               : (m / 8) * 1024 + (m % 8) * 128 + (((kk / 4) ^ (m % 8)) * 16) + (kk % 4) * 4;
     *reinterpret_cast<float*>(sm + off) = A[m * 8 + kk];
   }
@@ -50,10 +56,11 @@ __global__ void k(const float* A, const float* Bm, float* D, uint32_t mbs, uint3
   if (t == 0) {
     const uint32_t ad = su32(sa), bd = su32(sb);
     const uint64_t adesc = (uint64_t)((ad >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-                           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+                           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) |
+                           ((uint64_t)(amaj == 2 ? 1 : 2) << 61);
     const uint64_t bdesc = (uint64_t)((bd >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
                            ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-    const uint32_t id = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)amaj << 15) | ((uint32_t)(32 >> 3) << 17) |
+    const uint32_t id = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(amaj ? 1 : 0) << 15) | ((uint32_t)(32 >> 3) << 17) |
                         ((uint32_t)(128 >> 4) << 24);
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 0, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
                  ::"r"(tmem), "l"(adesc), "l"(bdesc), "r"(id) : "memory");
@@ -94,18 +101,22 @@ int main() {
   cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 40 * 1024);
   const uint32_t opts[4] = {128, 1024, 4096, 8192};
-  for (int amaj = 0; amaj <= 1; ++amaj)
-    for (uint32_t mbs : {1024u, 4096u})
-      for (uint32_t lbo : opts)
-        for (uint32_t sbo : opts) {
-          if (amaj == 0 && (mbs != 1024u || lbo != 128u || sbo != 1024u)) continue;
+  for (int amaj = 0; amaj <= 2; amaj += 2)
+    for (uint32_t mbs : {1024u, 2048u, 4096u})
+      for (uint32_t kgs : {512u, 1024u})
+        for (int swap = 0; swap < 2; ++swap) {
+          const uint32_t lbo = amaj ? (swap ? kgs : mbs) : 128u, sbo = amaj ? (swap ? mbs : kgs) : 1024u;
+          if (amaj == 0 && (mbs != 1024u || kgs != 512u || swap)) continue;
+          if (amaj == 2 && kgs * 2 > mbs) continue;  // the two K groups fit inside one M block's span
           cudaMemset(dD, 0, D.size() * 4);
-          k<<<1, 128, 40 * 1024>>>(dA, dB, dD, mbs, lbo, sbo, amaj);
+          k<<<1, 128, 40 * 1024>>>(dA, dB, dD, mbs, lbo, sbo, amaj, kgs);
           cudaError_t e = cudaDeviceSynchronize();
           if (e != cudaSuccess) { printf("mbs %u lbo %u sbo %u: %s\n", mbs, lbo, sbo, cudaGetErrorString(e)); return 1; }
           cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost);
           double err = 0; for (size_t i = 0; i < D.size(); ++i) err = fmax(err, fabs(D[i] - R[i]));
-          printf("a_major %d  M-block stride %5u  LBO %5u  SBO %5u : max abs err %g%s  D[0][0..3] %g %g %g %g ref %g %g %g %g\n", amaj, mbs, lbo, sbo, err, err < 1e-3 ? "   <== OK" : "", D[0], D[1], D[2], D[3], R[0], R[1], R[2], R[3]);
+          printf("a_major %d  M-block stride %5u  K-group stride %5u  LBO %5u  SBO %5u : max abs err %g%s\n", amaj,
+                 mbs, kgs, lbo, sbo, err, err < 1e-3 ? "   <== OK" : "");
         }
+  (void)opts;
   return 0;
 }
