@@ -145,6 +145,15 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
+// MN-major tf32 (the only valid MN-major tf32 layout, SWIZZLE_128B_BASE32B = type 1): 128-B rows of
+// 32 MN elements per K index, 4-row atoms with the 32-B chunk index XOR (k % 4) (what TMA's
+// SWIZZLE_128B_ATOM_32B writes), K groups of 4 rows SBO = 512 B apart, 32-element MN blocks LBO
+// apart (tools/micro/umma_mn_test.cu).
+__device__ __forceinline__ uint64_t mn32_desc(uint32_t saddr, uint32_t lbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)(512 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)1 << 61);
+}
+constexpr uint32_t kAMajorMN = 1u << 15;  // instruction descriptor: A is MN-major
 __host__ __device__ constexpr uint32_t idesc(int n) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
 }
@@ -566,10 +575,11 @@ cudaError_t launch(const Args& a, const CUtensorMap* maps, cudaStream_t st) {
 // ---- FNO forward truncated DFT on the tensor core -------------------------------------------
 // Vh[b][c][m'] = sum_i V[b][i][c] F[m'][i] for C = 64 channels, 2M = 32 modes. One work unit =
 // a sample pair: M = 128 rows (2 samples x 64 channels), N = 32 modes, K = all n cells in blocks
-// of 128 (4 chunks of 32). V is channel-contiguous (an MN-major A operand, which kind::tf32 does
-// not accept on this part), so the TMA lands four 32-channel x 32-cell boxes per chunk and the
-// converter warps transpose them into the K-major 128-byte-swizzled hi / lo buffers while
-// splitting (3xTF32). Each 128-cell block accumulates in TMEM (K = 128, as the other contractions);
+// of 128 (4 chunks of 32). V is channel-contiguous, an MN-major A operand: the TMA lands four
+// 32-channel x 32-cell boxes per chunk in the SWIZZLE_128B_ATOM_32B layout, which is exactly the
+// MN-major tf32 canonical layout, so the MMA reads them in place as A_hi and the converter warps
+// only write the lo parts (3xTF32) into a buffer of the same layout (SNOP_DFT_MN = 1; 0 keeps the
+// round-1 transpose into K-major hi / lo: 240 vs 216 us per layer). Each 128-cell block accumulates in TMEM (K = 128, as the other contractions);
 // the epilogue adds the blocks' results in registers in block order and writes Vh once.
 // Two rings: TMA landing stages (raw boxes + the pre-split F chunk, which the MMA reads in place;
 // freed by the MMA commit) and converted K-major hi / lo A slots.
@@ -587,9 +597,16 @@ struct alignas(1024) DftTcLand {
 };
 static_assert(offsetof(DftTcLand, b_lo) == offsetof(DftTcLand, b_hi) + DFT_NT * KC * sizeof(float),
               "the N = 64 hi|lo MMA reads b_hi and b_lo as one 64-row K-major operand");
+#ifndef SNOP_DFT_MN
+#define SNOP_DFT_MN 1  // A (the activations) read MN-major in place; 0: transposed to K-major
+#endif
 struct alignas(1024) DftTcConv {
+#if SNOP_DFT_MN
+  float a_lo[TM * KC];  // lo parts of the landed boxes, same MN-major layout
+#else
   float a_hi[TM * KC];  // K-major [128 rows][32 cells] (swizzled)
   float a_lo[TM * KC];
+#endif
 };
 struct DftTcSmem {
   DftTcLand land[DFT_LAND];
@@ -605,7 +622,10 @@ __device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int c0
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
       : "memory");
 }
-constexpr int DFT_NCONV = 8;
+#ifndef SNOP_DFT_NCONV
+#define SNOP_DFT_NCONV 8
+#endif
+constexpr int DFT_NCONV = SNOP_DFT_NCONV;
 constexpr int DFT_THREADS = (2 + DFT_NCONV + 4) * 32;  // producer, MMA, converters, 4 epilogue warps
 
 __global__ void __launch_bounds__(DFT_THREADS, 1)
@@ -676,8 +696,20 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
             const int sc = (int)(it % SC), sl = (int)(it % SL);
             bar_wait(&s.cfull[sc], (it / SC) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t ah = su32(s.cv[sc].a_hi), al = su32(s.cv[sc].a_lo);
             const uint32_t bh = su32(s.land[sl].b_hi), bl = su32(s.land[sl].b_lo);
+#if SNOP_DFT_MN
+            // A_hi = the landed boxes themselves (the tensor core truncates fp32 to tf32), MN-major:
+            // 4 boxes = 4 MN blocks of 32 channels, 4 KB apart; a k-step of 8 cells = 1024 B
+            const uint32_t ah = su32(s.land[sl].a_raw), al = su32(s.cv[sc].a_lo);
+#pragma unroll
+            for (int ks = 0; ks < KC / 8; ++ks) {
+              const uint32_t off = ks * 32, aoff = ks * 1024;
+              const uint32_t first = (c == 0 && ks == 0) ? 0u : 1u;
+              mma(d, mn32_desc(ah + aoff, 4096), sw128_desc(bh + off), id2 | kAMajorMN, first);
+              mma(d, mn32_desc(al + aoff, 4096), sw128_desc(bh + off), id | kAMajorMN, 1u);
+            }
+#else
+            const uint32_t ah = su32(s.cv[sc].a_hi), al = su32(s.cv[sc].a_lo);
 #pragma unroll
             for (int ks = 0; ks < KC / 8; ++ks) {
               const uint32_t off = ks * 32;
@@ -686,6 +718,7 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
               mma(d, sw128_desc(ah + off), sw128_desc(bh + off), id2, first);
               mma(d, sw128_desc(al + off), sw128_desc(bh + off), id, 1u);
             }
+#endif
             commit(&s.cempty[sc]);
             commit(&s.lempty[sl]);
           }
@@ -704,6 +737,14 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
         bar_wait(&s.full[sl], (it / SL) & 1);
         bar_wait(&s.cempty[sc], ((it / SC) & 1) ^ 1);  // the MMAs of chunk it - SC are done
         const float* ar = s.land[sl].a_raw;
+#if SNOP_DFT_MN
+        {  // lo = rnd_tf32(x - trunc_tf32(x)), element-wise in the landed layout (no transpose)
+          const float4* a4 = reinterpret_cast<const float4*>(ar);
+          float4* l4 = reinterpret_cast<float4*>(s.cv[sc].a_lo);
+#pragma unroll
+          for (int i = 0; i < TM * KC / 4 / (DFT_NCONV * 32); ++i) l4[ct + i * DFT_NCONV * 32] = split_lo(a4[ct + i * DFT_NCONV * 32]);
+        }
+#else
         float* ah = s.cv[sc].a_hi;
         float* al = s.cv[sc].a_lo;
         // task = (box q, 4-cell group kg, 4-channel group jc): four 16-B loads of the landed box,
@@ -732,6 +773,7 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
             *reinterpret_cast<float4*>(al + o) = split_lo(h);
           }
         }
+#endif
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) bar_arrive(&s.cfull[sc]);
@@ -890,7 +932,8 @@ bool fno_dft_tc(const float* V, const float* F, const float* F_lo, float* Vh, in
   const cuuint32_t bv[3] = {32, 32, 1};
   const cuuint32_t es[3] = {1, 1, 1};
   if (enc(&mv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(V), dv, sv, bv, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+          SNOP_DFT_MN ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
   if (!make_map(&mf, F, 32, n, n, 32) || !make_map(&mfl, F_lo, 32, n, n, 32)) return false;
   const int npairs = (B + 1) / 2;
