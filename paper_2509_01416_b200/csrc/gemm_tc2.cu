@@ -110,6 +110,8 @@ struct Args {
   int a1_pre, a2_pre, b1_pre, b2_pre;  // operand has a pre-split lo array (loaded, not converted)
   int tma_store;                       // N = 64, contiguous fp32 rows: epilogue stores by TMA
   int decouple;                        // mbarrier staging hand-off instead of per-tile named barriers
+  int b1_mn;      // B segment 1 is N-contiguous (MN-major): loaded as 32 x 32 boxes (32B-atom swizzle)
+  int64_t b1_bcol;  // its batch stride in elements along the contiguous (column) dimension
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -154,6 +156,7 @@ __device__ __forceinline__ uint64_t mn32_desc(uint32_t saddr, uint32_t lbo) {
          ((uint64_t)(512 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)1 << 61);
 }
 constexpr uint32_t kAMajorMN = 1u << 15;  // instruction descriptor: A is MN-major
+constexpr uint32_t kBMajorMN = 1u << 16;  // instruction descriptor: B is MN-major
 __host__ __device__ constexpr uint32_t idesc(int n) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
 }
@@ -271,8 +274,14 @@ __global__ void __launch_bounds__(threads<N>(), 1)
           tma_2d(s.st[st].a_hi, seg2 ? &tA2 : &tA1, kk, ar, &s.full[st]);
           if (apre) tma_2d(s.st[st].a_lo, seg2 ? &tA2l : &tA1l, kk, ar, &s.full[st]);
           if constexpr (!BR) {
-            tma_2d(s.st[st].b_hi, seg2 ? &tB2 : &tB1, kk, br, &s.full[st]);
-            if (bpre) tma_2d(s.st[st].b_lo, seg2 ? &tB2l : &tB1l, kk, br, &s.full[st]);
+            if (!seg2 && a.b1_mn) {  // N-contiguous B: boxes of [32 k][32 n] at 4 KB (MN blocks)
+              const int col = (int)(b * a.b1_bcol + n0);
+#pragma unroll
+              for (int h = 0; h < N / 32; ++h) tma_2d(s.st[st].b_hi + h * 32 * KC, &tB1, col + 32 * h, kk, &s.full[st]);
+            } else {
+              tma_2d(s.st[st].b_hi, seg2 ? &tB2 : &tB1, kk, br, &s.full[st]);
+              if (bpre) tma_2d(s.st[st].b_lo, seg2 ? &tB2l : &tB1l, kk, br, &s.full[st]);
+            }
           }
         }
       }
@@ -296,13 +305,25 @@ __global__ void __launch_bounds__(threads<N>(), 1)
           const uint32_t ah = su32(s.st[st].a_hi), al = su32(s.st[st].a_lo);
           const uint32_t bh = BR ? su32(s.bres + c * N * KC) : su32(s.st[st].b_hi);
           const uint32_t bl = BR ? su32(s.bres + (BR_CHUNKS + c) * N * KC) : su32(s.st[st].b_lo);
+          const bool bmn = !BR && a.b1_mn && !(g.ksplit > 0 && c * KC >= g.ksplit);
+          if (bmn) {  // MN-major B: 8 k = 2 four-row groups = 1024 B per k-step; MN blocks 4 KB apart
 #pragma unroll
-          for (int ks = 0; ks < KC / 8; ++ks) {
-            const uint32_t off = ks * 32;  // 8 tf32 = 32 B along K inside the swizzle row
-            const uint32_t first = (c == 0 && ks == 0) ? 0u : 1u;
-            mma(d, sw128_desc(al + off), sw128_desc(bh + off), id, first);  // small terms first
-            mma(d, sw128_desc(ah + off), sw128_desc(bl + off), id, 1u);
-            mma(d, sw128_desc(ah + off), sw128_desc(bh + off), id, 1u);
+            for (int ks = 0; ks < KC / 8; ++ks) {
+              const uint32_t off = ks * 32, boff = ks * 1024;
+              const uint32_t first = (c == 0 && ks == 0) ? 0u : 1u;
+              mma(d, sw128_desc(al + off), mn32_desc(bh + boff, 4096), id | kBMajorMN, first);
+              mma(d, sw128_desc(ah + off), mn32_desc(bl + boff, 4096), id | kBMajorMN, 1u);
+              mma(d, sw128_desc(ah + off), mn32_desc(bh + boff, 4096), id | kBMajorMN, 1u);
+            }
+          } else {
+#pragma unroll
+            for (int ks = 0; ks < KC / 8; ++ks) {
+              const uint32_t off = ks * 32;  // 8 tf32 = 32 B along K inside the swizzle row
+              const uint32_t first = (c == 0 && ks == 0) ? 0u : 1u;
+              mma(d, sw128_desc(al + off), sw128_desc(bh + off), id, first);  // small terms first
+              mma(d, sw128_desc(ah + off), sw128_desc(bl + off), id, 1u);
+              mma(d, sw128_desc(ah + off), sw128_desc(bh + off), id, 1u);
+            }
           }
           commit(&s.empty[st]);
         }
@@ -833,7 +854,9 @@ __global__ void __launch_bounds__(DFT_THREADS, 1)
 bool gemm_tc2(const GemmArgs& g, cudaStream_t st, int64_t mfold, cudaError_t* err) {
   using namespace tc2;
   *err = cudaSuccess;
-  if (mfold > 0 || g.beta != 0.f || g.K > 128 || g.N > 128 || g.sak != 1 || g.sbk != 1) return false;
+  // B segment 1 may be N-contiguous (sbn == 1, MN-major): N a multiple of 32, K-chunks whole
+  const bool b1mn = g.sbn == 1 && g.sbk != 1 && g.N % 32 == 0 && !g.B_lo;
+  if (mfold > 0 || g.beta != 0.f || g.K > 128 || g.N > 128 || g.sak != 1 || (g.sbk != 1 && !b1mn)) return false;
   if (g.ksplit > 0 && (g.ksplit % KC != 0 || g.sak2 != 1 || g.sbk2 != 1)) return false;
   if (g.rowdot_w && g.N > 128) return false;
   const int K1 = g.ksplit > 0 ? g.ksplit : g.K, K2 = g.ksplit > 0 ? g.K - g.ksplit : 0;
@@ -851,7 +874,23 @@ bool gemm_tc2(const GemmArgs& g, cudaStream_t st, int64_t mfold, cudaError_t* er
   CUtensorMap maps[9];  // A1 A2 B1 B2, their pre-split lo parts (copies of the hi maps when absent), C
   std::memset(maps, 0, sizeof(maps));
   const int64_t rowsA1 = (g.batch - 1) * a.a1_brows + g.M, rowsB1 = (g.batch - 1) * a.b1_brows + g.N;
-  if (!make_map(&maps[0], g.A, rowsA1, K1, g.sam, TM) || !make_map(&maps[2], g.B, rowsB1, K1, g.sbn, NT)) return false;
+  a.b1_mn = b1mn ? 1 : 0;
+  a.b1_bcol = b1mn ? g.sbb : 0;
+  if (!make_map(&maps[0], g.A, rowsA1, K1, g.sam, TM)) return false;
+  if (b1mn) {  // [K rows][batch * (column stride)] fp32, 32 x 32 boxes in the 32B-atom swizzle
+    EncodeFn enc = encoder();
+    const cuuint64_t dims[2] = {(cuuint64_t)((g.batch - 1) * g.sbb + g.N), (cuuint64_t)K1};
+    const cuuint64_t strides[1] = {(cuuint64_t)(g.sbk * 4)};
+    const cuuint32_t box[2] = {32, (cuuint32_t)KC};
+    const cuuint32_t es[2] = {1, 1};
+    if (!enc || (reinterpret_cast<uintptr_t>(g.B) & 15) || ((g.sbk * 4) & 15) ||
+        enc(&maps[2], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(g.B), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  } else if (!make_map(&maps[2], g.B, rowsB1, K1, g.sbn, NT)) {
+    return false;
+  }
   a.a1_pre = g.A_lo && make_map(&maps[4], g.A_lo, rowsA1, K1, g.sam, TM);
   a.b1_pre = g.B_lo && make_map(&maps[6], g.B_lo, rowsB1, K1, g.sbn, NT);
   if (g.ksplit > 0) {

@@ -46,9 +46,8 @@ struct snop_op {
   float* FT = nullptr;                  // forward DFT transposed, [n][2M] (fno_dft64)
   // pre-split 3xTF32 lo parts of the constant GEMM operands (TMA engine loads them, no conversion)
   float *Ginv_lo = nullptr, *P1W_lo = nullptr, *F_lo = nullptr;
-  // spectral mixing as a tensor-core GEMM (per layer): the per-mode real form of R as two K-major
-  // B segments [2][M][2C][C] (rows n = 2o + {0: U_re, 1: U_im}; segment 0 multiplies V_re,
-  // segment 1 V_im), and their lo parts
+  // spectral mixing as tensor-core GEMMs (per layer): the per-mode real forms of R, K-major,
+  // [4][M][C][C] = {Rr^T, -Ri^T (U_re), Ri^T, Rr^T (U_im)} with [o][c] rows, and their lo parts
   std::vector<float*> mixB, mixB_lo;
   // exact operator
   int order = 16;
@@ -636,6 +635,7 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
     ctx.launches++;
   }
   for (int l = l0 ? 1 : 0; l < op.layers; ++l) {
+    bool u_mn = false;  // U written mode-major [2M][B][C] by the tensor-core mixing
     // forward truncated DFT: Vh[b][c][m'] = sum_i V[b][i][c] F[m'][i]. Tensor-core engine: one
     // GEMM over all B*C rows (batch folded into M); FFMA engine: batched per sample.
     GemmArgs f{};
@@ -669,24 +669,27 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
     }
     // complex channel mixing per retained mode
     if (tc_done && use_tc(ctx) && ctx.opt.fno_mix == 0) {
-      // on the tensor core: per mode m, [U_re | U_im] = [V_re | V_im] . [[Rr, Ri], [-Ri, Rr]] as ONE
-      // mode-batched 3xTF32 GEMM, samples x 2C outputs x 2C, reading the mode-major spectra Vh
-      // [2M][B][C] (re rows, then im rows) as two K segments. With the outputs ordered n = 2o + im
-      // the U address [b][o][m + M im] is affine in n (stride M), so the engine's epilogue writes
-      // the [b][o][m'] rows the inverse GEMM consumes directly.
-      const size_t seg = (size_t)2 * M * C * C;
-      GemmArgs mx{};
-      mx.M = B; mx.N = 2 * C; mx.K = 2 * C; mx.batch = M;
-      mx.A = Vh; mx.sam = C; mx.sak = 1; mx.sab = (int64_t)B * C;
-      mx.ksplit = C;
-      mx.A2 = Vh + (size_t)M * B * C; mx.sam2 = C; mx.sak2 = 1; mx.sab2 = (int64_t)B * C;
-      mx.B = op.mixB[l]; mx.sbn = C; mx.sbk = 1; mx.sbb = (int64_t)2 * C * C;
-      mx.B2 = op.mixB[l] + seg; mx.sbn2 = C; mx.sbk2 = 1; mx.sbb2 = (int64_t)2 * C * C;
-      mx.B_lo = op.mixB_lo[l];
-      mx.B2_lo = op.mixB_lo[l] + seg;
-      mx.C = U; mx.scb = 1; mx.scm = (int64_t)C * 2 * M; mx.scn = M;
-      mx.alpha = 1.f; mx.act = ACT_NONE;
-      SNOP_TRY(gemm(ctx, mx));
+      // on the tensor core: per mode m, U_re = [V_re | V_im] . [Rr ; -Ri] and U_im = [V_re | V_im] .
+      // [Ri ; Rr] - two mode-batched 3xTF32 GEMMs (samples x C outputs x 2C, the mode-major spectra
+      // Vh [2M][B][C] read as two K segments) writing U' [2M][B][C] (mode-major, channel rows
+      // contiguous: whole-tile TMA stores); the inverse GEMM then reads U' as an N-contiguous
+      // (MN-major) B operand
+      const size_t MCC = (size_t)M * C * C;
+      for (int part = 0; part < 2; ++part) {
+        GemmArgs mx{};
+        mx.M = B; mx.N = C; mx.K = 2 * C; mx.batch = M;
+        mx.A = Vh; mx.sam = C; mx.sak = 1; mx.sab = (int64_t)B * C;
+        mx.ksplit = C;
+        mx.A2 = Vh + (size_t)M * B * C; mx.sam2 = C; mx.sak2 = 1; mx.sab2 = (int64_t)B * C;
+        mx.B = op.mixB[l] + (2 * part) * MCC; mx.sbn = C; mx.sbk = 1; mx.sbb = (int64_t)C * C;
+        mx.B2 = op.mixB[l] + (2 * part + 1) * MCC; mx.sbn2 = C; mx.sbk2 = 1; mx.sbb2 = (int64_t)C * C;
+        mx.B_lo = op.mixB_lo[l] + (2 * part) * MCC;
+        mx.B2_lo = op.mixB_lo[l] + (2 * part + 1) * MCC;
+        mx.C = U + (size_t)part * M * B * C; mx.scb = (int64_t)B * C; mx.scm = C; mx.scn = 1;
+        mx.alpha = 1.f; mx.act = ACT_NONE;
+        SNOP_TRY(gemm(ctx, mx));
+      }
+      u_mn = true;
     } else if (C == 64 && tc_done) {  // the tensor-core DFT wrote Vh mode-major
       const size_t sm = (size_t)(128 * 128 + 128 * (MIX_S + 4)) * sizeof(float);
       cudaFuncSetAttribute(fno_mix64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -706,7 +709,11 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
       GemmArgs iv{};
       iv.M = n; iv.N = C; iv.K = 2 * M + C; iv.batch = B;
       iv.A = op.Ginv; iv.sam = 2 * M; iv.sak = 1; iv.sab = 0;
-      iv.B = U; iv.sbn = 2 * M; iv.sbk = 1; iv.sbb = (int64_t)C * 2 * M;
+      if (u_mn) {  // U' [2M][B][C]: element (b, o, m') at m' B C + b C + o
+        iv.B = U; iv.sbn = 1; iv.sbk = (int64_t)B * C; iv.sbb = C;
+      } else {
+        iv.B = U; iv.sbn = 2 * M; iv.sbk = 1; iv.sbb = (int64_t)C * 2 * M;
+      }
       iv.ksplit = 2 * M;
       iv.A2 = V; iv.sam2 = C; iv.sak2 = 1; iv.sab2 = (int64_t)n * C;
       iv.B2 = op.W[l]; iv.sbn2 = C; iv.sbk2 = 1; iv.sbb2 = 0;
@@ -721,7 +728,11 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
       GemmArgs iv{};
       iv.M = n; iv.N = C; iv.K = 2 * M; iv.batch = B;
       iv.A = op.Ginv; iv.sam = 2 * M; iv.sak = 1; iv.sab = 0;
-      iv.B = U; iv.sbn = 2 * M; iv.sbk = 1; iv.sbb = (int64_t)C * 2 * M;
+      if (u_mn) {
+        iv.B = U; iv.sbn = 1; iv.sbk = (int64_t)B * C; iv.sbb = C;
+      } else {
+        iv.B = U; iv.sbn = 2 * M; iv.sbk = 1; iv.sbb = (int64_t)C * 2 * M;
+      }
       iv.C = Vn; iv.scm = C; iv.scn = 1; iv.scb = (int64_t)n * C;
       iv.alpha = 1.f; iv.act = ACT_NONE;
       SNOP_TRY(gemm(ctx, iv));
@@ -1521,19 +1532,17 @@ snop_status snop_fno_create(snop_ctx* ctx, const snop_grid* grid, double tstar, 
   for (int l = 0; l < layers; ++l) {
     op->Rr.push_back(op->upload(p, M * C * C));
     op->Ri.push_back(op->upload(p + M * C * C, M * C * C));
-    {  // U_re = V_re Rr - V_im Ri, U_im = V_re Ri + V_im Rr per mode; output column n = 2o + im
+    {  // U_re = V_re Rr - V_im Ri, U_im = V_re Ri + V_im Rr per mode, as B operands [o][c]
       const float *rr = p, *ri = p + M * C * C;
       std::vector<float> mb(4 * M * C * C);
-      const size_t seg = 2 * M * C * C;
       for (size_t m = 0; m < M; ++m)
         for (size_t c = 0; c < C; ++c)
           for (size_t o = 0; o < C; ++o) {
-            const size_t src = (m * C + c) * C + o;
-            const size_t re = (m * 2 * C + 2 * o) * C + c, im = re + C;  // rows 2o, 2o + 1
-            mb[re] = rr[src];
-            mb[im] = ri[src];
-            mb[seg + re] = -ri[src];
-            mb[seg + im] = rr[src];
+            const size_t src = (m * C + c) * C + o, dst = (m * C + o) * C + c;
+            mb[0 * M * C * C + dst] = rr[src];
+            mb[1 * M * C * C + dst] = -ri[src];
+            mb[2 * M * C * C + dst] = ri[src];
+            mb[3 * M * C * C + dst] = rr[src];
           }
       op->mixB.push_back(op->upload(mb.data(), mb.size()));
       op->mixB_lo.push_back(op->upload_lo(mb.data(), mb.size()));
