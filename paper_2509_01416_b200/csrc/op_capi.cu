@@ -351,18 +351,37 @@ __global__ void __launch_bounds__(32 * DFT_S) fno_dft64(int B, int n, const floa
 
 // Layer-0 spectral mixing from the source spectrum (affine-lift folding): U[b][o][m] + i U[b][o][M+m]
 // = (Sh[b][m] + i Sh[b][M+m]) (P[m][o] + i P[M+m][o]) + Q[m][o] + i Q[M+m][o].
+// MN: U written mode-major U'[m'][b][o] (consecutive threads -> consecutive channels: coalesced)
+// for the inverse GEMM's MN-major B operand; otherwise [b][o][m'].
+template <bool MN>
 __global__ void fno_mix_l0(int B, int C, int M, const float* __restrict__ Sh, const float* __restrict__ P,
                            const float* __restrict__ Q, float* __restrict__ U) {
   const size_t total = (size_t)B * C * M;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
-    const int m = (int)(e % M);
-    const size_t bo = e / M;
-    const int o = (int)(bo % C);
-    const size_t b = bo / C;
+    int m, o;
+    size_t b;
+    if constexpr (MN) {  // e = (m * B + b) * C + o
+      o = (int)(e % C);
+      const size_t mb = e / C;
+      b = mb % B;
+      m = (int)(mb / B);
+    } else {
+      m = (int)(e % M);
+      const size_t bo = e / M;
+      o = (int)(bo % C);
+      b = bo / C;
+    }
     const float sr = Sh[b * 2 * M + m], si = Sh[b * 2 * M + M + m];
     const float pr = P[(size_t)m * C + o], pi = P[(size_t)(M + m) * C + o];
-    U[bo * 2 * M + m] = fmaf(sr, pr, fmaf(-si, pi, Q[(size_t)m * C + o]));
-    U[bo * 2 * M + M + m] = fmaf(sr, pi, fmaf(si, pr, Q[(size_t)(M + m) * C + o]));
+    const float ur = fmaf(sr, pr, fmaf(-si, pi, Q[(size_t)m * C + o]));
+    const float ui = fmaf(sr, pi, fmaf(si, pr, Q[(size_t)(M + m) * C + o]));
+    if constexpr (MN) {
+      U[((size_t)m * B + b) * C + o] = ur;
+      U[((size_t)(M + m) * B + b) * C + o] = ui;
+    } else {
+      U[(b * C + o) * 2 * M + m] = ur;
+      U[(b * C + o) * 2 * M + M + m] = ui;
+    }
   }
 }
 
@@ -619,13 +638,19 @@ snop_status op_predict_dev(Ctx& ctx, snop_op& op, int B, const double* in, doubl
     // source spectrum S^[b][m'] = sum_i S[b][i] F[m'][i]  (B x 2M x n)
     GemmArgs fs = rowmajor(B, 2 * M, n, X, n, op.F, n, Vh, 2 * M, nullptr, ACT_NONE);
     SNOP_TRY(gemm(ctx, fs));
-    fno_mix_l0<<<grid_for(ctx, (size_t)B * C * M), 256, 0, ctx.stream>>>(B, C, M, Vh, op.l0_P, op.l0_Q, U);
+    const bool l0mn = C % 32 == 0;  // the engine's MN-major B needs whole 32-column boxes
+    if (l0mn) fno_mix_l0<true><<<grid_for(ctx, (size_t)B * C * M), 256, 0, ctx.stream>>>(B, C, M, Vh, op.l0_P, op.l0_Q, U);
+    else fno_mix_l0<false><<<grid_for(ctx, (size_t)B * C * M), 256, 0, ctx.stream>>>(B, C, M, Vh, op.l0_P, op.l0_Q, U);
     ctx.launches++;
     GemmArgs iv{};
     iv.M = n; iv.N = C; iv.K = 2 * M; iv.batch = B;
     iv.A = op.Ginv; iv.sam = 2 * M; iv.sak = 1; iv.sab = 0;
     iv.A_lo = op.Ginv_lo;
-    iv.B = U; iv.sbn = 2 * M; iv.sbk = 1; iv.sbb = (int64_t)C * 2 * M;
+    if (l0mn) {  // U' mode-major (MN-major B)
+      iv.B = U; iv.sbn = 1; iv.sbk = (int64_t)B * C; iv.sbb = C;
+    } else {
+      iv.B = U; iv.sbn = 2 * M; iv.sbk = 1; iv.sbb = (int64_t)C * 2 * M;
+    }
     iv.C = V; iv.scm = C; iv.scn = 1; iv.scb = (int64_t)n * C;
     iv.bias = op.l0_C; iv.alpha = 1.f; iv.act = op.act;
     iv.r2_a = op.l0_A; iv.r2_b = op.l0_B; iv.r2_s = X; iv.r2_sb = n; iv.r2_x = op.xc;
