@@ -36,7 +36,8 @@ inline cudaError_t device_once(DeviceOnce& d, int* sms, F&& setup) {
 
 enum Act : int { ACT_RELU = 0, ACT_TANH = 1, ACT_GELU = 2, ACT_NONE = 3 };
 
-// GELU(x) = x Phi(x) = 0.5 x (1 + erf(x / sqrt 2)) (exact-erf form), erf from
+// GELU(x) = x Phi(x) = 0.5 x (1 + erf(x / sqrt 2)) (exact-erf form). Default: erfc
+// from A&S 7.1.28 (SNOP_GELU_AS28, one MUFU, below). Alternative (SNOP_GELU_AS28 = 0): erf from
 // Abramowitz & Stegun 7.1.26: erf(z) = 1 - t (a1 + a2 t + ... + a5 t^4) exp(-z^2), t = 1/(1 + p z),
 // |error| <= 1.5e-7 (<= 5e-7 absolute on GELU in fp32 arithmetic). The reciprocal and the
 // exponential are the raw flush-to-zero MUFU ops (rcp.approx.ftz, ex2.approx.ftz: __fdividef /
@@ -61,6 +62,34 @@ __device__ __forceinline__ float ex2_ftz(float x) {
 #define SNOP_GELU_C2 (-1.005091295e+00f)
 #define SNOP_GELU_C3 (2.011695713e-01f)
 #define SNOP_GELU_C4 (-1.801917326e-01f)
+#ifndef SNOP_GELU_AS28
+#define SNOP_GELU_AS28 1
+#endif
+#if SNOP_GELU_AS28
+// A&S 7.1.28: erf(y) = 1 - (1 + a1 y + ... + a6 y^6)^-16, |error| <= 3e-7; with y = |x|/sqrt 2 the
+// factors 1/sqrt 2^i are folded into the coefficients, so erfc(|x|/sqrt 2) = r^16 with
+// r = 1 / poly(|x|): ONE MUFU (the reciprocal) per GELU instead of two (reciprocal and exp2) -
+// the epilogues of the FNO GEMMs are bound by the MUFU rate (16 per SM per clock). |error| <=
+// 7.5e-7 absolute on GELU in fp32 (swept over [-12, 12], 1-ulp reciprocal included).
+#define SNOP_GELU_B1 (4.986734697e-02f)
+#define SNOP_GELU_B2 (2.114100615e-02f)
+#define SNOP_GELU_B3 (3.277626324e-03f)
+#define SNOP_GELU_B4 (3.800357500e-05f)
+#define SNOP_GELU_B5 (4.889063564e-05f)
+#define SNOP_GELU_B6 (5.382975000e-06f)
+__device__ __forceinline__ float gelu_f(float x) {
+  // GELU = max(x, 0) - (|x| / 2) erfc(|x| / sqrt 2)
+  const float y = fabsf(x);
+  const float p = fmaf(fmaf(fmaf(fmaf(fmaf(fmaf(SNOP_GELU_B6, y, SNOP_GELU_B5), y, SNOP_GELU_B4), y, SNOP_GELU_B3), y,
+                                SNOP_GELU_B2), y, SNOP_GELU_B1), y, 1.0f);
+  float r = rcp_ftz(p);
+  r *= r;
+  r *= r;
+  r *= r;
+  r *= r;
+  return fmaf(-0.5f * y, r, fmaxf(x, 0.0f));
+}
+#else
 __device__ __forceinline__ float gelu_f(float x) {
   // GELU = x/2 + |x|/2 erf(z) = max(x, 0) - (|x|/2) t P(t) e^{-z^2}, z = |x|/sqrt 2, and
   // |x|/2 = z / sqrt 2: the factor 1/sqrt 2 is folded into the A&S coefficients (a_i / sqrt 2).
@@ -70,6 +99,8 @@ __device__ __forceinline__ float gelu_f(float x) {
   const float e = ex2_ftz((z * z) * -1.44269504088896340736f);  // exp(-z^2)
   return fmaf(z, p * e, fmaxf(x, 0.0f));
 }
+
+#endif
 
 // Two GELUs with packed FP32 (fma.rn.f32x2 / mul.rn.f32x2 -> FFMA2 / FMUL2): the same operations
 // in the same order per element as gelu_f (bit-identical results) in ~9 instead of ~13 issue slots
@@ -92,6 +123,25 @@ __device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsig
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+#if SNOP_GELU_AS28
+__device__ __forceinline__ void gelu2(float& xa, float& xb) {
+  const unsigned long long y = f2_pk(fabsf(xa), fabsf(xb));
+  unsigned long long p = f2_fma(f2_pk(SNOP_GELU_B6, SNOP_GELU_B6), y, f2_pk(SNOP_GELU_B5, SNOP_GELU_B5));
+  p = f2_fma(p, y, f2_pk(SNOP_GELU_B4, SNOP_GELU_B4));
+  p = f2_fma(p, y, f2_pk(SNOP_GELU_B3, SNOP_GELU_B3));
+  p = f2_fma(p, y, f2_pk(SNOP_GELU_B2, SNOP_GELU_B2));
+  p = f2_fma(p, y, f2_pk(SNOP_GELU_B1, SNOP_GELU_B1));
+  p = f2_fma(p, y, f2_pk(1.0f, 1.0f));
+  float pa, pb;
+  f2_upk(p, pa, pb);
+  unsigned long long r = f2_pk(rcp_ftz(pa), rcp_ftz(pb));
+  r = f2_mul(r, r);
+  r = f2_mul(r, r);
+  r = f2_mul(r, r);
+  r = f2_mul(r, r);
+  f2_upk(f2_fma(f2_mul(y, f2_pk(-0.5f, -0.5f)), r, f2_pk(fmaxf(xa, 0.0f), fmaxf(xb, 0.0f))), xa, xb);
+}
+#else
 __device__ __forceinline__ void gelu2(float& xa, float& xb) {
   const unsigned long long z = f2_mul(f2_pk(fabsf(xa), fabsf(xb)), f2_pk(0.70710678118654752440f, 0.70710678118654752440f));
   float da, db;
@@ -107,6 +157,8 @@ __device__ __forceinline__ void gelu2(float& xa, float& xb) {
   const unsigned long long e = f2_pk(ex2_ftz(ga), ex2_ftz(gb));
   f2_upk(f2_fma(z, f2_mul(p, e), f2_pk(fmaxf(xa, 0.0f), fmaxf(xb, 0.0f))), xa, xb);
 }
+
+#endif
 
 __device__ __forceinline__ float act_f(float x, int act) {
   switch (act) {
