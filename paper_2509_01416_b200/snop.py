@@ -185,6 +185,8 @@ class _Args:
         import torch
         ext = torch.cuda.ExternalStream(ctx.stream_ptr)
         ext.wait_stream(torch.cuda.current_stream())
+        if len(ctx._pending) > 4096:  # bound what many unsynchronised calls keep alive
+            ctx.synchronize()
         ctx._pending.extend(self.keep)
         ctx._pending.extend(self.outs)
 
