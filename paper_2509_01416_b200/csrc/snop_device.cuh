@@ -173,16 +173,6 @@ __device__ __forceinline__ double rel_change(double num, double den, int norm) {
   return num > 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : 0.0;
 }
 
-// Predicated FP64 ops (no select instructions in the scan; the predicate is lane-constant).
-__device__ __forceinline__ void pfma(double& d, double a, double b, double c, bool p) {
-  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t@q fma.rn.f64 %0, %1, %2, %3;\n\t}"
-      : "+d"(d) : "d"(a), "d"(b), "d"(c), "r"((unsigned)p));
-}
-__device__ __forceinline__ void pmul(double& d, double a, double b, bool p) {
-  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q mul.rn.f64 %0, %1, %2;\n\t}"
-      : "+d"(d) : "d"(a), "d"(b), "r"((unsigned)p));
-}
-
 // Stage Sigma_s0 and the external source in shared memory for the solve (the per-iteration flux
 // update then reads no global memory).
 #ifndef SNOP_STAGE_SS
@@ -407,6 +397,9 @@ __device__ __forceinline__ void maps_phase(const SweepConsts& sc, SweepSmem<K, N
 //   2. 5-step shuffle scan of the lane totals -> the lane's exclusive entry map (Ax, Bx);
 //   3. exclusive map of chunk e = (Ax, Bx) composed with prefix e-1: E-1 independent
 //      compositions, processed in descending e so each reads its prefix before it is replaced.
+#ifndef SNOP_SCAN_REG_E
+#define SNOP_SCAN_REG_E 4
+#endif
 template <int K, int NT, bool FWD, bool CL>
 __device__ __forceinline__ void scan_one(SweepSmem<K, NT>& sm, int q, int lane, int gslot) {
   constexpr int E = NT / 32;
@@ -416,95 +409,96 @@ __device__ __forceinline__ void scan_one(SweepSmem<K, NT>& sm, int q, int lane, 
   const double* a = sm.agg[q][0] + base;
   const double* b = sm.agg[q][FWD ? 1 : 2] + base;
   double* XA = sm.xmap[q][FWD ? 0 : 1] + base;
-  double* XB = sm.agg[q][FWD ? 1 : 2] + base;  // in place: chunk e's offset is read before it is replaced
-  // Loads are batched ahead of the dependent chain in runs of H chunks: stores to the xmap
-  // scratch may alias later agg loads as far as the compiler knows, so without batching every
-  // step would pay a full shared-memory round trip.
-  constexpr int H = E < 4 ? E : 4;
-  double A = 1.0, B = 0.0;
+  double* XB = sm.agg[q][FWD ? 1 : 2] + base;  // in place: every offset is read before any is replaced
+  // 1. inclusive prefixes of the own run, kept in registers (the kernel is bound by shared-memory
+  //    wavefronts as much as by FP64 issue: no scratch round trip). Runs longer than SNOP_SCAN_REG_E chunks keep
+  //    only the run total and recompose the prefixes from the chunk maps in step 3.
+  constexpr bool REG = E <= SNOP_SCAN_REG_E;
+  constexpr int EP = REG ? E : 1;
+  double pa[EP], pb[EP];
+  if constexpr (REG) {
 #pragma unroll
-  for (int e0 = 0; e0 < E; e0 += H) {
-    double av[H], bv[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-      av[h] = a[D * (e0 + h)];
-      bv[h] = b[D * (e0 + h)];
+    for (int e = 0; e < E; ++e) {
+      pa[e] = a[D * e];
+      pb[e] = b[D * e];
     }
 #pragma unroll
-    for (int h = 0; h < H; ++h) {
-      if (e0 + h == 0) {
-        A = av[0];
-        B = bv[0];
-      } else {
-        B = fma(av[h], B, bv[h]);
-        A *= av[h];
+    for (int e = 1; e < E; ++e) {
+      pb[e] = fma(pa[e], pb[e - 1], pb[e]);
+      pa[e] *= pa[e - 1];
+    }
+  } else {
+    double ta = 1.0, tb = 0.0;
+#pragma unroll
+    for (int e0 = 0; e0 < E; e0 += 4) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        av[h] = a[D * (e0 + h)];
+        bv[h] = b[D * (e0 + h)];
       }
-      XA[D * (e0 + h)] = A;
-      XB[D * (e0 + h)] = B;
-    }
-  }
-#ifdef SNOP_SCAN_R4
-  // experiment (opt-in, measured slower than radix 2 on B200): radix-4 Kogge-Stone over the 32
-  // lane totals, strides 1, 4, 16, each step composing lanes L-3o, L-2o, L-o, L as a 2-level tree
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 2) {
-    double a1 = __shfl_up_sync(0xffffffffu, A, o), b1 = __shfl_up_sync(0xffffffffu, B, o);
-    double a2 = __shfl_up_sync(0xffffffffu, A, 2 * o), b2 = __shfl_up_sync(0xffffffffu, B, 2 * o);
-    double a3 = __shfl_up_sync(0xffffffffu, A, 3 * o), b3 = __shfl_up_sync(0xffffffffu, B, 3 * o);
-    if (lane < o) { a1 = 1.0; b1 = 0.0; }
-    if (lane < 2 * o) { a2 = 1.0; b2 = 0.0; }
-    if (lane < 3 * o) { a3 = 1.0; b3 = 0.0; }
-    // (3 then 2) and (1 then own), then combine: f then g = (Af Ag, Ag Bf + Bg)
-    const double ax = a3 * a2, bx = fma(a2, b3, b2);
-    const double ay = a1 * A, by = fma(A, b1, B);
-    B = fma(ay, bx, by);
-    A = ax * ay;
+      for (int h = 0; h < 4; ++h) {
+        tb = fma(av[h], tb, bv[h]);
+        ta *= av[h];
+      }
+    }
+    pa[0] = ta;
+    pb[0] = tb;
   }
-#else
-  // radix-2 Kogge-Stone over the 32 lane totals (5 dependent shuffle rounds)
+  // 2. shift the run totals up one lane: the lanes then hold (identity, T_0, ..., T_30), whose
+  //    inclusive scan is the exclusive scan of the totals, and lane 0's identity is what an
+  //    out-of-range lane reads in the rounds below (x * 1 and x + A * 0 are exact), so the
+  //    dependent chain has no predicates or selects: 5 rounds of shuffle + FMA.
+  double A = __shfl_up_sync(0xffffffffu, pa[EP - 1], 1), B = __shfl_up_sync(0xffffffffu, pb[EP - 1], 1);
+  if (lane == 0) {
+    A = 1.0;
+    B = 0.0;
+  }
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const double ap = __shfl_up_sync(0xffffffffu, A, o), bq = __shfl_up_sync(0xffffffffu, B, o);
-    pfma(B, A, bq, B, lane >= o);  // predicated: no selects on the dependent chain
-    pmul(A, A, ap, lane >= o);
+    const int srcl = max(lane - o, 0);
+    const double ap = __shfl_sync(0xffffffffu, A, srcl), bq = __shfl_sync(0xffffffffu, B, srcl);
+    B = fma(A, bq, B);
+    A *= ap;
   }
-#endif
-  double Ax = __shfl_up_sync(0xffffffffu, A, 1), Bx = __shfl_up_sync(0xffffffffu, B, 1);
-  if (lane == 0) {
-    Ax = 1.0;
-    Bx = 0.0;
-  }
-  if (lane == 31) {
-    sm.total[q][FWD ? 0 : 2] = A;
-    sm.total[q][FWD ? 1 : 3] = B;
+  if (lane == 31) {  // whole-domain map = exclusive map of run 31 followed by run 31
+    const double TA = A * pa[EP - 1], TB = fma(pa[EP - 1], B, pb[EP - 1]);
+    sm.total[q][FWD ? 0 : 2] = TA;
+    sm.total[q][FWD ? 1 : 3] = TB;
     if constexpr (CL) {
-      sm.ctot[gslot][q][FWD ? 0 : 2] = A;
-      sm.ctot[gslot][q][FWD ? 1 : 3] = B;
+      sm.ctot[gslot][q][FWD ? 0 : 2] = TA;
+      sm.ctot[gslot][q][FWD ? 1 : 3] = TB;
     }
   }
-  // exclusive maps, descending in runs of H: each run reads its prefixes before replacing them
+  // 3. exclusive map of chunk e = (A, B) followed by the prefix through chunk e-1
+  if constexpr (REG) {
+    XA[0] = A;
+    XB[0] = B;
 #pragma unroll
-  for (int e1 = E - 1; e1 >= 1; e1 -= H) {
-    double pa[H], pb[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-      const int e = e1 - h;
-      if (e >= 1) {
-        pa[h] = XA[D * (e - 1)];
-        pb[h] = XB[D * (e - 1)];
-      }
+    for (int e = 1; e < E; ++e) {
+      XA[D * e] = A * pa[e - 1];
+      XB[D * e] = fma(pa[e - 1], B, pb[e - 1]);
     }
+  } else {
+    double ra = A, rb = B;
 #pragma unroll
-    for (int h = 0; h < H; ++h) {
-      const int e = e1 - h;
-      if (e >= 1) {
-        XA[D * e] = Ax * pa[h];
-        XB[D * e] = fma(pa[h], Bx, pb[h]);
+    for (int e0 = 0; e0 < E; e0 += 4) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {  // (chunk maps read before their slots are replaced below)
+        av[h] = a[D * (e0 + h)];
+        bv[h] = b[D * (e0 + h)];
+      }
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        XA[D * (e0 + h)] = ra;
+        XB[D * (e0 + h)] = rb;
+        rb = fma(av[h], rb, bv[h]);
+        ra *= av[h];
       }
     }
   }
-  XA[0] = Ax;
-  XB[0] = Bx;
 }
 
 // Phase B: one warp per (pair, direction) scans the NT chunk maps of the CTA into the exclusive
@@ -576,10 +570,13 @@ __device__ __forceinline__ void replay_phase(const SweepConsts& sc, SweepSmem<K,
       TAb = ba;
       TBb = bb;
     } else {
-      TAf = sm.total[q][0];
-      TBf = sm.total[q][1];
-      TAb = sm.total[q][2];
-      TBb = sm.total[q][3];
+      TAf = TBf = TAb = TBb = 0.0;
+      if (w.rr || w.rl) {  // (vacuum faces need no whole-domain map: no shared-memory reads)
+        TAf = sm.total[q][0];
+        TBf = sm.total[q][1];
+        TAb = sm.total[q][2];
+        TBb = sm.total[q][3];
+      }
     }
     double psi_right_in = 0.0, psi_left_in = 0.0;
     if (w.rr || w.rl) {
@@ -661,7 +658,7 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
   SweepCtl w;
   w.t = t;
   w.lane = t & 31;
-  w.warp = t >> 5;
+  w.warp = __shfl_sync(0xffffffffu, t >> 5, 0);  // warp-uniform for the compiler: uniform branches around the scans
   w.crank = CL ? cl_rank() : 0;
   w.csz = CL ? cl_size() : 1;
   w.cbase = w.crank * NT * K;
