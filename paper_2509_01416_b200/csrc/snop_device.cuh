@@ -117,6 +117,15 @@ __device__ __forceinline__ double warp_max_nonneg(double v) {
   return __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
 }
 
+// max(acc, |x|) for a non-negative accumulator, on the bit patterns (4 integer instructions
+// instead of the ~8 of fmax's NaN handling; a NaN pattern is larger than every number, so NaNs are
+// sticky and reach the convergence test).
+__device__ __forceinline__ double absmax_acc(double acc, double x) {
+  const unsigned long long a = (unsigned long long)__double_as_longlong(acc);
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
+  return __longlong_as_double((long long)(a > b ? a : b));
+}
+
 // Two independent block maxima of non-negative values (|d|, |phi|) with a single barrier.
 template <int NT>
 __device__ __forceinline__ void block_max2(double& a, double& b, double* scratch, int phase) {
@@ -131,9 +140,9 @@ __device__ __forceinline__ void block_max2(double& a, double& b, double* scratch
   __syncthreads();
   double ra = s[0], rb = s[NW];
 #pragma unroll
-  for (int w = 1; w < NW; ++w) {
-    ra = fmax(ra, s[w]);
-    rb = fmax(rb, s[NW + w]);
+  for (int w = 1; w < NW; ++w) {  // (non-negative values: maxima on the bit patterns)
+    ra = absmax_acc(ra, s[w]);
+    rb = absmax_acc(rb, s[NW + w]);
   }
   a = ra;
   b = rb;
@@ -164,6 +173,16 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* scratch
 }
 
 // relative change from the two reduced quantities (zero rule pinned in oracle)
+// The rel-Linf stopping test on the two reduced maxima without the division: sets `nan` when
+// num/den would be NaN (the caller stops, non-converged) and returns num/den < tol otherwise
+// (den > 0: num < tol den; 0/0 counts as 0, x/0 as +inf).
+__device__ __forceinline__ bool linf_converged(double num, double den, double tol, bool& nan) {
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  nan = (num != num) || (den != den) || (num == inf && den == inf);
+  if (den > 0.0) return num < tol * den;
+  return num == 0.0 && 0.0 < tol;
+}
+
 __device__ __forceinline__ double rel_change(double num, double den, int norm) {
   if (norm == 1) {
     num = sqrt(num);
@@ -752,8 +771,8 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
           const double pn = 0.5 * (FL + FR);
           const double d = pn - sm.phi[o];
           if (cfg.norm == 0) {
-            num = fmax(num, fabs(d));
-            den = fmax(den, fabs(pn));
+            num = absmax_acc(num, d);
+            den = absmax_acc(den, pn);
           } else {
             num = fma(d, d, num);
             den = fma(pn, pn, den);
@@ -794,8 +813,8 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
     // phi = sum_n w_n psi_avg,n = mean of the two edge scalar fluxes (diamond difference); the
     // next sweep's emission; the convergence norm's two reductions. Specialised per norm and for
     // threads whose K cells are all real cells (no per-cell predicates on the common path).
-    auto phi_cell = [&](int j) -> double {
-      const double pn = 0.5 * (acc.Fl[j] + ((j + 1 < K) ? acc.Fl[j + 1] : acc.Fr));
+    auto phi_cell = [&](int j, double& pn) -> double {
+      pn = 0.5 * (acc.Fl[j] + ((j + 1 < K) ? acc.Fl[j + 1] : acc.Fr));
       if constexpr (WJ) {
         const double JR = (j + 1 < K) ? acc.Jl[j + 1] : acc.Jr;
         if (io.jc) io.jc[c0 + j] = 0.5 * (acc.Jl[j] + JR);
@@ -812,24 +831,27 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
       if (full) {
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-          const double d = phi_cell(j);
-          num = fmax(num, fabs(d));
-          den = fmax(den, fabs(sm.phi[j * NT + t]));
+          double pn;
+          const double d = phi_cell(j, pn);
+          num = absmax_acc(num, d);
+          den = absmax_acc(den, pn);
         }
       } else {
 #pragma unroll
         for (int j = 0; j < K; ++j)
           if (c0 + j < Nc) {
-            const double d = phi_cell(j);
-            num = fmax(num, fabs(d));
-            den = fmax(den, fabs(sm.phi[j * NT + t]));
+            double pn;
+            const double d = phi_cell(j, pn);
+            num = absmax_acc(num, d);
+            den = absmax_acc(den, pn);
           }
       }
     } else {
 #pragma unroll
       for (int j = 0; j < K; ++j)
         if (c0 + j < Nc) {
-          const double d = phi_cell(j), pn = sm.phi[j * NT + t];
+          double pn;
+          const double d = phi_cell(j, pn);
           num = fma(d, d, num);
           den = fma(pn, pn, den);
         }
@@ -838,11 +860,21 @@ __device__ int si_solve(const SweepConsts& sc, const SolveConfig& cfg, SweepSmem
     }
     SNOP_TSTAMP(ti2);
     SNOP_TACC(6, ti1, ti2);
-    const double rel = rel_change(num, den, cfg.norm);
-    if (!(rel == rel)) break;  // NaN: stop, reported non-converged
-    if (rel < cfg.tol) {
-      conv = true;
-      break;
+    if (cfg.norm == 0) {
+      bool nan;
+      const bool done = linf_converged(num, den, cfg.tol, nan);
+      if (nan) break;  // NaN: stop, reported non-converged
+      if (done) {
+        conv = true;
+        break;
+      }
+    } else {
+      const double rel = rel_change(num, den, cfg.norm);
+      if (!(rel == rel)) break;
+      if (rel < cfg.tol) {
+        conv = true;
+        break;
+      }
     }
   }
   if (WJ && io.leak) {  // balance diagnostic: net leakages of the last sweep
