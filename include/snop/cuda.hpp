@@ -193,6 +193,25 @@ inline EigenSolution power_iteration(Context& ctx, const Grid1D& grid, int order
   return e;
 }
 
+// sweep, batched over instances: emission [B][Nc][order] -> psi_avg [B][order][Nc]
+// and the net outgoing partial currents at the two faces.
+struct SweepResult {
+  std::vector<double> psi_avg, outflow_left, outflow_right;
+};
+inline SweepResult sweep(Context& ctx, const Grid1D& grid, int order, int batch, const std::vector<double>& sigma_t,
+                         const std::vector<double>& emission, int boundary_left = SNOP_BC_VACUUM,
+                         int boundary_right = SNOP_BC_VACUUM) {
+  SweepResult r;
+  r.psi_avg.resize(emission.size());
+  r.outflow_left.resize(batch);
+  r.outflow_right.resize(batch);
+  const snop_grid g = grid.c();
+  check(snop_sweep_batched(ctx.get(), SNOP_MEM_HOST, &g, order, batch, sigma_t.data(), emission.data(),
+                           boundary_left, boundary_right, r.psi_avg.data(), r.outflow_left.data(),
+                           r.outflow_right.data()));
+  return r;
+}
+
 // SPEC.md:393-401
 inline std::vector<double> recast_source(Context& ctx, int batch, int n_cells, const std::vector<double>& S,
                                          const std::vector<double>& phi, const std::vector<double>& sigma_t,

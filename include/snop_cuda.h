@@ -160,6 +160,25 @@ snop_status snop_source_iteration_batched(
     const snop_solver_config* cfg, const double* initial_phi,
     double* phi_out, double* current_out, int32_t* iterations, uint8_t* converged);
 
+/*
+ * Batched transport sweep — replaces
+ *   sweep(grid, quadrature, sigma_t, emission, bc) -> (psi_avg, boundary_outflow_left, boundary_outflow_right)
+ *   (SPEC.md:115-123), for B independent instances: ONE diamond-difference sweep of all `order`
+ *   directions with a per-cell-per-direction emission, the cell-average angular flux materialised.
+ * sigma_t [B][Nc]; emission [B][Nc][order] = q(x_i, mu_n) with n ascending in mu (the order of
+ * snop_gauss_legendre: n < order/2 are mu < 0); psi_avg_out [B][order][Nc]. outflow_left/right [B]
+ * (nullable) = sum over directions of w |mu| (psi_out - psi_in) at x = 0 / x = L (net outgoing
+ * partial currents). Boundary order as in source_iteration: reflective left -> the mu < 0
+ * directions first; reflective right only -> mu > 0 first; a reflective right face next to a
+ * reflective left one is lagged, i.e. zero inflow for a single sweep. Nonpositive sigma_t ->
+ * SNOP_INVALID_ARGUMENT. This is the HBM-bound form of the sweep (16 B per cell.angle update);
+ * the fused solvers below never materialise psi.
+ */
+snop_status snop_sweep_batched(
+    snop_ctx* ctx, int32_t memspace, const snop_grid* grid, int32_t order, int32_t batch,
+    const double* sigma_t, const double* emission, int32_t bc_left, int32_t bc_right,
+    double* psi_avg_out, double* outflow_left, double* outflow_right);
+
 /* source_iteration + balance diagnostic: as snop_source_iteration_batched,
  * plus leakage_out[b][2] = the NET outflows (outgoing minus incoming partial currents) at x = 0 and
  * x = L of the last sweep -- the quantities the balance report needs. */

@@ -121,6 +121,38 @@ void oracle_rng_stream(uint64_t seed, int32_t n_u64, uint64_t* u64, int32_t n_un
   for (int i = 0; i < n_normal; ++i) nrm[i] = c.normal();
 }
 
+// sweep, batched: emission [B][Nc][N], psi_avg [B][N][Nc], net outflows [B].
+int oracle_sweep_batched(const snop_grid* grid, int32_t order, int32_t batch, const double* st,
+                         const double* emission, int32_t bc_left, int32_t bc_right, double* psi_avg,
+                         double* out_left, double* out_right, int32_t n_threads) {
+  try {
+    const Grid1D g{grid->length_cm, grid->n_cells};
+    const Quadrature q = gauss_legendre(order);
+    const std::size_t Nc = g.n_cells, N = order;
+    const Boundary bl = bc_left ? Boundary::Reflective : Boundary::Vacuum;
+    const Boundary br = bc_right ? Boundary::Reflective : Boundary::Vacuum;
+    std::string err;
+    int code = 0;
+    std::mutex mu;
+    parallel_chunks(batch, batch, [&](std::size_t, std::size_t b0, std::size_t b1) {
+      for (std::size_t b = b0; b < b1; ++b) {
+        try {
+          sweep(g, q, st + b * Nc, emission + b * Nc * N, bl, br, psi_avg + b * N * Nc,
+                out_left ? out_left + b : nullptr, out_right ? out_right + b : nullptr);
+        } catch (...) {
+          std::lock_guard<std::mutex> lk(mu);
+          code = map_exc();
+          err = g_err;
+        }
+      }
+    }, n_threads);
+    if (code) { g_err = err; return code; }
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
 int oracle_source_iteration_batched(const snop_grid* grid, int32_t order, int32_t batch,
                                     const double* st, const double* ss0, const double* ss1,
                                     const double* src, const snop_solver_config* ccfg,

@@ -26,6 +26,7 @@ EXPORTS = [
     "snop_op_save", "snop_op_load", "snop_model_write_deeponet", "snop_model_write_fno", "snop_model_inspect",
     "snop_grf_sample", "snop_normalize_source", "snop_generate_dataset", "snop_dataset_write", "snop_dataset_read",
     "snop_source_iteration_leakage_batched", "snop_balance_report", "snop_ctx_set_options", "snop_ctx_get_options",
+    "snop_sweep_batched",
 ]
 
 _lib = None
@@ -63,6 +64,7 @@ def load():
         vp, i32, C.POINTER(SnopGrid), i32, i32, i32, vp, vp, vp, vp, vp, C.POINTER(SnopSolverConfig), vp, vp, vp,
         vp, vp, vp, vp]
     lib.snop_recast_source.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, dbl, dbl, vp]
+    lib.snop_sweep_batched.argtypes = [vp, i32, C.POINTER(SnopGrid), i32, i32, vp, vp, i32, i32, vp, vp, vp]
     lib.snop_deeponet_create.argtypes = [vp, C.POINTER(SnopGrid), dbl, dbl, i32, i32, vp, vp, i32, vp, vp, i32,
                                          C.c_float, C.POINTER(vp)]
     lib.snop_fno_create.argtypes = [vp, C.POINTER(SnopGrid), dbl, dbl, i32, i32, i32, i32, i32, vp, C.POINTER(vp)]

@@ -584,6 +584,36 @@ snop_status snop_power_iteration_batched(snop_ctx* ctx, int32_t memspace, const 
   return drain_flags(*ctx);
 }
 
+snop_status snop_sweep_batched(snop_ctx* ctx, int32_t memspace, const snop_grid* grid, int32_t order, int32_t batch,
+                               const double* sigma_t, const double* emission, int32_t bc_left, int32_t bc_right,
+                               double* psi_avg_out, double* outflow_left, double* outflow_right) {
+  if (!ctx) return invalid("ctx is NULL");
+  SNOP_TRY(check_grid(grid, order));
+  if (batch < 0) return invalid("batch must be >= 0");
+  if ((bc_left != 0 && bc_left != 1) || (bc_right != 0 && bc_right != 1))
+    return invalid("boundary must be VACUUM(0) or REFLECTIVE(1)");
+  if (batch == 0) return SNOP_OK;
+  if (!sigma_t || !emission || !psi_avg_out) return invalid("required array pointer is NULL");
+  cudaSetDevice(ctx->device);
+  const size_t B = batch, Nc = grid->n_cells, N = order;
+  if (memspace == SNOP_MEM_DEVICE)
+    return launch_sweep(*ctx, *grid, order, batch, sigma_t, emission, bc_left, bc_right, psi_avg_out, outflow_left,
+                        outflow_right);
+  if (memspace != SNOP_MEM_HOST) return invalid("memspace must be HOST(0) or DEVICE(1)");
+  const double *st, *em;
+  double *psi, *ol, *orr;
+  SNOP_TRY(stage_in(*ctx, 0, sigma_t, B * Nc, &st));
+  SNOP_TRY(stage_in(*ctx, 1, emission, B * Nc * N, &em));
+  SNOP_TRY(stage_out_alloc(*ctx, 2, psi_avg_out, B * Nc * N, &psi));
+  SNOP_TRY(stage_out_alloc(*ctx, 3, outflow_left, B, &ol));
+  SNOP_TRY(stage_out_alloc(*ctx, 4, outflow_right, B, &orr));
+  SNOP_TRY(launch_sweep(*ctx, *grid, order, batch, st, em, bc_left, bc_right, psi, ol, orr));
+  SNOP_TRY(copy_out(*ctx, psi_avg_out, psi, B * Nc * N));
+  SNOP_TRY(copy_out(*ctx, outflow_left, ol, B));
+  SNOP_TRY(copy_out(*ctx, outflow_right, orr, B));
+  return drain_flags(*ctx);
+}
+
 snop_status snop_recast_source(snop_ctx* ctx, int32_t memspace, int32_t batch, int32_t n_cells, const double* source,
                                const double* phi, const double* sigma_t, const double* sigma_s0,
                                double sigma_t_star, double sigma_s0_star, double* out) {

@@ -88,6 +88,11 @@ snop_status launch_power_iteration_big(Ctx& ctx, const snop_grid& g, int order, 
 snop_status launch_balance(Ctx& ctx, const snop_grid& g, int batch, const double* st, const double* ss_out,
                            const double* src, const double* phi, const double* leak, double* residual);
 
+// Standalone transport sweep (sweep.cu): emission [B][Nc][N], psi_avg [B][N][Nc],
+// net outgoing partial currents per instance (nullable).
+snop_status launch_sweep(Ctx& ctx, const snop_grid& g, int order, int batch, const double* st, const double* em,
+                         int bc_left, int bc_right, double* psi, double* out_left, double* out_right);
+
 snop_status launch_recast(Ctx& ctx, size_t n, const double* S, const double* phi, const double* st,
                           const double* ss, double tstar, double sstar, double* out);
 

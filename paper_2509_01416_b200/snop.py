@@ -286,6 +286,29 @@ def source_iteration(grid: Grid1D, order: int, sigma_t, sigma_s0, source, config
     return FixedSourceResult(phi, it, cv, cur, lk)
 
 
+def sweep(grid: Grid1D, order: int, sigma_t, emission, boundary_left: int = 0, boundary_right: int = 0,
+          ctx: Context | None = None, sync: bool = True):
+    """sweep, batched: one diamond-difference sweep of all directions.
+    sigma_t [B][Nc], emission [B][Nc][order] (direction index ascending in mu); returns
+    (psi_avg [B][order][Nc], outflow_left [B], outflow_right [B]) with the net outgoing partial
+    currents at the two faces. boundary_*: 0 vacuum, 1 reflective."""
+    ctx = ctx or default_context()
+    a = _Args(sigma_t, emission)
+    B = int(sigma_t.shape[0])
+    n, N = grid.n_cells, int(order)
+    st, em = a.inp(sigma_t, shape=(B, n)), a.inp(emission, shape=(B, n, N))
+    psi, psi_p = a.out((B, N, n))
+    ol, ol_p = a.out((B,))
+    orr, or_p = a.out((B,))
+    g = grid.c()
+    a.ready(ctx)
+    _capi.check(ctx._lib.snop_sweep_batched(ctx.h, a.memspace, C.byref(g), N, B, st, em, int(boundary_left),
+                                            int(boundary_right), psi_p, ol_p, or_p))
+    if a.device and sync:
+        ctx.synchronize()
+    return psi, ol, orr
+
+
 def balance_report(grid: Grid1D, sigma_t, sigma_s0_out, source, phi, leakage, ctx: Context | None = None):
     """balance_report (SPEC.md:136-148), batched [B][Nc]; leakage [B][2] from source_iteration."""
     ctx = ctx or default_context()

@@ -82,6 +82,21 @@ def rng_stream(seed: int, n: int):
     return u, f, g
 
 
+def sweep(length, n_cells, order, sigma_t, emission, bc_left=0, bc_right=0, n_threads=0):
+    """Oracle sweep: emission [B][Nc][N] -> psi_avg [B][N][Nc], net outflows [B]."""
+    st = np.ascontiguousarray(sigma_t, dtype=np.float64)
+    em = np.ascontiguousarray(emission, dtype=np.float64)
+    B = st.shape[0]
+    psi = np.empty((B, order, n_cells))
+    ol = np.empty(B)
+    orr = np.empty(B)
+    grid = make_grid(length, n_cells)
+    _check(lib().oracle_sweep_batched(C.byref(grid), C.c_int32(order), C.c_int32(B), _p(st), _p(em),
+                                      C.c_int32(bc_left), C.c_int32(bc_right), _p(psi), _p(ol), _p(orr),
+                                      C.c_int32(n_threads)))
+    return psi, ol, orr
+
+
 def source_iteration(length, n_cells, order, sigma_t, sigma_s0, source, cfg: SnopSolverConfig,
                      sigma_s1=None, initial_phi=None, n_threads=0, want_current=False, want_leak=False):
     st = np.ascontiguousarray(sigma_t, dtype=np.float64)
