@@ -7,12 +7,13 @@
 // 16 B of HBM traffic per cell.angle update (+ Sigma_t, 8 B per cell, served once from DRAM and
 // then from L1/L2), so it is HBM-bound and is measured against the copy roofline.
 //
-// Mapping. Thread = one +/-mu pair of one instance; it marches the mu > 0 direction left to
-// right and the mu < 0 direction right to left (two independent recurrences per thread; a
-// reflective face makes one wait for the other's outflow, SURVEY §9 #2 ordering). B*N/2 chains
-// are the parallelism (65536 for BASELINE C2/C5); CTA = one warp, so the grid balances over the
-// 148 SMs. The recurrence is serial in the cell index but needs one dependent 3-instruction
-// chain per cell; everything else (reciprocal, loads, stores) is off the chain.
+// Mapping. Thread = one direction of one instance, marching the slab (mu > 0 left to right,
+// mu < 0 right to left): B*N chains are the parallelism (65536 for BASELINE C2/C5), CTA = one
+// warp, so the grid balances over the 148 SMs at ~14 resident warps each. The recurrence is serial
+// in the cell index but needs one dependent 3-instruction chain per cell; everything else
+// (reciprocal, loads, stores) is off the chain. A reflective face makes the directions of one sign
+// wait for the others' outflow (SURVEY §9 #2 ordering): two launches, the second reading its
+// inflows from the first one's outflow workspace.
 //   * loads: emission [B][Nc][N] makes the N/2 same-sign directions of a cell contiguous, so the
 //     lanes of an instance read one segment per cell. Each thread copies its own q and Sigma_t
 //     values with 8-byte cp.async into a private slot of an S-stage shared-memory ring (tiles of
@@ -20,9 +21,9 @@
 //   * stores: psi_avg [B][N][Nc] is direction-major, so a thread's T results of a tile are
 //     contiguous but the lanes are Nc apart: the warp transposes each tile through shared memory
 //     and writes whole rows (T contiguous cells per row, 32/T rows per instruction).
-//   * partial currents: w mu (psi_out - psi_in) at both faces per pair into a workspace; a second
-//     tiny kernel sums the pairs of an instance in ascending order (deterministic, the oracle's
-//     order).
+//   * partial currents: every chain's outflow goes to a workspace [B][N]; a tiny kernel forms
+//     w mu (psi_out - psi_in) per pair and sums the pairs of an instance in ascending order
+//     (deterministic, the oracle's order).
 #include <string>
 
 #define SNOP_PHASE_SYM g_phase_cycles_sweep
@@ -33,21 +34,20 @@ using namespace snop_dev;
 
 namespace {
 
-constexpr int kT = 8;  // cells per tile
-constexpr int kS = 3;  // ring stages (kS - 1 tiles in flight; 7 one-warp CTAs per SM must fit: 28.6 KB each)
-
-constexpr int kG = 16;  // most instances a warp can span on the vector path (H >= 2)
+constexpr int kT = 8;   // cells per tile
+constexpr int kS = 4;   // ring stages (kS - 1 tiles in flight per warp)
+constexpr int kG = 16;  // most (instance, sign) groups a warp can span on the vector path (N/2 >= 2)
 
 // V16 = false (any order / cell count / alignment): every thread copies its own q and Sigma_t
 // values with 8-byte cp.async. V16 = true (N/2 a power of two, even cell count, 16-byte aligned
-// arrays): even lanes copy the q of a lane pair with 16-byte cp.async.cg (8-byte cp.async.ca
-// serialises its shared-memory writes: 17 wavefronts per request in ncu, the LSU data pipe at 87%),
-// and Sigma_t is copied once per instance of the warp instead of once per lane.
+// arrays): even lanes copy the q of a lane pair (adjacent directions) with 16-byte cp.async.cg
+// (8-byte cp.async.ca serialises its shared-memory writes: 17 wavefronts per request in ncu, the
+// LSU data pipe at 87%), and Sigma_t is copied once per (instance, sign) group of the warp.
 template <bool V16>
 struct SweepTileSmem {
-  double q[kS][2][kT][32];   // emission of the thread's two directions, [stage][fwd/bwd][cell][lane]
-  double st[kS][2][V16 ? kG : kT][V16 ? kT : 32];  // Sigma_t: [..][instance][cell] or [..][cell][lane]
-  double out[2][32][kT + 1]; // psi_avg of the current tile, [fwd/bwd][lane][cell] (+1: conflict-free)
+  double q[kS][kT][32];                           // emission, [stage][cell in sweep order][lane]
+  double st[kS][V16 ? kG : kT][V16 ? kT : 32];    // Sigma_t: [..][group][ascending cell] or [..][cell][lane]
+  double out[32][kT + 1];                         // psi_avg of the current tile, [lane][cell] (+1: conflict-free)
 };
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
@@ -55,194 +55,170 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool val
   const int n = valid ? 8 : 0;  // src-size 0: zero fill (cells beyond the slab)
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   const int n = valid ? 16 : 0;
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// One march over the slab for the enabled directions of this thread's pair.
-//   F: mu > 0, cells ascending, inflow in_f at x = 0;  Bk: mu < 0, cells descending, inflow in_b.
-template <bool F, bool Bk, bool V16>
-__device__ __forceinline__ void march(SweepTileSmem<V16>& sm, int Nc, int N, int lane, bool valid, double c,
-                                      int grp, int grank, int gsize,     // V16: instance slot / rank / lanes in the warp
-                                      const double* __restrict__ st_b,   // Sigma_t of the instance
-                                      const double* __restrict__ em_f,   // &emission[b][0][n+]
-                                      const double* __restrict__ em_b,   // &emission[b][0][n-]
-                                      double* __restrict__ psi, size_t row_f, size_t row_b,
-                                      double in_f, double in_b, double& out_f, double& out_b, bool& bad) {
-  const int ntiles = (Nc + kT - 1) / kT;
+// Directions [n_lo, n_lo + n_cnt) of every instance; chain gt = b * n_cnt + (n - n_lo). infl: null
+// (vacuum inflow) or the outflow workspace of the previous launch (inflow of direction n = outflow
+// of its mirror image N-1-n at the same face).
+template <bool V16>
+__global__ void __launch_bounds__(32)
+sweep_kernel(const __grid_constant__ SweepConsts sc, int batch, int order, int n_lo, int n_cnt,
+             const double* __restrict__ st_g, const double* __restrict__ em_g, double* __restrict__ psi,
+             const double* __restrict__ infl, double* __restrict__ outw /* [B][N] */, int* __restrict__ flags) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<SweepTileSmem<V16>*>(smem_raw);
+  const int lane = threadIdx.x, Nc = sc.n_cells, H = sc.n_pairs, N = order;
+  const long long total = (long long)batch * n_cnt;
+  const long long gt = (long long)blockIdx.x * 32 + lane;
+  const bool valid = gt < total;
+  const long long g = valid ? gt : total - 1;
+  const int b = (int)(g / n_cnt), n = n_lo + (int)(g - (long long)b * n_cnt);
+  const bool fwd = n >= H;
+  const double c = sc.c[fwd ? n - H : H - 1 - n];
+  const double* st_b = st_g + (size_t)b * Nc;
+  const double* em_n = em_g + (size_t)b * Nc * N + n;
+  const size_t row = valid ? ((size_t)b * N + n) * Nc : ~(size_t)0;
+  // vector path: the lanes of this warp that share (instance, sign) (N/2 a power of two)
+  const int hw = H < 32 ? H : 32;
+  const int grp = V16 ? lane / hw : 0, grank = lane % hw;
+  const int ntiles = (Nc + kT - 1) / kT, nfull = Nc / kT;
+
+  // Loop-invariant addressing (the kernel was issue-bound at ~66 instructions per cell with the
+  // addresses and bounds recomputed per cell): global q pointer of tile 0 / cell 0 and its
+  // per-cell and per-tile steps; Sigma_t tile read offsets; write-out row pointers.
+  const long long dq = fwd ? (long long)N : -(long long)N;       // doubles per cell step
+  const double* qp = em_n + (fwd ? 0 : (size_t)(Nc - 1) * N);    // cell of sweep step 0
+  const int xr = fwd ? 0 : 1;  // V16: a backward group's tile is stored ascending: sweep step j at j ^ 1 of
+                               // the reversed pair order (see issue()), i.e. compile-time j +- xr
+  constexpr int RPI = 32 / kT;
+  const int e = lane % kT, rsub = lane / kT;
+  const unsigned fwd_mask = __ballot_sync(0xffffffffu, fwd);
+  double* wb[kT];     // row r = it * RPI + rsub: address of this lane's element in the row's tile 0
+  int wo[kT];         // its index in sm.out
+  unsigned rfw = 0, rok = 0;
+#pragma unroll
+  for (int it = 0; it < kT; ++it) {
+    const int r = it * RPI + rsub;
+    const size_t base = __shfl_sync(0xffffffffu, (unsigned long long)row, r);
+    const bool rf = (fwd_mask >> r) & 1u;
+    rfw |= (rf ? 1u : 0u) << it;
+    rok |= (base != ~(size_t)0 ? 1u : 0u) << it;
+    wb[it] = psi + (base != ~(size_t)0 ? base : 0) + e + (rf ? 0 : Nc - kT);
+    wo[it] = r * (kT + 1) + (rf ? e : kT - 1 - e);
+  }
+  double* const outp = &sm.out[0][0];
+
   auto issue = [&](int k) {
     if (k < ntiles) {
       const int slot = k % kS;
+      const bool full = k < nfull;
       if constexpr (V16) {
-        // q: the even lane of a lane pair copies both lanes' values (adjacent directions); the
-        // mu < 0 directions descend with the lane, so their pair lands swapped (read at lane ^ 1)
-        if ((lane & 1) == 0) {
+        if ((lane & 1) == 0) {  // q of this lane and the next (adjacent directions, same cell)
+          const double* src = qp + (long long)k * kT * dq;
 #pragma unroll
           for (int j = 0; j < kT; ++j) {
-            if constexpr (F) {
-              const int i = k * kT + j;
-              const bool ok = valid && i < Nc;
-              cp_async16(&sm.q[slot][0][j][lane], em_f + (size_t)(ok ? i : 0) * N, ok);
-            }
-            if constexpr (Bk) {
-              const int i = Nc - 1 - k * kT - j;
-              const bool ok = valid && i >= 0;
-              cp_async16(&sm.q[slot][1][j][lane], em_b - 1 + (size_t)(ok ? i : 0) * N, ok);
-            }
+            const bool ok = valid && (full || k * kT + j < Nc);
+            cp_async16(&sm.q[slot][j][lane], ok ? src : em_n, ok);
+            src += dq;
           }
         }
-        // Sigma_t: the lanes of an instance copy its tile once, two cells per copy, ascending
-        for (int m2 = grank; m2 < kT / 2; m2 += gsize) {
-          if constexpr (F) {
-            const int i = k * kT + 2 * m2;
-            const bool ok = valid && i < Nc;  // (even Nc: i + 1 < Nc as well)
-            cp_async16(&sm.st[slot][0][grp][2 * m2], st_b + (ok ? i : 0), ok);
-          }
-          if constexpr (Bk) {
-            const int i = Nc - (k + 1) * kT + 2 * m2;
-            const bool ok = valid && i >= 0;
-            cp_async16(&sm.st[slot][1][grp][2 * m2], st_b + (ok ? i : 0), ok);
-          }
+        // Sigma_t of the group's tile, two ascending cells per copy (even Nc and kT: never split);
+        // a backward group stores the pairs in descending order, so sweep step j reads slot j ^ 1
+        const int a0 = fwd ? k * kT : Nc - (k + 1) * kT;
+        for (int m2 = grank; m2 < kT / 2; m2 += hw) {
+          const int i = a0 + 2 * m2;
+          const bool ok = valid && i >= 0 && i < Nc;
+          cp_async16(&sm.st[slot][grp][fwd ? 2 * m2 : kT - 2 - 2 * m2], st_b + (ok ? i : 0), ok);
         }
       } else {
+        const double* src = qp + (long long)k * kT * dq;
 #pragma unroll
         for (int j = 0; j < kT; ++j) {
-          if constexpr (F) {
-            const int i = k * kT + j;
-            const bool ok = valid && i < Nc;
-            cp_async8(&sm.q[slot][0][j][lane], em_f + (size_t)(ok ? i : 0) * N, ok);
-            cp_async8(&sm.st[slot][0][j][lane], st_b + (ok ? i : 0), ok);
-          }
-          if constexpr (Bk) {
-            const int i = Nc - 1 - k * kT - j;
-            const bool ok = valid && i >= 0;
-            cp_async8(&sm.q[slot][1][j][lane], em_b + (size_t)(ok ? i : 0) * N, ok);
-            cp_async8(&sm.st[slot][1][j][lane], st_b + (ok ? i : 0), ok);
-          }
+          const int sidx = k * kT + j, i = fwd ? sidx : Nc - 1 - sidx;
+          const bool ok = valid && sidx < Nc;
+          cp_async8(&sm.q[slot][j][lane], ok ? src : em_n, ok);
+          cp_async8(&sm.st[slot][j][lane], st_b + (ok ? i : 0), ok);
+          src += dq;
         }
       }
     }
     cp_async_commit();  // (an empty group past the last tile keeps the wait count uniform)
   };
+
 #pragma unroll
   for (int k = 0; k < kS - 1; ++k) issue(k);
-  double pf = in_f, pb = in_b;
+  double psi_e = infl ? infl[(size_t)b * N + (N - 1 - n)] : 0.0;  // edge flux entering the next cell
+  bool bad = false;
+  auto cell = [&](int slot, int j) {
+    double s;
+    if constexpr (V16) s = (&sm.st[slot][grp][0])[(j & 1) ? j - xr : j + xr];
+    else s = sm.st[slot][j][lane];
+    const double q = sm.q[slot][j][lane];
+    bad |= !(s > 0.0);
+    const double avg = fma(c, psi_e, q) * rcp_fast(s + c);
+    psi_e = fma(2.0, avg, -psi_e);
+    sm.out[lane][j] = avg;
+  };
   for (int k = 0; k < ntiles; ++k) {
     issue(k + kS - 1);
-    cp_async_wait<kS - 1>();  // this thread's copies of tile k have landed
+    cp_async_wait<kS - 1>();          // this thread's copies of tile k have landed
     if constexpr (V16) __syncwarp();  // ... and the other lanes' (pair partner, Sigma_t tile)
     const int slot = k % kS;
+    if (k < nfull) {
 #pragma unroll
-    for (int j = 0; j < kT; ++j) {
-      if constexpr (F) {
-        const int i = k * kT + j;
-        if (i < Nc) {
-          const double s = V16 ? sm.st[slot][0][grp][j] : sm.st[slot][0][j][lane], q = sm.q[slot][0][j][lane];
-          bad |= valid && !(s > 0.0);
-          const double avg = fma(c, pf, q) * rcp_fast(s + c);
-          pf = fma(2.0, avg, -pf);
-          sm.out[0][lane][j] = avg;
-        }
-      }
-      if constexpr (Bk) {
-        const int i = Nc - 1 - k * kT - j;
-        if (i >= 0) {
-          const double s = V16 ? sm.st[slot][1][grp][kT - 1 - j] : sm.st[slot][1][j][lane];
-          const double q = sm.q[slot][1][j][V16 ? lane ^ 1 : lane];
-          bad |= valid && !(s > 0.0);
-          const double avg = fma(c, pb, q) * rcp_fast(s + c);
-          pb = fma(2.0, avg, -pb);
-          sm.out[1][lane][j] = avg;
-        }
-      }
-    }
-    __syncwarp();
-    // write-out: 32/kT rows of kT contiguous cells per instruction
-    constexpr int RPI = 32 / kT;
-    const int e = lane % kT, rsub = lane / kT;
+      for (int j = 0; j < kT; ++j) cell(slot, j);
+      __syncwarp();
+      // write-out: 32/kT rows of kT contiguous cells per instruction
 #pragma unroll
-    for (int it = 0; it < kT; ++it) {
-      const int row = it * RPI + rsub;
-      if constexpr (F) {
-        const size_t base = __shfl_sync(0xffffffffu, (unsigned long long)row_f, row);
-        const int i = k * kT + e;
-        const double v = sm.out[0][row][e];
-        if (base != ~(size_t)0 && i < Nc) __stcs(psi + base + i, v);
+      for (int it = 0; it < kT; ++it) {
+        const double v = outp[wo[it]];
+        const long long off = ((rfw >> it) & 1u) ? (long long)k * kT : -(long long)k * kT;
+        if ((rok >> it) & 1u) __stcs(wb[it] + off, v);
       }
-      if constexpr (Bk) {
-        const size_t base = __shfl_sync(0xffffffffu, (unsigned long long)row_b, row);
-        const int i = Nc - (k + 1) * kT + e;  // ascending cells of the descending tile
-        const double v = sm.out[1][row][kT - 1 - e];
-        if (base != ~(size_t)0 && i >= 0) __stcs(psi + base + i, v);
+    } else {  // ragged last tile
+#pragma unroll
+      for (int j = 0; j < kT; ++j)
+        if (k * kT + j < Nc) cell(slot, j);
+      __syncwarp();
+#pragma unroll
+      for (int it = 0; it < kT; ++it) {
+        const bool rf = (rfw >> it) & 1u;
+        const int i = rf ? k * kT + e : Nc - (k + 1) * kT + e;
+        const double v = outp[wo[it]];
+        const long long off = rf ? (long long)k * kT : -(long long)k * kT;
+        if (((rok >> it) & 1u) && i >= 0 && i < Nc) __stcs(wb[it] + off, v);
       }
     }
     __syncwarp();
   }
-  out_f = pf;
-  out_b = pb;
-}
-
-template <bool V16>
-__global__ void __launch_bounds__(32)
-sweep_kernel(const __grid_constant__ SweepConsts sc, int batch, int order, int bc_left, int bc_right,
-             const double* __restrict__ st_g, const double* __restrict__ em_g, double* __restrict__ psi_g,
-             double* __restrict__ part /* [B][H][2] */, int* __restrict__ flags) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto& sm = *reinterpret_cast<SweepTileSmem<V16>*>(smem_raw);
-  const int lane = threadIdx.x, Nc = sc.n_cells, H = sc.n_pairs, N = order;
-  const long long total = (long long)batch * H;
-  const long long gt = (long long)blockIdx.x * 32 + lane;
-  const bool valid = gt < total;
-  const long long g = valid ? gt : total - 1;
-  const int b = (int)(g / H), p = (int)(g - (long long)b * H);
-  const double c = sc.c[p];
-  const double* st_b = st_g + (size_t)b * Nc;
-  const double* em_f = em_g + (size_t)b * Nc * N + (H + p);
-  const double* em_b = em_g + (size_t)b * Nc * N + (H - 1 - p);
-  const size_t row_f = valid ? ((size_t)b * N + (H + p)) * Nc : ~(size_t)0;
-  const size_t row_b = valid ? ((size_t)b * N + (H - 1 - p)) * Nc : ~(size_t)0;
-  // vector path: the lanes of this warp that belong to the same instance (H a power of two)
-  const int hw = H < 32 ? H : 32;
-  const int grp = V16 ? lane / hw : 0, grank = lane % hw, gsize = hw;
-  const bool rl = bc_left == 1, rr = bc_right == 1;
-  bool bad = false;
-  double in_l = 0.0, in_r = 0.0, out_l = 0.0, out_r = 0.0, d0, d1;
-  if (!rl && !rr) {  // both inflows known: the two directions march together
-    march<true, true, V16>(sm, Nc, N, lane, valid, c, grp, grank, gsize, st_b, em_f, em_b, psi_g, row_f, row_b, 0.0, 0.0, out_r, out_l, bad);
-  } else if (rr && !rl) {  // mu > 0 first; its outflow at x = L is the mu < 0 inflow
-    march<true, false, V16>(sm, Nc, N, lane, valid, c, grp, grank, gsize, st_b, em_f, em_b, psi_g, row_f, row_b, 0.0, 0.0, out_r, d0, bad);
-    in_r = out_r;
-    march<false, true, V16>(sm, Nc, N, lane, valid, c, grp, grank, gsize, st_b, em_f, em_b, psi_g, row_f, row_b, 0.0, in_r, d1, out_l, bad);
-  } else {  // reflective left (a reflective right face is lagged: zero inflow for a single sweep)
-    march<false, true, V16>(sm, Nc, N, lane, valid, c, grp, grank, gsize, st_b, em_f, em_b, psi_g, row_f, row_b, 0.0, 0.0, d0, out_l, bad);
-    in_l = out_l;
-    march<true, false, V16>(sm, Nc, N, lane, valid, c, grp, grank, gsize, st_b, em_f, em_b, psi_g, row_f, row_b, in_l, 0.0, out_r, d1, bad);
-  }
-  (void)d0;
-  (void)d1;
-  if (valid) {
-    const double wm = sc.wmu[p];
-    part[2 * gt] = wm * (out_l - in_l);
-    part[2 * gt + 1] = wm * (out_r - in_r);
-  }
+  bad = bad && valid;
+  if (valid) outw[(size_t)b * N + n] = psi_e;
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, FLAG_BAD_SIGMA_T);
 }
 
-__global__ void sweep_outflow_kernel(int batch, int H, const double* __restrict__ part,
+// Net outgoing partial currents: sum over pairs, ascending (the oracle's order), of
+// w mu (psi_out - psi_in); a reflected inflow equals the outflow it mirrors.
+__global__ void sweep_outflow_kernel(const __grid_constant__ SweepConsts sc, int batch, int order, int refl_left,
+                                     int refl_right_first, const double* __restrict__ outw,
                                      double* __restrict__ out_left, double* __restrict__ out_right) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= batch) return;
+  const int H = sc.n_pairs;
+  const double* o = outw + (size_t)b * order;
   double l = 0.0, r = 0.0;
-  for (int p = 0; p < H; ++p) {  // ascending pair order (the oracle's)
-    l += part[2 * ((size_t)b * H + p)];
-    r += part[2 * ((size_t)b * H + p) + 1];
+  for (int p = 0; p < H; ++p) {
+    const double lo = o[H - 1 - p], ro = o[H + p];
+    l += sc.wmu[p] * (lo - (refl_left ? lo : 0.0));
+    r += sc.wmu[p] * (ro - (refl_right_first ? ro : 0.0));
   }
   if (out_left) out_left[b] = l;
   if (out_right) out_right[b] = r;
@@ -257,33 +233,46 @@ snop_status launch_sweep(Ctx& ctx, const snop_grid& g, int order, int batch, con
   if (batch == 0) return SNOP_OK;
   const SweepConsts sc = make_consts(g, order);
   const int H = order / 2;
-  const size_t chains = (size_t)batch * H;
-  double* part = static_cast<double*>(ctx.slot(130, chains * 2 * sizeof(double)));
-  if (!part) {
+  double* outw = static_cast<double*>(ctx.slot(130, (size_t)batch * order * sizeof(double)));
+  if (!outw) {
     set_error("sweep: workspace allocation failed");
     return SNOP_CUDA_ERROR;
   }
   static_assert(sizeof(SweepTileSmem<false>) <= 48 * 1024 && sizeof(SweepTileSmem<true>) <= 48 * 1024,
                 "sweep tile ring exceeds the default dynamic smem limit");
   static bool carveout_set[64] = {};
-  if (ctx.device >= 0 && ctx.device < 64 && !carveout_set[ctx.device]) {  // 7 one-warp CTAs per SM
+  if (ctx.device >= 0 && ctx.device < 64 && !carveout_set[ctx.device]) {  // ~14 one-warp CTAs per SM
     cudaFuncSetAttribute(sweep_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(sweep_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
     carveout_set[ctx.device] = true;
   }
-  const unsigned blocks = (unsigned)((chains + 31) / 32);
   const bool pow2 = (H & (H - 1)) == 0;
   const bool aligned = ((reinterpret_cast<uintptr_t>(st) | reinterpret_cast<uintptr_t>(em)) & 15) == 0;
-  if (pow2 && H >= 2 && g.n_cells % 2 == 0 && aligned)
-    sweep_kernel<true><<<blocks, 32, sizeof(SweepTileSmem<true>), ctx.stream>>>(sc, batch, order, bc_left, bc_right, st,
-                                                                                em, psi, part, ctx.d_flags);
-  else
-    sweep_kernel<false><<<blocks, 32, sizeof(SweepTileSmem<false>), ctx.stream>>>(sc, batch, order, bc_left, bc_right,
-                                                                                  st, em, psi, part, ctx.d_flags);
-  ctx.launches++;
-  sweep_outflow_kernel<<<(batch + 127) / 128, 128, 0, ctx.stream>>>(batch, H, part, out_left, out_right);
+  const bool v16 = pow2 && H >= 2 && g.n_cells % 2 == 0 && aligned;
+  auto launch = [&](int n_lo, int n_cnt, const double* infl) {
+    const unsigned blocks = (unsigned)(((size_t)batch * n_cnt + 31) / 32);
+    if (v16)
+      sweep_kernel<true><<<blocks, 32, sizeof(SweepTileSmem<true>), ctx.stream>>>(sc, batch, order, n_lo, n_cnt, st, em,
+                                                                                  psi, infl, outw, ctx.d_flags);
+    else
+      sweep_kernel<false><<<blocks, 32, sizeof(SweepTileSmem<false>), ctx.stream>>>(sc, batch, order, n_lo, n_cnt, st,
+                                                                                    em, psi, infl, outw, ctx.d_flags);
+    ctx.launches++;
+  };
+  const bool rl = bc_left == 1, rr = bc_right == 1;
+  if (!rl && !rr) {
+    launch(0, order, nullptr);  // both inflows known: every direction at once
+  } else if (rr && !rl) {
+    launch(H, H, nullptr);  // mu > 0 first; its outflow at x = L is the mu < 0 inflow
+    launch(0, H, outw);
+  } else {
+    launch(0, H, nullptr);  // reflective left: mu < 0 first (a reflective right face is lagged:
+    launch(H, H, outw);     // zero inflow for a single sweep)
+  }
+  sweep_outflow_kernel<<<(batch + 127) / 128, 128, 0, ctx.stream>>>(sc, batch, order, rl ? 1 : 0,
+                                                                     (rr && !rl) ? 1 : 0, outw, out_left, out_right);
   ctx.launches++;
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

@@ -8,6 +8,14 @@ import torch
 from paper_2509_01416_b200 import snop
 
 ctx = snop.default_context()
+import os
+if os.environ.get("L2_FETCH"):  # experiment: cudaLimitMaxL2FetchGranularity (0x05)
+    import ctypes
+    rt = ctypes.CDLL("libcudart.so.12")
+    print("cudaDeviceSetLimit ->", rt.cudaDeviceSetLimit(5, ctypes.c_size_t(int(os.environ["L2_FETCH"]))))
+    v = ctypes.c_size_t()
+    rt.cudaDeviceGetLimit(ctypes.byref(v), 5)
+    print("MaxL2FetchGranularity =", v.value)
 for name in sys.argv[1:] or ["c2", "c5"]:
     B, Nc, N = (2048, 2000, 32) if name == "c2" else (4096, 1024, 16)
     gen = torch.Generator(device="cuda").manual_seed(1)
@@ -19,14 +27,17 @@ for name in sys.argv[1:] or ["c2", "c5"]:
         for _ in range(3):
             snop.sweep(g, N, st, em, *bc)
         ts = []
-        for _ in range(10):
+        R = 8  # calls per timed region: the host prepares call i+1 while the device runs call i
+        for _ in range(5):
             with torch.cuda.stream(ext):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
                 snop.sweep(g, N, st, em, *bc, sync=False)
+                e0.record()
+                for _ in range(R):
+                    snop.sweep(g, N, st, em, *bc, sync=False)
                 e1.record()
             ctx.synchronize()
-            ts.append(e0.elapsed_time(e1))
+            ts.append(e0.elapsed_time(e1) / R)
         ms = sorted(ts)[len(ts) // 2]
         byts = B * Nc * (16.0 * N + 8.0)
         print(f"{name} bc={bc}: {ms:.3f} ms/sweep, {B*Nc*N/ms/1e6:.1f} G updates/s, {byts/ms/1e6:.0f} GB/s", flush=True)
