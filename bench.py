@@ -208,6 +208,68 @@ def eigen_arms(snop, ctx, stream, args):
     return out
 
 
+def sweep_arm(snop, ctx, stream, args):
+    """The standalone transport sweep (snop_sweep_batched) at the C2 and C5 sizes:
+    one diamond-difference sweep of all directions with a per-direction emission, psi materialised.
+    This is the HBM-bound form of the sweep kernel (16 B per cell.angle update + 8 B per cell of
+    Sigma_t); inputs and outputs (1.1-2.1 GB) are far larger than L2. Device-resident inputs, R
+    back-to-back calls between CUDA events; the CPU oracle's sweep on a sample, all host threads."""
+    import torch
+    from tests import oracle_lib as O
+    th = O.hardware_threads()
+    peak, peak_kind = peaks()
+    prof = {}
+    pj = ROOT / "profiles" / "r2_sweep_dram_bytes.json"
+    if pj.exists():
+        prof = json.loads(pj.read_text())
+    out = {}
+    for name, B, Nc, N in (("c2", 2048, 2000, 32), ("c5", 4096, 1024, 16)):
+        gen = torch.Generator(device="cuda").manual_seed(1234)
+        st = torch.rand((B, Nc), generator=gen, device="cuda", dtype=torch.float64) * 1.8 + 0.2
+        em = torch.rand((B, Nc, N), generator=gen, device="cuda", dtype=torch.float64)
+        g = snop.Grid1D(10.0, Nc)
+        R = 8
+        snop.sweep(g, N, st, em, ctx=ctx)
+        ts = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            snop.sweep(g, N, st, em, ctx=ctx, sync=False)  # (the device is busy while the host enqueues the rest)
+            e0.record(stream)
+            for _ in range(R):
+                psi, ol, orr = snop.sweep(g, N, st, em, ctx=ctx, sync=False)
+            e1.record(stream)
+            ctx.synchronize()
+            ts.append(e0.elapsed_time(e1) / 1e3 / R)
+        t = float(np.min(ts))
+        alg = B * Nc * (16.0 * N + 8.0)
+        n_cpu = max(th, 16)
+        idx = np.arange(n_cpu)
+        hs, he = st[idx].cpu().numpy(), em[idx].cpu().numpy()
+        t0 = time.perf_counter()
+        reps = 0
+        while time.perf_counter() - t0 < 2.0:
+            o_psi, _, _ = O.sweep(10.0, Nc, N, hs, he, n_threads=th)
+            reps += 1
+        tc = (time.perf_counter() - t0) / reps
+        err = float(np.max(np.abs(psi[idx].cpu().numpy() - o_psi)) / np.max(np.abs(o_psi)))
+        pr = prof.get(name, {})
+        out[name] = {
+            "workload": f"{B} x {Nc} cells x S{N}, vacuum faces, emission [B][Nc][N] -> psi_avg [B][N][Nc]",
+            "ms_per_sweep": 1e3 * t, "updates_per_sec": B * Nc * N / t,
+            "roofline": {"bound": "hbm", "achieved": alg / t / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": alg / t / 1e9 / peak, "peak_source": peak_kind,
+                         "traffic": (pr.get("dram_bytes_read", 0) + pr.get("dram_bytes_write", 0)) or None,
+                         "traffic_source": "profile-derived (profiles/r2_sweep_dram_bytes.json), not measured here",
+                         "note": "algorithmic bytes = 16 B per update (q in, psi out) + 8 B per cell (Sigma_t)"},
+            "cpu_baseline": {"updates_per_sec": n_cpu * Nc * N / tc, "cores": th, "kind": "port",
+                             "sample": f"oracle sweep of the first {n_cpu} instances, {reps} repetitions"},
+            "psi_parity_vs_oracle_sample": err,
+        }
+        del st, em, psi
+    return out
+
+
 def hybrid_arms(snop, ctx, stream, args):
     """SP / CP hybrid eigen solves (paper Eqs. A5-A8) on the first
     args.hybrid_batch instances of C3 (512 x 4096 x S32 single-group eigen): stage 1 = power
@@ -476,6 +538,7 @@ def run_gpu(args):
     c5 = None if (args.no_c5 or world > 1) else c5_arm(snop, ctx, stream, args)
     eig = None if (args.no_eigen or world > 1) else eigen_arms(snop, ctx, stream, args)
     hyb = None if (args.no_hybrid or world > 1) else hybrid_arms(snop, ctx, stream, args)
+    swp = None if (args.no_sweep or world > 1) else sweep_arm(snop, ctx, stream, args)
 
     if rank != 0:
         if world > 1:
@@ -522,6 +585,8 @@ def run_gpu(args):
         line.update(eig)
     if hyb is not None:
         line["c3_hybrid_eigen"] = hyb
+    if swp is not None:
+        line["sweep_standalone"] = swp
     if not args.no_cpu_baseline and world == 1:
         from tests import oracle_lib as O
         th = O.hardware_threads()
@@ -549,6 +614,7 @@ def main():
     ap.add_argument("--no-warm-start", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 FNO warm-start arm")
     ap.add_argument("--no-hybrid", action="store_true", help="skip the C3 SP/CP hybrid eigen arm")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the standalone sweep arm")
     ap.add_argument("--hybrid-batch", type=int, default=32)
     args = ap.parse_args()
     if args.impl == "reference":

@@ -299,6 +299,37 @@ struct HybridEigenSolution : EigenSolution {  // EigenSolution + stage diagnosti
 
 enum class HybridAlgorithm { SP, CP };
 
+// power_iteration(grid, quadrature, materials, config, inner_solver, initial) with a
+// neural-operator-backed inner_solver: the within-group solve is the operator's
+// recast fixed point (SP) or that prediction refined by a model-based source iteration (CP) --
+// stage 1 of the hybrids on its own. The model-based inner solver is snop::power_iteration.
+struct OperatorEigenSolution : EigenSolution {
+  std::vector<uint8_t> diverged;
+};
+inline OperatorEigenSolution power_iteration(HybridAlgorithm inner_solver, const SolutionOperator& op, int order,
+                                             const MultiGroupMaterials& m, const SolverConfig& cfg,
+                                             double recast_tolerance = 1e-4, int recast_max_iterations = 50) {
+  const size_t n = (size_t)m.batch * m.groups * op.n_cells();
+  if (m.sigma_t.size() != n || m.nu_sigma_f.size() != n || m.sigma_s0.size() != n * m.groups ||
+      m.chi.size() != (size_t)m.batch * m.groups || (!m.sigma_s1.empty() && m.sigma_s1.size() != n))
+    throw InvalidArgument("power_iteration: array sizes do not match batch/groups/n_cells");
+  OperatorEigenSolution e;
+  e.k.resize(m.batch);
+  e.phi.resize(n);
+  e.outer_iterations.resize(m.batch);
+  e.total_inner_iterations.resize(m.batch);
+  e.converged.resize(m.batch);
+  e.diverged.resize(m.batch);
+  const snop_solver_config c = cfg.c();
+  check(snop_power_iteration_operator_batched(
+      op.context().get(), op.get(),
+      inner_solver == HybridAlgorithm::SP ? SNOP_INNER_RECAST_FIXED_POINT : SNOP_INNER_PREDICT_REFINE, SNOP_MEM_HOST,
+      order, m.batch, m.groups, m.sigma_t.data(), m.sigma_s0.data(), m.sigma_s1.empty() ? nullptr : m.sigma_s1.data(),
+      m.nu_sigma_f.data(), m.chi.data(), &c, recast_tolerance, recast_max_iterations, e.k.data(), e.phi.data(),
+      e.outer_iterations.data(), e.total_inner_iterations.data(), e.converged.data(), e.diverged.data()));
+  return e;
+}
+
 // sp_eigen / cp_eigen: stage 1 with the operator as the within-group solver,
 // stage 2 model-based from (k_NO, phi_NO); divergence falls back to the cold start.
 inline HybridEigenSolution hybrid_eigen(HybridAlgorithm alg, const SolutionOperator& op, int order,

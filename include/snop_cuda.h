@@ -291,6 +291,22 @@ snop_status snop_precondition_fixed_source(
  * An instance whose stage 1 diverged or degenerated restarts stage 2 cold; fallback[b] = 1.
  * Layouts as snop_power_iteration_batched; the operator's grid is the problem grid. stage1_k =
  * k_NO; stage*_inner count recast iterations (+ refinement sweeps for CP) / sweeps. */
+/* power_iteration(grid, quadrature, materials, config, inner_solver, initial) with a
+ * neural-operator-backed inner_solver ("inner_solver is any procedure with the
+ * source_iteration contract ... this indirection is what SP/CP plug into"): the power iteration whose
+ * within-group solve is the operator -- stage 1 of SP (inner_solver = RECAST_FIXED_POINT, Eqs. A5-A6)
+ * or of CP (PREDICT_REFINE, Eqs. A7-A8) on its own, from the flat start (k = 1). The model-based
+ * inner solver is snop_power_iteration_batched. inner_iterations counts recast iterations (+ refinement
+ * sweeps for PREDICT_REFINE); diverged[b] = 1 where the operator iteration diverged or the fission
+ * integral degenerated (then converged[b] = 0 and k / phi hold the last iterate). */
+typedef enum { SNOP_INNER_RECAST_FIXED_POINT = 0, SNOP_INNER_PREDICT_REFINE = 1 } snop_inner_solver;
+snop_status snop_power_iteration_operator_batched(
+    snop_ctx* ctx, snop_op* op, int32_t inner_solver, int32_t memspace, int32_t order, int32_t batch,
+    int32_t n_groups, const double* sigma_t, const double* sigma_s0, const double* sigma_s1,
+    const double* nu_sigma_f, const double* chi, const snop_solver_config* cfg, double recast_tolerance,
+    int32_t recast_max_iterations, double* k_out, double* phi_out, int32_t* outer_iterations,
+    int64_t* inner_iterations, uint8_t* converged, uint8_t* diverged);
+
 snop_status snop_sp_eigen_batched(
     snop_ctx* ctx, snop_op* op, int32_t memspace, int32_t order, int32_t batch, int32_t n_groups,
     const double* sigma_t, const double* sigma_s0, const double* sigma_s1, const double* nu_sigma_f,

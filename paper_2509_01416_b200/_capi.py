@@ -26,7 +26,7 @@ EXPORTS = [
     "snop_op_save", "snop_op_load", "snop_model_write_deeponet", "snop_model_write_fno", "snop_model_inspect",
     "snop_grf_sample", "snop_normalize_source", "snop_generate_dataset", "snop_dataset_write", "snop_dataset_read",
     "snop_source_iteration_leakage_batched", "snop_balance_report", "snop_ctx_set_options", "snop_ctx_get_options",
-    "snop_sweep_batched",
+    "snop_sweep_batched", "snop_power_iteration_operator_batched",
 ]
 
 _lib = None
@@ -75,6 +75,9 @@ def load():
     lib.snop_recast_fixed_point.argtypes = [vp, vp, i32, i32, vp, vp, vp, dbl, i32, i32, vp, vp, vp, vp]
     lib.snop_precondition_fixed_source.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp, vp, dbl, i32,
                                                    C.POINTER(SnopSolverConfig), vp, vp, vp, vp, vp]
+    lib.snop_power_iteration_operator_batched.argtypes = [
+        vp, vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, C.POINTER(SnopSolverConfig), dbl, i32, vp, vp, vp, vp,
+        vp, vp]
     for fn in ("snop_sp_eigen_batched", "snop_cp_eigen_batched"):
         getattr(lib, fn).argtypes = [vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, C.POINTER(SnopSolverConfig), dbl,
                                      i32, vp, vp, vp, vp, vp, vp, vp, vp, vp]

@@ -1197,9 +1197,26 @@ struct HybridOut {
   uint8_t *conv, *fb;
 };
 
+// Result of a stage-1-only run (power iteration with the operator as inner solver): the stage-1
+// flux and eigenvalue, converged = the dual test was met, fb = diverged or degenerate.
+__global__ void hy_stage1_out(int G, int Nc, const double* __restrict__ phi1, double* __restrict__ phi,
+                              const double* __restrict__ k1, double* __restrict__ k, const uint8_t* __restrict__ active,
+                              uint8_t* __restrict__ fb, const uint8_t* __restrict__ div, uint8_t* __restrict__ conv) {
+  const int b = blockIdx.x;
+  const size_t GN = (size_t)G * Nc;
+  for (size_t i = threadIdx.x; i < GN; i += blockDim.x) phi[b * GN + i] = phi1[b * GN + i];
+  if (threadIdx.x == 0) {
+    const bool f = fb[b] || div[b];
+    if (k != k1) k[b] = k1[b];
+    fb[b] = f ? 1 : 0;
+    conv[b] = (!f && !active[b]) ? 1 : 0;
+  }
+}
+
 snop_status hybrid_eigen_dev(Ctx& ctx, snop_op& op, int algorithm, int order, int B, int G, const double* st,
                              const double* ss0, const double* ss1, const double* nsf, const double* chi,
-                             const snop_solver_config& cfg, double rtol, int rmax, const HybridOut& o) {
+                             const snop_solver_config& cfg, double rtol, int rmax, const HybridOut& o,
+                             bool stage1_only = false) {
   const int Nc = op.grid.n_cells;
   const size_t N = (size_t)B * Nc, GNB = N * G;
   const double dx = op.grid.length_cm / Nc;
@@ -1267,6 +1284,11 @@ snop_status hybrid_eigen_dev(Ctx& ctx, snop_op& op, int algorithm, int order, in
                                      (uint64_t)rmax, (uint64_t)cfg.max_outer, (uint64_t)cfg.max_inner,
                                      (uint64_t)cfg.norm, (uint64_t)cfg.bc_left, (uint64_t)cfg.bc_right};
   SNOP_TRY(device_loop(ctx, key, body));
+  if (stage1_only) {
+    hy_stage1_out<<<B, HY_THREADS, 0, s>>>(G, Nc, phi1, o.phi, o.k1, o.k, active, o.fb, div, o.conv);
+    ctx.launches++;
+    return cuda_status("hybrid stage 1 output", cudaGetLastError());
+  }
   hy_stage2_init<<<B, HY_THREADS, 0, s>>>(G, Nc, phi1, o.k1, k0, o.fb, div);
   ctx.launches++;
   return launch_power_iteration(ctx, op.grid, order, B, G, st, ss0, ss1, nsf, chi, cfg, k0, phi1, o.k, o.phi,
@@ -1849,7 +1871,8 @@ static snop_status hybrid_eigen(snop_ctx* ctx, snop_op* op, int algorithm, int32
                                 const double* sigma_s1, const double* nu_sigma_f, const double* chi,
                                 const snop_solver_config* cfg, double rtol, int32_t rmax, double* k_out,
                                 double* phi_out, double* stage1_k, int32_t* stage1_outer, int64_t* stage1_inner,
-                                int32_t* stage2_outer, int64_t* stage2_inner, uint8_t* converged, uint8_t* fallback) {
+                                int32_t* stage2_outer, int64_t* stage2_inner, uint8_t* converged, uint8_t* fallback,
+                                bool stage1_only = false) {
   SNOP_TRY(check_op(ctx, op));
   if (!cfg) return invalid("config is NULL");
   if (order < 2 || order > 128 || order % 2) return invalid("quadrature order must be even in [2,128]");
@@ -1861,7 +1884,7 @@ static snop_status hybrid_eigen(snop_ctx* ctx, snop_op* op, int algorithm, int32
   if (op->grid.n_cells > kMaxCells) return invalid("n_cells exceeds the per-CTA sweep limit");
   if (batch == 0) return SNOP_OK;
   if (!sigma_t || !sigma_s0 || !nu_sigma_f || !chi || !k_out || !phi_out || !stage1_k || !stage1_outer ||
-      !stage1_inner || !stage2_outer || !stage2_inner || !converged || !fallback)
+      !stage1_inner || (!stage1_only && (!stage2_outer || !stage2_inner)) || !converged || !fallback)
     return invalid("NULL array");
   const bool host = memspace == SNOP_MEM_HOST;
   if (!host && memspace != SNOP_MEM_DEVICE) return invalid("memspace must be HOST(0) or DEVICE(1)");
@@ -1889,15 +1912,18 @@ static snop_status hybrid_eigen(snop_ctx* ctx, snop_op* op, int algorithm, int32
     if (!o.k || !o.phi || !o.k1 || !o.outer1 || !o.outer2 || !o.inner1 || !o.inner2 || !o.conv || !o.fb)
       return cuda_status("cudaMalloc", cudaErrorMemoryAllocation);
   }
-  SNOP_TRY(hybrid_eigen_dev(*ctx, *op, algorithm, order, batch, G, st, ss, s1, nsf, ch, *cfg, rtol, rmax, o));
+  SNOP_TRY(hybrid_eigen_dev(*ctx, *op, algorithm, order, batch, G, st, ss, s1, nsf, ch, *cfg, rtol, rmax, o,
+                            stage1_only));
   if (!host) return SNOP_OK;
   SNOP_TRY(unstage(*ctx, k_out, o.k, B));
   SNOP_TRY(unstage(*ctx, phi_out, o.phi, n));
-  SNOP_TRY(unstage(*ctx, stage1_k, o.k1, B));
+  if (stage1_k != k_out) SNOP_TRY(unstage(*ctx, stage1_k, o.k1, B));
   SNOP_TRY(unstage(*ctx, stage1_outer, o.outer1, B));
   SNOP_TRY(unstage(*ctx, stage1_inner, o.inner1, B));
-  SNOP_TRY(unstage(*ctx, stage2_outer, o.outer2, B));
-  SNOP_TRY(unstage(*ctx, stage2_inner, o.inner2, B));
+  if (!stage1_only) {
+    SNOP_TRY(unstage(*ctx, stage2_outer, o.outer2, B));
+    SNOP_TRY(unstage(*ctx, stage2_inner, o.inner2, B));
+  }
   SNOP_TRY(unstage(*ctx, converged, o.conv, B));
   SNOP_TRY(unstage(*ctx, fallback, o.fb, B));
   return drain(*ctx);
@@ -1913,6 +1939,20 @@ static snop_status hybrid_eigen(snop_ctx* ctx, snop_op* op, int algorithm, int32
   memspace, order, batch, n_groups, sigma_t, sigma_s0, sigma_s1, nu_sigma_f, chi, cfg, recast_tolerance,         \
       recast_max_iterations, k_out, phi_out, stage1_k, stage1_outer, stage1_inner, stage2_outer, stage2_inner,    \
       converged, fallback
+
+// power_iteration with the operator as inner_solver: stage 1 of SP / CP on its own.
+snop_status snop_power_iteration_operator_batched(
+    snop_ctx* ctx, snop_op* op, int32_t inner_solver, int32_t memspace, int32_t order, int32_t batch,
+    int32_t n_groups, const double* sigma_t, const double* sigma_s0, const double* sigma_s1,
+    const double* nu_sigma_f, const double* chi, const snop_solver_config* cfg, double recast_tolerance,
+    int32_t recast_max_iterations, double* k_out, double* phi_out, int32_t* outer_iterations,
+    int64_t* inner_iterations, uint8_t* converged, uint8_t* diverged) {
+  if (inner_solver != SNOP_INNER_RECAST_FIXED_POINT && inner_solver != SNOP_INNER_PREDICT_REFINE)
+    return invalid("inner_solver must be RECAST_FIXED_POINT(0) or PREDICT_REFINE(1)");
+  return hybrid_eigen(ctx, op, inner_solver, memspace, order, batch, n_groups, sigma_t, sigma_s0, sigma_s1, nu_sigma_f,
+                      chi, cfg, recast_tolerance, recast_max_iterations, k_out, phi_out, k_out, outer_iterations,
+                      inner_iterations, nullptr, nullptr, converged, diverged, true);
+}
 
 snop_status snop_sp_eigen_batched(SNOP_HYBRID_ARGS) { return hybrid_eigen(ctx, op, 0, SNOP_HYBRID_FWD); }
 snop_status snop_cp_eigen_batched(SNOP_HYBRID_ARGS) { return hybrid_eigen(ctx, op, 1, SNOP_HYBRID_FWD); }

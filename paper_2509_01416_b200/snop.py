@@ -578,6 +578,54 @@ def _hybrid_eigen(fn: str, op: SolutionOperator, order: int, sigma_t, sigma_s0, 
     return HybridEigenSolution(k, phi, k1, o1, i1, o2, i2, cv, fb)
 
 
+INNER_RECAST_FIXED_POINT, INNER_PREDICT_REFINE = 0, 1
+
+
+@dataclass
+class OperatorEigenSolution:
+    """EigenSolution of a power iteration whose inner solver is a SolutionOperator."""
+    k: object
+    phi: object
+    outer_iterations: object
+    total_inner_iterations: object
+    converged: object
+    diverged: object
+
+
+def power_iteration_with_operator(op: SolutionOperator, order: int, sigma_t, sigma_s0, nu_sigma_f, chi,
+                                  config: SolverConfig | None = None, inner_solver: int = INNER_RECAST_FIXED_POINT,
+                                  recast_tolerance: float = 1e-4, recast_max_iterations: int = 50,
+                                  sigma_s1=None) -> OperatorEigenSolution:
+    """power_iteration(..., inner_solver = neural-operator-backed): the within-group
+    solve is the operator's recast fixed point (INNER_RECAST_FIXED_POINT: stage 1 of SP) or that
+    prediction refined by a model-based source iteration (INNER_PREDICT_REFINE: stage 1 of CP).
+    Layouts as power_iteration; flat start, k = 1."""
+    config = config or SolverConfig()
+    a = _Args(sigma_t, sigma_s0, nu_sigma_f, chi, sigma_s1)
+    B, G, n = (int(x) for x in sigma_t.shape)
+    if n != op.grid.n_cells:
+        raise ValueError("sigma_t last dim must equal the operator grid's n_cells")
+    st = a.inp(sigma_t, shape=(B, G, n))
+    ss = a.inp(sigma_s0, shape=(B, G, G, n))
+    nsf = a.inp(nu_sigma_f, shape=(B, G, n))
+    ch = a.inp(chi, shape=(B, G))
+    s1 = a.inp(sigma_s1, shape=(B, G, n))
+    k, k_p = a.out((B,))
+    phi, phi_p = a.out((B, G, n))
+    o1, o1_p = a.out((B,), np.int32)
+    i1, i1_p = a.out((B,), np.int64)
+    cv, cv_p = a.out((B,), np.uint8)
+    dv, dv_p = a.out((B,), np.uint8)
+    cfg = config.c()
+    a.ready(op.ctx)
+    _capi.check(op.ctx._lib.snop_power_iteration_operator_batched(
+        op.ctx.h, op.h, int(inner_solver), a.memspace, int(order), B, G, st, ss, s1, nsf, ch, C.byref(cfg),
+        float(recast_tolerance), int(recast_max_iterations), k_p, phi_p, o1_p, i1_p, cv_p, dv_p))
+    if a.device:
+        op.ctx.synchronize()
+    return OperatorEigenSolution(k, phi, o1, i1, cv, dv)
+
+
 def sp_eigen(op: SolutionOperator, order: int, sigma_t, sigma_s0, nu_sigma_f, chi, config: SolverConfig | None = None,
              recast_tolerance: float = 1e-4, recast_max_iterations: int = 50, sigma_s1=None) -> HybridEigenSolution:
     """SP eigen solve (paper Eq. A5-A6), batched; layouts as power_iteration."""

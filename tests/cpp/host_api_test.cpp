@@ -79,6 +79,21 @@ int main() {
     auto h = hybrid_eigen(HybridAlgorithm::CP, xop, 32, mg, ec);
     EXPECT(std::fabs(h.k[0] - e.k[0]) < 1e-6 && h.converged[0] == 1 && h.fallback[0] == 0);
     EXPECT(std::fabs(h.stage1_k[0] - e.k[0]) < 1e-5);
+    // power_iteration with the operator as inner_solver = that stage 1 on its own
+    auto p1 = power_iteration(HybridAlgorithm::CP, xop, 32, mg, ec);
+    EXPECT(p1.k[0] == h.stage1_k[0] && p1.outer_iterations[0] == h.stage1_outer[0] && p1.converged[0] == 1 &&
+           p1.diverged[0] == 0);
+  }
+  {  // standalone sweep: zero emission, vacuum -> psi = 0, outflow 0; a reflective pair of
+    // faces with uniform emission keeps the net outflow at the reflective left face at zero
+    std::vector<double> st(100, 1.0), em(100 * 8, 0.0);
+    auto z = sweep(ctx, g, 8, 1, st, em);
+    double mx = 0.0;
+    for (double v : z.psi_avg) mx = std::fmax(mx, std::fabs(v));
+    EXPECT(mx == 0.0 && z.outflow_left[0] == 0.0 && z.outflow_right[0] == 0.0);
+    std::fill(em.begin(), em.end(), 0.5);
+    auto r = sweep(ctx, g, 8, 1, st, em, SNOP_BC_REFLECTIVE, SNOP_BC_VACUUM);
+    EXPECT(r.outflow_left[0] == 0.0 && r.outflow_right[0] > 0.0);
   }
   // zero fission -> DegenerateProblem
   mg.nu_sigma_f.assign(300, 0.0);

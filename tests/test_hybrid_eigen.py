@@ -171,3 +171,40 @@ def test_gpu_divergence_fallback_and_device_memspace():
     rd = _run_dev(snop, op, SP, order, *d, cfg, recast_tolerance=1e-6)
     assert np.array_equal(rd.k.cpu().numpy(), r.k)
     assert np.array_equal(rd.phi.cpu().numpy(), r.phi)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("alg", [SP, CP])
+def test_gpu_power_iteration_with_operator_inner_solver(alg):
+    """power_iteration with a neural-operator-backed inner_solver = stage 1 of
+    SP / CP on its own: against the oracle's stage 1 (Table 9, exact operator), bit-identical to the
+    stage-1 diagnostics of the two-stage entry points, and k-infinity for the reflective medium."""
+    snop = _dev()
+    p = W.three_group_table9()
+    order = 8
+    cfg = O.make_config(1e-7, 1e-8, 1e-7)
+    o = O.OracleOperator.exact(p.length, p.n_cells, order, (1.0, 0.5), cfg).hybrid_eigen(
+        alg, order, p.sigma_t, p.sigma_s0, p.nu_sigma_f, p.chi, cfg)
+    op = snop.SolutionOperator.exact(snop.Grid1D(p.length, p.n_cells), order, (1.0, 0.5), _dev_cfg(snop, cfg))
+    r = snop.power_iteration_with_operator(op, order, p.sigma_t, p.sigma_s0, p.nu_sigma_f, p.chi, _dev_cfg(snop, cfg),
+                                           inner_solver=alg)
+    assert r.converged[0] and not r.diverged[0]
+    assert abs(int(r.outer_iterations[0]) - int(o["stage1_outer"][0])) <= 1
+    assert abs(r.k[0] - o["stage1_k"][0]) / o["stage1_k"][0] < 1e-7
+    two = _run_dev(snop, op, alg, order, p.sigma_t, p.sigma_s0, p.nu_sigma_f, p.chi, cfg)
+    assert r.k[0] == two.stage1_k[0] and int(r.outer_iterations[0]) == int(two.stage1_outer[0])
+    assert int(r.total_inner_iterations[0]) == int(two.stage1_inner[0])
+    # the stage-1 flux is normalised to a unit fission integral (SPEC.md:183); with a Sigma_t deviation it is
+    # the recast model's eigenmode (isotropic approximation, paper Eq. 23), not the transport one
+    dx = p.length / p.n_cells
+    assert abs(dx * float(np.sum(p.nu_sigma_f[0] * r.phi[0])) - 1.0) < 1e-12
+    # reflective infinite medium: k = nu Sigma_f / Sigma_a at stage 1 (SPEC.md:185)
+    n = 20
+    cfg2 = O.make_config(1e-10, 1e-10, 1e-9, bc_left=1, bc_right=1)
+    op2 = snop.SolutionOperator.exact(snop.Grid1D(10.0, n), order, (1.0, 0.5), _dev_cfg(snop, cfg2))
+    st, ss, nsf, chi = _homogeneous(n, 1.0, 0.6, 0.5, B=3)
+    r2 = snop.power_iteration_with_operator(op2, order, st, ss, nsf, chi, _dev_cfg(snop, cfg2), inner_solver=alg,
+                                            recast_tolerance=1e-11, recast_max_iterations=200)
+    assert np.all(np.abs(r2.k - 0.5 / 0.4) < 1e-6) and r2.converged.all()
+    with pytest.raises(Exception):
+        snop.power_iteration_with_operator(op2, order, st, ss, nsf, chi, _dev_cfg(snop, cfg2), inner_solver=7)
