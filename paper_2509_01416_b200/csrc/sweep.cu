@@ -24,6 +24,7 @@
 //   * partial currents: every chain's outflow goes to a workspace [B][N]; a tiny kernel forms
 //     w mu (psi_out - psi_in) per pair and sums the pairs of an instance in ascending order
 //     (deterministic, the oracle's order).
+#include <mutex>
 #include <string>
 
 #define SNOP_PHASE_SYM g_phase_cycles_sweep
@@ -240,14 +241,14 @@ snop_status launch_sweep(Ctx& ctx, const snop_grid& g, int order, int batch, con
   }
   static_assert(sizeof(SweepTileSmem<false>) <= 48 * 1024 && sizeof(SweepTileSmem<true>) <= 48 * 1024,
                 "sweep tile ring exceeds the default dynamic smem limit");
-  static bool carveout_set[64] = {};
-  if (ctx.device >= 0 && ctx.device < 64 && !carveout_set[ctx.device]) {  // ~14 one-warp CTAs per SM
-    cudaFuncSetAttribute(sweep_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(sweep_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
-    carveout_set[ctx.device] = true;
-  }
+  static std::once_flag carveout_once[64];  // per device: ~14 one-warp CTAs per SM need the full carve-out
+  if (ctx.device >= 0 && ctx.device < 64)
+    std::call_once(carveout_once[ctx.device], [] {
+      cudaFuncSetAttribute(sweep_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
+      cudaFuncSetAttribute(sweep_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
+    });
   const bool pow2 = (H & (H - 1)) == 0;
   const bool aligned = ((reinterpret_cast<uintptr_t>(st) | reinterpret_cast<uintptr_t>(em)) & 15) == 0;
   const bool v16 = pow2 && H >= 2 && g.n_cells % 2 == 0 && aligned;
