@@ -169,8 +169,11 @@ struct EigenParams {
 // PS = pair-split cluster (see si_solve): every CTA of the cluster runs the whole outer loop
 // redundantly on private working copies of phi / old / q_ext (ranks > 0 in psw_g), only the inner
 // sweeps are divided; rank 0 owns the outputs.
-template <int K, int NT, bool ANISO, bool CL, bool PS = false>
-__global__ void __launch_bounds__(NT, min_blocks<K, NT>())
+// WIDE: one CTA per SM is enough (the batch fits the SMs in one wave), so the register cap of the
+// two-CTAs-per-SM build (128; the eigen kernel spills ~450 B per thread under it) is lifted: no
+// spills, same arithmetic (C4, one wave of 128 CTAs: 27.6 -> 23.6 ms).
+template <int K, int NT, bool ANISO, bool CL, bool PS = false, bool WIDE = false>
+__global__ void __launch_bounds__(NT, WIDE ? 1 : min_blocks<K, NT>())
 power_iteration_kernel(const __grid_constant__ SweepConsts sc, const SolveConfig icfg, const EigenParams ep,
                        const double* __restrict__ st_g, const double* __restrict__ ss0_g,
                        const double* __restrict__ ss1_g, const double* __restrict__ nsf_g,
@@ -554,6 +557,11 @@ inline snop_status launch_pi_t(snop_impl::Ctx& ctx, const SweepConsts& sc, const
   const size_t smem = smem_bytes<K, NT>();
   auto kern = PS ? power_iteration_kernel<K, NT, false, false, PS>
                  : (aniso ? power_iteration_kernel<K, NT, true, CL> : power_iteration_kernel<K, NT, false, CL>);
+  if constexpr (!CL && !PS && (min_blocks<K, NT>() > 1)) {
+    if (batch <= ctx.sm_count)  // one wave at one CTA per SM: the register-rich build
+      kern = aniso ? power_iteration_kernel<K, NT, true, false, false, true>
+                   : power_iteration_kernel<K, NT, false, false, false, true>;
+  }
   if (PS && aniso) {
     snop_impl::set_error("pair-split eigen kernel is isotropic only");
     return SNOP_INVALID_ARGUMENT;
