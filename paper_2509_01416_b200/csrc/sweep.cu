@@ -35,8 +35,7 @@ using namespace snop_dev;
 
 namespace {
 
-constexpr int kT = 8;   // cells per tile
-constexpr int kS = 4;   // ring stages (kS - 1 tiles in flight per warp)
+constexpr int kS = 4;   // ring stages (kS - 1 tiles of T = 8 or 16 cells in flight per warp)
 constexpr int kG = 16;  // most (instance, sign) groups a warp can span on the vector path (N/2 >= 2)
 
 // V16 = false (any order / cell count / alignment): every thread copies its own q and Sigma_t
@@ -44,11 +43,11 @@ constexpr int kG = 16;  // most (instance, sign) groups a warp can span on the v
 // arrays): even lanes copy the q of a lane pair (adjacent directions) with 16-byte cp.async.cg
 // (8-byte cp.async.ca serialises its shared-memory writes: 17 wavefronts per request in ncu, the
 // LSU data pipe at 87%), and Sigma_t is copied once per (instance, sign) group of the warp.
-template <bool V16>
+template <bool V16, int T>
 struct SweepTileSmem {
-  double q[kS][kT][32];                           // emission, [stage][cell in sweep order][lane]
-  double st[kS][V16 ? kG : kT][V16 ? kT : 32];    // Sigma_t: [..][group][ascending cell] or [..][cell][lane]
-  double out[32][kT + 1];                         // psi_avg of the current tile, [lane][cell] (+1: conflict-free)
+  double q[kS][T][32];                           // emission, [stage][cell in sweep order][lane]
+  double st[kS][V16 ? kG : T][V16 ? T : 32];    // Sigma_t: [..][group][ascending cell] or [..][cell][lane]
+  double out[32][T + 1];                         // psi_avg of the current tile, [lane][cell] (+1: conflict-free)
 };
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
@@ -70,13 +69,13 @@ __device__ __forceinline__ void cp_async_wait() {
 // Directions [n_lo, n_lo + n_cnt) of every instance; chain gt = b * n_cnt + (n - n_lo). infl: null
 // (vacuum inflow) or the outflow workspace of the previous launch (inflow of direction n = outflow
 // of its mirror image N-1-n at the same face).
-template <bool V16>
-__global__ void __launch_bounds__(32)
+template <bool V16, int T>
+__global__ void __launch_bounds__(32, T == 8 ? 14 : 7)
 sweep_kernel(const __grid_constant__ SweepConsts sc, int batch, int order, int n_lo, int n_cnt,
              const double* __restrict__ st_g, const double* __restrict__ em_g, double* __restrict__ psi,
              const double* __restrict__ infl, double* __restrict__ outw /* [B][N] */, int* __restrict__ flags) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto& sm = *reinterpret_cast<SweepTileSmem<V16>*>(smem_raw);
+  auto& sm = *reinterpret_cast<SweepTileSmem<V16, T>*>(smem_raw);
   const int lane = threadIdx.x, Nc = sc.n_cells, H = sc.n_pairs, N = order;
   const long long total = (long long)batch * n_cnt;
   const long long gt = (long long)blockIdx.x * 32 + lane;
@@ -91,7 +90,7 @@ sweep_kernel(const __grid_constant__ SweepConsts sc, int batch, int order, int n
   // vector path: the lanes of this warp that share (instance, sign) (N/2 a power of two)
   const int hw = H < 32 ? H : 32;
   const int grp = V16 ? lane / hw : 0, grank = lane % hw;
-  const int ntiles = (Nc + kT - 1) / kT, nfull = Nc / kT;
+  const int ntiles = (Nc + T - 1) / T, nfull = Nc / T;
 
   // Loop-invariant addressing (the kernel was issue-bound at ~66 instructions per cell with the
   // addresses and bounds recomputed per cell): global q pointer of tile 0 / cell 0 and its
@@ -100,55 +99,80 @@ sweep_kernel(const __grid_constant__ SweepConsts sc, int batch, int order, int n
   const double* qp = em_n + (fwd ? 0 : (size_t)(Nc - 1) * N);    // cell of sweep step 0
   const int xr = fwd ? 0 : 1;  // V16: a backward group's tile is stored ascending: sweep step j at j ^ 1 of
                                // the reversed pair order (see issue()), i.e. compile-time j +- xr
-  constexpr int RPI = 32 / kT;
-  const int e = lane % kT, rsub = lane / kT;
+  constexpr int RPI = 32 / T;
+  const int e = lane % T, rsub = lane / T;
   const unsigned fwd_mask = __ballot_sync(0xffffffffu, fwd);
-  double* wb[kT];     // row r = it * RPI + rsub: address of this lane's element in the row's tile 0
-  int wo[kT];         // its index in sm.out
+  double* wb[T];     // row r = it * RPI + rsub: address of this lane's element in the row's current tile
+  int wo[T];         // its index in sm.out
   unsigned rfw = 0, rok = 0;
 #pragma unroll
-  for (int it = 0; it < kT; ++it) {
+  for (int it = 0; it < T; ++it) {
     const int r = it * RPI + rsub;
     const size_t base = __shfl_sync(0xffffffffu, (unsigned long long)row, r);
     const bool rf = (fwd_mask >> r) & 1u;
     rfw |= (rf ? 1u : 0u) << it;
     rok |= (base != ~(size_t)0 ? 1u : 0u) << it;
-    wb[it] = psi + (base != ~(size_t)0 ? base : 0) + e + (rf ? 0 : Nc - kT);
-    wo[it] = r * (kT + 1) + (rf ? e : kT - 1 - e);
+    wb[it] = psi + (base != ~(size_t)0 ? base : 0) + e + (rf ? 0 : Nc - T);
+    wo[it] = r * (T + 1) + (rf ? e : T - 1 - e);
   }
   double* const outp = &sm.out[0][0];
 
+  // Sigma_t tile copies of the vector path: lane rank r of a group copies cell pair r (and, in
+  // 2-lane groups, also pair r + 2) of the group's 8-cell tile; a backward group stores the pairs in
+  // descending order, so sweep step j reads slot j ^ 1.
+  constexpr int NCP = T / 4;  // most Sigma_t copies per lane (2-lane groups)
   auto issue = [&](int k) {
     if (k < ntiles) {
       const int slot = k % kS;
-      const bool full = k < nfull;
-      if constexpr (V16) {
-        if ((lane & 1) == 0) {  // q of this lane and the next (adjacent directions, same cell)
-          const double* src = qp + (long long)k * kT * dq;
+      const double* src = qp + (long long)k * T * dq;
+      const int a0 = fwd ? k * T : Nc - (k + 1) * T;  // first (ascending) cell of the group's tile
+      if (k < nfull) {  // interior tile: no bounds to check
+        if constexpr (V16) {
+          if ((lane & 1) == 0) {  // q of this lane and the next (adjacent directions, same cell)
 #pragma unroll
-          for (int j = 0; j < kT; ++j) {
-            const bool ok = valid && (full || k * kT + j < Nc);
-            cp_async16(&sm.q[slot][j][lane], ok ? src : em_n, ok);
+            for (int j = 0; j < T; ++j) {
+              cp_async16(&sm.q[slot][j][lane], src, valid);
+              src += dq;
+            }
+          }
+#pragma unroll
+          for (int cpy = 0; cpy < NCP; ++cpy) {
+            const int m2 = grank + cpy * hw;
+            if (m2 < T / 2)
+              cp_async16(&sm.st[slot][grp][fwd ? 2 * m2 : T - 2 - 2 * m2], st_b + a0 + 2 * m2, valid);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < T; ++j) {
+            cp_async8(&sm.q[slot][j][lane], src, valid);
+            cp_async8(&sm.st[slot][j][lane], st_b + (fwd ? a0 + j : a0 + T - 1 - j), valid);
             src += dq;
           }
         }
-        // Sigma_t of the group's tile, two ascending cells per copy (even Nc and kT: never split);
-        // a backward group stores the pairs in descending order, so sweep step j reads slot j ^ 1
-        const int a0 = fwd ? k * kT : Nc - (k + 1) * kT;
-        for (int m2 = grank; m2 < kT / 2; m2 += hw) {
-          const int i = a0 + 2 * m2;
-          const bool ok = valid && i >= 0 && i < Nc;
-          cp_async16(&sm.st[slot][grp][fwd ? 2 * m2 : kT - 2 - 2 * m2], st_b + (ok ? i : 0), ok);
-        }
-      } else {
-        const double* src = qp + (long long)k * kT * dq;
+      } else {  // ragged last tile
+        if constexpr (V16) {
+          if ((lane & 1) == 0) {
 #pragma unroll
-        for (int j = 0; j < kT; ++j) {
-          const int sidx = k * kT + j, i = fwd ? sidx : Nc - 1 - sidx;
-          const bool ok = valid && sidx < Nc;
-          cp_async8(&sm.q[slot][j][lane], ok ? src : em_n, ok);
-          cp_async8(&sm.st[slot][j][lane], st_b + (ok ? i : 0), ok);
-          src += dq;
+            for (int j = 0; j < T; ++j) {
+              const bool ok = valid && k * T + j < Nc;
+              cp_async16(&sm.q[slot][j][lane], ok ? src : em_n, ok);
+              src += dq;
+            }
+          }
+          for (int m2 = grank; m2 < T / 2; m2 += hw) {
+            const int i = a0 + 2 * m2;
+            const bool ok = valid && i >= 0 && i < Nc;  // (even Nc and T: a pair is never split)
+            cp_async16(&sm.st[slot][grp][fwd ? 2 * m2 : T - 2 - 2 * m2], st_b + (ok ? i : 0), ok);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < T; ++j) {
+            const int sidx = k * T + j, i = fwd ? sidx : Nc - 1 - sidx;
+            const bool ok = valid && sidx < Nc;
+            cp_async8(&sm.q[slot][j][lane], ok ? src : em_n, ok);
+            cp_async8(&sm.st[slot][j][lane], st_b + (ok ? i : 0), ok);
+            src += dq;
+          }
         }
       }
     }
@@ -175,28 +199,52 @@ sweep_kernel(const __grid_constant__ SweepConsts sc, int batch, int order, int n
     if constexpr (V16) __syncwarp();  // ... and the other lanes' (pair partner, Sigma_t tile)
     const int slot = k % kS;
     if (k < nfull) {
+      // all loads, then the independent part (reciprocals, q r, c r), then the dependent chain:
+      // written out in phases because the compiler otherwise serialises the cells (each cell's
+      // loads after the previous cell's store)
+      double sv[T], qv[T];
 #pragma unroll
-      for (int j = 0; j < kT; ++j) cell(slot, j);
+      for (int j = 0; j < T; ++j) {
+        if constexpr (V16) sv[j] = (&sm.st[slot][grp][0])[(j & 1) ? j - xr : j + xr];
+        else sv[j] = sm.st[slot][j][lane];
+        qv[j] = sm.q[slot][j][lane];
+      }
+#pragma unroll
+      for (int j = 0; j < T; ++j) {
+        bad |= !(sv[j] > 0.0);
+        const double r = rcp_fast(sv[j] + c);
+        qv[j] *= r;     // q r
+        sv[j] = c * r;  // c r
+      }
+#pragma unroll
+      for (int j = 0; j < T; ++j) {
+        const double avg = fma(sv[j], psi_e, qv[j]);  // (q + c psi_in) r
+        psi_e = fma(2.0, avg, -psi_e);
+        qv[j] = avg;
+      }
+#pragma unroll
+      for (int j = 0; j < T; ++j) sm.out[lane][j] = qv[j];
       __syncwarp();
-      // write-out: 32/kT rows of kT contiguous cells per instruction
+      // write-out: 32/T rows of T contiguous cells per instruction; the row pointers advance by
+      // one tile in their sweep direction
 #pragma unroll
-      for (int it = 0; it < kT; ++it) {
+      for (int it = 0; it < T; ++it) {
         const double v = outp[wo[it]];
-        const long long off = ((rfw >> it) & 1u) ? (long long)k * kT : -(long long)k * kT;
-        if ((rok >> it) & 1u) __stcs(wb[it] + off, v);
+        if ((rok >> it) & 1u) __stcs(wb[it], v);
+        wb[it] += ((rfw >> it) & 1u) ? T : -T;
       }
     } else {  // ragged last tile
 #pragma unroll
-      for (int j = 0; j < kT; ++j)
-        if (k * kT + j < Nc) cell(slot, j);
+      for (int j = 0; j < T; ++j)
+        if (k * T + j < Nc) cell(slot, j);
       __syncwarp();
 #pragma unroll
-      for (int it = 0; it < kT; ++it) {
+      for (int it = 0; it < T; ++it) {
         const bool rf = (rfw >> it) & 1u;
-        const int i = rf ? k * kT + e : Nc - (k + 1) * kT + e;
+        const int i = rf ? k * T + e : Nc - (k + 1) * T + e;
         const double v = outp[wo[it]];
-        const long long off = rf ? (long long)k * kT : -(long long)k * kT;
-        if (((rok >> it) & 1u) && i >= 0 && i < Nc) __stcs(wb[it] + off, v);
+        if (((rok >> it) & 1u) && i >= 0 && i < Nc) __stcs(wb[it], v);
+        wb[it] += rf ? T : -T;
       }
     }
     __syncwarp();
@@ -239,32 +287,44 @@ snop_status launch_sweep(Ctx& ctx, const snop_grid& g, int order, int batch, con
     set_error("sweep: workspace allocation failed");
     return SNOP_CUDA_ERROR;
   }
-  static_assert(sizeof(SweepTileSmem<false>) <= 48 * 1024 && sizeof(SweepTileSmem<true>) <= 48 * 1024,
+  static_assert(sizeof(SweepTileSmem<false, 16>) <= 48 * 1024 && sizeof(SweepTileSmem<true, 16>) <= 48 * 1024,
                 "sweep tile ring exceeds the default dynamic smem limit");
-  static std::once_flag carveout_once[64];  // per device: ~14 one-warp CTAs per SM need the full carve-out
+  static std::once_flag carveout_once[64];  // per device: 7-14 one-warp CTAs per SM need the full carve-out
   if (ctx.device >= 0 && ctx.device < 64)
     std::call_once(carveout_once[ctx.device], [] {
-      cudaFuncSetAttribute(sweep_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           cudaSharedmemCarveoutMaxShared);
-      cudaFuncSetAttribute(sweep_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           cudaSharedmemCarveoutMaxShared);
+      const auto a = cudaFuncAttributePreferredSharedMemoryCarveout;
+      cudaFuncSetAttribute(sweep_kernel<true, 8>, a, cudaSharedmemCarveoutMaxShared);
+      cudaFuncSetAttribute(sweep_kernel<false, 8>, a, cudaSharedmemCarveoutMaxShared);
+      cudaFuncSetAttribute(sweep_kernel<true, 16>, a, cudaSharedmemCarveoutMaxShared);
+      cudaFuncSetAttribute(sweep_kernel<false, 16>, a, cudaSharedmemCarveoutMaxShared);
     });
   const bool pow2 = (H & (H - 1)) == 0;
   const bool aligned = ((reinterpret_cast<uintptr_t>(st) | reinterpret_cast<uintptr_t>(em)) & 15) == 0;
   const bool v16 = pow2 && H >= 2 && g.n_cells % 2 == 0 && aligned;
   auto launch = [&](int n_lo, int n_cnt, const double* infl) {
     const unsigned blocks = (unsigned)(((size_t)batch * n_cnt + 31) / 32);
-    if (v16)
-      sweep_kernel<true><<<blocks, 32, sizeof(SweepTileSmem<true>), ctx.stream>>>(sc, batch, order, n_lo, n_cnt, st, em,
-                                                                                  psi, infl, outw, ctx.d_flags);
-    else
-      sweep_kernel<false><<<blocks, 32, sizeof(SweepTileSmem<false>), ctx.stream>>>(sc, batch, order, n_lo, n_cnt, st,
-                                                                                    em, psi, infl, outw, ctx.d_flags);
+    // 16-cell tiles (128-byte output rows, half the per-tile overhead) for narrow quadratures, when
+    // the launch still fits one wave at their 7 CTAs per SM (a second wave would double the time of
+    // these long marches). Measured: C5 (S16) 0.296 -> 0.292 ms, but C2 (S32) 0.421 -> 0.433 ms.
+    const bool t16 = order <= 16 && blocks <= 7u * (unsigned)ctx.sm_count && g.n_cells >= 64;
+#define SNOP_SWEEP_LAUNCH(V, TT)                                                                              \
+  sweep_kernel<V, TT><<<blocks, 32, sizeof(SweepTileSmem<V, TT>), ctx.stream>>>(sc, batch, order, n_lo, n_cnt, st, em, \
+                                                                                psi, infl, outw, ctx.d_flags)
+    if (v16 && t16) SNOP_SWEEP_LAUNCH(true, 16);
+    else if (v16) SNOP_SWEEP_LAUNCH(true, 8);
+    else if (t16) SNOP_SWEEP_LAUNCH(false, 16);
+    else SNOP_SWEEP_LAUNCH(false, 8);
+#undef SNOP_SWEEP_LAUNCH
     ctx.launches++;
   };
   const bool rl = bc_left == 1, rr = bc_right == 1;
   if (!rl && !rr) {
+#ifdef SNOP_SWEEP_ONE_LAUNCH
     launch(0, order, nullptr);  // both inflows known: every direction at once
+#else
+    launch(0, H, nullptr);  // both inflows known; one sign per launch (warps of uniform direction)
+    launch(H, H, nullptr);
+#endif
   } else if (rr && !rl) {
     launch(H, H, nullptr);  // mu > 0 first; its outflow at x = L is the mu < 0 inflow
     launch(0, H, outw);
