@@ -607,8 +607,9 @@ __device__ __forceinline__ void replay_phase(const SweepConsts& sc, SweepSmem<K,
         if (w.rr && w.rl && t == 0) sm.lag[(w.it + 1) & 1][p] = fma(TAf, psi_left_in, TBf);
       }
     }
-    const double cta_left = fma(EfA, psi_left_in, EfB);
-    const double cta_right = fma(EbA, psi_right_in, EbB);
+    // (one CTA: the entry maps are the identity; spelled out so no 1 * x + 0 is left on the chain)
+    const double cta_left = CL ? fma(EfA, psi_left_in, EfB) : psi_left_in;
+    const double cta_right = CL ? fma(EbA, psi_right_in, EbB) : psi_right_in;
     const int pt = SweepSmem<K, NT>::spos(t);
     double psi = fma(sm.xmap[q][0][pt], cta_left, sm.agg[q][1][pt]);
     double psib = fma(sm.xmap[q][1][pt], cta_right, sm.agg[q][2][pt]);
