@@ -107,6 +107,18 @@ def test_sweep_thin_cells_and_device_arrays():
 
 
 @gpu
+@pytest.mark.parametrize("Nc,N", [(200001, 2), (65536, 4)])
+def test_sweep_long_slab(Nc, N):
+    """Slabs far beyond the solvers' resident limits (any n_cells up to 2^26 is valid):
+    the march has no per-instance size limit; odd / even cell counts take the two load paths."""
+    from paper_2509_01416_b200 import snop
+    st, em = _case(2, Nc, N, 9)
+    psi, ol, orr = snop.sweep(snop.Grid1D(50.0, Nc), N, st, em, 0, 1)
+    o_psi, o_ol, o_or = O.sweep(50.0, Nc, N, st, em, 0, 1)
+    assert _rel(psi, o_psi) < PSI_RTOL and _rel(ol, o_ol) < PSI_RTOL and np.max(np.abs(orr - o_or)) < 1e-14
+
+
+@gpu
 def test_sweep_errors_and_empty():
     from paper_2509_01416_b200 import snop
     from paper_2509_01416_b200.errors import InvalidArgument
