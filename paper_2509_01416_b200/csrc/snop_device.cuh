@@ -411,11 +411,11 @@ __device__ __forceinline__ void maps_phase(const SweepConsts& sc, SweepSmem<K, N
 // One (pair, direction) scan by one warp. Lane l owns chunks l*E .. l*E+E-1 in sweep order; with
 // the padded layout those E chunk maps are contiguous in shared memory (ascending for the forward
 // sweep, descending for the backward one), so every access is base + compile-time offset.
-//   1. serial inclusive prefix over the lane's E chunks, written to the exclusive-map array as
-//      scratch (stores are fire-and-forget: the chain is E-1 dependent DFMA/DMUL pairs);
-//   2. 5-step shuffle scan of the lane totals -> the lane's exclusive entry map (Ax, Bx);
-//   3. exclusive map of chunk e = (Ax, Bx) composed with prefix e-1: E-1 independent
-//      compositions, processed in descending e so each reads its prefix before it is replaced.
+//   1. serial inclusive prefixes over the lane's E chunks, in registers (runs of more than
+//      SNOP_SCAN_REG_E chunks keep only the total and recompose the prefixes in step 3);
+//   2. the run totals shifted up one lane, then a 5-round shuffle scan of (identity, T_0 .. T_30)
+//      -> the lane's exclusive entry map (A, B), with no predicates on the dependent chain;
+//   3. exclusive map of chunk e = (A, B) composed with prefix e-1 (E-1 independent compositions).
 #ifndef SNOP_SCAN_REG_E
 #define SNOP_SCAN_REG_E 4
 #endif
