@@ -81,7 +81,7 @@ gpu = pytest.mark.gpu
 @gpu
 @pytest.mark.parametrize("bc", [(0, 0), (1, 0), (0, 1), (1, 1)])
 @pytest.mark.parametrize("B,Nc,N", [(3, 1, 2), (5, 7, 4), (4, 64, 8), (9, 1000, 16), (6, 2000, 32), (2, 517, 6),
-                                    (3, 4099, 64), (2100, 66, 32), (4200, 67, 16), (3, 300, 4)])  # (large batches: more than
+                                    (3, 4099, 64), (2100, 66, 32), (4200, 67, 16), (3, 300, 4), (2, 100, 128), (3, 98, 12)])  # (large batches: more than
     # one wave of CTAs; N <= 16 in one wave: 16-cell tiles, otherwise 8-cell tiles)
 def test_sweep_parity(bc, B, Nc, N):
     from paper_2509_01416_b200 import snop
