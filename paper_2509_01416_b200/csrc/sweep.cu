@@ -319,12 +319,33 @@ snop_status launch_sweep(Ctx& ctx, const snop_grid& g, int order, int batch, con
   };
   const bool rl = bc_left == 1, rr = bc_right == 1;
   if (!rl && !rr) {
-#ifdef SNOP_SWEEP_ONE_LAUNCH
-    launch(0, order, nullptr);  // both inflows known: every direction at once
-#else
-    launch(0, H, nullptr);  // both inflows known; one sign per launch (warps of uniform direction)
-    launch(H, H, nullptr);
-#endif
+    // Both inflows known. One launch per direction sign: run back to back they beat one launch of
+    // mixed-direction work on C2 (0.421 vs 0.461 ms: with both ends of every slab streaming at once
+    // the DRAM efficiency drops); for narrow quadratures (half rows of q shorter than a 128-byte DRAM
+    // line) the second launch goes to a second stream so its ramp-up overlaps the first one's tail
+    // (C5 0.292 -> 0.284 ms; on C2 the concurrent form is the slow one again, 0.462 ms).
+    if (order <= 16) {
+      if (!ctx.aux) {
+        if (cudaStreamCreateWithFlags(&ctx.aux, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx.ev_join, cudaEventDisableTiming) != cudaSuccess) {
+          set_error("sweep: stream / event creation failed");
+          return SNOP_CUDA_ERROR;
+        }
+      }
+      cudaEventRecord(ctx.ev_fork, ctx.stream);
+      cudaStreamWaitEvent(ctx.aux, ctx.ev_fork, 0);
+      launch(0, H, nullptr);
+      cudaStream_t main_s = ctx.stream;
+      ctx.stream = ctx.aux;
+      launch(H, H, nullptr);
+      cudaEventRecord(ctx.ev_join, ctx.aux);
+      ctx.stream = main_s;
+      cudaStreamWaitEvent(ctx.stream, ctx.ev_join, 0);
+    } else {
+      launch(0, H, nullptr);
+      launch(H, H, nullptr);
+    }
   } else if (rr && !rl) {
     launch(H, H, nullptr);  // mu > 0 first; its outflow at x = L is the mu < 0 inflow
     launch(0, H, outw);
