@@ -22,3 +22,12 @@ b = grab(1).astype(np.float64)
 sw = int(r.total_inner_iterations[0]) * 8  # per CTA sweeps (8 CTAs; thread 0 of each)
 names = ["wait replays", "push partials", "cluster barrier", "owner update+push", "norm reduce"]
 print("cycles per sweep per CTA:", {n: round(b[i] / sw) for i, n in enumerate(names)}, "pairs", round(b[5] / sw), "phi", round(b[6] / sw))
+# whole-loop accounting (slot 8 = the outer loop, 7 = inside si_solve calls, 9 = per-group source build + staging)
+outers = int(r.outer_iterations[0])
+print("outers", outers, "sweeps", int(r.total_inner_iterations[0]),
+      "| cycles per outer per CTA: whole loop", round(b[8] / (8 * outers)), "in si_solve", round(b[7] / (8 * outers)),
+      "source build + staging", round(b[9] / (8 * outers)),
+      "| loop cycles per sweep", round(b[8] / sw), "si_solve cycles per sweep", round(b[7] / sw))
+import time
+t0 = time.perf_counter(); r = snop.power_iteration(g, p.order, *args, cfg); torch.cuda.synchronize()
+print("wall ms", 1e3 * (time.perf_counter() - t0))
